@@ -1,0 +1,184 @@
+/*
+ * spmat.h -- C ABI of libspmat: a B200-native (sm_100a) distributed fp64 MatMult on a
+ * row-partitioned MPIAIJ matrix assembled on the device by COO, with a star-forest (SF) halo
+ * exchange over NCCL.  The method is the one of arXiv 2406.08646 (PETSc/TAO on GPU-based
+ * exascale systems); citations "P:n" are lines of that paper's text.
+ *
+ * Plain C: no torch or CUDA types in the signatures.  Streams are passed as `void *`
+ * holding a cudaStream_t (NULL = the legacy default stream).  Every call returns an
+ * spmat_status; a human-readable message for the last failure on the calling thread is
+ * available from spmat_last_error().
+ *
+ * Process model: one process (rank) per GPU.  Collective calls must be made by every rank
+ * of the communicator in the same order.
+ *
+ * Ownership: handles are opaque and caller-owned, freed by the matching *_destroy.  Data
+ * pointers are borrowed for the duration of the call (host arrays) or until the work
+ * enqueued on `stream` completes (device arrays).
+ */
+#ifndef SPMAT_H
+#define SPMAT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SPMAT_OK = 0,
+  SPMAT_ERR_ARG = 1,      /* bad argument (null handle, negative size, x == y, bad op) */
+  SPMAT_ERR_RANGE = 2,    /* COO index >= M or >= N; SF root offset outside the owner */
+  SPMAT_ERR_STATE = 3,    /* call out of order (bcast_end without begin, op mismatch) */
+  SPMAT_ERR_MISMATCH = 4, /* ranks disagree on global sizes / local sizes do not sum */
+  SPMAT_ERR_OOM = 5,      /* device allocation failed */
+  SPMAT_ERR_CUDA = 6,     /* CUDA runtime error (possibly from earlier asynchronous work) */
+  SPMAT_ERR_NCCL = 7      /* NCCL missing (nranks > 1) or an NCCL error */
+} spmat_status;
+
+/* MatSetValuesCOO(A, v, mode).  Reading (Z2): INSERT sets every
+   stored nonzero to +0.0 + (sum of its contributions); ADD adds that sum to the value. */
+typedef enum { SPMAT_INSERT = 0, SPMAT_ADD = 1 } spmat_mode;
+
+/* PetscSFBcast op: MPI_REPLACE or MPI_SUM ("add the source values or ... replace the
+   destination values"). */
+typedef enum { SF_REPLACE = 0, SF_SUM = 1 } sf_op;
+
+typedef struct spmat_comm_s *spmat_comm_t;
+typedef struct spmat_s *spmat_t;
+typedef struct sf_s *sf_t;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int spmat_version(void);
+
+/* Thread-local message describing the last failure (never NULL). */
+const char *spmat_last_error(void);
+
+/* ------------------------------------------------------------------ communicator --- */
+
+/* Fill id[128] with a fresh NCCL unique id.  Called on rank 0 only; the caller broadcasts
+   the bytes to the other ranks (e.g. with torch.distributed).  Needs NCCL. */
+int spmat_comm_unique_id(unsigned char id[128]);
+
+/* Create the per-rank communicator on CUDA device `device`.  Collective when nranks > 1
+   (NCCL communicator from `id`); with nranks == 1 `id` may be NULL and NCCL is not used.
+   Creates the library's high-priority communication stream on that device. */
+int spmat_comm_create(const unsigned char *id, int nranks, int rank, int device,
+                      spmat_comm_t *out);
+
+/* Poll asynchronous NCCL errors (ncclCommGetAsyncError) and sticky CUDA errors. */
+int spmat_comm_check(spmat_comm_t comm);
+
+int spmat_comm_destroy(spmat_comm_t comm);
+
+/* ------------------------------------------------------------------- star forest --- */
+
+/* PetscSF creation: "created collectively by specifying, for each leaf on the
+   current process, the owner rank and an offset of the corresponding root on the owner".
+     nroots           number of roots owned by this rank (valid offsets are [0, nroots))
+     nleaves          number of leaves on this rank
+     ilocal           leaf l's index in leafdata (host or device array of nleaves); NULL
+                      means leaf l is leafdata[l]
+     remote_rank      owner rank of leaf l's root (host or device, nleaves entries)
+     remote_offset    root offset on the owner (host or device, nleaves entries)
+   Collective and host-synchronising.  Errors: SPMAT_ERR_ARG (rank outside [0,nranks),
+   duplicate ilocal), SPMAT_ERR_RANGE (offset >= owner's nroots; reported on every rank).
+   The plan groups leaves by owner rank ascending, then (root offset, leaf index). */
+int sf_create(spmat_comm_t comm, int64_t nroots, int64_t nleaves, const int64_t *ilocal,
+              const int32_t *remote_rank, const int64_t *remote_offset, sf_t *out);
+
+/* Split-phase broadcast root -> leaf.  rootdata (nroots doubles) and leafdata
+   (covering every ilocal) are DEVICE arrays.  Begin enqueues pack -> NCCL send/recv ->
+   unpack on the library's communication stream after the work already on `stream`; it
+   never blocks the host.  End makes `stream` wait for that work.  Between begin and end
+   the caller may enqueue independent work on `stream`; it must not write rootdata or read
+   leafdata.  Leaf entries not in the SF are untouched.  End must name the same buffers and
+   op as begin (else SPMAT_ERR_STATE). */
+int sf_bcast_begin(sf_t sf, const double *rootdata, double *leafdata, int op, void *stream);
+int sf_bcast_end(sf_t sf, const double *rootdata, double *leafdata, int op, void *stream);
+
+/* info[0..7] = nroots, nleaves, n_send_neighbours, n_recv_neighbours, n_send_values,
+   n_recv_values, n_self_edges, packed (1 if any pack or unpack kernel is needed) */
+int sf_get_info(sf_t sf, int64_t info[8]);
+
+/* Test hook: what = 0 recv neighbour ranks, 1 recv counts, 2 leaf indices in receive
+   order, 3 send neighbour ranks, 4 send counts, 5 root offsets in send order
+   (all int64).  Copies min(cap, len) values into host_buf; *len = full length. */
+int sf_export(sf_t sf, int what, void *host_buf, int64_t cap, int64_t *len);
+
+int sf_destroy(sf_t sf);
+
+/* ------------------------------------------------------------------------ matrix --- */
+
+/* MatSetPreallocationCOO(A, n, i, j).  Symbolic COO assembly.
+     m_local, n_local   rows / columns owned by this rank (contiguous ranges in rank order,
+                        P:661-662); they must sum to M / N over ranks
+     ncoo               length of coo_i / coo_j on this rank
+     coo_i, coo_j       global int64 indices, host or device memory (detected); not
+                        retained ("can be freed after this stage")
+   Entries with i < 0 or j < 0 are ignored.  Off-rank rows are routed to their
+   owners over NCCL; the owner sorts contributions by (i, j, src rank, k), splits the
+   diagonal block (columns in [cstart, cend)) from the off-diagonal block, builds colmap
+   (sorted unique ghost columns), the per-nonzero contribution plan (jmap/perm), the COO
+   send/receive plans and the halo SF.  Collective and host-synchronising.
+   Errors: SPMAT_ERR_RANGE if i >= M or j >= N (message names the rank and k; reported on
+   every rank), SPMAT_ERR_MISMATCH if ranks disagree on M, N or the local sizes. */
+int spmat_create_coo(spmat_comm_t comm, int64_t m_local, int64_t n_local, int64_t M,
+                     int64_t N, int64_t ncoo, const int64_t *coo_i, const int64_t *coo_j,
+                     spmat_t *out);
+
+/* MatSetValuesCOO(A, v, mode).  v: DEVICE array of this rank's ncoo doubles in
+   the order of coo_i/coo_j.  Enqueue-only: send-buffer gather -> NCCL value exchange on
+   the comm stream, overlapped with the kernel that finishes every nonzero whose
+   contributions are all local; nonzeros with received contributions are finished after the
+   exchange.  Each nonzero is summed by one thread in ascending (src rank, k) order: no
+   atomics, deterministic.  Collective. */
+int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream);
+
+/* MatMult y = A x.  x: n_local doubles, y: m_local doubles, x != y.
+   Device pointers: enqueue-only -- halo bcast_begin (x -> ghost vector) on the comm stream,
+   diagonal-block SpMV on `stream`, bcast_end, off-diagonal SpMV-add on `stream`.
+   Host pointers (pinned or pageable; memtype detected as in P:252-260): x is copied to the
+   device and y back inside the call's stream order; the call then returns after y is
+   written.  Collective. */
+int spmat_mult(spmat_t A, const double *x, double *y, void *stream);
+
+/* Parts of MatMult for isolated timing: part bit 1 = diagonal SpMV (y = A_d x), bit 2 =
+   halo exchange (x -> ghost vector), bit 4 = off-diagonal SpMV-add (y += A_o ghosts).
+   part 7 == spmat_mult on device pointers. */
+int spmat_mult_part(spmat_t A, const double *x, double *y, int part, void *stream);
+
+/* info[0..15] = rstart, rend, cstart, cend, nnz_d, nnz_o, n_ghost, n_offdiag_rows,
+   n_contrib, n_send (COO entries sent), n_recv (COO entries received), n_mixed (nonzeros
+   with received contributions), spmv_kernel_id, n_rowblocks, max_row_nnz, plan_builds */
+int spmat_get_info(spmat_t A, int64_t info[16]);
+
+/* Test hook: copy a device array to host.  All integer arrays are returned as int64.
+     0 rowptr_d[m+1]   1 col_d (local)   2 val_d (f64)   3 rowptr_o[m+1] (full rows)
+     4 col_o (ghost index)   5 val_o (f64)   6 colmap (global ghost columns)
+     7 jmap[nnz_d+nnz_o+1] (diag nonzeros then offdiag nonzeros)
+     8 contribution source rank per jmap entry   9 contribution index per jmap entry: k for
+       local entries, position within the message from that source rank for received ones
+     10 send_count[nranks]  11 send_k (COO k's sent, destination-major)
+     12 recv_count[nranks]  13 rows_o (compressed off-diagonal rows)
+   *len = full length; min(cap, len) values are copied. */
+int spmat_export(spmat_t A, int what, void *host_buf, int64_t cap, int64_t *len);
+
+/* The halo SF (leaves = ghost columns in colmap order).  Borrowed: do not destroy. */
+int spmat_get_halo_sf(spmat_t A, sf_t *borrowed);
+
+/* Per-kernel timing with CUDA events recorded on the launching streams.  enable=1 starts
+   recording around the diagonal SpMV and off-diagonal SpMV-add of every spmat_mult;
+   spmat_profile_read() synchronises, returns the summed milliseconds and launch counts
+   (ms[0]/n[0] diagonal SpMV, ms[1]/n[1] off-diagonal, ms[2]/n[2] halo on the comm stream)
+   and clears them. */
+int spmat_profile(spmat_t A, int enable);
+int spmat_profile_read(spmat_t A, double ms[4], int64_t n[4]);
+
+int spmat_destroy(spmat_t A);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPMAT_H */

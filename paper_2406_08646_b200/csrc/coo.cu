@@ -1,0 +1,820 @@
+// coo.cu -- device COO assembly: MatSetPreallocationCOO / MatSetValuesCOO.
+//
+// Symbolic (spmat_create_coo), all on the device except the tiny per-rank
+// count vectors:
+//   1. classify every entry k: ignored (i<0 or j<0), range error, or owner rank
+//   2. stable radix sort of (owner, k) -> per-destination k lists; the off-rank ones are the
+//      COO send plan ("destined for ... a send buffer")
+//   3. NCCL exchange of the (i, j) of off-rank entries ("exchanges information about remote
+//      entries")
+//   4. contributions in canonical (src rank, k) order -> 64-bit key (i - rstart) * N + j;
+//      stable LSD radix sort by key keeps (src, k) order inside equal keys (reading Z1)
+//   5. run-length heads -> nonzeros; diag / offdiag split by column ownership;
+//      CSR row pointers; colmap = sorted unique ghost columns; jmap/perm per block
+//   6. the halo SF from colmap
+// Numeric (spmat_set_values_coo): gather the send buffer, start the NCCL value
+// exchange on the comm stream, then one thread per nonzero sums its contribution segment
+// ("each thread accumulates into a single nonzero entry", no atomics).  Nonzeros
+// whose segment contains received values are finished after the exchange, still in
+// canonical order, so the result is bit-identical to a serial sum in (src, k) order.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <memory>
+
+#include "internal.h"
+
+namespace spmat {
+
+// ------------------------------------------------------------------ helpers
+struct Tmp {
+  DevBuf<char> buf;
+  int ensure(size_t bytes) {
+    if (bytes <= buf.n) return SPMAT_OK;
+    return buf.alloc(bytes);
+  }
+};
+
+#define CUB_CALL(tmp, stream, call_with_tmp)                                       \
+  do {                                                                             \
+    size_t _bytes = 0;                                                             \
+    void *d_temp_storage = nullptr;                                                \
+    size_t &temp_storage_bytes = _bytes;                                           \
+    SP_CUDA(call_with_tmp);                                                        \
+    SP_TRY((tmp).ensure(_bytes));                                                  \
+    d_temp_storage = (tmp).buf.get();                                              \
+    SP_CUDA(call_with_tmp);                                                        \
+  } while (0)
+
+static inline unsigned nblk(int64_t n, int t = 256) {
+  int64_t b = (n + t - 1) / t;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)1 << 30));
+}
+
+static inline int bits_for(uint64_t maxval) {  // bits needed to represent 0..maxval
+  int b = 0;
+  while (b < 64 && (maxval >> b) != 0) ++b;
+  return std::max(b, 1);
+}
+
+#define GRID_STRIDE(t, n) \
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (n); t += (int64_t)gridDim.x * blockDim.x)
+
+// ------------------------------------------------------------------ symbolic kernels
+__global__ void k_classify(const int64_t *__restrict__ ci, const int64_t *__restrict__ cj,
+                           int64_t n, int64_t M, int64_t N, const int64_t *__restrict__ roff,
+                           int P, uint32_t *__restrict__ dest,
+                           unsigned long long *__restrict__ bad_k) {
+  GRID_STRIDE(k, n) {
+    int64_t i = ci[k], j = cj[k];
+    uint32_t d = (uint32_t)P;  // P = dropped
+    if (i >= 0 && j >= 0) {
+      if (i >= M || j >= N) {
+        atomicMin(bad_k, (unsigned long long)k);
+      } else {  // owner: largest r with roff[r] <= i (upper bound - 1)
+        int lo = 0, hi = P;  // invariant: roff[lo] <= i < roff[hi]
+        while (hi - lo > 1) {
+          int mid = (lo + hi) >> 1;
+          if (roff[mid] <= i) lo = mid; else hi = mid;
+        }
+        d = (uint32_t)lo;
+      }
+    }
+    dest[k] = d;
+  }
+}
+
+__global__ void k_iota(uint32_t *__restrict__ out, int64_t n) {
+  GRID_STRIDE(t, n) out[t] = (uint32_t)t;
+}
+
+// dofs[d] = lower_bound(sorted, d) for d = 0..P+1
+__global__ void k_bounds(const uint32_t *__restrict__ sorted, int64_t n, int P,
+                         int64_t *__restrict__ dofs) {
+  int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d > P + 1) return;
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (sorted[mid] < (uint32_t)d) lo = mid + 1; else hi = mid;
+  }
+  dofs[d] = lo;
+}
+
+__global__ void k_gather_ij(const int64_t *__restrict__ ci, const int64_t *__restrict__ cj,
+                            const uint32_t *__restrict__ ks, int64_t n,
+                            longlong2 *__restrict__ out) {
+  GRID_STRIDE(t, n) {
+    uint32_t k = ks[t];
+    out[t] = make_longlong2(ci[k], cj[k]);
+  }
+}
+
+// received entries: recv position t -> canonical position; value index = ncoo + t
+__global__ void k_keys_recv(const longlong2 *__restrict__ rij, int64_t nrecv, int64_t before,
+                            int64_t nlocal, int64_t rstart, int64_t N, uint64_t ncoo,
+                            uint64_t *__restrict__ key, uint32_t *__restrict__ val) {
+  GRID_STRIDE(t, nrecv) {
+    longlong2 e = rij[t];
+    int64_t pos = t < before ? t : t + nlocal;
+    key[pos] = (uint64_t)(e.x - rstart) * (uint64_t)N + (uint64_t)e.y;
+    val[pos] = (uint32_t)(ncoo + (uint64_t)t);
+  }
+}
+
+__global__ void k_keys_local(const int64_t *__restrict__ ci, const int64_t *__restrict__ cj,
+                             const uint32_t *__restrict__ ks, int64_t nlocal, int64_t before,
+                             int64_t rstart, int64_t N, uint64_t *__restrict__ key,
+                             uint32_t *__restrict__ val) {
+  GRID_STRIDE(u, nlocal) {
+    uint32_t k = ks[u];
+    key[before + u] = (uint64_t)(ci[k] - rstart) * (uint64_t)N + (uint64_t)cj[k];
+    val[before + u] = k;
+  }
+}
+
+__global__ void k_heads(const uint64_t *__restrict__ key, int64_t n, uint32_t *__restrict__ head) {
+  GRID_STRIDE(t, n) head[t] = (t == 0 || key[t] != key[t - 1]) ? 1u : 0u;
+}
+
+// per nonzero z (segment start s = segstart[z]): row, column, block, row counts
+__global__ void k_nz_classify(const uint64_t *__restrict__ key, const uint32_t *__restrict__ segstart,
+                              int64_t nnz, int64_t N, int64_t cstart, int64_t cend,
+                              uint32_t *__restrict__ isdiag, int32_t *__restrict__ cnt_d,
+                              int32_t *__restrict__ cnt_o) {
+  GRID_STRIDE(z, nnz) {
+    uint64_t kk = key[segstart[z]];
+    int64_t row = (int64_t)(kk / (uint64_t)N), col = (int64_t)(kk % (uint64_t)N);
+    bool d = col >= cstart && col < cend;
+    isdiag[z] = d ? 1u : 0u;
+    atomicAdd(d ? &cnt_d[row] : &cnt_o[row], 1);
+  }
+}
+
+__global__ void k_nz_cols(const uint64_t *__restrict__ key, const uint32_t *__restrict__ segstart,
+                          const uint32_t *__restrict__ isdiag, const uint32_t *__restrict__ pos_d,
+                          int64_t nnz, int64_t N, int64_t cstart, int32_t *__restrict__ col_d,
+                          int64_t *__restrict__ ocol) {
+  GRID_STRIDE(z, nnz) {
+    uint64_t kk = key[segstart[z]];
+    int64_t col = (int64_t)(kk % (uint64_t)N);
+    if (isdiag[z]) col_d[pos_d[z]] = (int32_t)(col - cstart);
+    else ocol[z - pos_d[z]] = col;
+  }
+}
+
+__global__ void k_ghost_index(const int64_t *__restrict__ ocol, int64_t nnz_o,
+                              const int64_t *__restrict__ colmap, int64_t ng,
+                              int32_t *__restrict__ col_o) {
+  GRID_STRIDE(t, nnz_o) {
+    int64_t c = ocol[t], lo = 0, hi = ng;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (colmap[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    col_o[t] = (int32_t)lo;
+  }
+}
+
+// contribution t belongs to nonzero zid1[t] - 1 (zid1 = inclusive scan of run heads);
+// flag whether that nonzero is diagonal
+__global__ void k_cflag(const uint32_t *__restrict__ zid1, const uint32_t *__restrict__ isdiag,
+                        int64_t n, uint32_t *__restrict__ cflag) {
+  GRID_STRIDE(t, n) cflag[t] = isdiag[zid1[t] - 1];
+}
+
+__global__ void k_perm(const uint32_t *__restrict__ val, const uint32_t *__restrict__ cflag,
+                       const uint32_t *__restrict__ cpos_d, int64_t n, int64_t total_d,
+                       uint32_t *__restrict__ perm) {
+  GRID_STRIDE(t, n) {
+    int64_t at = cflag[t] ? (int64_t)cpos_d[t] : total_d + (t - (int64_t)cpos_d[t]);
+    perm[at] = val[t];
+  }
+}
+
+__global__ void k_jmap(const uint32_t *__restrict__ segstart, const uint32_t *__restrict__ isdiag,
+                       const uint32_t *__restrict__ pos_d, const uint32_t *__restrict__ cpos_d,
+                       int64_t nnz, int64_t nnz_d, int64_t total_d, int64_t nt,
+                       uint32_t *__restrict__ jmap) {
+  GRID_STRIDE(z, nnz) {
+    int64_t s = segstart[z];
+    if (isdiag[z]) jmap[pos_d[z]] = cpos_d[s];
+    else jmap[nnz_d + (z - pos_d[z])] = (uint32_t)(total_d + (s - (int64_t)cpos_d[s]));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) jmap[nnz] = (uint32_t)nt;
+}
+
+__global__ void k_mixed_flag(const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm,
+                             int64_t nnz, uint64_t ncoo, uint32_t *__restrict__ flag) {
+  GRID_STRIDE(z, nnz) {
+    uint32_t f = 0;
+    for (uint32_t t = jmap[z]; t < jmap[z + 1]; ++t)
+      if (perm[t] >= ncoo) { f = 1; break; }
+    flag[z] = f;
+  }
+}
+
+__global__ void k_nonempty(const int32_t *__restrict__ cnt, int64_t m, uint32_t *__restrict__ f) {
+  GRID_STRIDE(r, m) f[r] = cnt[r] > 0 ? 1u : 0u;
+}
+
+__global__ void k_gather_i32(const int32_t *__restrict__ src, const int32_t *__restrict__ idx,
+                             int64_t n, int32_t *__restrict__ dst) {
+  GRID_STRIDE(t, n) dst[t] = src[idx[t]];
+}
+
+// ------------------------------------------------------------------ numeric kernels
+__global__ void k_send_gather(const double *__restrict__ v, const uint32_t *__restrict__ sp,
+                              int64_t n, double *__restrict__ out) {
+  GRID_STRIDE(t, n) out[t] = v[sp[t]];
+}
+
+// Nonzeros whose contributions are all local: s = +0.0; s = s + v[k] in canonical order.
+// A nonzero that meets a received contribution is left for k_numeric_mixed.
+__global__ void k_numeric_local(const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm,
+                                const double *__restrict__ v, uint64_t ncoo, int64_t nnz_d,
+                                int64_t nnz, double *__restrict__ val_d,
+                                double *__restrict__ val_o, int mode) {
+  GRID_STRIDE(z, nnz) {
+    uint32_t t0 = jmap[z], t1 = jmap[z + 1];
+    double s = 0.0;
+    bool local = true;
+    for (uint32_t t = t0; t < t1; ++t) {
+      uint32_t p = perm[t];
+      if (p >= ncoo) { local = false; break; }
+      s = __dadd_rn(s, v[p]);
+    }
+    if (local) {
+      double *a = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
+      *a = mode == SPMAT_INSERT ? __dadd_rn(0.0, s) : __dadd_rn(*a, s);
+    }
+  }
+}
+
+__global__ void k_numeric_mixed(const uint32_t *__restrict__ mixed, int64_t nmixed,
+                                const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm,
+                                const double *__restrict__ v, const double *__restrict__ recv,
+                                uint64_t ncoo, int64_t nnz_d, double *__restrict__ val_d,
+                                double *__restrict__ val_o, int mode) {
+  GRID_STRIDE(q, nmixed) {
+    int64_t z = mixed[q];
+    double s = 0.0;
+    for (uint32_t t = jmap[z]; t < jmap[z + 1]; ++t) {
+      uint32_t p = perm[t];
+      s = __dadd_rn(s, p < ncoo ? v[p] : recv[p - ncoo]);
+    }
+    double *a = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
+    *a = mode == SPMAT_INSERT ? __dadd_rn(0.0, s) : __dadd_rn(*a, s);
+  }
+}
+
+// ------------------------------------------------------------------ symbolic driver
+static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_t M, int64_t N,
+                       int64_t ncoo, const int64_t *coo_i, const int64_t *coo_j, spmat_s **out) {
+  const int P = c->nranks, me = c->rank;
+  cudaStream_t st = c->setup_stream;
+  // ---- layout agreement (a1): allgather (m, n, M, N, ncoo-ok)
+  int64_t mine[4] = {m_local, n_local, M, N};
+  std::vector<int64_t> all(4 * (size_t)P);
+  SP_TRY(c->allgather_i64(mine, 4, all.data()));
+  std::vector<int64_t> roff(P + 1, 0), coff(P + 1, 0);
+  bool mismatch = false;
+  for (int r = 0; r < P; ++r) {
+    if (all[4 * r + 2] != M || all[4 * r + 3] != N) mismatch = true;
+    if (all[4 * r] < 0 || all[4 * r + 1] < 0) mismatch = true;
+    roff[r + 1] = roff[r] + all[4 * r];
+    coff[r + 1] = coff[r] + all[4 * r + 1];
+  }
+  if (roff[P] != M || coff[P] != N) mismatch = true;
+  if (mismatch)
+    return fail(SPMAT_ERR_MISMATCH,
+                "spmat_create_coo: ranks disagree on M,N or local sizes do not sum (M=%lld N=%lld)",
+                (long long)M, (long long)N);
+  const int64_t rstart = roff[me], cstart = coff[me], cend = coff[me + 1];
+  if (m_local > INT32_MAX - 1) return fail(SPMAT_ERR_ARG, "m_local must be < 2^31");
+
+  Tmp tmp;
+  // ---- inputs on the device (memtype detection); not retained
+  DevBuf<int64_t> di, dj;
+  const int64_t *ci = coo_i, *cj = coo_j;
+  if (ncoo > 0) {
+    if (!coo_i || !coo_j) return fail(SPMAT_ERR_ARG, "spmat_create_coo: null coo_i/coo_j");
+    if (!is_device_ptr(coo_i)) {
+      SP_TRY(di.alloc(ncoo));
+      SP_CUDA(cudaMemcpyAsync(di.get(), coo_i, ncoo * 8, cudaMemcpyHostToDevice, st));
+      ci = di.get();
+    }
+    if (!is_device_ptr(coo_j)) {
+      SP_TRY(dj.alloc(ncoo));
+      SP_CUDA(cudaMemcpyAsync(dj.get(), coo_j, ncoo * 8, cudaMemcpyHostToDevice, st));
+      cj = dj.get();
+    }
+  }
+  if ((uint64_t)ncoo >= (1ull << 32)) return fail(SPMAT_ERR_ARG, "ncoo must be < 2^32");
+
+  // ---- 1. classify
+  DevBuf<int64_t> droff;
+  SP_TRY(droff.alloc(P + 1));
+  SP_CUDA(cudaMemcpyAsync(droff.get(), roff.data(), (P + 1) * 8, cudaMemcpyHostToDevice, st));
+  DevBuf<unsigned long long> dbad;
+  SP_TRY(dbad.alloc(1));
+  SP_CUDA(cudaMemsetAsync(dbad.get(), 0xff, 8, st));
+  DevBuf<uint32_t> dest, dest2, kk, kk2;
+  SP_TRY(dest.alloc(ncoo));
+  if (ncoo > 0) {
+    k_classify<<<nblk(ncoo), 256, 0, st>>>(ci, cj, ncoo, M, N, droff.get(), P, dest.get(), dbad.get());
+    SP_LAUNCH();
+  }
+  unsigned long long bad = ~0ull;
+  SP_CUDA(cudaMemcpyAsync(&bad, dbad.get(), 8, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  {
+    int64_t b = bad == ~0ull ? -1 : (int64_t)bad;
+    std::vector<int64_t> allbad(P);
+    SP_TRY(c->allgather_i64(&b, 1, allbad.data()));
+    for (int r = 0; r < P; ++r)
+      if (allbad[r] >= 0)
+        return fail(SPMAT_ERR_RANGE, "spmat_create_coo: COO index out of range on rank %d at k=%lld",
+                    r, (long long)allbad[r]);
+  }
+
+  // ---- 2. stable sort (dest, k) -> per-destination k lists
+  SP_TRY(kk.alloc(ncoo));
+  SP_TRY(kk2.alloc(ncoo));
+  SP_TRY(dest2.alloc(ncoo));
+  std::vector<int64_t> dofs(P + 2, 0);
+  if (ncoo > 0) {
+    k_iota<<<nblk(ncoo), 256, 0, st>>>(kk.get(), ncoo);
+    SP_LAUNCH();
+    cub::DoubleBuffer<uint32_t> dk(dest.get(), dest2.get()), dv(kk.get(), kk2.get());
+    int eb = bits_for((uint64_t)P);
+    CUB_CALL(tmp, st, cub::DeviceRadixSort::SortPairs(d_temp_storage, temp_storage_bytes, dk, dv,
+                                                      ncoo, 0, eb, st));
+    DevBuf<int64_t> ddofs;
+    SP_TRY(ddofs.alloc(P + 2));
+    k_bounds<<<1, 64 * ((P + 2 + 63) / 64), 0, st>>>(dk.Current(), ncoo, P, ddofs.get());
+    SP_LAUNCH();
+    SP_CUDA(cudaMemcpyAsync(dofs.data(), ddofs.get(), (P + 2) * 8, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    if (dv.Current() != kk.get()) std::swap(kk.p, kk2.p);
+  }
+  kk2.release();
+  dest.release();
+  dest2.release();
+  spmat_s *A = new spmat_s();
+  std::unique_ptr<spmat_s, int (*)(spmat_s *)> guard(A, [](spmat_s *a) { return spmat_destroy(a); });
+  A->comm = c;
+  A->M = M; A->N = N; A->m = m_local; A->n = n_local;
+  A->rstart = rstart; A->rend = roff[me + 1]; A->cstart = cstart; A->cend = cend;
+  A->roff = roff; A->coff = coff;
+  A->ncoo = ncoo;
+  const int64_t nlocal = dofs[me + 1] - dofs[me];
+  A->send_count.assign(P, 0);
+  A->send_off.assign(P + 1, 0);
+  for (int d = 0; d < P; ++d) A->send_count[d] = d == me ? 0 : dofs[d + 1] - dofs[d];
+  for (int d = 0; d < P; ++d) A->send_off[d + 1] = A->send_off[d] + A->send_count[d];
+  A->nsend = A->send_off[P];
+  SP_TRY(A->sendperm.alloc(A->nsend));
+  if (dofs[me] > 0)
+    SP_CUDA(cudaMemcpyAsync(A->sendperm.get(), kk.get(), dofs[me] * 4, cudaMemcpyDeviceToDevice, st));
+  if (dofs[P] - dofs[me + 1] > 0)
+    SP_CUDA(cudaMemcpyAsync(A->sendperm.get() + dofs[me], kk.get() + dofs[me + 1],
+                            (dofs[P] - dofs[me + 1]) * 4, cudaMemcpyDeviceToDevice, st));
+
+  // ---- 3. exchange (i, j) of off-rank entries
+  {
+    std::vector<int64_t> allc((size_t)P * P);
+    SP_TRY(c->allgather_i64(A->send_count.data(), P, allc.data()));
+    A->recv_count.assign(P, 0);
+    A->recv_off.assign(P + 1, 0);
+    for (int s = 0; s < P; ++s) A->recv_count[s] = s == me ? 0 : allc[(size_t)s * P + me];
+    for (int s = 0; s < P; ++s) A->recv_off[s + 1] = A->recv_off[s] + A->recv_count[s];
+    A->nrecv = A->recv_off[P];
+  }
+  if ((uint64_t)ncoo + (uint64_t)A->nrecv >= (1ull << 32))
+    return fail(SPMAT_ERR_ARG, "ncoo + received entries must be < 2^32");
+  DevBuf<longlong2> sij, rij;
+  SP_TRY(sij.alloc(A->nsend));
+  SP_TRY(rij.alloc(A->nrecv));
+  if (A->nsend > 0) {
+    k_gather_ij<<<nblk(A->nsend), 256, 0, st>>>(ci, cj, A->sendperm.get(), A->nsend, sij.get());
+    SP_LAUNCH();
+  }
+  SP_TRY(c->exchange_dev(sij.get(), A->send_off.data(), A->send_count.data(), rij.get(),
+                         A->recv_off.data(), A->recv_count.data(), sizeof(longlong2), st));
+  sij.release();
+
+  // ---- 4. canonical contributions, keyed (row, col), stable radix sort
+  const int64_t nt = nlocal + A->nrecv;
+  if (nt >= INT32_MAX) return fail(SPMAT_ERR_ARG, "more than 2^31 contributions on one rank");
+  A->ncontrib = nt;
+  DevBuf<uint64_t> key, key2;
+  DevBuf<uint32_t> val, val2;
+  SP_TRY(key.alloc(nt));
+  SP_TRY(val.alloc(nt));
+  const int64_t before = A->recv_off[me];  // received from src < me
+  if (A->nrecv > 0) {
+    k_keys_recv<<<nblk(A->nrecv), 256, 0, st>>>(rij.get(), A->nrecv, before, nlocal, rstart, N,
+                                                (uint64_t)ncoo, key.get(), val.get());
+    SP_LAUNCH();
+  }
+  if (nlocal > 0) {
+    k_keys_local<<<nblk(nlocal), 256, 0, st>>>(ci, cj, kk.get() + dofs[me], nlocal, before,
+                                               rstart, N, key.get(), val.get());
+    SP_LAUNCH();
+  }
+  rij.release();
+  kk.release();
+  di.release();
+  dj.release();
+  if (nt > 0) {
+    SP_TRY(key2.alloc(nt));
+    SP_TRY(val2.alloc(nt));
+    cub::DoubleBuffer<uint64_t> dk(key.get(), key2.get());
+    cub::DoubleBuffer<uint32_t> dv(val.get(), val2.get());
+    uint64_t maxkey = (uint64_t)std::max<int64_t>(m_local, 1) * (uint64_t)std::max<int64_t>(N, 1) - 1;
+    CUB_CALL(tmp, st, cub::DeviceRadixSort::SortPairs(d_temp_storage, temp_storage_bytes, dk, dv,
+                                                      (int)nt, 0, bits_for(maxkey), st));
+    if (dk.Current() != key.get()) std::swap(key.p, key2.p);
+    if (dv.Current() != val.get()) std::swap(val.p, val2.p);
+    key2.release();
+    val2.release();
+  }
+
+  // ---- 5. nonzeros
+  DevBuf<uint32_t> head, zid, segstart;
+  SP_TRY(head.alloc(nt));
+  SP_TRY(zid.alloc(nt));
+  SP_TRY(segstart.alloc(nt));
+  int64_t nnz = 0;
+  if (nt > 0) {
+    k_heads<<<nblk(nt), 256, 0, st>>>(key.get(), nt, head.get());
+    SP_LAUNCH();
+    CUB_CALL(tmp, st, cub::DeviceScan::InclusiveSum(d_temp_storage, temp_storage_bytes, head.get(),
+                                                    zid.get(), (int)nt, st));
+    DevBuf<int> dn;
+    SP_TRY(dn.alloc(1));
+    CUB_CALL(tmp, st, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes,
+                                                 cub::CountingInputIterator<uint32_t>(0), head.get(),
+                                                 segstart.get(), dn.get(), (int)nt, st));
+    int hn = 0;
+    SP_CUDA(cudaMemcpyAsync(&hn, dn.get(), 4, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    nnz = hn;
+  }
+  head.release();
+  DevBuf<uint32_t> isdiag, pos_d;
+  DevBuf<int32_t> cnt_d, cnt_o;
+  SP_TRY(isdiag.alloc(nnz));
+  SP_TRY(pos_d.alloc(nnz));
+  SP_TRY(cnt_d.alloc(m_local + 1));
+  SP_TRY(cnt_o.alloc(m_local + 1));
+  SP_CUDA(cudaMemsetAsync(cnt_d.get(), 0, (m_local + 1) * 4, st));
+  SP_CUDA(cudaMemsetAsync(cnt_o.get(), 0, (m_local + 1) * 4, st));
+  int64_t nnz_d = 0;
+  if (nnz > 0) {
+    k_nz_classify<<<nblk(nnz), 256, 0, st>>>(key.get(), segstart.get(), nnz, N, cstart, cend,
+                                             isdiag.get(), cnt_d.get(), cnt_o.get());
+    SP_LAUNCH();
+    CUB_CALL(tmp, st, cub::DeviceScan::ExclusiveSum(d_temp_storage, temp_storage_bytes,
+                                                    isdiag.get(), pos_d.get(), (int)nnz, st));
+    uint32_t last[2];
+    SP_CUDA(cudaMemcpyAsync(&last[0], pos_d.get() + nnz - 1, 4, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaMemcpyAsync(&last[1], isdiag.get() + nnz - 1, 4, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    nnz_d = (int64_t)last[0] + last[1];
+  }
+  const int64_t nnz_o = nnz - nnz_d;
+  A->nnz_d = nnz_d;
+  A->nnz_o = nnz_o;
+  // diag CSR
+  SP_TRY(A->rowptr_d.alloc(m_local + 1));
+  CUB_CALL(tmp, st, cub::DeviceScan::ExclusiveSum(d_temp_storage, temp_storage_bytes, cnt_d.get(),
+                                                  A->rowptr_d.get(), (int)(m_local + 1), st));
+  SP_TRY(A->col_d.alloc(nnz_d));
+  SP_TRY(A->val_d.alloc(nnz_d));
+  DevBuf<int64_t> ocol;
+  SP_TRY(ocol.alloc(nnz_o));
+  if (nnz > 0) {
+    k_nz_cols<<<nblk(nnz), 256, 0, st>>>(key.get(), segstart.get(), isdiag.get(), pos_d.get(), nnz,
+                                         N, cstart, A->col_d.get(), ocol.get());
+    SP_LAUNCH();
+  }
+  key.release();
+  // colmap = sorted unique ghost columns
+  if (nnz_o > 0) {
+    DevBuf<int64_t> sorted;
+    SP_TRY(sorted.alloc(nnz_o));
+    CUB_CALL(tmp, st, cub::DeviceRadixSort::SortKeys(d_temp_storage, temp_storage_bytes,
+                                                     (const uint64_t *)ocol.get(),
+                                                     (uint64_t *)sorted.get(), (int)nnz_o, 0,
+                                                     bits_for((uint64_t)N), st));
+    DevBuf<int64_t> uniq;
+    SP_TRY(uniq.alloc(nnz_o));
+    DevBuf<int> dn;
+    SP_TRY(dn.alloc(1));
+    CUB_CALL(tmp, st, cub::DeviceSelect::Unique(d_temp_storage, temp_storage_bytes, sorted.get(),
+                                                uniq.get(), dn.get(), (int)nnz_o, st));
+    int ng = 0;
+    SP_CUDA(cudaMemcpyAsync(&ng, dn.get(), 4, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    A->n_ghost = ng;
+    SP_TRY(A->colmap.alloc(ng));
+    SP_CUDA(cudaMemcpyAsync(A->colmap.get(), uniq.get(), (size_t)ng * 8, cudaMemcpyDeviceToDevice, st));
+    SP_TRY(A->col_o.alloc(nnz_o));
+    k_ghost_index<<<nblk(nnz_o), 256, 0, st>>>(ocol.get(), nnz_o, A->colmap.get(), ng, A->col_o.get());
+    SP_LAUNCH();
+  }
+  ocol.release();
+  // compressed offdiag rows
+  {
+    DevBuf<uint32_t> ne;
+    SP_TRY(ne.alloc(m_local));
+    DevBuf<int32_t> rows;
+    SP_TRY(rows.alloc(m_local));
+    DevBuf<int> dn;
+    SP_TRY(dn.alloc(1));
+    int nro = 0;
+    if (m_local > 0 && nnz_o > 0) {
+      k_nonempty<<<nblk(m_local), 256, 0, st>>>(cnt_o.get(), m_local, ne.get());
+      SP_LAUNCH();
+      CUB_CALL(tmp, st, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes,
+                                                   cub::CountingInputIterator<int32_t>(0), ne.get(),
+                                                   rows.get(), dn.get(), (int)m_local, st));
+      SP_CUDA(cudaMemcpyAsync(&nro, dn.get(), 4, cudaMemcpyDeviceToHost, st));
+      SP_CUDA(cudaStreamSynchronize(st));
+    }
+    A->n_ro = nro;
+    SP_TRY(A->rows_o.alloc(nro));
+    SP_TRY(A->rowptr_o.alloc(nro + 1));
+    if (nro > 0) {
+      SP_CUDA(cudaMemcpyAsync(A->rows_o.get(), rows.get(), (size_t)nro * 4, cudaMemcpyDeviceToDevice, st));
+      DevBuf<int32_t> cc;
+      SP_TRY(cc.alloc(nro + 1));
+      SP_CUDA(cudaMemsetAsync(cc.get() + nro, 0, 4, st));
+      k_gather_i32<<<nblk(nro), 256, 0, st>>>(cnt_o.get(), A->rows_o.get(), nro, cc.get());
+      SP_LAUNCH();
+      CUB_CALL(tmp, st, cub::DeviceScan::ExclusiveSum(d_temp_storage, temp_storage_bytes, cc.get(),
+                                                      A->rowptr_o.get(), nro + 1, st));
+    }
+    SP_TRY(A->val_o.alloc(nnz_o));
+  }
+  // ---- jmap / perm in block order (diag nonzeros, then offdiag nonzeros)
+  SP_TRY(A->jmap.alloc(nnz + 1));
+  SP_TRY(A->perm.alloc(nt));
+  if (nt > 0) {
+    // zid holds inclusive sums of the run heads (1-based nonzero ids)
+    DevBuf<uint32_t> cflag, cpos;
+    SP_TRY(cflag.alloc(nt));
+    SP_TRY(cpos.alloc(nt));
+    k_cflag<<<nblk(nt), 256, 0, st>>>(zid.get(), isdiag.get(), nt, cflag.get());
+    SP_LAUNCH();
+    CUB_CALL(tmp, st, cub::DeviceScan::ExclusiveSum(d_temp_storage, temp_storage_bytes, cflag.get(),
+                                                    cpos.get(), (int)nt, st));
+    uint32_t last[2];
+    SP_CUDA(cudaMemcpyAsync(&last[0], cpos.get() + nt - 1, 4, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaMemcpyAsync(&last[1], cflag.get() + nt - 1, 4, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    int64_t total_d = (int64_t)last[0] + last[1];
+    k_perm<<<nblk(nt), 256, 0, st>>>(val.get(), cflag.get(), cpos.get(), nt, total_d, A->perm.get());
+    SP_LAUNCH();
+    k_jmap<<<nblk(nnz), 256, 0, st>>>(segstart.get(), isdiag.get(), pos_d.get(), cpos.get(), nnz,
+                                      nnz_d, total_d, nt, A->jmap.get());
+    SP_LAUNCH();
+  } else {
+    SP_CUDA(cudaMemsetAsync(A->jmap.get(), 0, 4, st));
+  }
+  val.release();
+  zid.release();
+  segstart.release();
+  isdiag.release();
+  pos_d.release();
+  // ---- mixed nonzeros (with received contributions)
+  if (A->nrecv > 0 && nnz > 0) {
+    DevBuf<uint32_t> flag, ids;
+    SP_TRY(flag.alloc(nnz));
+    SP_TRY(ids.alloc(nnz));
+    k_mixed_flag<<<nblk(nnz), 256, 0, st>>>(A->jmap.get(), A->perm.get(), nnz, (uint64_t)ncoo, flag.get());
+    SP_LAUNCH();
+    DevBuf<int> dn;
+    SP_TRY(dn.alloc(1));
+    CUB_CALL(tmp, st, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes,
+                                                 cub::CountingInputIterator<uint32_t>(0), flag.get(),
+                                                 ids.get(), dn.get(), (int)nnz, st));
+    int nm = 0;
+    SP_CUDA(cudaMemcpyAsync(&nm, dn.get(), 4, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    A->n_mixed = nm;
+    SP_TRY(A->mixed.alloc(nm));
+    if (nm) SP_CUDA(cudaMemcpyAsync(A->mixed.get(), ids.get(), (size_t)nm * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  SP_TRY(A->sendbuf.alloc(A->nsend));
+  SP_TRY(A->recvbuf.alloc(A->nrecv));
+  SP_TRY(A->lvec.alloc(A->n_ghost));
+  SP_CUDA(cudaEventCreateWithFlags(&A->ev_send_ready, cudaEventDisableTiming));
+  SP_CUDA(cudaEventCreateWithFlags(&A->ev_recv_done, cudaEventDisableTiming));
+
+  // ---- 6. halo SF from colmap: leaf g -> (owner(colmap[g]), colmap[g] - cstart_owner)
+  {
+    std::vector<int64_t> cm(A->n_ghost), off(A->n_ghost);
+    std::vector<int32_t> own(A->n_ghost);
+    if (A->n_ghost)
+      SP_CUDA(cudaMemcpyAsync(cm.data(), A->colmap.get(), A->n_ghost * 8, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    for (int64_t g = 0; g < A->n_ghost; ++g) {
+      int q = (int)(std::upper_bound(coff.begin(), coff.end(), cm[g]) - coff.begin()) - 1;
+      own[g] = q;
+      off[g] = cm[g] - coff[q];
+    }
+    SP_TRY(sf_build(c, n_local, A->n_ghost, nullptr, own.data(), off.data(), &A->halo));
+  }
+  SP_TRY(spmv_prepare(A, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  A->plan_builds = 1;
+  *out = guard.release();
+  return SPMAT_OK;
+}
+
+}  // namespace spmat
+
+using namespace spmat;
+
+extern "C" {
+
+int spmat_create_coo(spmat_comm_t comm, int64_t m_local, int64_t n_local, int64_t M, int64_t N,
+                     int64_t ncoo, const int64_t *coo_i, const int64_t *coo_j, spmat_t *out) {
+  if (!comm || !out) return fail(SPMAT_ERR_ARG, "spmat_create_coo: null argument");
+  *out = nullptr;
+  if (ncoo < 0) return fail(SPMAT_ERR_ARG, "spmat_create_coo: negative ncoo");
+  DeviceGuard g(comm->device);
+  return create_impl(comm, m_local, n_local, M, N, ncoo, coo_i, coo_j, out);
+}
+
+int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
+  if (!A) return fail(SPMAT_ERR_ARG, "spmat_set_values_coo: null matrix");
+  if (mode != SPMAT_INSERT && mode != SPMAT_ADD)
+    return fail(SPMAT_ERR_ARG, "spmat_set_values_coo: bad mode %d", mode);
+  if (A->ncoo > 0 && !v) return fail(SPMAT_ERR_ARG, "spmat_set_values_coo: null v");
+  if (mode == SPMAT_ADD && !A->values_set)
+    return fail(SPMAT_ERR_STATE, "spmat_set_values_coo: ADD before any INSERT");
+  spmat_comm_s *c = A->comm;
+  DeviceGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nnz = A->nnz_d + A->nnz_o;
+  const bool exchange = c->nranks > 1;
+  if (exchange) {
+    if (A->nsend > 0) {
+      k_send_gather<<<nblk(A->nsend), 256, 0, s>>>(v, A->sendperm.get(), A->nsend, A->sendbuf.get());
+      SP_LAUNCH();
+    }
+    SP_CUDA(cudaEventRecord(A->ev_send_ready, s));
+    SP_CUDA(cudaStreamWaitEvent(c->comm_stream, A->ev_send_ready, 0));
+    SP_TRY(c->exchange_dev(A->sendbuf.get(), A->send_off.data(), A->send_count.data(),
+                           A->recvbuf.get(), A->recv_off.data(), A->recv_count.data(),
+                           sizeof(double), c->comm_stream));
+    SP_CUDA(cudaEventRecord(A->ev_recv_done, c->comm_stream));
+  }
+  if (nnz > 0) {
+    k_numeric_local<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
+                                              A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
+    SP_LAUNCH();
+  }
+  if (exchange) {
+    SP_CUDA(cudaStreamWaitEvent(s, A->ev_recv_done, 0));
+    if (A->n_mixed > 0) {
+      k_numeric_mixed<<<nblk(A->n_mixed), 256, 0, s>>>(A->mixed.get(), A->n_mixed, A->jmap.get(),
+                                                      A->perm.get(), v, A->recvbuf.get(),
+                                                      (uint64_t)A->ncoo, A->nnz_d, A->val_d.get(),
+                                                      A->val_o.get(), mode);
+      SP_LAUNCH();
+    }
+  }
+  A->values_set = true;
+  return SPMAT_OK;
+}
+
+int spmat_get_info(spmat_t A, int64_t info[16]) {
+  if (!A || !info) return fail(SPMAT_ERR_ARG, "spmat_get_info: null argument");
+  int64_t v[16] = {A->rstart, A->rend, A->cstart, A->cend, A->nnz_d, A->nnz_o, A->n_ghost,
+                   A->n_ro, A->ncontrib, A->nsend, A->nrecv, A->n_mixed, A->kernel_id,
+                   A->n_rowblocks, A->max_row_nnz, A->plan_builds};
+  memcpy(info, v, sizeof v);
+  return SPMAT_OK;
+}
+
+int spmat_get_halo_sf(spmat_t A, sf_t *borrowed) {
+  if (!A || !borrowed) return fail(SPMAT_ERR_ARG, "spmat_get_halo_sf: null argument");
+  *borrowed = A->halo;
+  return SPMAT_OK;
+}
+
+int spmat_export(spmat_t A, int what, void *host_buf, int64_t cap, int64_t *len) {
+  if (!A || !len) return fail(SPMAT_ERR_ARG, "spmat_export: null argument");
+  DeviceGuard g(A->comm->device);
+  SP_CUDA(cudaDeviceSynchronize());
+  const int P = A->comm->nranks;
+  std::vector<int64_t> out;
+  std::vector<double> outd;
+  bool is_double = false;
+  auto pull32 = [&](const int32_t *d, int64_t n) -> int {
+    std::vector<int32_t> h(n);
+    if (n) SP_CUDA(cudaMemcpy(h.data(), d, n * 4, cudaMemcpyDeviceToHost));
+    out.assign(h.begin(), h.end());
+    return SPMAT_OK;
+  };
+  auto pullu32 = [&](const uint32_t *d, int64_t n) -> int {
+    std::vector<uint32_t> h(n);
+    if (n) SP_CUDA(cudaMemcpy(h.data(), d, n * 4, cudaMemcpyDeviceToHost));
+    out.assign(h.begin(), h.end());
+    return SPMAT_OK;
+  };
+  auto pulld = [&](const double *d, int64_t n) -> int {
+    outd.resize(n);
+    if (n) SP_CUDA(cudaMemcpy(outd.data(), d, n * 8, cudaMemcpyDeviceToHost));
+    is_double = true;
+    return SPMAT_OK;
+  };
+  switch (what) {
+    case 0: SP_TRY(pull32(A->rowptr_d.get(), A->m + 1)); break;
+    case 1: SP_TRY(pull32(A->col_d.get(), A->nnz_d)); break;
+    case 2: SP_TRY(pulld(A->val_d.get(), A->nnz_d)); break;
+    case 3: {  // full-length offdiag row pointer from the compressed form
+      std::vector<int64_t> rows, rp;
+      SP_TRY(pull32(A->rows_o.get(), A->n_ro));
+      rows = out;
+      if (A->n_ro) {
+        SP_TRY(pull32(A->rowptr_o.get(), A->n_ro + 1));
+        rp = out;
+      } else {
+        rp.assign(1, 0);
+      }
+      out.assign(A->m + 1, 0);
+      for (int64_t q = 0; q < A->n_ro; ++q) out[rows[q] + 1] = rp[q + 1] - rp[q];
+      for (int64_t r = 0; r < A->m; ++r) out[r + 1] += out[r];
+      break;
+    }
+    case 4: SP_TRY(pull32(A->col_o.get(), A->nnz_o)); break;
+    case 5: SP_TRY(pulld(A->val_o.get(), A->nnz_o)); break;
+    case 6:
+      out.resize(A->n_ghost);
+      if (A->n_ghost) SP_CUDA(cudaMemcpy(out.data(), A->colmap.get(), A->n_ghost * 8, cudaMemcpyDeviceToHost));
+      break;
+    case 7: SP_TRY(pullu32(A->jmap.get(), A->nnz_d + A->nnz_o + 1)); break;
+    case 8:
+    case 9: {
+      SP_TRY(pullu32(A->perm.get(), A->ncontrib));
+      std::vector<int64_t> perm = out;
+      out.resize(perm.size());
+      for (size_t t = 0; t < perm.size(); ++t) {
+        int64_t p = perm[t];
+        if (p < A->ncoo) {
+          out[t] = what == 8 ? A->comm->rank : p;
+        } else {
+          int64_t q = p - A->ncoo;
+          int s = (int)(std::upper_bound(A->recv_off.begin(), A->recv_off.end(), q) - A->recv_off.begin()) - 1;
+          out[t] = what == 8 ? s : q - A->recv_off[s];
+        }
+      }
+      break;
+    }
+    case 10: out = A->send_count; break;
+    case 11: SP_TRY(pullu32(A->sendperm.get(), A->nsend)); break;
+    case 12: out = A->recv_count; break;
+    case 13: SP_TRY(pull32(A->rows_o.get(), A->n_ro)); break;
+    default: return fail(SPMAT_ERR_ARG, "spmat_export: unknown what=%d", what);
+  }
+  (void)P;
+  if (is_double) {
+    *len = (int64_t)outd.size();
+    if (host_buf && cap > 0) memcpy(host_buf, outd.data(), 8 * std::min<int64_t>(cap, *len));
+  } else {
+    *len = (int64_t)out.size();
+    if (host_buf && cap > 0) memcpy(host_buf, out.data(), 8 * std::min<int64_t>(cap, *len));
+  }
+  return SPMAT_OK;
+}
+
+int spmat_destroy(spmat_t A) {
+  if (!A) return SPMAT_OK;
+  {
+    DeviceGuard g(A->comm->device);
+    cudaDeviceSynchronize();
+    if (A->halo) sf_free(A->halo);
+    if (A->ev_send_ready) cudaEventDestroy(A->ev_send_ready);
+    if (A->ev_recv_done) cudaEventDestroy(A->ev_recv_done);
+    for (auto &v : A->prof_ev)
+      for (cudaEvent_t e : v) cudaEventDestroy(e);
+    // DevBuf members free themselves in ~spmat_s (device still selected here)
+    A->rowptr_d.release(); A->col_d.release(); A->val_d.release();
+    A->rows_o.release(); A->rowptr_o.release(); A->col_o.release(); A->val_o.release();
+    A->colmap.release(); A->lvec.release(); A->jmap.release(); A->perm.release();
+    A->mixed.release(); A->sendperm.release(); A->sendbuf.release(); A->recvbuf.release();
+    A->rowblocks.release(); A->xstage.release(); A->ystage.release();
+  }
+  delete A;
+  return SPMAT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,223 @@
+// internal.h -- shared internals of libspmat (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "nccl.h"
+#include "spmat.h"
+
+namespace spmat {
+
+// ------------------------------------------------------------------ errors
+void set_error(const char *fmt, ...);
+int fail(int status, const char *fmt, ...);
+
+#define SP_CUDA(expr)                                                                    \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return ::spmat::fail(_e == cudaErrorMemoryAllocation ? SPMAT_ERR_OOM : SPMAT_ERR_CUDA, \
+                           "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+#define SP_TRY(expr)                    \
+  do {                                  \
+    int _s = (expr);                    \
+    if (_s != SPMAT_OK) return _s;      \
+  } while (0)
+
+#define SP_LAUNCH()  SP_CUDA(cudaGetLastError())
+
+// ------------------------------------------------------------------ NCCL (dlopen'ed)
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *);
+  const char *(*GetErrorString)(ncclResult_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t,
+                            ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t);
+};
+int nccl_api(NcclApi **out);
+
+#define SP_NCCL(api, expr)                                                               \
+  do {                                                                                   \
+    ncclResult_t _r = (expr);                                                            \
+    if (_r != ncclSuccess)                                                               \
+      return ::spmat::fail(SPMAT_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #expr,    \
+                           (api)->GetErrorString(_r));                                   \
+  } while (0)
+
+// ------------------------------------------------------------------ device guard
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+// ------------------------------------------------------------------ device buffers
+template <typename T>
+struct DevBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  int alloc(size_t count) {
+    release();
+    n = count;
+    if (count == 0) return SPMAT_OK;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      return fail(SPMAT_ERR_OOM, "cudaMalloc(%zu bytes): %s", count * sizeof(T),
+                  cudaGetErrorString(e));
+    }
+    return SPMAT_OK;
+  }
+  T *get() const { return p; }
+};
+
+// is `p` a device (or managed) pointer?
+bool is_device_ptr(const void *p);
+
+// ------------------------------------------------------------------ communicator
+struct Comm {
+  int nranks = 1, rank = 0, device = 0;
+  ncclComm_t nccl = nullptr;
+  NcclApi *api = nullptr;
+  cudaStream_t comm_stream = nullptr;   // high priority, non-blocking
+  cudaStream_t setup_stream = nullptr;  // used by collective setup calls
+  int num_sms = 148;
+
+  // Collectives used by setup (host-synchronising).  All operate on host arrays.
+  int allgather_i64(const int64_t *send, int64_t count, int64_t *recv_host);  // recv: count*P
+  int allreduce_max_i64(int64_t *v, int64_t count);
+  // Exchange variable-size int64 payloads (host-side counts known on both sides):
+  // send[d] of scount[d] elements to d, recv from s of rcount[s] elements; device buffers.
+  int exchange_dev(const void *d_send, const int64_t *soff, const int64_t *scount,
+                   void *d_recv, const int64_t *roff, const int64_t *rcount,
+                   size_t elem_bytes, cudaStream_t stream);
+};
+
+}  // namespace spmat
+
+struct spmat_comm_s : spmat::Comm {};
+
+// ------------------------------------------------------------------ star forest
+struct sf_s {
+  spmat_comm_s *comm = nullptr;
+  int64_t nroots = 0, nleaves = 0;
+  // receive side (leaves), neighbours ascending, excluding self
+  std::vector<int> rnbr;
+  std::vector<int64_t> rcount, roff;     // per neighbour, offsets into recv order
+  std::vector<int64_t> leaf_start;       // leaf index of first leaf if contiguous, else -1
+  spmat::DevBuf<int64_t> d_leaf_idx;     // leaf indices in recv order (all neighbours)
+  int64_t nrecv = 0;
+  // send side (roots), requesters ascending, excluding self
+  std::vector<int> snbr;
+  std::vector<int64_t> scount, soff;
+  std::vector<int64_t> root_start;       // first root offset if contiguous, else -1
+  spmat::DevBuf<int64_t> d_root_idx;     // root offsets in send order
+  int64_t nsend = 0;
+  // self edges (leaf and root on this rank)
+  spmat::DevBuf<int64_t> d_self_leaf, d_self_root;
+  int64_t nself = 0;
+  // buffers
+  spmat::DevBuf<double> d_sendbuf, d_recvbuf;
+  bool need_pack = false, need_unpack_any = false;
+  // host copies for export
+  std::vector<int64_t> h_leaf_idx, h_root_idx;
+  // split-phase state
+  cudaEvent_t ev_begin = nullptr, ev_done = nullptr;
+  cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;  // profiling (comm stream)
+  bool pending = false;
+  const double *p_root = nullptr;
+  double *p_leaf = nullptr;
+  int p_op = -1;
+};
+
+namespace spmat {
+// build an SF from host leaf arrays (ilocal may be null); collective
+int sf_build(spmat_comm_s *comm, int64_t nroots, int64_t nleaves, const int64_t *h_ilocal,
+             const int32_t *h_rank, const int64_t *h_offset, sf_s **out);
+int sf_begin(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stream,
+             cudaEvent_t *prof /* optional pair recorded on the comm stream */);
+int sf_end(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stream);
+void sf_free(sf_s *sf);
+}  // namespace spmat
+
+// ------------------------------------------------------------------ matrix
+struct spmat_s {
+  spmat_comm_s *comm = nullptr;
+  int64_t M = 0, N = 0, m = 0, n = 0;
+  int64_t rstart = 0, rend = 0, cstart = 0, cend = 0;
+  std::vector<int64_t> roff, coff;  // P+1 ownership offsets
+  // diagonal block CSR (int32 local)
+  int64_t nnz_d = 0;
+  spmat::DevBuf<int32_t> rowptr_d, col_d;
+  spmat::DevBuf<double> val_d;
+  // off-diagonal block: compressed rows
+  int64_t nnz_o = 0, n_ro = 0;
+  spmat::DevBuf<int32_t> rows_o, rowptr_o, col_o;
+  spmat::DevBuf<double> val_o;
+  int64_t n_ghost = 0;
+  spmat::DevBuf<int64_t> colmap;
+  spmat::DevBuf<double> lvec;
+  sf_s *halo = nullptr;
+  // COO plan: nonzeros in block order (diag then offdiag)
+  int64_t ncoo = 0, ncontrib = 0;
+  spmat::DevBuf<uint32_t> jmap;     // nnz_d + nnz_o + 1
+  spmat::DevBuf<uint32_t> perm;     // ncontrib: k (< ncoo) or ncoo + recv position
+  int64_t n_mixed = 0;
+  spmat::DevBuf<uint32_t> mixed;    // nonzero ids (block order) with received contributions
+  // COO value exchange plan
+  std::vector<int64_t> send_count, recv_count, send_off, recv_off;  // per rank
+  int64_t nsend = 0, nrecv = 0;
+  spmat::DevBuf<uint32_t> sendperm;  // k's, destination-major
+  spmat::DevBuf<double> sendbuf, recvbuf;
+  cudaEvent_t ev_send_ready = nullptr, ev_recv_done = nullptr;
+  bool values_set = false;
+  // SpMV schedule
+  int kernel_id = 0;
+  int64_t n_rowblocks = 0, max_row_nnz = 0;
+  spmat::DevBuf<int32_t> rowblocks;  // n_rowblocks + 1 row boundaries
+  // host staging for host x / y
+  spmat::DevBuf<double> xstage, ystage;
+  // profiling
+  bool profile = false;
+  std::vector<cudaEvent_t> prof_ev[3];  // pairs per kind
+  size_t prof_n[3] = {0, 0, 0};
+  int64_t plan_builds = 0;
+};
+
+namespace spmat {
+int spmv_prepare(spmat_s *A, cudaStream_t stream);  // row blocks + kernel choice
+int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream);
+int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
+}  // namespace spmat

@@ -1,0 +1,397 @@
+// sf.cu -- star-forest (PetscSF) plan and split-phase broadcast over NCCL.
+//
+// P:446-482.  "Leaves are locally indexed with integers, while roots are globally indexed
+// via tuples of (owner rank, offset).  A PetscSF is created collectively by specifying, for
+// each leaf on the current process, the owner rank and an offset of the corresponding root
+// on the owner.  PETSc analyzes the graph and derives the communication pattern."
+// Bcast moves root values to leaves with REPLACE or SUM; when roots or leaves are not
+// consecutive "PETSc will call its pack or unpack kernels".  With REPLACE and
+// consecutive indices the user buffers are the transport buffers directly.
+//
+// B200 design: the plan (grouping, contiguity detection) is built on the host once; each
+// Bcast is fully stream-ordered on the library's high-priority comm stream: pack kernel
+// (only for non-consecutive roots) -> grouped ncclSend/ncclRecv -> self-edge copy kernel ->
+// unpack kernel (only for non-consecutive leaves or SUM).  No host synchronisation.
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "internal.h"
+
+namespace spmat {
+
+__global__ void k_gather(const double *__restrict__ src, const int64_t *__restrict__ idx,
+                         double *__restrict__ dst, int64_t n) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; t < n; t += stride) dst[t] = src[idx[t]];
+}
+
+// leaf[lidx[t]] = src[sidx ? sidx[t] : t]  (REPLACE)  or  += (SUM)
+__global__ void k_scatter(const double *__restrict__ src, const int64_t *__restrict__ sidx,
+                          double *__restrict__ leaf, const int64_t *__restrict__ lidx, int64_t n,
+                          int op) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; t < n; t += stride) {
+    double v = src[sidx ? sidx[t] : t];
+    int64_t l = lidx[t];
+    leaf[l] = op == SF_REPLACE ? v : leaf[l] + v;
+  }
+}
+
+static inline unsigned grid_for(int64_t n, int threads, int sms) {
+  int64_t b = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)sms * 8;
+  return (unsigned)std::max<int64_t>(1, std::min(b, cap));
+}
+
+void sf_free(sf_s *sf) {
+  if (!sf) return;
+  if (sf->ev_begin) cudaEventDestroy(sf->ev_begin);
+  if (sf->ev_done) cudaEventDestroy(sf->ev_done);
+  delete sf;
+}
+
+int sf_build(spmat_comm_s *comm, int64_t nroots, int64_t nleaves, const int64_t *h_ilocal,
+             const int32_t *h_rank, const int64_t *h_offset, sf_s **out) {
+  *out = nullptr;
+  const int P = comm->nranks, me = comm->rank;
+  // ---- local validation, agreed collectively so that no rank is left in a collective
+  int64_t st[2] = {SPMAT_OK, 0};
+  std::string msg;
+  if (nroots < 0 || nleaves < 0) {
+    st[0] = SPMAT_ERR_ARG;
+    msg = "negative nroots/nleaves";
+  }
+  for (int64_t l = 0; l < nleaves && st[0] == SPMAT_OK; ++l) {
+    if (h_rank[l] < 0 || h_rank[l] >= P) {
+      st[0] = SPMAT_ERR_ARG;
+      char b[128];
+      snprintf(b, sizeof b, "leaf %lld: remote rank %d outside [0,%d)", (long long)l,
+               h_rank[l], P);
+      msg = b;
+    } else if (h_offset[l] < 0) {
+      st[0] = SPMAT_ERR_RANGE;
+      char b[128];
+      snprintf(b, sizeof b, "leaf %lld: negative root offset", (long long)l);
+      msg = b;
+    } else if (h_ilocal && h_ilocal[l] < 0) {
+      st[0] = SPMAT_ERR_ARG;
+      msg = "negative ilocal";
+    }
+  }
+  if (st[0] == SPMAT_OK && h_ilocal) {
+    std::vector<int64_t> s(h_ilocal, h_ilocal + nleaves);
+    std::sort(s.begin(), s.end());
+    if (std::adjacent_find(s.begin(), s.end()) != s.end()) {
+      st[0] = SPMAT_ERR_ARG;
+      msg = "duplicate ilocal entries";
+    }
+  }
+  SP_TRY(comm->allreduce_max_i64(st, 1));
+  if (st[0] != SPMAT_OK)
+    return fail((int)st[0], "sf_create: %s", msg.empty() ? "error on another rank" : msg.c_str());
+
+  // ---- order leaves by (owner rank, root offset, leaf index)
+  auto leaf_of = [&](int64_t l) { return h_ilocal ? h_ilocal[l] : l; };
+  std::vector<int64_t> ord(nleaves);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+    if (h_rank[a] != h_rank[b]) return h_rank[a] < h_rank[b];
+    if (h_offset[a] != h_offset[b]) return h_offset[a] < h_offset[b];
+    return leaf_of(a) < leaf_of(b);
+  });
+  sf_s *sf = new sf_s();
+  sf->comm = comm;
+  sf->nroots = nroots;
+  sf->nleaves = nleaves;
+  std::vector<int64_t> cnt(P, 0);
+  for (int64_t l = 0; l < nleaves; ++l) cnt[h_rank[l]]++;
+  std::vector<int64_t> self_leaf, self_root, req_off;  // req_off: offsets requested, by owner
+  std::vector<int64_t> req_start(P + 1, 0);
+  for (int q = 0; q < P; ++q) req_start[q + 1] = req_start[q] + (q == me ? 0 : cnt[q]);
+  req_off.resize(req_start[P]);
+  sf->h_leaf_idx.resize(req_start[P]);
+  {
+    std::vector<int64_t> fill(P, 0);
+    for (int64_t t = 0; t < nleaves; ++t) {
+      int64_t l = ord[t];
+      int q = h_rank[l];
+      if (q == me) {
+        self_leaf.push_back(leaf_of(l));
+        self_root.push_back(h_offset[l]);
+      } else {
+        int64_t at = req_start[q] + fill[q]++;
+        req_off[at] = h_offset[l];
+        sf->h_leaf_idx[at] = leaf_of(l);
+      }
+    }
+  }
+  for (int q = 0; q < P; ++q) {
+    if (q == me || cnt[q] == 0) continue;
+    sf->rnbr.push_back(q);
+    sf->rcount.push_back(cnt[q]);
+    sf->roff.push_back(req_start[q]);
+    bool contig = true;
+    for (int64_t t = 1; t < cnt[q] && contig; ++t)
+      contig = sf->h_leaf_idx[req_start[q] + t] == sf->h_leaf_idx[req_start[q]] + t;
+    sf->leaf_start.push_back(contig ? sf->h_leaf_idx[req_start[q]] : -1);
+    if (!contig) sf->need_unpack_any = true;
+  }
+  sf->nrecv = req_start[P];
+  sf->nself = (int64_t)self_leaf.size();
+  // self-edge offsets are validated locally
+  int64_t bad = -1;
+  for (size_t t = 0; t < self_root.size(); ++t)
+    if (self_root[t] >= nroots) bad = self_root[t];
+
+  // ---- exchange request counts and offsets
+  std::vector<int64_t> mine(P, 0), all((size_t)P * P, 0);
+  for (int q = 0; q < P; ++q) mine[q] = q == me ? 0 : cnt[q];
+  int s = comm->allgather_i64(mine.data(), P, all.data());
+  if (s != SPMAT_OK) {
+    sf_free(sf);
+    return s;
+  }
+  std::vector<int64_t> scount(P), sstart(P + 1, 0);
+  for (int p = 0; p < P; ++p) scount[p] = all[(size_t)p * P + me];
+  for (int p = 0; p < P; ++p) sstart[p + 1] = sstart[p] + scount[p];
+  sf->nsend = sstart[P];
+  sf->h_root_idx.resize(sf->nsend);
+  if (P > 1) {
+    DevBuf<int64_t> dreq, dgot;
+    std::vector<int64_t> rc(P);
+    for (int q = 0; q < P; ++q) rc[q] = req_start[q + 1] - req_start[q];
+    if ((s = dreq.alloc(req_off.size())) || (s = dgot.alloc(sf->nsend))) {
+      sf_free(sf);
+      return s;
+    }
+    cudaError_t e = cudaSuccess;
+    if (!req_off.empty())
+      e = cudaMemcpyAsync(dreq.get(), req_off.data(), req_off.size() * 8, cudaMemcpyHostToDevice,
+                          comm->setup_stream);
+    if (e == cudaSuccess) {
+      s = comm->exchange_dev(dreq.get(), req_start.data(), rc.data(), dgot.get(), sstart.data(),
+                             scount.data(), sizeof(int64_t), comm->setup_stream);
+      if (s != SPMAT_OK) {
+        sf_free(sf);
+        return s;
+      }
+      if (sf->nsend)
+        e = cudaMemcpyAsync(sf->h_root_idx.data(), dgot.get(), sf->nsend * 8,
+                            cudaMemcpyDeviceToHost, comm->setup_stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(comm->setup_stream);
+    }
+    if (e != cudaSuccess) {
+      sf_free(sf);
+      return fail(SPMAT_ERR_CUDA, "sf_create exchange: %s", cudaGetErrorString(e));
+    }
+  }
+  for (int64_t t = 0; t < sf->nsend; ++t)
+    if (sf->h_root_idx[t] >= nroots) bad = sf->h_root_idx[t];
+  int64_t st2[1] = {bad >= 0 ? (int64_t)SPMAT_ERR_RANGE : (int64_t)SPMAT_OK};
+  s = comm->allreduce_max_i64(st2, 1);
+  if (s != SPMAT_OK || st2[0] != SPMAT_OK) {
+    sf_free(sf);
+    if (s != SPMAT_OK) return s;
+    if (bad >= 0)
+      return fail(SPMAT_ERR_RANGE, "sf_create: root offset %lld >= nroots %lld on rank %d",
+                  (long long)bad, (long long)nroots, me);
+    return fail(SPMAT_ERR_RANGE, "sf_create: root offset out of range on another rank");
+  }
+  for (int p = 0; p < P; ++p) {
+    if (p == me || scount[p] == 0) continue;
+    sf->snbr.push_back(p);
+    sf->scount.push_back(scount[p]);
+    sf->soff.push_back(sstart[p]);
+    bool contig = true;
+    for (int64_t t = 1; t < scount[p] && contig; ++t)
+      contig = sf->h_root_idx[sstart[p] + t] == sf->h_root_idx[sstart[p]] + t;
+    sf->root_start.push_back(contig ? sf->h_root_idx[sstart[p]] : -1);
+    if (!contig) sf->need_pack = true;
+  }
+  // ---- device arrays
+  DeviceGuard g(comm->device);
+  auto up = [&](DevBuf<int64_t> &d, const std::vector<int64_t> &h) -> int {
+    int r = d.alloc(h.size());
+    if (r) return r;
+    if (!h.empty()) {
+      cudaError_t e = cudaMemcpy(d.get(), h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return fail(SPMAT_ERR_CUDA, "sf upload: %s", cudaGetErrorString(e));
+    }
+    return SPMAT_OK;
+  };
+  if ((s = up(sf->d_leaf_idx, sf->h_leaf_idx)) || (s = up(sf->d_root_idx, sf->h_root_idx)) ||
+      (s = up(sf->d_self_leaf, self_leaf)) || (s = up(sf->d_self_root, self_root)) ||
+      (s = sf->d_sendbuf.alloc(sf->need_pack ? sf->nsend : 0)) ||
+      (s = sf->d_recvbuf.alloc(sf->nrecv))) {
+    sf_free(sf);
+    return s;
+  }
+  if (cudaEventCreateWithFlags(&sf->ev_begin, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&sf->ev_done, cudaEventDisableTiming) != cudaSuccess) {
+    sf_free(sf);
+    return fail(SPMAT_ERR_CUDA, "sf_create: event creation failed");
+  }
+  *out = sf;
+  return SPMAT_OK;
+}
+
+int sf_begin(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stream,
+             cudaEvent_t *prof) {
+  if (sf->pending) return fail(SPMAT_ERR_STATE, "sf_bcast_begin: a bcast is already pending");
+  if (op != SF_REPLACE && op != SF_SUM) return fail(SPMAT_ERR_ARG, "sf_bcast: bad op %d", op);
+  spmat_comm_s *c = sf->comm;
+  cudaStream_t cs = c->comm_stream;
+  SP_CUDA(cudaEventRecord(sf->ev_begin, stream));
+  SP_CUDA(cudaStreamWaitEvent(cs, sf->ev_begin, 0));
+  if (prof) SP_CUDA(cudaEventRecord(prof[0], cs));
+  const int T = 256;
+  if (sf->need_pack && sf->nsend > 0) {
+    k_gather<<<grid_for(sf->nsend, T, c->num_sms), T, 0, cs>>>(root, sf->d_root_idx.get(),
+                                                              sf->d_sendbuf.get(), sf->nsend);
+    SP_LAUNCH();
+  }
+  if (c->nranks > 1 && (!sf->rnbr.empty() || !sf->snbr.empty())) {
+    NcclApi *api = c->api;
+    SP_NCCL(api, api->GroupStart());
+    for (size_t a = 0; a < sf->rnbr.size(); ++a) {
+      double *dst = (op == SF_REPLACE && sf->leaf_start[a] >= 0) ? leaf + sf->leaf_start[a]
+                                                                  : sf->d_recvbuf.get() + sf->roff[a];
+      SP_NCCL(api, api->Recv(dst, sf->rcount[a], ncclFloat64, sf->rnbr[a], c->nccl, cs));
+    }
+    for (size_t a = 0; a < sf->snbr.size(); ++a) {
+      const double *src = sf->root_start[a] >= 0 ? root + sf->root_start[a]
+                                                 : sf->d_sendbuf.get() + sf->soff[a];
+      SP_NCCL(api, api->Send(src, sf->scount[a], ncclFloat64, sf->snbr[a], c->nccl, cs));
+    }
+    SP_NCCL(api, api->GroupEnd());
+  }
+  if (sf->nself > 0) {
+    k_scatter<<<grid_for(sf->nself, T, c->num_sms), T, 0, cs>>>(
+        root, sf->d_self_root.get(), leaf, sf->d_self_leaf.get(), sf->nself, op);
+    SP_LAUNCH();
+  }
+  for (size_t a = 0; a < sf->rnbr.size(); ++a) {
+    bool in_place = op == SF_REPLACE && sf->leaf_start[a] >= 0;
+    if (in_place) continue;
+    k_scatter<<<grid_for(sf->rcount[a], T, c->num_sms), T, 0, cs>>>(
+        sf->d_recvbuf.get() + sf->roff[a], nullptr, leaf, sf->d_leaf_idx.get() + sf->roff[a],
+        sf->rcount[a], op);
+    SP_LAUNCH();
+  }
+  if (prof) SP_CUDA(cudaEventRecord(prof[1], cs));
+  SP_CUDA(cudaEventRecord(sf->ev_done, cs));
+  sf->pending = true;
+  sf->p_root = root;
+  sf->p_leaf = leaf;
+  sf->p_op = op;
+  return SPMAT_OK;
+}
+
+int sf_end(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stream) {
+  if (!sf->pending) return fail(SPMAT_ERR_STATE, "sf_bcast_end without sf_bcast_begin");
+  if (root != sf->p_root || leaf != sf->p_leaf || op != sf->p_op)
+    return fail(SPMAT_ERR_STATE, "sf_bcast_end: buffers or op differ from sf_bcast_begin");
+  SP_CUDA(cudaStreamWaitEvent(stream, sf->ev_done, 0));
+  sf->pending = false;
+  return SPMAT_OK;
+}
+
+}  // namespace spmat
+
+using namespace spmat;
+
+extern "C" {
+
+int sf_create(spmat_comm_t comm, int64_t nroots, int64_t nleaves, const int64_t *ilocal,
+              const int32_t *remote_rank, const int64_t *remote_offset, sf_t *out) {
+  if (!comm || !out) return fail(SPMAT_ERR_ARG, "sf_create: null argument");
+  *out = nullptr;
+  if (nleaves > 0 && (!remote_rank || !remote_offset))
+    return fail(SPMAT_ERR_ARG, "sf_create: null leaf arrays");
+  DeviceGuard g(comm->device);
+  // accept host or device leaf arrays (memtype detection)
+  std::vector<int64_t> il, ro;
+  std::vector<int32_t> rr;
+  const int64_t *pil = ilocal;
+  const int32_t *prr = remote_rank;
+  const int64_t *pro = remote_offset;
+  if (nleaves > 0) {
+    if (ilocal && is_device_ptr(ilocal)) {
+      il.resize(nleaves);
+      SP_CUDA(cudaMemcpy(il.data(), ilocal, nleaves * 8, cudaMemcpyDeviceToHost));
+      pil = il.data();
+    }
+    if (is_device_ptr(remote_rank)) {
+      rr.resize(nleaves);
+      SP_CUDA(cudaMemcpy(rr.data(), remote_rank, nleaves * 4, cudaMemcpyDeviceToHost));
+      prr = rr.data();
+    }
+    if (is_device_ptr(remote_offset)) {
+      ro.resize(nleaves);
+      SP_CUDA(cudaMemcpy(ro.data(), remote_offset, nleaves * 8, cudaMemcpyDeviceToHost));
+      pro = ro.data();
+    }
+  }
+  return sf_build(comm, nroots, nleaves, pil, prr, pro, out);
+}
+
+int sf_bcast_begin(sf_t sf, const double *rootdata, double *leafdata, int op, void *stream) {
+  if (!sf) return fail(SPMAT_ERR_ARG, "sf_bcast_begin: null sf");
+  if ((sf->nsend > 0 || sf->nself > 0) && !rootdata)
+    return fail(SPMAT_ERR_ARG, "sf_bcast_begin: null rootdata");
+  if ((sf->nrecv > 0 || sf->nself > 0) && !leafdata)
+    return fail(SPMAT_ERR_ARG, "sf_bcast_begin: null leafdata");
+  DeviceGuard g(sf->comm->device);
+  return sf_begin(sf, rootdata, leafdata, op, (cudaStream_t)stream, nullptr);
+}
+
+int sf_bcast_end(sf_t sf, const double *rootdata, double *leafdata, int op, void *stream) {
+  if (!sf) return fail(SPMAT_ERR_ARG, "sf_bcast_end: null sf");
+  DeviceGuard g(sf->comm->device);
+  return sf_end(sf, rootdata, leafdata, op, (cudaStream_t)stream);
+}
+
+int sf_get_info(sf_t sf, int64_t info[8]) {
+  if (!sf || !info) return fail(SPMAT_ERR_ARG, "sf_get_info: null argument");
+  info[0] = sf->nroots;
+  info[1] = sf->nleaves;
+  info[2] = (int64_t)sf->snbr.size();
+  info[3] = (int64_t)sf->rnbr.size();
+  info[4] = sf->nsend;
+  info[5] = sf->nrecv;
+  info[6] = sf->nself;
+  info[7] = (sf->need_pack || sf->need_unpack_any) ? 1 : 0;
+  return SPMAT_OK;
+}
+
+int sf_export(sf_t sf, int what, void *host_buf, int64_t cap, int64_t *len) {
+  if (!sf || !len) return fail(SPMAT_ERR_ARG, "sf_export: null argument");
+  std::vector<int64_t> v;
+  switch (what) {
+    case 0: v.assign(sf->rnbr.begin(), sf->rnbr.end()); break;
+    case 1: v = sf->rcount; break;
+    case 2: v = sf->h_leaf_idx; break;
+    case 3: v.assign(sf->snbr.begin(), sf->snbr.end()); break;
+    case 4: v = sf->scount; break;
+    case 5: v = sf->h_root_idx; break;
+    default: return fail(SPMAT_ERR_ARG, "sf_export: unknown what=%d", what);
+  }
+  *len = (int64_t)v.size();
+  if (host_buf && cap > 0) memcpy(host_buf, v.data(), sizeof(int64_t) * std::min<int64_t>(cap, *len));
+  return SPMAT_OK;
+}
+
+int sf_destroy(sf_t sf) {
+  if (!sf) return SPMAT_OK;
+  {
+    DeviceGuard g(sf->comm->device);
+    cudaStreamSynchronize(sf->comm->comm_stream);
+  }
+  sf_free(sf);
+  return SPMAT_OK;
+}
+
+}  // extern "C"

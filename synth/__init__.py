@@ -152,6 +152,7 @@ def stencil_coo(shape, npts: int, rows=None, values: str = "int", seed: int = DE
 
     ``shape`` lists grid sizes fastest axis first, e.g. (nx, ny, nz).  ``rows=(lo, hi)``
     selects the generating rows (a rank's owned rows); entry ``k = (g - lo) * S + s``.
+    ``rows`` may also be a 1-D tensor of row ids (entries in that order).
     values: "int"  -> Laplacian weights, centre 2*ndim (or 26 for 27-pt), neighbours -1
             "real" -> hash(seed, i, j) -> U(-1, 1)
     """
@@ -159,10 +160,13 @@ def stencil_coo(shape, npts: int, rows=None, values: str = "int", seed: int = DE
     n_total = 1
     for s in shape:
         n_total *= s
-    lo, hi = (0, n_total) if rows is None else rows
     offs = stencil_offsets(ndim, npts)
     S = len(offs)
-    g = torch.arange(lo, hi, dtype=I64, device=device)
+    if rows is None or isinstance(rows, tuple):
+        lo, hi = (0, n_total) if rows is None else rows
+        g = torch.arange(lo, hi, dtype=I64, device=device)
+    else:  # explicit list of generating rows (sampled full-size parity checks)
+        g = rows.to(device=device, dtype=I64)
     cs = _coords(g, shape)
     i = g.repeat_interleave(S)
     jcols = []
@@ -179,7 +183,7 @@ def stencil_coo(shape, npts: int, rows=None, values: str = "int", seed: int = DE
         centre = float(npts - 1)
         w = torch.full((S,), -1.0, dtype=F64, device=device)
         w[offs.index(tuple([0] * ndim))] = centre
-        v = w.repeat(hi - lo)
+        v = w.repeat(g.numel())
     elif values == "real":
         v = uniform_pm1(hash_ids(seed, i, j))
     else:

@@ -1,0 +1,354 @@
+"""GPU parity: libspmat (CUDA, through the C ABI) vs the CPU oracle on seeded inputs.
+
+Bars (BASELINE.json north_star): COO structure, contribution plans and halo plans
+bit-exact; integer-valued inputs bit-exact; fp64 real-valued SpMV within relative max-norm
+1e-12.  Assembled values are bit-exact in real mode too (both sides
+sum contributions in ascending (src, k) order, reading Z1).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def sp():
+    import paper_2406_08646_b200 as sp
+    sp.load()
+    return sp
+
+
+@pytest.fixture(scope="module")
+def comm(sp):
+    torch.cuda.set_device(0)
+    c = sp.Comm(device=0, nranks=1, rank=0)
+    yield c
+    c.close()
+
+
+def dev(t):
+    return t.to("cuda")
+
+
+def rel_err(y, ref):
+    ref = np.asarray(ref)
+    d = np.max(np.abs(np.asarray(y) - ref)) if ref.size else 0.0
+    s = np.max(np.abs(ref)) if ref.size else 0.0
+    return d / s if s > 0 else d
+
+
+def canon(a):
+    """Canonicalise -0.0 -> +0.0 for bit comparisons (reading Z18)."""
+    a = np.asarray(a, dtype=np.float64).copy()
+    a[a == 0] = 0.0
+    return a
+
+
+def check_structure(A, O, r=0):
+    """Structure, colmap and contribution plan bit-exact vs the oracle rank r."""
+    assert np.array_equal(A.export("rowptr_d"), O.export(r, "rowptr_d"))
+    assert np.array_equal(A.export("col_d"), O.export(r, "col_d"))
+    assert np.array_equal(A.export("rowptr_o"), O.export(r, "rowptr_o"))
+    assert np.array_equal(A.export("col_o"), O.export(r, "col_o"))
+    assert np.array_equal(A.export("colmap"), O.export(r, "colmap"))
+    assert np.array_equal(A.export("jmap"), O.export(r, "jmap"))
+    assert np.array_equal(A.export("csrc"), O.export(r, "csrc"))
+
+
+def run_single(sp, comm, M, N, i, j, v, x, mode_values=True):
+    A = sp.Mat(comm, M, N, M, N, dev(i), dev(j))
+    vd = dev(v)
+    A.set_values(vd)
+    xd = dev(x)
+    yd = torch.empty(M, dtype=torch.float64, device="cuda")
+    A.mult(xd, yd)
+    torch.cuda.synchronize()
+    return A, yd.cpu().numpy()
+
+
+CASES = {
+    "c1_5pt64": lambda values: (4096, 4096) + synth.stencil_coo((64, 64), 5, values=values),
+    "7pt_ragged": lambda values: (40 * 37 * 23,) * 2 + synth.stencil_coo((40, 37, 23), 7, values=values),
+    "q1_9": lambda values: (9 ** 3,) * 2 + synth.q1_coo(9, variant="lap", values=values),
+    "q1mass_7": lambda values: (7 ** 3,) * 2 + synth.q1_coo(7, variant="mass", values=values),
+    "el_6": lambda values: (3 * 6 ** 3,) * 2 + synth.elasticity_coo(6, values=values),
+    "27pt_2d9": lambda values: (81, 81) + synth.stencil_coo((9, 9), 9, values=values),
+}
+
+
+@pytest.mark.parametrize("values", ["int", "real"])
+@pytest.mark.parametrize("case", list(CASES))
+def test_single_rank_parity(sp, comm, case, values):
+    M, N, i, j, v = CASES[case](values)
+    O = oracle.OracleMat(M, N, [M], [N], [i], [j])
+    O.set_values([v])
+    x = synth.x_vector(0, N, values)
+    A, y = run_single(sp, comm, M, N, i, j, v, x)
+    check_structure(A, O)
+    # assembled values: bit-exact (canonical (src,k) order on both sides)
+    assert np.array_equal(canon(A.export("val_d")), canon(O.export(0, "val_d")))
+    yo = O.mult(x.numpy())
+    if values == "int":
+        assert np.array_equal(canon(y), canon(yo))
+    else:
+        assert rel_err(y, yo) <= TOL
+    info = A.info()
+    assert info["nnz_d"] == O.info(0, "nnz_d") and info["n_ghost"] == 0
+    A.close()
+
+
+def test_p1_pins_on_gpu(sp, comm):
+    """Closed forms evaluated by the GPU path: A.1 and polynomial x (P3, P4)."""
+    n = 33
+    M = n ** 3
+    i, j, v = synth.stencil_coo((n, n, n), 7)
+    A = sp.Mat(comm, M, M, M, M, dev(i), dev(j))
+    A.set_values(dev(v))
+    g = torch.arange(M, device="cuda")
+    ix, iy, iz = g % n, (g // n) % n, g // (n * n)
+    y = torch.empty(M, dtype=torch.float64, device="cuda")
+    A.mult(torch.ones(M, dtype=torch.float64, device="cuda"), y)
+    want = sum(((c == 0) | (c == n - 1)).double() for c in (ix, iy, iz))
+    assert torch.equal(y, want)
+    A.mult((ix * ix + iy * iy + iz * iz).double(), y)
+    interior = (ix > 0) & (ix < n - 1) & (iy > 0) & (iy < n - 1) & (iz > 0) & (iz < n - 1)
+    assert torch.all(y[interior] == -6)
+    A.close()
+
+
+def test_nnz_closed_forms_gpu(sp, comm):
+    for (M, i, j, want) in [
+        (64 * 64, *synth.stencil_coo((64, 64), 5)[:2], 5 * 64 * 64 - 4 * 64),
+        (20 ** 3, *synth.stencil_coo((20,) * 3, 7)[:2], 7 * 20 ** 3 - 6 * 20 ** 2),
+        (10 ** 3, *synth.q1_coo(10)[:2], (3 * 10 - 2) ** 3),
+        (3 * 5 ** 3, *synth.elasticity_coo(5)[:2], 9 * (3 * 5 - 2) ** 3),
+    ]:
+        A = sp.Mat(comm, M, M, M, M, dev(i), dev(j))
+        assert A.info()["nnz_d"] == want
+        A.close()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_coo_fuzz(sp, comm, seed):
+    rng = np.random.default_rng(seed)
+    M, N = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+    n = int(rng.integers(0, 4000))
+    i, j, v = synth.random_coo(M, N, n, dup_frac=0.5, neg_frac=0.2, seed=seed)
+    O = oracle.OracleMat(M, N, [M], [N], [i], [j])
+    O.set_values([v])
+    A = sp.Mat(comm, M, N, M, N, dev(i), dev(j))
+    check_structure(A, O)
+    A.set_values(dev(v))
+    assert np.array_equal(canon(A.export("val_d")), canon(O.export(0, "val_d")))
+    x = synth.x_vector(0, N, "int", seed=seed)
+    y = torch.empty(M, dtype=torch.float64, device="cuda")
+    A.mult(dev(x), y)
+    assert np.array_equal(canon(y.cpu().numpy()), canon(O.mult(x.numpy())))
+    # ADD accumulates onto the INSERTed values
+    A.set_values(dev(v), sp.ADD)
+    O.set_values([v], oracle.ADD)
+    assert np.array_equal(canon(A.export("val_d")), canon(O.export(0, "val_d")))
+    A.close()
+
+
+def test_long_rows(sp, comm):
+    """Rows longer than the row-block cap take the CTA-reduction path."""
+    M, N = 50, 6000
+    rows, cols = [], []
+    for r in range(M):
+        L = 5000 if r in (3, 17) else (700 if r == 30 else r % 9)
+        rows.append(np.full(L, r))
+        cols.append(np.random.default_rng(r).choice(N, L, replace=False))
+    i = torch.from_numpy(np.concatenate(rows).astype(np.int64))
+    j = torch.from_numpy(np.concatenate(cols).astype(np.int64))
+    v = torch.from_numpy(np.random.default_rng(1).integers(-4, 5, i.numel()).astype(np.float64))
+    O = oracle.OracleMat(M, N, [M], [N], [i], [j])
+    O.set_values([v])
+    A = sp.Mat(comm, M, N, M, N, dev(i), dev(j))
+    A.set_values(dev(v))
+    assert A.info()["max_row_nnz"] == 5000
+    for values in ("int", "real"):
+        x = synth.x_vector(0, N, values)
+        y = torch.empty(M, dtype=torch.float64, device="cuda")
+        A.mult(dev(x), y)
+        yo = O.mult(x.numpy())
+        if values == "int":
+            assert np.array_equal(y.cpu().numpy(), yo)
+        else:
+            assert rel_err(y.cpu().numpy(), yo) <= TOL
+    A.close()
+
+
+def test_spec_example_gpu(sp, comm):
+    """SPEC.md L280-291 worked example through the GPU path."""
+    i = torch.tensor([0, 0, 1, -1])
+    j = torch.tensor([0, 1, 1, 2])
+    v = torch.tensor([1.0, 2.0, 3.0, 9.0], dtype=torch.float64)
+    A = sp.Mat(comm, 2, 3, 2, 3, dev(i), dev(j))
+    A.set_values(dev(v))
+    x = torch.tensor([1.0, 10.0, 100.0], dtype=torch.float64, device="cuda")
+    y = torch.empty(2, dtype=torch.float64, device="cuda")
+    A.mult(x, y)
+    assert y.tolist() == [21.0, 30.0]
+    A.set_values(dev(v), sp.ADD)
+    A.set_values(dev(v), sp.ADD)
+    A.mult(x, y)
+    assert y.tolist() == [63.0, 90.0]
+    A.close()
+
+
+def test_host_pointers_and_memtype(sp, comm):
+    """coo_i/j and x/y may be host memory (memtype detection)."""
+    M = 20 * 20
+    i, j, v = synth.stencil_coo((20, 20), 5, values="real")
+    A = sp.Mat(comm, M, M, M, M, i.numpy(), j.numpy())
+    A.set_values(dev(v))
+    x = synth.x_vector(0, M, "real")
+    xh = x.pin_memory()
+    yh = torch.empty(M, dtype=torch.float64).pin_memory()
+    A.mult(xh, yh)
+    yd = torch.empty(M, dtype=torch.float64, device="cuda")
+    A.mult(dev(x), yd)
+    assert torch.equal(yh, yd.cpu())
+    A.close()
+
+
+def test_empty_and_degenerate(sp, comm):
+    # no COO at all
+    A = sp.Mat(comm, 5, 5, 5, 5, torch.empty(0, dtype=torch.int64, device="cuda"),
+               torch.empty(0, dtype=torch.int64, device="cuda"))
+    assert A.info()["nnz_d"] == 0
+    A.set_values(torch.empty(0, dtype=torch.float64, device="cuda"))
+    y = torch.full((5,), 7.0, dtype=torch.float64, device="cuda")
+    A.mult(torch.ones(5, dtype=torch.float64, device="cuda"), y)
+    assert torch.all(y == 0)
+    A.close()
+    # all entries negative
+    i = torch.tensor([-1, -2, 0], device="cuda")
+    j = torch.tensor([0, 1, -5], device="cuda")
+    A = sp.Mat(comm, 3, 3, 3, 3, i, j)
+    assert A.info()["nnz_d"] == 0
+    A.close()
+    # 0 x 0 matrix
+    A = sp.Mat(comm, 0, 0, 0, 0, torch.empty(0, dtype=torch.int64, device="cuda"),
+               torch.empty(0, dtype=torch.int64, device="cuda"))
+    A.close()
+
+
+def test_errors(sp, comm):
+    i = torch.tensor([0, 1, 7, 1], device="cuda")
+    j = torch.tensor([0, 1, 0, 9], device="cuda")
+    with pytest.raises(sp.SpmatError) as e:
+        sp.Mat(comm, 5, 5, 5, 5, i, j)
+    assert e.value.status == sp.SPMAT_ERR_RANGE and "k=2" in e.value.message
+    with pytest.raises(sp.SpmatError) as e:
+        sp.Mat(comm, 4, 5, 5, 5, i[:2], j[:2])
+    assert e.value.status == sp.SPMAT_ERR_MISMATCH
+    A = sp.Mat(comm, 5, 5, 5, 5, i[:2], j[:2])
+    x = torch.ones(5, dtype=torch.float64, device="cuda")
+    with pytest.raises(sp.SpmatError) as e:
+        A.mult(x, torch.empty_like(x))
+    assert e.value.status == sp.SPMAT_ERR_STATE  # mult before set_values
+    with pytest.raises(sp.SpmatError) as e:
+        A.set_values(torch.ones(2, dtype=torch.float64, device="cuda"), sp.ADD)
+    assert e.value.status == sp.SPMAT_ERR_STATE  # ADD before INSERT
+    A.set_values(torch.ones(2, dtype=torch.float64, device="cuda"))
+    with pytest.raises(sp.SpmatError) as e:
+        A.mult(x, x)
+    assert e.value.status == sp.SPMAT_ERR_ARG
+    A.close()
+
+
+def test_sf_single_rank(sp, comm):
+    """Self-edge SF: fan-in, holes, REPLACE and SUM vs the oracle graph walk."""
+    rng = np.random.default_rng(3)
+    nroots, nleaves, space = 50, 40, 64
+    il = rng.permutation(space)[:nleaves]
+    ro = rng.integers(0, nroots, nleaves)
+    root = torch.from_numpy(rng.integers(-9, 9, nroots).astype(np.float64))
+    leaf0 = torch.from_numpy(rng.integers(-9, 9, space).astype(np.float64))
+    sf = sp.StarForest(comm, nroots, il, np.zeros(nleaves), ro)
+    for op in (sp.REPLACE, sp.SUM):
+        want = oracle.sf_bcast([nroots], [(il, np.zeros(nleaves), ro)], [root.numpy()],
+                               [leaf0.numpy()], op)[0]
+        rd = dev(root)
+        leaf = dev(leaf0)
+        sf.bcast_begin(rd, leaf, op)
+        sf.bcast_end(rd, leaf, op)
+        assert np.array_equal(leaf.cpu().numpy(), want)
+    sf.close()
+    with pytest.raises(sp.SpmatError):
+        sp.StarForest(comm, 3, None, [0], [3])  # offset >= nroots
+
+
+def test_sf_state_errors(sp, comm):
+    sf = sp.StarForest(comm, 3, None, [0, 0, 0], [0, 1, 2])
+    r = torch.arange(3, dtype=torch.float64, device="cuda")
+    l = torch.zeros(3, dtype=torch.float64, device="cuda")
+    with pytest.raises(sp.SpmatError) as e:
+        sf.bcast_end(r, l)
+    assert e.value.status == sp.SPMAT_ERR_STATE
+    sf.bcast_begin(r, l, sp.REPLACE)
+    with pytest.raises(sp.SpmatError) as e:
+        sf.bcast_end(r, l, sp.SUM)
+    assert e.value.status == sp.SPMAT_ERR_STATE
+    sf.bcast_end(r, l, sp.REPLACE)
+    assert l.tolist() == [0.0, 1.0, 2.0]
+    sf.close()
+
+
+def test_repeated_set_values_no_replan(sp, comm):
+    """Repeated numeric assembly reuses the plan."""
+    M = 30 * 30
+    i, j, v = synth.stencil_coo((30, 30), 5, values="real")
+    A = sp.Mat(comm, M, M, M, M, dev(i), dev(j))
+    for s in range(3):
+        A.set_values(dev(v * (s + 1)))
+    assert A.info()["plan_builds"] == 1
+    O = oracle.OracleMat(M, M, [M], [M], [i], [j])
+    O.set_values([v * 3])
+    assert np.array_equal(canon(A.export("val_d")), canon(O.export(0, "val_d")))
+    A.close()
+
+
+def test_determinism(sp, comm):
+    M = 64 ** 3
+    i, j, v = synth.stencil_coo((64, 64, 64), 7, values="real", device="cuda")
+    A = sp.Mat(comm, M, M, M, M, i, j)
+    A.set_values(v)
+    x = synth.x_vector(0, M, "real", device="cuda")
+    y1 = torch.empty(M, dtype=torch.float64, device="cuda")
+    y2 = torch.empty_like(y1)
+    A.mult(x, y1)
+    A.mult(x, y2)
+    assert torch.equal(y1, y2)
+    A.close()
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_full_size_sampled(sp, comm, cfg):
+    """Full BASELINE sizes in the bench launch configuration: sampled rows vs the oracle
+    computed one by one from the COO definition, plus A.1 over every row."""
+    i, j, v, sizes = synth.config_rank_coo(cfg, 1, 0, values="real", device="cuda")
+    M = sizes[0]
+    A = sp.Mat(comm, M, M, M, M, i, j)
+    A.set_values(v)
+    x = synth.x_vector(0, M, "real", device="cuda")
+    y = torch.empty(M, dtype=torch.float64, device="cuda")
+    A.mult(x, y)
+    rows = torch.unique(torch.cat([torch.randint(0, M, (1500,), generator=torch.Generator().manual_seed(5)),
+                                   torch.tensor([0, 1, M // 2, M - 2, M - 1])]))
+    if cfg == "c2":
+        ih, jh, vh = synth.stencil_coo(synth.config_shape(cfg), 7, rows=rows, values="real")
+    else:
+        ih, jh, vh = i.cpu(), j.cpu(), v.cpu()
+    ys = oracle.sample_rows(ih, jh, vh, rows.numpy(), x.cpu().numpy())
+    assert rel_err(y[rows.cuda()].cpu().numpy(), ys) <= TOL
+    del i, j, v
+    A.close()
