@@ -490,11 +490,12 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
   A->nnz_d = nnz_d;
   A->nnz_o = nnz_o;
   // diag CSR
-  SP_TRY(A->rowptr_d.alloc(m_local + 1));
+  // +8 padding: the bulk-copy SpMV rounds tile bounds out to 16-byte multiples
+  SP_TRY(A->rowptr_d.alloc(m_local + 1 + 8));
   CUB_CALL(tmp, st, cub::DeviceScan::ExclusiveSum(d_temp_storage, temp_storage_bytes, cnt_d.get(),
                                                   A->rowptr_d.get(), (int)(m_local + 1), st));
-  SP_TRY(A->col_d.alloc(nnz_d));
-  SP_TRY(A->val_d.alloc(nnz_d));
+  SP_TRY(A->col_d.alloc(nnz_d + 8));
+  SP_TRY(A->val_d.alloc(nnz_d + 8));
   DevBuf<int64_t> ocol;
   SP_TRY(ocol.alloc(nnz_o));
   if (nnz > 0) {
@@ -811,7 +812,7 @@ int spmat_destroy(spmat_t A) {
     A->rows_o.release(); A->rowptr_o.release(); A->col_o.release(); A->val_o.release();
     A->colmap.release(); A->lvec.release(); A->jmap.release(); A->perm.release();
     A->mixed.release(); A->sendperm.release(); A->sendbuf.release(); A->recvbuf.release();
-    A->rowblocks.release(); A->xstage.release(); A->ystage.release();
+    A->rowblocks.release(); A->rbp.release(); A->longrows.release(); A->xstage.release(); A->ystage.release();
   }
   delete A;
   return SPMAT_OK;

@@ -207,6 +207,10 @@ struct spmat_s {
   int kernel_id = 0;
   int64_t n_rowblocks = 0, max_row_nnz = 0;
   spmat::DevBuf<int32_t> rowblocks;  // n_rowblocks + 1 row boundaries
+  spmat::DevBuf<int2> rbp;           // n_rowblocks + 1 (first row, first nonzero) pairs
+  spmat::DevBuf<int32_t> longrows;   // rows with more than kLong nonzeros
+  int64_t n_long = 0;
+  int tma_grid = 0;                  // persistent grid of the bulk-copy SpMV
   // host staging for host x / y
   spmat::DevBuf<double> xstage, ystage;
   // profiling

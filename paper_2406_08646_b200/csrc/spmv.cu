@@ -32,7 +32,21 @@ constexpr int kTile = 1792;         // target nonzeros per row block (7 * 256)
 constexpr int kLong = 256;          // rows longer than this get their own block
 constexpr int kCap = kTile + kLong; // shared-memory product buffer (doubles)
 
-enum { KERNEL_STREAM = 1, KERNEL_VECTOR = 2 };
+enum { KERNEL_STREAM = 1, KERNEL_VECTOR = 2, KERNEL_TMA = 3 };
+
+// bulk-copy (TMA engine) pipeline of the persistent SpMV
+constexpr int kStages = 3;
+constexpr int kValCap = kCap + 2;   // doubles per stage (16-byte alignment slop)
+constexpr int kColCap = kCap + 4;   // ints per stage
+constexpr int kRpCap = kRows + 8;   // row-pointer ints per stage
+struct __align__(16) TmaStage {
+  double val[kValCap];
+  int col[kColCap];
+  int rp[kRpCap];
+  int4 hdr;  // r0, r1, p0, p1 of the row block held by this stage
+  int4 pad;
+};
+constexpr size_t kTmaSmem = kStages * sizeof(TmaStage) + kStages * sizeof(unsigned long long);
 
 #define GRID_STRIDE(t, n) \
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (n); t += (int64_t)gridDim.x * blockDim.x)
@@ -80,6 +94,15 @@ __global__ void k_long_bounds(const int32_t *__restrict__ rows, int64_t n,
   }
 }
 
+__global__ void k_rb_pairs(const int32_t *__restrict__ rows, const int32_t *__restrict__ rowptr,
+                           int64_t n, int2 *__restrict__ out) {
+  GRID_STRIDE(t, n) out[t] = make_int2(rows[t], rowptr[rows[t]]);
+}
+
+__global__ void k_spmv_tma(const int2 *__restrict__ rb, int n_blocks, const int32_t *__restrict__ rowptr,
+                           const int32_t *__restrict__ col, const double *__restrict__ val,
+                           const double *__restrict__ x, double *__restrict__ y);
+
 #define CUB_CALL(tmp, call_with_tmp)                     \
   do {                                                   \
     size_t temp_storage_bytes = 0;                       \
@@ -92,9 +115,10 @@ __global__ void k_long_bounds(const int32_t *__restrict__ rows, int64_t n,
 
 int spmv_prepare(spmat_s *A, cudaStream_t st) {
   const int64_t m = A->m, nnz = A->nnz_d;
-  A->kernel_id = KERNEL_STREAM;
+  A->kernel_id = KERNEL_TMA;
   const char *env = getenv("SPMAT_SPMV_KERNEL");
   if (env && !strcmp(env, "vector")) A->kernel_id = KERNEL_VECTOR;
+  if (env && !strcmp(env, "stream")) A->kernel_id = KERNEL_STREAM;
   A->max_row_nnz = 0;
   A->n_rowblocks = 0;
   if (m == 0) {
@@ -146,6 +170,22 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   A->n_rowblocks = nu - 1;
   SP_TRY(A->rowblocks.alloc(nu));
   SP_CUDA(cudaMemcpyAsync(A->rowblocks.get(), uniq.get(), (size_t)nu * 4, cudaMemcpyDeviceToDevice, st));
+  SP_TRY(A->rbp.alloc(nu));
+  k_rb_pairs<<<nblk(nu), 256, 0, st>>>(A->rowblocks.get(), A->rowptr_d.get(), nu, A->rbp.get());
+  SP_LAUNCH();
+  A->n_long = nlong;
+  SP_TRY(A->longrows.alloc(nlong));
+  if (nlong)
+    SP_CUDA(cudaMemcpyAsync(A->longrows.get(), longrows.get(), (size_t)nlong * 4, cudaMemcpyDeviceToDevice, st));
+  // persistent grid: as many CTAs as fit (2 per SM at ~80 KB of shared memory each)
+  static bool attr_set = false;
+  if (!attr_set) {
+    SP_CUDA(cudaFuncSetAttribute(k_spmv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+    attr_set = true;
+  }
+  int per_sm = 0;
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_tma, kThreads, kTmaSmem));
+  A->tma_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * A->comm->num_sms, A->n_rowblocks));
   SP_CUDA(cudaStreamSynchronize(st));
   return SPMAT_OK;
 }
@@ -237,6 +277,176 @@ __global__ void __launch_bounds__(256) k_spmv_vector(const int32_t *__restrict__
   if (lane == 0) y[row] = s;
 }
 
+
+// ------------------------------------------------------------------ bulk-copy (TMA) SpMV
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(phase)
+      : "memory");
+}
+// global -> shared bulk copy on the TMA engine, completion counted on an mbarrier;
+// L2 evict_first: val/col/rowptr are streamed once, x should stay resident
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         unsigned long long *bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// Persistent CTAs, each owning a contiguous range of row blocks.  Thread 0 keeps kStages
+// row blocks in flight: val, col and row-pointer slices of a row block land in a shared
+// memory stage through cp.async.bulk, tracked by that stage's mbarrier.  All threads then
+// (1) gather x and overwrite val with the products in place, (2) sum rows -- one thread per
+// row, left to right, when the block has >= kThreads/2 rows (the stencil case, bit-identical
+// to a serial CSR loop), otherwise W lanes per row with a shuffle reduction -- and (3) free
+// the stage, which thread 0 refills with the row block kStages ahead.
+__global__ void __launch_bounds__(kThreads, 2)
+    k_spmv_tma(const int2 *__restrict__ rb, int n_blocks, const int32_t *__restrict__ rowptr,
+               const int32_t *__restrict__ col, const double *__restrict__ val,
+               const double *__restrict__ x, double *__restrict__ y) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  TmaStage *st = reinterpret_cast<TmaStage *>(smem);
+  unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + kStages * sizeof(TmaStage));
+  const int tid = threadIdx.x;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int b0 = (int)((long long)n_blocks * c / G), b1 = (int)((long long)n_blocks * (c + 1) / G);
+  const int nb = b1 - b0;
+  if (nb <= 0) return;
+  uint64_t policy = 0;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+  }
+  __syncthreads();
+  // thread 0: issue row block `it` (relative to b0) into stage it % kStages
+  int2 nA, nB;  // prefetched bounds of the next block to issue
+  auto issue = [&](int it, int2 A, int2 B) {
+    const int s = it % kStages;
+    const int r0 = A.x, r1 = B.x, p0 = A.y, p1 = B.y;
+    st[s].hdr = make_int4(r0, r1, p0, p1);
+    if (p1 - p0 > kCap) {  // long row: done by k_spmv_long
+      mbar_arrive_tx(&bars[s], 0);
+      return;
+    }
+    const int va = p0 & ~1, ve = (p1 + 1) & ~1;
+    const int ca = p0 & ~3, ce = (p1 + 3) & ~3;
+    const int ra = r0 & ~3, re = (r1 + 4) & ~3;
+    const uint32_t bytes = (uint32_t)((ve - va) * 8 + (ce - ca) * 4 + (re - ra) * 4);
+    mbar_arrive_tx(&bars[s], bytes);
+    if (ve > va) bulk_g2s(st[s].val, val + va, (ve - va) * 8, &bars[s], policy);
+    if (ce > ca) bulk_g2s(st[s].col, col + ca, (ce - ca) * 4, &bars[s], policy);
+    bulk_g2s(st[s].rp, rowptr + ra, (re - ra) * 4, &bars[s], policy);
+  };
+  if (tid == 0) {
+    const int pre = min(kStages, nb);
+    for (int it = 0; it < pre; ++it) issue(it, rb[b0 + it], rb[b0 + it + 1]);
+    if (pre < nb) {
+      nA = rb[b0 + pre];
+      nB = rb[b0 + pre + 1];
+    }
+  }
+  __syncthreads();  // stage headers visible
+  for (int it = 0; it < nb; ++it) {
+    const int s = it % kStages;
+    mbar_wait(&bars[s], (uint32_t)((it / kStages) & 1));
+    const int4 h = st[s].hdr;
+    const int r0 = h.x, r1 = h.y, p0 = h.z, p1 = h.w, n = p1 - p0;
+    if (n <= kCap) {
+      double *sv = st[s].val + (p0 - (p0 & ~1));
+      const int *sc = st[s].col + (p0 - (p0 & ~3));
+      const int *rp = st[s].rp - (r0 & ~3);  // rp[r] = rowptr[r]
+      constexpr int U = 8;
+      for (int base = 0; base < n; base += kThreads * U) {
+        int cc[U];
+        double xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = base + u * kThreads + tid;
+          cc[u] = e < n ? sc[e] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = cc[u] >= 0 ? __ldg(x + cc[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = base + u * kThreads + tid;
+          if (e < n) sv[e] = __dmul_rn(sv[e], xv[u]);
+        }
+      }
+      __syncthreads();
+      const int nrows = r1 - r0;
+      if (nrows * 2 >= kThreads) {
+        for (int r = r0 + tid; r < r1; r += kThreads) {
+          const int a = rp[r] - p0, z = rp[r + 1] - p0;
+          double acc = 0.0;
+          for (int e = a; e < z; ++e) acc = __dadd_rn(acc, sv[e]);
+          y[r] = acc;
+        }
+      } else {
+        int W = 1;
+        while (W < 32 && nrows * W * 2 <= kThreads) W <<= 1;
+        const int r = r0 + tid / W, lane = tid % W;
+        double acc = 0.0;
+        if (r < r1) {
+          const int a = rp[r] - p0, z = rp[r + 1] - p0;
+          for (int e = a + lane; e < z; e += W) acc = __dadd_rn(acc, sv[e]);
+        }
+        for (int o = W >> 1; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o, W));
+        if (r < r1 && lane == 0) y[r] = acc;
+      }
+    }
+    __syncthreads();  // stage s consumed by every thread
+    if (tid == 0 && it + kStages < nb) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
+      issue(it + kStages, nA, nB);
+      if (it + kStages + 1 < nb) {
+        nA = nB;
+        nB = rb[b0 + it + kStages + 2];
+      }
+    }
+  }
+}
+
+// one CTA per row longer than kCap nonzeros (rows the staged kernels skip)
+__global__ void __launch_bounds__(kThreads) k_spmv_long(const int32_t *__restrict__ rows,
+                                                        const int32_t *__restrict__ rowptr,
+                                                        const int32_t *__restrict__ col,
+                                                        const double *__restrict__ val,
+                                                        const double *__restrict__ x,
+                                                        double *__restrict__ y) {
+  __shared__ double red[kThreads / 32];
+  const int r = rows[blockIdx.x];
+  const int a = rowptr[r], z = rowptr[r + 1];
+  if (z - a <= kCap) return;
+  double s = 0.0;
+  for (int e = a + threadIdx.x; e < z; e += kThreads) s = __dadd_rn(s, __dmul_rn(val[e], __ldg(x + col[e])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) t = __dadd_rn(t, red[w]);
+    y[r] = t;
+  }
+}
+
 // y[rows_o[q]] = y[rows_o[q]] + (sum over the compressed off-diagonal row, left to right)
 __global__ void __launch_bounds__(256) k_spmv_offdiag(const int32_t *__restrict__ rows,
                                                       const int32_t *__restrict__ rowptr,
@@ -267,6 +477,18 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s) {
       k_spmv_vector<32><<<nblk(A->m * 32), 256, 0, s>>>(A->rowptr_d.get(), A->col_d.get(), A->val_d.get(), x, y, A->m);
     }
     SP_LAUNCH();
+    return SPMAT_OK;
+  }
+  if (A->kernel_id == KERNEL_TMA) {
+    k_spmv_tma<<<(unsigned)A->tma_grid, kThreads, kTmaSmem, s>>>(A->rbp.get(), (int)A->n_rowblocks,
+                                                               A->rowptr_d.get(), A->col_d.get(),
+                                                               A->val_d.get(), x, y);
+    SP_LAUNCH();
+    if (A->n_long > 0) {
+      k_spmv_long<<<(unsigned)A->n_long, kThreads, 0, s>>>(A->longrows.get(), A->rowptr_d.get(),
+                                                           A->col_d.get(), A->val_d.get(), x, y);
+      SP_LAUNCH();
+    }
     return SPMAT_OK;
   }
   k_spmv_stream<<<(unsigned)A->n_rowblocks, kThreads, 0, s>>>(A->rowblocks.get(), A->rowptr_d.get(),

@@ -352,3 +352,26 @@ def test_full_size_sampled(sp, comm, cfg):
     assert rel_err(y[rows.cuda()].cpu().numpy(), ys) <= TOL
     del i, j, v
     A.close()
+
+
+@pytest.mark.parametrize("kernel", ["tma", "stream", "vector"])
+@pytest.mark.parametrize("case", ["7pt_ragged", "q1_9", "el_6", "c1_5pt64"])
+def test_kernel_variants(sp, comm, kernel, case, monkeypatch):
+    """Every diagonal SpMV variant (chosen at create time) against the oracle."""
+    monkeypatch.setenv("SPMAT_SPMV_KERNEL", kernel)
+    M, N, i, j, v = CASES[case]("real")
+    O = oracle.OracleMat(M, N, [M], [N], [i], [j])
+    O.set_values([v])
+    x = synth.x_vector(0, N, "real")
+    A, y = run_single(sp, comm, M, N, i, j, v, x)
+    assert A.info()["spmv_kernel_id"] == {"stream": 1, "vector": 2, "tma": 3}[kernel]
+    assert rel_err(y, O.mult(x.numpy())) <= TOL
+    # integer mode is exact in any summation order
+    vi = CASES[case]("int")[4]
+    A.set_values(dev(vi))
+    xi = synth.x_vector(0, N, "int")
+    yd = torch.empty(M, dtype=torch.float64, device="cuda")
+    A.mult(dev(xi), yd)
+    O.set_values([vi])
+    assert np.array_equal(canon(yd.cpu().numpy()), canon(O.mult(xi.numpy())))
+    A.close()
