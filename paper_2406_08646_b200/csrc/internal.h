@@ -206,7 +206,7 @@ struct spmat_s {
   // SpMV schedule
   int kernel_id = 0;
   int64_t n_rowblocks = 0, max_row_nnz = 0;
-  spmat::DevBuf<int32_t> rowblocks;  // n_rowblocks + 1 row boundaries
+  int lanes = 1;                     // lanes per row of the diagonal SpMV (row statistics)
   spmat::DevBuf<int2> rbp;           // n_rowblocks + 1 (first row, first nonzero) pairs
   spmat::DevBuf<int32_t> longrows;   // rows with more than kLong nonzeros
   int64_t n_long = 0;

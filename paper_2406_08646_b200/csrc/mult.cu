@@ -1,0 +1,116 @@
+// mult.cu -- MatMult orchestration: halo SF broadcast on the comm stream overlapped with
+// the diagonal SpMV, then the off-diagonal SpMV-add.
+//
+// The halo exchange is issued first on the high-priority comm stream (NCCL), the diagonal
+// SpMV runs on the caller's stream meanwhile, and the off-diagonal SpMV-add waits on the
+// halo event on the device: the host never blocks (contrast the MPI path of P:492-509).
+#include "internal.h"
+
+namespace spmat {
+
+static cudaEvent_t *prof_pair(spmat_s *A, int kind) {
+  auto &v = A->prof_ev[kind];
+  size_t i = A->prof_n[kind];
+  if (2 * i + 2 > v.size()) {
+    cudaEvent_t a, b;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return nullptr;
+    v.push_back(a);
+    v.push_back(b);
+  }
+  A->prof_n[kind]++;
+  return &v[2 * i];
+}
+
+static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStream_t s) {
+  const bool halo = (part & 2) && A->comm->nranks > 1;
+  cudaEvent_t *pe;
+  if (halo) {
+    pe = A->profile ? prof_pair(A, 2) : nullptr;
+    SP_TRY(sf_begin(A->halo, x, A->lvec.get(), SF_REPLACE, s, pe));
+  }
+  if (part & 1) {
+    pe = A->profile ? prof_pair(A, 0) : nullptr;
+    if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
+    SP_TRY(spmv_diag(A, x, y, s));
+    if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
+  }
+  if (halo) SP_TRY(sf_end(A->halo, x, A->lvec.get(), SF_REPLACE, s));
+  if ((part & 4) && A->n_ro > 0) {
+    pe = A->profile ? prof_pair(A, 1) : nullptr;
+    if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
+    SP_TRY(spmv_offdiag(A, y, s));
+    if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
+  }
+  return SPMAT_OK;
+}
+
+}  // namespace spmat
+
+using namespace spmat;
+
+extern "C" {
+
+int spmat_mult(spmat_t A, const double *x, double *y, void *stream) {
+  if (!A) return fail(SPMAT_ERR_ARG, "spmat_mult: null matrix");
+  if ((A->n > 0 && !x) || (A->m > 0 && !y)) return fail(SPMAT_ERR_ARG, "spmat_mult: null x or y");
+  if (x && (const void *)x == (const void *)y) return fail(SPMAT_ERR_ARG, "spmat_mult: x and y alias");
+  if (!A->values_set && A->nnz_d + A->nnz_o > 0)
+    return fail(SPMAT_ERR_STATE, "spmat_mult before spmat_set_values_coo");
+  DeviceGuard g(A->comm->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool hx = A->n > 0 && !is_device_ptr(x);
+  const bool hy = A->m > 0 && !is_device_ptr(y);
+  if (!hx && !hy) return mult_impl(A, x, y, 7, s);
+  // host buffers: stage through device copies inside the stream order
+  const double *dx = x;
+  double *dy = y;
+  if (hx) {
+    if (A->xstage.n < (size_t)A->n) SP_TRY(A->xstage.alloc(A->n));
+    SP_CUDA(cudaMemcpyAsync(A->xstage.get(), x, A->n * 8, cudaMemcpyHostToDevice, s));
+    dx = A->xstage.get();
+  }
+  if (hy) {
+    if (A->ystage.n < (size_t)A->m) SP_TRY(A->ystage.alloc(A->m));
+    dy = A->ystage.get();
+  }
+  SP_TRY(mult_impl(A, dx, dy, 7, s));
+  if (hy) SP_CUDA(cudaMemcpyAsync(y, dy, A->m * 8, cudaMemcpyDeviceToHost, s));
+  SP_CUDA(cudaStreamSynchronize(s));
+  return SPMAT_OK;
+}
+
+int spmat_mult_part(spmat_t A, const double *x, double *y, int part, void *stream) {
+  if (!A) return fail(SPMAT_ERR_ARG, "spmat_mult_part: null matrix");
+  if (part < 1 || part > 7) return fail(SPMAT_ERR_ARG, "spmat_mult_part: bad part %d", part);
+  if (x && (const void *)x == (const void *)y) return fail(SPMAT_ERR_ARG, "spmat_mult_part: x and y alias");
+  DeviceGuard g(A->comm->device);
+  return mult_impl(A, x, y, part, (cudaStream_t)stream);
+}
+
+int spmat_profile(spmat_t A, int enable) {
+  if (!A) return fail(SPMAT_ERR_ARG, "spmat_profile: null matrix");
+  A->profile = enable != 0;
+  return SPMAT_OK;
+}
+
+int spmat_profile_read(spmat_t A, double ms[4], int64_t n[4]) {
+  if (!A || !ms || !n) return fail(SPMAT_ERR_ARG, "spmat_profile_read: null argument");
+  DeviceGuard g(A->comm->device);
+  SP_CUDA(cudaDeviceSynchronize());
+  for (int k = 0; k < 4; ++k) {
+    ms[k] = 0.0;
+    n[k] = 0;
+  }
+  for (int k = 0; k < 3; ++k) {
+    for (size_t i = 0; i < A->prof_n[k]; ++i) {
+      float t = 0.f;
+      SP_CUDA(cudaEventElapsedTime(&t, A->prof_ev[k][2 * i], A->prof_ev[k][2 * i + 1]));
+      ms[k] += t;
+    }
+    n[k] = (int64_t)A->prof_n[k];
+    A->prof_n[k] = 0;
+  }
+  return SPMAT_OK;
+}
+
+}  // extern "C"
