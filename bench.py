@@ -34,6 +34,8 @@ import torch  # noqa: E402
 
 import synth  # noqa: E402
 
+KERNEL_NAMES = {1: "k_spmv_stream (diagonal-block SpMV)", 2: "k_spmv_vector (diagonal-block SpMV)",
+                3: "k_spmv_tma<W> (diagonal-block SpMV, bulk-copy staged)"}
 METRIC = "MatMult GFLOP/s & HBM GB/s (% roofline), fp64, at 1/2/4/8 B200"
 UNIT = "GFLOP/s"
 FALLBACK_HBM = 6650.0
@@ -322,7 +324,7 @@ def main():
     if os.path.exists(tp):
         try:
             tr = json.load(open(tp)).get(f"{cfg}_P{P}")
-            traffic = tr
+            traffic = tr.get("traffic_bytes_per_launch") if tr else None
         except Exception:
             traffic = None
     gflops = 2 * nnz_global / t_step / 1e9
@@ -348,7 +350,7 @@ def main():
         },
         "hbm_gbs_per_gpu": gbs_gpu,
         "pct_hbm_roofline": gbs_gpu / hbm_peak,
-        "roofline": {"bound": "hbm", "kernel": "k_spmv_stream (diagonal-block SpMV)",
+        "roofline": {"bound": "hbm", "kernel": KERNEL_NAMES.get(info["spmv_kernel_id"], "?"),
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
                      "algorithmic_bytes_per_launch": diag_bytes,
