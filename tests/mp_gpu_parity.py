@@ -1,0 +1,269 @@
+"""Multi-rank GPU parity (one process per GPU, NCCL).  Launched by tests/test_gpu_multirank.py:
+
+    torchrun --nproc-per-node P --master-addr 127.0.0.1 tests/mp_gpu_parity.py
+
+Every rank builds the oracle's in-process P-rank simulation of the same global problem and
+checks ITS OWN part of the GPU result against it: CSR structure, colmap, contribution plan
+(jmap, source ranks, source positions), COO send/receive plans, halo SF plan -- all
+bit-exact -- assembled values bit-exact, and y (integer inputs bit-exact, real inputs within
+1e-12 relative max-norm, and equal to the P=1 global product).
+"""
+import os
+import sys
+import traceback
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import paper_2406_08646_b200 as sp  # noqa: E402
+import synth  # noqa: E402
+
+TOL = 1e-12
+
+
+def canon(a):
+    a = np.asarray(a, dtype=np.float64).copy()
+    a[a == 0] = 0.0
+    return a
+
+
+def rel_err(y, ref):
+    ref = np.asarray(ref)
+    if ref.size == 0:
+        return 0.0
+    s = np.max(np.abs(ref))
+    d = np.max(np.abs(np.asarray(y) - ref))
+    return d / s if s > 0 else d
+
+
+class Ctx:
+    def __init__(self):
+        self.P = dist.get_world_size()
+        self.r = dist.get_rank()
+        self.comm = sp.Comm()
+
+    def log(self, *a):
+        print(f"[rank {self.r}]", *a, flush=True)
+
+
+def oracle_positions(O, r):
+    """Oracle contribution list of rank r as (src, position-in-message-from-src or k)."""
+    csrc, ck = O.export(r, "csrc"), O.export(r, "ck")
+    pos = ck.copy()
+    P = O.P
+    for src in range(P):
+        if src == r:
+            continue
+        sc = O.export(src, "send_count")
+        sk = O.export(src, "send_k")
+        start = int(np.sum(sc[:r]))
+        seg = sk[start:start + sc[r]]
+        where = {int(k): p for p, k in enumerate(seg)}
+        m = csrc == src
+        pos[m] = [where[int(k)] for k in ck[m]]
+    return csrc, pos
+
+
+def check_matrix(c, name, M, N, row_sizes, col_sizes, coo, values, x_global, exact_y):
+    """coo: list over ranks of (i, j, v) CPU tensors (every rank has all of them)."""
+    P, r = c.P, c.r
+    O = oracle.OracleMat(M, N, row_sizes, col_sizes, [t[0] for t in coo], [t[1] for t in coo])
+    O.set_values([t[2] for t in coo])
+    i, j, v = coo[r]
+    A = sp.Mat(c.comm, row_sizes[r], col_sizes[r], M, N, i.cuda(), j.cuda())
+    A.set_values(v.cuda())
+    info = A.info()
+    assert info["rstart"] == O.info(r, "rstart") and info["cstart"] == O.info(r, "cstart")
+    for key in ("rowptr_d", "col_d", "rowptr_o", "col_o", "colmap", "jmap", "send_count",
+                "recv_count", "send_k"):
+        g, o = A.export(key), O.export(r, key)
+        assert np.array_equal(g, o), f"{name}: {key} differs on rank {r}"
+    osrc, opos = oracle_positions(O, r)
+    assert np.array_equal(A.export("csrc"), osrc), f"{name}: contribution sources differ"
+    assert np.array_equal(A.export("cpos"), opos), f"{name}: contribution positions differ"
+    for key in ("val_d", "val_o"):
+        assert np.array_equal(canon(A.export(key)), canon(O.export(r, key))), f"{name}: {key} differ"
+    # halo SF plan
+    hs = A.halo_sf()
+    lo, lof = O.export(r, "leaf_owner"), O.export(r, "leaf_offset")
+    nbrs = [q for q in range(P) if np.any(lo == q)]
+    assert list(sp.sf_export(hs, "recv_ranks")) == nbrs
+    assert list(sp.sf_export(hs, "recv_counts")) == [int(np.sum(lo == q)) for q in nbrs]
+    assert np.array_equal(sp.sf_export(hs, "leaf_idx"), np.concatenate(
+        [np.nonzero(lo == q)[0] for q in nbrs]) if nbrs else np.zeros(0, np.int64))
+    rc, ro = O.export(r, "root_count"), O.export(r, "root_offsets")
+    req = [p for p in range(P) if rc[p] > 0]
+    assert list(sp.sf_export(hs, "send_ranks")) == req
+    assert list(sp.sf_export(hs, "send_counts")) == [int(rc[p]) for p in req]
+    assert np.array_equal(sp.sf_export(hs, "root_idx"), ro)
+    # MatMult
+    off = np.concatenate([[0], np.cumsum(col_sizes)])
+    roff = np.concatenate([[0], np.cumsum(row_sizes)])
+    xl = torch.from_numpy(np.ascontiguousarray(x_global[off[r]:off[r + 1]])).cuda()
+    y = torch.empty(row_sizes[r], dtype=torch.float64, device="cuda")
+    A.mult(xl, y)
+    torch.cuda.synchronize()
+    yo = O.mult(x_global)[roff[r]:roff[r + 1]]
+    yg = y.cpu().numpy()
+    if exact_y:
+        assert np.array_equal(canon(yg), canon(yo)), f"{name}: y not bit-exact on rank {r}"
+    else:
+        assert rel_err(yg, yo) <= TOL, f"{name}: y rel err {rel_err(yg, yo)}"
+    # repeated MatMult and ADD re-assembly through the same plan
+    A.set_values(v.cuda(), sp.ADD)
+    A.mult(xl, y)
+    O.set_values([t[2] for t in coo], oracle.ADD)
+    yo2 = O.mult(x_global)[roff[r]:roff[r + 1]]
+    assert rel_err(y.cpu().numpy(), yo2) <= TOL
+    assert A.info()["plan_builds"] == 1
+    A.close()
+    return info, yg
+
+
+def case_stencil(c, values):
+    P = c.P
+    shape = (12, 10, 4 * P)
+    M = int(np.prod(shape))
+    sizes = synth.slab_sizes(shape, P)
+    off = synth.offsets_from_sizes(sizes)
+    coo = [synth.stencil_coo(shape, 7, rows=(off[q], off[q + 1]), values=values) for q in range(P)]
+    x = synth.x_vector(0, M, values).numpy()
+    info, y = check_matrix(c, f"7pt-{values}", M, M, sizes, sizes, coo, values, x, exact_y=True)
+    nb = (c.r > 0) + (c.r < P - 1)
+    assert info["n_ghost"] == nb * 12 * 10
+    # global vs partitioned (P7): the single-rank product of the same global matrix
+    i1, j1, v1 = synth.stencil_coo(shape, 7, values=values)
+    O1 = oracle.OracleMat(M, M, [M], [M], [i1], [j1])
+    O1.set_values([v1])
+    y1 = O1.mult(x)[off[c.r]:off[c.r + 1]]
+    if values == "int":
+        assert np.array_equal(canon(y), canon(y1))
+    else:
+        assert rel_err(y, y1) <= 1e-14
+
+
+def case_q1(c, values):
+    P = c.P
+    n = 4 * P
+    M = n ** 3
+    sizes = synth.slab_sizes((n, n, n), P)
+    coo = [synth.q1_coo(n, elems=synth.q1_slab_elems(n, P, q), variant="mass", values=values)
+           for q in range(P)]
+    x = synth.x_vector(0, M, values).numpy()
+    info, _ = check_matrix(c, f"q1-{values}", M, M, sizes, sizes, coo, values, x,
+                        exact_y=(values == "int"))
+    if c.r < P - 1:
+        assert info["n_send"] > 0
+    if c.r > 0:
+        assert info["n_mixed"] > 0
+
+
+def case_elasticity(c):
+    P = c.P
+    n = 2 * P
+    M = 3 * n ** 3
+    sizes = synth.slab_sizes((n, n, n), P, dof=3)
+    nodes = sizes[0] // 3
+    coo = [synth.elasticity_coo(n, nodes=(q * nodes, (q + 1) * nodes), values="real") for q in range(P)]
+    x = synth.x_vector(0, M, "real").numpy()
+    check_matrix(c, "elasticity", M, M, sizes, sizes, coo, "real", x, exact_y=False)
+
+
+def case_random(c, seed):
+    P = c.P
+    rng = np.random.default_rng(seed)
+    M, N = int(rng.integers(P, 200)), int(rng.integers(P, 200))
+    cuts = np.sort(rng.integers(0, M + 1, P - 1))
+    rs = list(np.diff(np.concatenate([[0], cuts, [M]])).astype(int))
+    if seed % 2 == 0:
+        rs = synth.split_sizes(M, P)
+    cs = synth.split_sizes(N, P)
+    coo = [synth.random_coo(M, N, int(rng.integers(0, 800)), dup_frac=0.5, neg_frac=0.2,
+                            seed=seed * 31 + q) for q in range(P)]
+    x = synth.x_vector(0, N, "int", seed=seed).numpy()
+    check_matrix(c, f"random{seed}", M, N, rs, cs, coo, "int", x, exact_y=True)
+
+
+def case_sf(c, seed):
+    """Standalone SF: random graph with holes and fan-in, REPLACE and SUM vs graph walk."""
+    P, r = c.P, c.r
+    rng = np.random.default_rng(seed)
+    nroots = [int(rng.integers(0, 20)) for _ in range(P)]
+    owners = [q for q in range(P) if nroots[q] > 0]
+    leaves, rootdata, leafdata = [], [], []
+    for p in range(P):
+        nl = int(rng.integers(0, 30)) if owners else 0
+        space = nl + int(rng.integers(0, 5))
+        il = rng.permutation(space)[:nl].astype(np.int64)
+        rr = rng.choice(owners, nl).astype(np.int64) if nl else np.zeros(0, np.int64)
+        ro = np.array([rng.integers(0, nroots[q]) for q in rr], dtype=np.int64)
+        leaves.append((il, rr, ro))
+        rootdata.append(rng.integers(-50, 50, nroots[p]).astype(float))
+        leafdata.append(rng.integers(-50, 50, space).astype(float))
+    il, rr, ro = leaves[r]
+    sf = sp.StarForest(c.comm, nroots[r], il, rr, ro)
+    for op in (sp.REPLACE, sp.SUM):
+        want = oracle.sf_bcast(nroots, leaves, rootdata, leafdata, op)[r]
+        root = torch.from_numpy(rootdata[r]).cuda()
+        leaf = torch.from_numpy(leafdata[r]).cuda()
+        sf.bcast_begin(root, leaf, op)
+        sf.bcast_end(root, leaf, op)
+        assert np.array_equal(leaf.cpu().numpy(), want), f"sf seed {seed} op {op} rank {r}"
+    sf.close()
+
+
+def case_errors(c):
+    P, r = c.P, c.r
+    # only the last rank has an out-of-range index: every rank must report it
+    i = torch.tensor([0, 1] if r < P - 1 else [0, 99], device="cuda") + c.r * 2
+    j = torch.tensor([0, 1], device="cuda")
+    try:
+        sp.Mat(c.comm, 2, 2, 2 * P, 2 * P, i, j)
+        raise AssertionError("range error not raised")
+    except sp.SpmatError as e:
+        assert e.status == sp.SPMAT_ERR_RANGE, e
+        assert f"rank {P - 1}" in e.message
+    try:
+        sp.Mat(c.comm, 2 if r else 3, 2, 2 * P, 2 * P, i[:0], j[:0])
+        raise AssertionError("mismatch not raised")
+    except sp.SpmatError as e:
+        assert e.status == sp.SPMAT_ERR_MISMATCH, e
+
+
+def main():
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = Ctx()
+    failures = 0
+    cases = [("stencil-int", lambda: case_stencil(c, "int")),
+             ("stencil-real", lambda: case_stencil(c, "real")),
+             ("q1-int", lambda: case_q1(c, "int")), ("q1-real", lambda: case_q1(c, "real")),
+             ("elasticity", lambda: case_elasticity(c))]
+    cases += [(f"random{s}", (lambda s=s: case_random(c, s))) for s in range(6)]
+    cases += [(f"sf{s}", (lambda s=s: case_sf(c, s))) for s in range(6)]
+    cases += [("errors", lambda: case_errors(c))]
+    for name, fn in cases:
+        try:
+            fn()
+            dist.barrier()
+            if c.r == 0:
+                c.log(f"PASS {name}")
+        except Exception:
+            failures += 1
+            c.log(f"FAIL {name}\n{traceback.format_exc()}")
+            dist.barrier()
+    c.comm.close()
+    dist.destroy_process_group()
+    if c.r == 0:
+        print(f"MULTIRANK P={c.P} failures={failures}", flush=True)
+    sys.exit(1 if failures else 0)
+
+
+if __name__ == "__main__":
+    main()
