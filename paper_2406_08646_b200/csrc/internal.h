@@ -211,6 +211,7 @@ struct spmat_s {
   spmat::DevBuf<int32_t> longrows;   // rows with more than kLong nonzeros
   int64_t n_long = 0;
   int tma_grid = 0;                  // persistent grid of the bulk-copy SpMV
+  spmat::DevBuf<unsigned int> sched; // its block counter + finished-CTA counter
   // host staging for host x / y
   spmat::DevBuf<double> xstage, ystage;
   // profiling

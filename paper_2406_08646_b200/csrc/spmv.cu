@@ -48,7 +48,7 @@ struct __align__(16) TmaStage {
   int4 hdr;                // r0, r1, p0, p1 of the block in this stage
   int4 pad;
 };
-constexpr size_t kTmaSmem = kStages * sizeof(TmaStage) + kStages * sizeof(unsigned long long);
+constexpr size_t kTmaSmem = kStages * sizeof(TmaStage) + 2 * kStages * sizeof(unsigned long long);
 
 #define GRID_STRIDE(t, n) \
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (n); t += (int64_t)gridDim.x * blockDim.x)
@@ -107,6 +107,9 @@ __device__ __forceinline__ void mbar_arrive_tx(unsigned long long *b, uint32_t b
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred P;\n"
@@ -138,62 +141,91 @@ __device__ __forceinline__ int ld_stream(const int *p) {
 }
 
 // ------------------------------------------------------------------ TMA-fed row kernel
-// Persistent CTAs; row block b = blockIdx.x + it * gridDim.x (all CTAs sweep the matrix
-// together, so a 3D stencil's +-plane x window stays L2-resident).  Thread 0 keeps kStages
-// blocks in flight; every thread then computes W-lane row dot products out of the stage.
+// Persistent, warp-specialised CTAs: warp kConsumerWarps is the producer, the other warps
+// consume.  The producer claims row blocks from a global counter (dynamic scheduling: CTAs
+// that start late -- e.g. behind an NCCL kernel -- simply take fewer blocks; blocks are
+// claimed in increasing order, so all CTAs sweep the matrix together and a 3D stencil's
+// +-plane x window stays L2-resident), and for each claimed block issues three bulk copies
+// (val, col, row pointers) into a free stage, completing on that stage's `full` mbarrier.
+// Consumers wait on `full`, compute W-lane row dot products straight out of shared memory,
+// and release the stage on its `empty` mbarrier (one arrive per consumer warp).  A stage
+// header with r0 = -1 ends the loop.  The last CTA to run out of blocks resets the counter
+// for the next launch (stream order makes that safe; CUDA-graph safe too).
+constexpr int kConsumerWarps = kThreads / 32;
+constexpr int kCtaThreads = kThreads + 32;
+
 template <int W>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kCtaThreads, 3)
     k_spmv_tma(const int2 *__restrict__ rb, int n_blocks, const int32_t *__restrict__ rowptr,
                const int32_t *__restrict__ col, const double *__restrict__ val,
-               const double *__restrict__ x, double *__restrict__ y) {
+               const double *__restrict__ x, double *__restrict__ y,
+               unsigned int *__restrict__ sched) {
   extern __shared__ __align__(128) unsigned char smem[];
   TmaStage *st = reinterpret_cast<TmaStage *>(smem);
-  unsigned long long *bars = reinterpret_cast<unsigned long long *>(smem + kStages * sizeof(TmaStage));
-  const int tid = threadIdx.x;
-  const int G = gridDim.x, b0 = blockIdx.x;
-  const int nb = n_blocks > b0 ? (n_blocks - b0 + G - 1) / G : 0;
-  if (nb <= 0) return;
-  uint64_t policy = 0;
+  unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + kStages * sizeof(TmaStage));
+  unsigned long long *empty = full + kStages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane32 = tid & 31;
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
   }
   __syncthreads();
-  int2 nA = make_int2(0, 0), nB = make_int2(0, 0);  // thread 0: bounds of the next block to issue
-  auto issue = [&](int it, int2 A, int2 B) {
-    const int s = it % kStages;
-    const int r0 = A.x, r1 = B.x, p0 = A.y, p1 = B.y;
-    st[s].hdr = make_int4(r0, r1, p0, p1);
-    if (p1 - p0 > kCap) {  // a single long row: k_spmv_long computes it
-      mbar_arrive_tx(&bars[s], 0);
-      return;
+  if (warp == kConsumerWarps) {  // ---------------- producer warp
+    if (lane32 != 0) return;
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    int b = (int)atomicAdd(sched, 1u);
+    int2 A = make_int2(0, 0), B = make_int2(0, 0);
+    if (b < n_blocks) {
+      A = rb[b];
+      B = rb[b + 1];
     }
-    const int va = p0 & ~1, ve = (p1 + 1) & ~1;
-    const int ca = p0 & ~3, ce = (p1 + 3) & ~3;
-    const int ra = r0 & ~3, re = (r1 + 4) & ~3;
-    mbar_arrive_tx(&bars[s], (uint32_t)((ve - va) * 8 + (ce - ca) * 4 + (re - ra) * 4));
-    if (ve > va) bulk_g2s(st[s].val, val + va, (ve - va) * 8, &bars[s], policy);
-    if (ce > ca) bulk_g2s(st[s].col, col + ca, (ce - ca) * 4, &bars[s], policy);
-    bulk_g2s(st[s].rp, rowptr + ra, (re - ra) * 4, &bars[s], policy);
-  };
-  if (tid == 0) {
-    const int pre = min(kStages, nb);
-    for (int it = 0; it < pre; ++it) issue(it, rb[b0 + it * G], rb[b0 + it * G + 1]);
-    if (pre < nb) {
-      nA = rb[b0 + pre * G];
-      nB = rb[b0 + pre * G + 1];
+    for (int it = 0;; ++it) {
+      const int s = it % kStages;
+      if (it >= kStages) mbar_wait(&empty[s], (uint32_t)(((it / kStages) - 1) & 1));
+      if (b >= n_blocks) {  // out of work: terminal header, then hand the counter back
+        st[s].hdr = make_int4(-1, 0, 0, 0);
+        mbar_arrive_tx(&full[s], 0);
+        __threadfence();
+        if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+          atomicExch(sched, 0u);
+          atomicExch(sched + 1, 0u);
+        }
+        return;
+      }
+      const int r0 = A.x, r1 = B.x, p0 = A.y, p1 = B.y;
+      st[s].hdr = make_int4(r0, r1, p0, p1);
+      if (p1 - p0 > kCap) {  // a single long row: k_spmv_long computes it
+        mbar_arrive_tx(&full[s], 0);
+      } else {
+        const int va = p0 & ~1, ve = (p1 + 1) & ~1;
+        const int ca = p0 & ~3, ce = (p1 + 3) & ~3;
+        const int ra = r0 & ~3, re = (r1 + 4) & ~3;
+        mbar_arrive_tx(&full[s], (uint32_t)((ve - va) * 8 + (ce - ca) * 4 + (re - ra) * 4));
+        if (ve > va) bulk_g2s(st[s].val, val + va, (ve - va) * 8, &full[s], policy);
+        if (ce > ca) bulk_g2s(st[s].col, col + ca, (ce - ca) * 4, &full[s], policy);
+        bulk_g2s(st[s].rp, rowptr + ra, (re - ra) * 4, &full[s], policy);
+      }
+      b = (int)atomicAdd(sched, 1u);  // claim the next block while the consumers work
+      if (b < n_blocks) {
+        A = rb[b];
+        B = rb[b + 1];
+      }
     }
   }
-  __syncthreads();  // headers of the first stages visible
+  // ---------------- consumer warps
   constexpr int RPP = kThreads / W;  // rows per pass
   constexpr int U = W == 1 ? 8 : 4;  // elements per lane in flight
   const int lane = tid % W;
-  for (int it = 0; it < nb; ++it) {
+  for (int it = 0;; ++it) {
     const int s = it % kStages;
-    mbar_wait(&bars[s], (uint32_t)((it / kStages) & 1));
+    mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
     const int4 h = st[s].hdr;
     const int r0 = h.x, r1 = h.y, p0 = h.z, p1 = h.w;
+    if (r0 < 0) break;
     if (p1 - p0 <= kCap) {
       const double *sv = st[s].val + (p0 & 1);  // sv[e - p0] = val[e]
       const int *sc = st[s].col + (p0 & 3);
@@ -224,15 +256,8 @@ __global__ void __launch_bounds__(kThreads, 3)
         if (lane == 0) y[r] = acc;
       }
     }
-    __syncthreads();  // stage s consumed by every thread
-    if (tid == 0 && it + kStages < nb) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(it + kStages, nA, nB);
-      if (it + kStages + 1 < nb) {
-        nA = rb[b0 + (it + kStages + 1) * G];
-        nB = rb[b0 + (it + kStages + 1) * G + 1];
-      }
-    }
+    __syncwarp();
+    if (lane32 == 0) mbar_arrive(&empty[s]);
   }
 }
 
@@ -362,7 +387,7 @@ static int tma_setup(spmat_s *A) {
     attr_set = true;
   }
   int per_sm = 0;
-  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_tma<W>, kThreads, kTmaSmem));
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_tma<W>, kCtaThreads, kTmaSmem));
   A->tma_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * A->comm->num_sms,
                                                              A->n_rowblocks));
   return SPMAT_OK;
@@ -426,6 +451,8 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   SP_TRY(A->longrows.alloc(nlong));
   if (nlong)
     SP_CUDA(cudaMemcpyAsync(A->longrows.get(), longrows.get(), (size_t)nlong * 4, cudaMemcpyDeviceToDevice, st));
+  SP_TRY(A->sched.alloc(2));
+  SP_CUDA(cudaMemsetAsync(A->sched.get(), 0, 8, st));
   switch (A->lanes) {
     case 1: SP_TRY(tma_setup<1>(A)); break;
     case 2: SP_TRY(tma_setup<2>(A)); break;
@@ -440,8 +467,9 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
 
 template <int W>
 static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s) {
-  k_spmv_tma<W><<<(unsigned)A->tma_grid, kThreads, kTmaSmem, s>>>(
-      A->rbp.get(), (int)A->n_rowblocks, A->rowptr_d.get(), A->col_d.get(), A->val_d.get(), x, y);
+  k_spmv_tma<W><<<(unsigned)A->tma_grid, kCtaThreads, kTmaSmem, s>>>(
+      A->rbp.get(), (int)A->n_rowblocks, A->rowptr_d.get(), A->col_d.get(), A->val_d.get(), x, y,
+      A->sched.get());
 }
 
 template <int W>
