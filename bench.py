@@ -290,6 +290,28 @@ def main():
     A.profile(False)
     t_diag = prof_ms[0] / max(prof_n[0], 1) / 1e3
     t_off = prof_ms[1] / max(prof_n[1], 1) / 1e3 if prof_n[1] else 0.0
+    t_halo = prof_ms[2] / max(prof_n[2], 1) / 1e3 if prof_n[2] else 0.0
+
+    # ---- isolated phases (diag only / halo only / offdiag only), same protocol
+    iso = {}
+    for name, part in (("diag", sp.PART_DIAG), ("halo", sp.PART_HALO), ("offdiag", sp.PART_OFFDIAG)):
+        if name != "diag" and P == 1:
+            continue
+        kk = max(10, min(a.steps, 100))
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(kk):
+            A.mult_part(x, y, part, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        iso[name] = max_over_ranks(ev0.elapsed_time(ev1) / kk)
+    A.mult(x, y, stream)  # restore y = A x after the partial products
+    torch.cuda.synchronize()
+    overlap = None
+    if P > 1 and min(iso["diag"], iso["halo"]) > 0:
+        overlap = (iso["diag"] + iso["halo"] + iso["offdiag"] - t_step * 1e3) / min(iso["diag"], iso["halo"])
 
     # ---- end to end through the public API with HOST buffers (pinned), copies inside
     e2e = None
@@ -356,7 +378,8 @@ def main():
                      "algorithmic_bytes_per_launch": diag_bytes,
                      "avg_launch_ms": t_diag * 1e3, "peak_source": peak_src},
         "phases_ms": {"diag_spmv": t_diag * 1e3, "offdiag_spmv": t_off * 1e3,
-                      "halo_bytes": halo_bytes},
+                      "halo_comm_stream": t_halo * 1e3, "halo_bytes": halo_bytes,
+                      "isolated": iso, "overlap_efficiency": overlap},
         "assembly": {"create_coo_s": t_create, "set_values_coo_ms": t_setvals * 1e3,
                      "coo_entries_per_rank": ncoo,
                      "set_values_GBps": (12 * ncoo + 12 * nnz_local) / t_setvals / 1e9},

@@ -388,7 +388,11 @@ static int tma_setup(spmat_s *A) {
   }
   int per_sm = 0;
   SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_tma<W>, kCtaThreads, kTmaSmem));
-  A->tma_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * A->comm->num_sms,
+  // SPMAT_RESERVE_SMS leaves SMs free for concurrently running kernels (e.g. NCCL's)
+  int reserve = 0;
+  if (const char *e = getenv("SPMAT_RESERVE_SMS")) reserve = std::max(0, atoi(e));
+  const int64_t sms = std::max<int64_t>(1, A->comm->num_sms - reserve);
+  A->tma_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * sms,
                                                              A->n_rowblocks));
   return SPMAT_OK;
 }
