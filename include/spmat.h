@@ -175,6 +175,16 @@ int spmat_get_halo_sf(spmat_t A, sf_t *borrowed);
 int spmat_profile(spmat_t A, int enable);
 int spmat_profile_read(spmat_t A, double ms[4], int64_t n[4]);
 
+/* Synchronise the device and report asynchronous failures of this matrix's work: CUDA
+   errors, NCCL async errors, and a device-initiated halo whose peer never answered. */
+int spmat_check(spmat_t A);
+
+/* Halo transport chosen at create time (collectively): 0 = single rank (none), 1 = NCCL
+   send/recv on the comm stream, 2 = device-initiated stores into the peer ghost vectors over
+   NVLink (CUDA IPC mappings; the NVSHMEM-SF analogue of P:533-562).  SPMAT_HALO=nccl in the
+   environment forces 1. */
+int spmat_halo_mode(spmat_t A);
+
 int spmat_destroy(spmat_t A);
 
 #ifdef __cplusplus

@@ -53,7 +53,7 @@ ABI_SYMBOLS = (
     "spmat_comm_check", "spmat_comm_destroy", "sf_create", "sf_bcast_begin", "sf_bcast_end",
     "sf_get_info", "sf_export", "sf_destroy", "spmat_create_coo", "spmat_set_values_coo",
     "spmat_mult", "spmat_mult_part", "spmat_get_info", "spmat_export", "spmat_get_halo_sf",
-    "spmat_profile", "spmat_profile_read", "spmat_destroy")
+    "spmat_profile", "spmat_profile_read", "spmat_check", "spmat_halo_mode", "spmat_destroy")
 
 
 class SpmatError(RuntimeError):
@@ -99,6 +99,8 @@ def load(path: str = LIB_PATH):
         "spmat_get_halo_sf": ([p, P(p)], i32),
         "spmat_profile": ([p, i32], i32),
         "spmat_profile_read": ([p, p, p], i32),
+        "spmat_check": ([p], i32),
+        "spmat_halo_mode": ([p], i32),
         "spmat_destroy": ([p], i32),
     }
     for name, (args, res) in sig.items():
@@ -247,6 +249,14 @@ def spmat_profile_read(A_h):
     return ms, n
 
 
+def spmat_check(A_h):
+    _check(load().spmat_check(A_h), "spmat_check")
+
+
+def spmat_halo_mode(A_h) -> int:
+    return int(load().spmat_halo_mode(A_h))
+
+
 def spmat_destroy(A_h):
     _check(load().spmat_destroy(A_h), "spmat_destroy")
 
@@ -346,6 +356,12 @@ class Mat:
 
     def halo_sf(self):
         return spmat_get_halo_sf(self.h)
+
+    def check(self):
+        spmat_check(self.h)
+
+    def halo_mode(self):
+        return spmat_halo_mode(self.h)
 
     def profile(self, enable=True):
         spmat_profile(self.h, enable)

@@ -632,6 +632,7 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
     SP_TRY(sf_build(c, n_local, A->n_ghost, nullptr, own.data(), off.data(), &A->halo));
   }
   SP_TRY(spmv_prepare(A, st));
+  SP_TRY(halo_peer_setup(A));
   SP_CUDA(cudaStreamSynchronize(st));
   A->plan_builds = 1;
   *out = guard.release();
@@ -703,6 +704,23 @@ int spmat_get_info(spmat_t A, int64_t info[16]) {
                    A->n_rowblocks, A->max_row_nnz, A->plan_builds};
   memcpy(info, v, sizeof v);
   return SPMAT_OK;
+}
+
+int spmat_check(spmat_t A) {
+  if (!A) return fail(SPMAT_ERR_ARG, "spmat_check: null matrix");
+  DeviceGuard g(A->comm->device);
+  SP_CUDA(cudaDeviceSynchronize());
+  if (A->peer && A->halo_err.get()) {
+    int e = 0;
+    SP_CUDA(cudaMemcpy(&e, A->halo_err.get(), 4, cudaMemcpyDeviceToHost));
+    if (e) return fail(SPMAT_ERR_NCCL, "device-initiated halo: a peer did not answer (timeout)");
+  }
+  return spmat_comm_check(A->comm);
+}
+
+int spmat_halo_mode(spmat_t A) {
+  if (!A) return -1;
+  return A->comm->nranks == 1 ? 0 : (A->peer ? 2 : 1);
 }
 
 int spmat_get_halo_sf(spmat_t A, sf_t *borrowed) {
@@ -802,6 +820,7 @@ int spmat_destroy(spmat_t A) {
   {
     DeviceGuard g(A->comm->device);
     cudaDeviceSynchronize();
+    halo_peer_release(A);
     if (A->halo) sf_free(A->halo);
     if (A->ev_send_ready) cudaEventDestroy(A->ev_send_ready);
     if (A->ev_recv_done) cudaEventDestroy(A->ev_recv_done);
@@ -812,7 +831,7 @@ int spmat_destroy(spmat_t A) {
     A->rows_o.release(); A->rowptr_o.release(); A->col_o.release(); A->val_o.release();
     A->colmap.release(); A->lvec.release(); A->jmap.release(); A->perm.release();
     A->mixed.release(); A->sendperm.release(); A->sendbuf.release(); A->recvbuf.release();
-    A->rbp.release(); A->sched.release(); A->longrows.release(); A->xstage.release(); A->ystage.release();
+    A->rbp.release(); A->sched.release(); A->halo_flags.release(); A->halo_puts.release(); A->halo_waits.release(); A->halo_counter.release(); A->halo_err.release(); A->longrows.release(); A->xstage.release(); A->ystage.release();
   }
   delete A;
   return SPMAT_OK;

@@ -172,6 +172,21 @@ int sf_end(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stre
 void sf_free(sf_s *sf);
 }  // namespace spmat
 
+// ------------------------------------------------------------------ device-initiated halo
+struct HaloPut {                       // one destination rank of my owned x entries
+  double *dst;                         // peer lvec + first leaf for me (IPC mapping)
+  int64_t count, root_start;           // contiguous x slice, or...
+  const int64_t *root_idx;             // ...gather indices (device), nullptr if contiguous
+  unsigned long long *peer_ready;      // destination's ready counter for me (IPC mapping)
+  unsigned long long *my_done;         // destination -> me: "lvec free" epoch (local)
+  int nchunk, pad;
+};
+struct HaloWait {                      // one sender of my ghost entries
+  unsigned long long *my_ready;        // local counter the sender bumps once per chunk
+  unsigned long long *peer_done;       // sender's "lvec free" flag for me (IPC mapping)
+  int nchunk, pad;
+};
+
 // ------------------------------------------------------------------ matrix
 struct spmat_s {
   spmat_comm_s *comm = nullptr;
@@ -219,10 +234,27 @@ struct spmat_s {
   std::vector<cudaEvent_t> prof_ev[3];  // pairs per kind
   size_t prof_n[3] = {0, 0, 0};
   int64_t plan_builds = 0;
+  // device-initiated halo over NVLink peer memory (halo.cu)
+  bool peer = false;
+  spmat::DevBuf<unsigned long long> halo_flags;  // [0,P) ready counters, [P,2P) done flags
+  std::vector<double *> peer_lvec;
+  std::vector<unsigned long long *> peer_flags;
+  spmat::DevBuf<HaloPut> halo_puts;
+  spmat::DevBuf<HaloWait> halo_waits;
+  spmat::DevBuf<unsigned int> halo_counter;
+  spmat::DevBuf<int> halo_err;
+  int n_puts = 0, n_waits = 0, put_chunks_total = 0;
+  int64_t epoch = 0;
+  cudaEvent_t ev_put_begin = nullptr, ev_put_done = nullptr;
 };
 
 namespace spmat {
 int spmv_prepare(spmat_s *A, cudaStream_t stream);  // row blocks + kernel choice
 int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream);
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
+int halo_peer_setup(spmat_s *A);                  // collective; leaves A->peer false on NCCL
+void halo_peer_release(spmat_s *A);
+int halo_peer_begin(spmat_s *A, const double *x, cudaStream_t s, cudaEvent_t *prof);
+int halo_peer_end(spmat_s *A, cudaStream_t s);
+int halo_peer_offdiag(spmat_s *A, double *y, cudaStream_t s, bool compute);
 }  // namespace spmat

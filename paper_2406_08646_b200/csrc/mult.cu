@@ -22,8 +22,31 @@ static cudaEvent_t *prof_pair(spmat_s *A, int kind) {
 }
 
 static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStream_t s) {
-  const bool halo = (part & 2) && A->comm->nranks > 1;
+  const bool multi = A->comm->nranks > 1;
   cudaEvent_t *pe;
+  if (multi && A->peer) {  // device-initiated halo over NVLink (halo.cu)
+    if (part & 2) {
+      pe = A->profile ? prof_pair(A, 2) : nullptr;
+      SP_TRY(halo_peer_begin(A, x, s, pe));
+    }
+    if (part & 1) {
+      pe = A->profile ? prof_pair(A, 0) : nullptr;
+      if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
+      SP_TRY(spmv_diag(A, x, y, s));
+      if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
+    }
+    if (part & 2) {
+      SP_TRY(halo_peer_end(A, s));
+      pe = (A->profile && (part & 4) && A->n_ro > 0) ? prof_pair(A, 1) : nullptr;
+      if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
+      SP_TRY(halo_peer_offdiag(A, y, s, (part & 4) != 0));
+      if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
+    } else if ((part & 4) && A->n_ro > 0) {
+      SP_TRY(spmv_offdiag(A, y, s));
+    }
+    return SPMAT_OK;
+  }
+  const bool halo = (part & 2) && multi;
   if (halo) {
     pe = A->profile ? prof_pair(A, 2) : nullptr;
     SP_TRY(sf_begin(A->halo, x, A->lvec.get(), SF_REPLACE, s, pe));

@@ -77,6 +77,7 @@ def check_matrix(c, name, M, N, row_sizes, col_sizes, coo, values, x_global, exa
     i, j, v = coo[r]
     A = sp.Mat(c.comm, row_sizes[r], col_sizes[r], M, N, i.cuda(), j.cuda())
     A.set_values(v.cuda())
+    c.halo_mode = A.halo_mode()
     info = A.info()
     assert info["rstart"] == O.info(r, "rstart") and info["cstart"] == O.info(r, "cstart")
     for key in ("rowptr_d", "col_d", "rowptr_o", "col_o", "colmap", "jmap", "send_count",
@@ -121,6 +122,11 @@ def check_matrix(c, name, M, N, row_sizes, col_sizes, coo, values, x_global, exa
     yo2 = O.mult(x_global)[roff[r]:roff[r + 1]]
     assert rel_err(y.cpu().numpy(), yo2) <= TOL
     assert A.info()["plan_builds"] == 1
+    # many back-to-back MatMults (exercises the halo epoch protocol), then check y again
+    for _ in range(20):
+        A.mult(xl, y)
+    A.check()
+    assert rel_err(y.cpu().numpy(), yo2) <= TOL
     A.close()
     return info, yg
 
@@ -261,6 +267,7 @@ def main():
     c.comm.close()
     dist.destroy_process_group()
     if c.r == 0:
+        print(f"halo_mode={getattr(c, 'halo_mode', -1)}", flush=True)
         print(f"MULTIRANK P={c.P} failures={failures}", flush=True)
     sys.exit(1 if failures else 0)
 

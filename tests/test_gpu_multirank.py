@@ -1,4 +1,5 @@
-"""Multi-rank GPU parity: launches tests/mp_gpu_parity.py with torchrun on P GPUs (NCCL)."""
+"""Multi-rank GPU parity: launches tests/mp_gpu_parity.py with torchrun on P GPUs (NCCL
+bootstrap), once per halo transport (device-initiated NVLink stores, and NCCL send/recv)."""
 import os
 import subprocess
 import sys
@@ -11,14 +12,20 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
+@pytest.mark.parametrize("halo", ["peer", "nccl"])
 @pytest.mark.parametrize("P", [2, 4, 8])
-def test_multirank_parity(P):
+def test_multirank_parity(P, halo):
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
+    env = dict(os.environ)
+    env["SPMAT_HALO"] = halo
+    port = 29611 + P + (0 if halo == "peer" else 20)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
-           "--master-addr=127.0.0.1", "--master-port=29611", os.path.join(HERE, "mp_gpu_parity.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(HERE, "mp_gpu_parity.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     sys.stdout.write(r.stdout[-6000:])
     sys.stderr.write(r.stderr[-6000:])
     assert r.returncode == 0
     assert f"MULTIRANK P={P} failures=0" in r.stdout
+    want = 2 if halo == "peer" else 1
+    assert f"halo_mode={want}" in r.stdout
