@@ -22,74 +22,30 @@
 #include <algorithm>
 #include <cstring>
 
+#include "halo_dev.cuh"
 #include "internal.h"
 
 namespace spmat {
 
-constexpr int kPutThreads = 512;
-constexpr int64_t kPutChunk = 16384;  // values per put CTA
-constexpr long long kSpinLimit = 20LL * 2000 * 1000 * 1000;  // ~20 s of SM clocks
+constexpr int kPutWarps = 4;  // warps per CTA of the standalone put kernel
 
 static inline int put_chunks(int64_t count) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(16, (count + kPutChunk - 1) / kPutChunk));
+  return (int)std::max<int64_t>(1, (count + kPutChunk - 1) / kPutChunk);
 }
 
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void red_release_sys_add(unsigned long long *p, unsigned long long v) {
-  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// returns false on timeout (and records it)
-__device__ bool spin_until_geq(const unsigned long long *flag, unsigned long long target, int *err) {
-  const long long t0 = clock64();
-  while (ld_acquire_sys(flag) < target) {
-    if (clock64() - t0 > kSpinLimit) {
-      atomicExch(err, 1);
-      return false;
-    }
-    __nanosleep(64);
-  }
-  return true;
-}
-
-// one CTA per (destination, chunk)
-__global__ void __launch_bounds__(kPutThreads) k_halo_put(const HaloPut *__restrict__ puts, int nputs,
-                                                          const double *__restrict__ x,
-                                                          unsigned long long epoch, int *err) {
-  // locate this CTA's destination and chunk
-  int c = blockIdx.x, d = 0;
-  while (d < nputs && c >= puts[d].nchunk) c -= puts[d++].nchunk;
-  if (d >= nputs) return;
-  const HaloPut p = puts[d];
-  __shared__ int ok;
-  if (threadIdx.x == 0) ok = epoch <= 1 ? 1 : spin_until_geq(p.my_done, epoch - 1, err);
-  __syncthreads();
-  if (!ok) return;
-  const int64_t per = (p.count + p.nchunk - 1) / p.nchunk;
-  const int64_t lo = c * per, hi = min(p.count, lo + per);
-  if (p.root_idx) {
-    for (int64_t t = lo + threadIdx.x; t < hi; t += kPutThreads) p.dst[t] = __ldg(x + p.root_idx[t]);
-  } else {
-    const double *src = x + p.root_start;
-    for (int64_t t = lo + threadIdx.x; t < hi; t += kPutThreads) p.dst[t] = __ldg(src + t);
-  }
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) red_release_sys_add(p.peer_ready, 1ull);
+// standalone put (halo-only MatMult parts, or a diagonal kernel without comm warps)
+__global__ void __launch_bounds__(32 * kPutWarps) k_halo_put(const HaloPut *__restrict__ puts, int nputs,
+                                                             int total, const double *__restrict__ x,
+                                                             unsigned long long epoch, int *err) {
+  const int c = blockIdx.x * kPutWarps + (threadIdx.x >> 5);
+  if (c < total) halo_put_warp(puts, nputs, c, x, epoch, err);
 }
 
 // y[rows[q]] += A_o lvec, after the senders' epoch-e data has landed; the last CTA releases lvec
 __global__ void __launch_bounds__(256) k_spmv_offdiag_peer(
     const int32_t *__restrict__ rows, const int32_t *__restrict__ rowptr,
-    const int32_t *__restrict__ col, const double *__restrict__ val, const double *lvec,
-    double *__restrict__ y, int64_t nro, const HaloWait *__restrict__ waits, int nwaits,
+    const int32_t *__restrict__ col, const double *__restrict__ val, const double *lvec_base,
+    int64_t lvec_stride, double *__restrict__ y, int64_t nro, const HaloWait *__restrict__ waits, int nwaits,
     unsigned long long epoch, unsigned int *counter, int *err, int signal) {
   __shared__ int ok;
   if (threadIdx.x == 0) {
@@ -99,6 +55,7 @@ __global__ void __launch_bounds__(256) k_spmv_offdiag_peer(
     ok = good;
   }
   __syncthreads();
+  const double *lvec = lvec_base + (int64_t)(epoch & 1) * lvec_stride;
   if (ok) {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nro;
          q += (int64_t)gridDim.x * blockDim.x) {
@@ -132,9 +89,16 @@ int halo_peer_setup(spmat_s *A) {
   for (size_t a = 0; a < sf->rnbr.size(); ++a)
     if (sf->leaf_start[a] < 0) fail = 1;
   if (sf->nself) fail = 1;
+  {  // agree on feasibility before allocating anything rank-specific
+    int64_t vote0[2] = {want ? 0 : 1, fail};
+    SP_TRY(c->allreduce_max_i64(vote0, 2));
+    if (vote0[0] || vote0[1]) return SPMAT_OK;  // NCCL halo on every rank
+  }
   SP_TRY(A->halo_flags.alloc(2 * (size_t)P));  // [0,P): ready from sender q; [P,2P): done from receiver q
   SP_CUDA(cudaMemset(A->halo_flags.get(), 0, 2 * P * sizeof(unsigned long long)));
-  if (A->lvec.n == 0) SP_TRY(A->lvec.alloc(1));
+  // two ghost buffers (epoch parity) so an owner never waits for the previous epoch's reads
+  A->lvec_stride = std::max<int64_t>(A->n_ghost, 1);
+  SP_TRY(A->lvec.alloc(2 * (size_t)A->lvec_stride));
   cudaIpcMemHandle_t hl, hf;
   memset(&hl, 0, sizeof hl);
   memset(&hf, 0, sizeof hf);
@@ -151,19 +115,20 @@ int halo_peer_setup(spmat_s *A) {
   if (vote[0] || vote[1]) return SPMAT_OK;  // NCCL halo on every rank
   // exchange handles and, per (receiver, sender), the receiver's leaf start for that sender
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  std::vector<int64_t> mine(16 + P, -1), all((size_t)(16 + P) * P);
+  std::vector<int64_t> mine(17 + P, -1), all((size_t)(17 + P) * P);
   memcpy(mine.data(), &hl, 64);
   memcpy(mine.data() + 8, &hf, 64);
-  for (size_t a = 0; a < sf->rnbr.size(); ++a) mine[16 + sf->rnbr[a]] = sf->leaf_start[a];
-  SP_TRY(c->allgather_i64(mine.data(), 16 + P, all.data()));
+  mine[16] = A->lvec_stride;
+  for (size_t a = 0; a < sf->rnbr.size(); ++a) mine[17 + sf->rnbr[a]] = sf->leaf_start[a];
+  SP_TRY(c->allgather_i64(mine.data(), 17 + P, all.data()));
   A->peer_lvec.assign(P, nullptr);
   A->peer_flags.assign(P, nullptr);
   int64_t open_fail = 0;
   auto open_rank = [&](int q) {
     if (A->peer_flags[q] || open_fail) return;
     cudaIpcMemHandle_t h1, h2;
-    memcpy(&h1, all.data() + (size_t)(16 + P) * q, 64);
-    memcpy(&h2, all.data() + (size_t)(16 + P) * q + 8, 64);
+    memcpy(&h1, all.data() + (size_t)(17 + P) * q, 64);
+    memcpy(&h2, all.data() + (size_t)(17 + P) * q + 8, 64);
     void *p1 = nullptr, *p2 = nullptr;
     if (cudaIpcOpenMemHandle(&p1, h1, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
         cudaIpcOpenMemHandle(&p2, h2, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
@@ -188,9 +153,10 @@ int halo_peer_setup(spmat_s *A) {
   int total_chunks = 0;
   for (size_t a = 0; a < sf->snbr.size(); ++a) {
     const int q = sf->snbr[a];
-    const int64_t lstart = all[(size_t)(16 + P) * q + 16 + me];
+    const int64_t lstart = all[(size_t)(17 + P) * q + 17 + me];
     HaloPut p;
     p.dst = A->peer_lvec[q] + lstart;
+    p.dst_stride = all[(size_t)(17 + P) * q + 16];
     p.count = sf->scount[a];
     p.root_start = sf->root_start[a] >= 0 ? sf->root_start[a] : 0;
     p.root_idx = sf->root_start[a] >= 0 ? nullptr : sf->d_root_idx.get() + sf->soff[a];
@@ -224,8 +190,6 @@ int halo_peer_setup(spmat_s *A) {
   A->put_chunks_total = total_chunks;
   A->epoch = 0;
   A->peer = true;
-  SP_CUDA(cudaEventCreateWithFlags(&A->ev_put_begin, cudaEventDisableTiming));
-  SP_CUDA(cudaEventCreateWithFlags(&A->ev_put_done, cudaEventDisableTiming));
   // every rank's flags are zero and every handle is open before the first put
   int64_t sync[1] = {0};
   SP_TRY(c->allreduce_max_i64(sync, 1));
@@ -239,32 +203,16 @@ void halo_peer_release(spmat_s *A) {
   }
   A->peer_lvec.clear();
   A->peer_flags.clear();
-  if (A->ev_put_begin) cudaEventDestroy(A->ev_put_begin);
-  if (A->ev_put_done) cudaEventDestroy(A->ev_put_done);
-  A->ev_put_begin = A->ev_put_done = nullptr;
   A->peer = false;
 }
 
-// enqueue the puts of epoch e on the comm stream (after the caller's pending work on s)
-int halo_peer_begin(spmat_s *A, const double *x, cudaStream_t s, cudaEvent_t *prof) {
-  spmat_comm_s *c = A->comm;
-  ++A->epoch;
+// standalone put of the current epoch on stream s
+int halo_peer_put(spmat_s *A, const double *x, cudaStream_t s) {
   if (A->n_puts == 0) return SPMAT_OK;
-  SP_CUDA(cudaEventRecord(A->ev_put_begin, s));
-  SP_CUDA(cudaStreamWaitEvent(c->comm_stream, A->ev_put_begin, 0));
-  if (prof) SP_CUDA(cudaEventRecord(prof[0], c->comm_stream));
-  k_halo_put<<<A->put_chunks_total, kPutThreads, 0, c->comm_stream>>>(
-      A->halo_puts.get(), A->n_puts, x, (unsigned long long)A->epoch, A->halo_err.get());
+  const int grid = (A->put_chunks_total + kPutWarps - 1) / kPutWarps;
+  k_halo_put<<<grid, 32 * kPutWarps, 0, s>>>(A->halo_puts.get(), A->n_puts, A->put_chunks_total, x,
+                                            (unsigned long long)A->epoch, A->halo_err.get());
   SP_LAUNCH();
-  if (prof) SP_CUDA(cudaEventRecord(prof[1], c->comm_stream));
-  SP_CUDA(cudaEventRecord(A->ev_put_done, c->comm_stream));
-  return SPMAT_OK;
-}
-
-// the caller may reuse x once the puts have read it
-int halo_peer_end(spmat_s *A, cudaStream_t s) {
-  if (A->n_puts == 0) return SPMAT_OK;
-  SP_CUDA(cudaStreamWaitEvent(s, A->ev_put_done, 0));
   return SPMAT_OK;
 }
 
@@ -275,7 +223,7 @@ int halo_peer_offdiag(spmat_s *A, double *y, cudaStream_t s, bool compute) {
   const int64_t nro = compute ? A->n_ro : 0;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nro + 255) / 256, 4L * A->comm->num_sms));
   k_spmv_offdiag_peer<<<grid, 256, 0, s>>>(A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(),
-                                           A->val_o.get(), A->lvec.get(), y, nro,
+                                           A->val_o.get(), A->lvec.get(), A->lvec_stride, y, nro,
                                            A->halo_waits.get(), A->n_waits,
                                            (unsigned long long)A->epoch, A->halo_counter.get(),
                                            A->halo_err.get(), 1);

@@ -175,6 +175,7 @@ void sf_free(sf_s *sf);
 // ------------------------------------------------------------------ device-initiated halo
 struct HaloPut {                       // one destination rank of my owned x entries
   double *dst;                         // peer lvec + first leaf for me (IPC mapping)
+  int64_t dst_stride;                  // peer lvec buffer stride (double-buffered by epoch)
   int64_t count, root_start;           // contiguous x slice, or...
   const int64_t *root_idx;             // ...gather indices (device), nullptr if contiguous
   unsigned long long *peer_ready;      // destination's ready counter for me (IPC mapping)
@@ -245,16 +246,16 @@ struct spmat_s {
   spmat::DevBuf<int> halo_err;
   int n_puts = 0, n_waits = 0, put_chunks_total = 0;
   int64_t epoch = 0;
-  cudaEvent_t ev_put_begin = nullptr, ev_put_done = nullptr;
+  int64_t lvec_stride = 0;          // peer mode: lvec holds two epochs' ghost buffers
 };
 
 namespace spmat {
 int spmv_prepare(spmat_s *A, cudaStream_t stream);  // row blocks + kernel choice
-int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream);
+// fuse_put: the bulk-copy SpMV's comm warps also perform this epoch's halo puts
+int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream, bool fuse_put = false);
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
 int halo_peer_setup(spmat_s *A);                  // collective; leaves A->peer false on NCCL
 void halo_peer_release(spmat_s *A);
-int halo_peer_begin(spmat_s *A, const double *x, cudaStream_t s, cudaEvent_t *prof);
-int halo_peer_end(spmat_s *A, cudaStream_t s);
+int halo_peer_put(spmat_s *A, const double *x, cudaStream_t s);  // standalone put kernel
 int halo_peer_offdiag(spmat_s *A, double *y, cudaStream_t s, bool compute);
 }  // namespace spmat

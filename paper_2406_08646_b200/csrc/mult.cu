@@ -25,18 +25,25 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
   const bool multi = A->comm->nranks > 1;
   cudaEvent_t *pe;
   if (multi && A->peer) {  // device-initiated halo over NVLink (halo.cu)
+    bool fused = false;
     if (part & 2) {
-      pe = A->profile ? prof_pair(A, 2) : nullptr;
-      SP_TRY(halo_peer_begin(A, x, s, pe));
+      ++A->epoch;
+      // the bulk-copy SpMV's comm warps do the puts; otherwise a standalone put kernel
+      fused = (part & 1) && A->kernel_id == 3 && A->m > 0 && A->n_rowblocks > 0;
+      if (!fused) {
+        pe = A->profile ? prof_pair(A, 2) : nullptr;
+        if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
+        SP_TRY(halo_peer_put(A, x, s));
+        if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
+      }
     }
     if (part & 1) {
       pe = A->profile ? prof_pair(A, 0) : nullptr;
       if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
-      SP_TRY(spmv_diag(A, x, y, s));
+      SP_TRY(spmv_diag(A, x, y, s, fused));
       if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
     }
     if (part & 2) {
-      SP_TRY(halo_peer_end(A, s));
       pe = (A->profile && (part & 4) && A->n_ro > 0) ? prof_pair(A, 1) : nullptr;
       if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
       SP_TRY(halo_peer_offdiag(A, y, s, (part & 4) != 0));

@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "halo_dev.cuh"
 #include "internal.h"
 
 namespace spmat {
@@ -141,8 +142,9 @@ __device__ __forceinline__ int ld_stream(const int *p) {
 }
 
 // ------------------------------------------------------------------ TMA-fed row kernel
-// Persistent, warp-specialised CTAs: warp kConsumerWarps is the producer, the other warps
-// consume.  The producer claims row blocks from a global counter (dynamic scheduling: CTAs
+// Persistent, warp-specialised CTAs: warp kConsumerWarps is the producer, warp
+// kConsumerWarps + 1 the comm warp (multi-GPU: stores this rank's boundary x entries into the
+// neighbours' ghost vectors over NVLink while the SpMV streams -- halo.cu), the rest consume.  The producer claims row blocks from a global counter (dynamic scheduling: CTAs
 // that start late -- e.g. behind an NCCL kernel -- simply take fewer blocks; blocks are
 // claimed in increasing order, so all CTAs sweep the matrix together and a 3D stencil's
 // +-plane x window stays L2-resident), and for each claimed block issues three bulk copies
@@ -152,14 +154,15 @@ __device__ __forceinline__ int ld_stream(const int *p) {
 // header with r0 = -1 ends the loop.  The last CTA to run out of blocks resets the counter
 // for the next launch (stream order makes that safe; CUDA-graph safe too).
 constexpr int kConsumerWarps = kThreads / 32;
-constexpr int kCtaThreads = kThreads + 32;
+constexpr int kCtaThreads = kThreads + 64;  // + producer warp + comm warp
 
 template <int W>
 __global__ void __launch_bounds__(kCtaThreads, 3)
     k_spmv_tma(const int2 *__restrict__ rb, int n_blocks, const int32_t *__restrict__ rowptr,
                const int32_t *__restrict__ col, const double *__restrict__ val,
                const double *__restrict__ x, double *__restrict__ y,
-               unsigned int *__restrict__ sched) {
+               unsigned int *__restrict__ sched, const HaloPut *__restrict__ puts, int nputs,
+               int put_chunks, unsigned long long epoch, int *halo_err) {
   extern __shared__ __align__(128) unsigned char smem[];
   TmaStage *st = reinterpret_cast<TmaStage *>(smem);
   unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + kStages * sizeof(TmaStage));
@@ -173,6 +176,10 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (warp == kConsumerWarps + 1) {  // ---------------- comm warp: fused halo puts (halo.cu)
+    for (int c = blockIdx.x; c < put_chunks; c += gridDim.x) halo_put_warp(puts, nputs, c, x, epoch, halo_err);
+    return;
+  }
   if (warp == kConsumerWarps) {  // ---------------- producer warp
     if (lane32 != 0) return;
     uint64_t policy;
@@ -470,10 +477,11 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
 }
 
 template <int W>
-static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s) {
+static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put) {
   k_spmv_tma<W><<<(unsigned)A->tma_grid, kCtaThreads, kTmaSmem, s>>>(
       A->rbp.get(), (int)A->n_rowblocks, A->rowptr_d.get(), A->col_d.get(), A->val_d.get(), x, y,
-      A->sched.get());
+      A->sched.get(), A->halo_puts.get(), A->n_puts, fuse_put ? A->put_chunks_total : 0,
+      (unsigned long long)A->epoch, A->halo_err.get());
 }
 
 template <int W>
@@ -482,7 +490,7 @@ static void launch_vector(spmat_s *A, const double *x, double *y, cudaStream_t s
                                                   x, y, A->m);
 }
 
-int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s) {
+int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put) {
   if (A->m == 0) return SPMAT_OK;
   if (A->kernel_id == KERNEL_VECTOR) {
     switch (std::max(A->lanes, 4)) {
@@ -496,12 +504,12 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s) {
   }
   if (A->kernel_id == KERNEL_TMA) {
     switch (A->lanes) {
-      case 1: launch_tma<1>(A, x, y, s); break;
-      case 2: launch_tma<2>(A, x, y, s); break;
-      case 4: launch_tma<4>(A, x, y, s); break;
-      case 8: launch_tma<8>(A, x, y, s); break;
-      case 16: launch_tma<16>(A, x, y, s); break;
-      default: launch_tma<32>(A, x, y, s); break;
+      case 1: launch_tma<1>(A, x, y, s, fuse_put); break;
+      case 2: launch_tma<2>(A, x, y, s, fuse_put); break;
+      case 4: launch_tma<4>(A, x, y, s, fuse_put); break;
+      case 8: launch_tma<8>(A, x, y, s, fuse_put); break;
+      case 16: launch_tma<16>(A, x, y, s, fuse_put); break;
+      default: launch_tma<32>(A, x, y, s, fuse_put); break;
     }
   } else {
     k_spmv_stream<<<(unsigned)A->n_rowblocks, kThreads, 0, s>>>(A->rbp.get(), A->rowptr_d.get(),
@@ -518,8 +526,9 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s) {
 
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t s) {
   if (A->n_ro == 0) return SPMAT_OK;
+  const double *lvec = A->lvec.get() + (A->peer ? (A->epoch & 1) * A->lvec_stride : 0);
   k_spmv_offdiag<<<nblk(A->n_ro), 256, 0, s>>>(A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(),
-                                              A->val_o.get(), A->lvec.get(), y, A->n_ro);
+                                              A->val_o.get(), lvec, y, A->n_ro);
   SP_LAUNCH();
   return SPMAT_OK;
 }
