@@ -232,16 +232,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = sp.Comm(device=local, nranks=P, rank=rank)
 
-    def barrier():
-        if P > 1:
-            torch.distributed.barrier()
-
-    def max_over_ranks(v):
-        if P == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+    from paper_2406_08646_b200 import dist as sdist
+    barrier, max_over_ranks = sdist.barrier, sdist.max_over_ranks
 
     # ---- inputs (seeded, synthetic, generated on the device)
     i, j, v, sizes = synth.config_rank_coo(cfg, P, rank, values=a.values, device="cuda")
@@ -271,11 +263,7 @@ def main():
     del i, j
     info = A.info()
     nnz_local = info["nnz_d"] + info["nnz_o"]
-    nnz_global = nnz_local
-    if P > 1:
-        t = torch.tensor([nnz_local], dtype=torch.int64, device="cuda")
-        torch.distributed.all_reduce(t)
-        nnz_global = int(t.item())
+    nnz_global = sdist.sum_over_ranks(nnz_local)
 
     x = synth.x_vector(off[rank], off[rank + 1], a.values, device="cuda")
     y = torch.empty(m, dtype=torch.float64, device="cuda")

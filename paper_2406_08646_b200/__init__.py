@@ -278,9 +278,8 @@ class Comm:
         if device is None:
             device = torch.cuda.current_device()
         if nranks > 1 and uid is None:
-            obj = [comm_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            uid = obj[0]
+            from . import dist as _d
+            uid = _d.share_unique_id(comm_unique_id)
         self.nranks, self.rank, self.device = nranks, rank, device
         self.h = comm_create(uid, nranks, rank, device)
 
