@@ -188,6 +188,24 @@ struct HaloWait {                      // one sender of my ghost entries
   int nchunk, pad;
 };
 
+// kernel-parameter bundles of the bulk-copy SpMV
+struct SpmvHalo {                      // fused NVLink halo puts (comm warps)
+  const HaloPut *puts;
+  int nputs, put_chunks;
+  unsigned long long epoch;
+  int *err;
+};
+struct SpmvTail {                      // fused off-diagonal SpMV-add (kernel tail)
+  const int32_t *order;                // claim index -> row block, boundary blocks first
+  int n_bblocks, enabled;
+  const int32_t *rows, *rowptr, *col;  // compressed off-diagonal block
+  const double *val, *lvec;            // lvec: this epoch's ghost buffer
+  int64_t n_ro;
+  const HaloWait *waits;
+  int nwaits, pad;
+  unsigned int *ctr;                   // [0] boundary-block warps done, [1] CTAs done with the tail
+};
+
 // ------------------------------------------------------------------ matrix
 struct spmat_s {
   spmat_comm_s *comm = nullptr;
@@ -227,6 +245,9 @@ struct spmat_s {
   spmat::DevBuf<int32_t> longrows;   // rows with more than kLong nonzeros
   int64_t n_long = 0;
   int tma_grid = 0;                  // persistent grid of the bulk-copy SpMV
+  spmat::DevBuf<int32_t> block_order;  // boundary row blocks first (fused off-diagonal tail)
+  int64_t n_bblocks = 0;
+  spmat::DevBuf<unsigned int> tail_ctr;
   spmat::DevBuf<unsigned int> sched; // its block counter + finished-CTA counter
   // host staging for host x / y
   spmat::DevBuf<double> xstage, ystage;
@@ -251,8 +272,10 @@ struct spmat_s {
 
 namespace spmat {
 int spmv_prepare(spmat_s *A, cudaStream_t stream);  // row blocks + kernel choice
-// fuse_put: the bulk-copy SpMV's comm warps also perform this epoch's halo puts
-int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream, bool fuse_put = false);
+// fuse_put: the bulk-copy SpMV's comm warps also perform this epoch's halo puts;
+// fuse_tail: its consumer warps also add A_o lvec after the last row block
+int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream, bool fuse_put = false,
+              bool fuse_tail = false);
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
 int halo_peer_setup(spmat_s *A);                  // collective; leaves A->peer false on NCCL
 void halo_peer_release(spmat_s *A);

@@ -37,12 +37,15 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
         if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
       }
     }
+    // full MatMult, no long rows: the off-diagonal SpMV-add runs in the same kernel's tail
+    const bool tail = fused && (part & 4) && A->n_ro > 0 && A->n_long == 0;
     if (part & 1) {
       pe = A->profile ? prof_pair(A, 0) : nullptr;
       if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
-      SP_TRY(spmv_diag(A, x, y, s, fused));
+      SP_TRY(spmv_diag(A, x, y, s, fused, tail));
       if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
     }
+    if (tail) return SPMAT_OK;
     if (part & 2) {
       pe = (A->profile && (part & 4) && A->n_ro > 0) ? prof_pair(A, 1) : nullptr;
       if (pe) SP_CUDA(cudaEventRecord(pe[0], s));

@@ -47,7 +47,7 @@ struct __align__(16) TmaStage {
   int col[kCap + 4];       // p0 rounded down to a multiple of 4
   int rp[kMaxRows + 8];    // r0 rounded down to a multiple of 4, through r1
   int4 hdr;                // r0, r1, p0, p1 of the block in this stage
-  int4 pad;
+  int4 flags;              // .x = 1: a boundary block (rows with off-diagonal entries)
 };
 constexpr size_t kTmaSmem = kStages * sizeof(TmaStage) + 2 * kStages * sizeof(unsigned long long);
 
@@ -92,6 +92,22 @@ __global__ void k_long_bounds(const int32_t *__restrict__ rows, int64_t n,
   }
 }
 
+// flag[b] = 1 if row block b holds a row with off-diagonal entries (rows_o sorted)
+__global__ void k_boundary_blocks(const int2 *__restrict__ rb, int64_t nb, const int32_t *__restrict__ rows_o,
+                                  int64_t nro, uint32_t *__restrict__ flag, uint32_t *__restrict__ nflag) {
+  GRID_STRIDE(b, nb) {
+    const int r0 = rb[b].x, r1 = rb[b + 1].x;
+    int64_t lo = 0, hi = nro;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (rows_o[mid] < r0) lo = mid + 1; else hi = mid;
+    }
+    const uint32_t f = (lo < nro && rows_o[lo] < r1) ? 1u : 0u;
+    flag[b] = f;
+    nflag[b] = 1u - f;
+  }
+}
+
 __global__ void k_rb_pairs(const int32_t *__restrict__ rows, const int32_t *__restrict__ rowptr,
                            int64_t n, int2 *__restrict__ out) {
   GRID_STRIDE(t, n) out[t] = make_int2(rows[t], rowptr[rows[t]]);
@@ -130,6 +146,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ double ld_stream(const double *p) {
   double v;
   asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -161,8 +182,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     k_spmv_tma(const int2 *__restrict__ rb, int n_blocks, const int32_t *__restrict__ rowptr,
                const int32_t *__restrict__ col, const double *__restrict__ val,
                const double *__restrict__ x, double *__restrict__ y,
-               unsigned int *__restrict__ sched, const HaloPut *__restrict__ puts, int nputs,
-               int put_chunks, unsigned long long epoch, int *halo_err) {
+               unsigned int *__restrict__ sched, const SpmvHalo halo, const SpmvTail tail) {
   extern __shared__ __align__(128) unsigned char smem[];
   TmaStage *st = reinterpret_cast<TmaStage *>(smem);
   unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + kStages * sizeof(TmaStage));
@@ -177,7 +197,8 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
   }
   __syncthreads();
   if (warp == kConsumerWarps + 1) {  // ---------------- comm warp: fused halo puts (halo.cu)
-    for (int c = blockIdx.x; c < put_chunks; c += gridDim.x) halo_put_warp(puts, nputs, c, x, epoch, halo_err);
+    for (int c = blockIdx.x; c < halo.put_chunks; c += gridDim.x)
+      halo_put_warp(halo.puts, halo.nputs, c, x, halo.epoch, halo.err);
     return;
   }
   if (warp == kConsumerWarps) {  // ---------------- producer warp
@@ -187,8 +208,9 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     int b = (int)atomicAdd(sched, 1u);
     int2 A = make_int2(0, 0), B = make_int2(0, 0);
     if (b < n_blocks) {
-      A = rb[b];
-      B = rb[b + 1];
+      const int blk = tail.order ? tail.order[b] : b;
+      A = rb[blk];
+      B = rb[blk + 1];
     }
     for (int it = 0;; ++it) {
       const int s = it % kStages;
@@ -205,6 +227,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
       }
       const int r0 = A.x, r1 = B.x, p0 = A.y, p1 = B.y;
       st[s].hdr = make_int4(r0, r1, p0, p1);
+      st[s].flags.x = (tail.enabled && b < tail.n_bblocks) ? 1 : 0;
       if (p1 - p0 > kCap) {  // a single long row: k_spmv_long computes it
         mbar_arrive_tx(&full[s], 0);
       } else {
@@ -218,8 +241,9 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
       }
       b = (int)atomicAdd(sched, 1u);  // claim the next block while the consumers work
       if (b < n_blocks) {
-        A = rb[b];
-        B = rb[b + 1];
+        const int blk = tail.order ? tail.order[b] : b;
+        A = rb[blk];
+        B = rb[blk + 1];
       }
     }
   }
@@ -233,6 +257,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     const int4 h = st[s].hdr;
     const int r0 = h.x, r1 = h.y, p0 = h.z, p1 = h.w;
     if (r0 < 0) break;
+    const int boundary = st[s].flags.x;
     if (p1 - p0 <= kCap) {
       const double *sv = st[s].val + (p0 & 1);  // sv[e - p0] = val[e]
       const int *sc = st[s].col + (p0 & 3);
@@ -264,7 +289,47 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
       }
     }
     __syncwarp();
-    if (lane32 == 0) mbar_arrive(&empty[s]);
+    if (lane32 == 0) {
+      mbar_arrive(&empty[s]);
+      if (boundary) {  // publish this warp's y rows of a boundary block to the tail
+        __threadfence();
+        atomicAdd(tail.ctr, 1u);
+      }
+    }
+  }
+  if (!tail.enabled) return;
+  // ---------------- fused off-diagonal tail: y[rows_o] += A_o lvec once every boundary block
+  // is written and every sender's epoch data has landed; then release the ghost buffer
+  if (tid == 0) {
+    const unsigned target = (unsigned)(kConsumerWarps * tail.n_bblocks);
+    const long long t0 = clock64();
+    while (ld_acquire_gpu(tail.ctr) < target) {
+      if (clock64() - t0 > kSpinLimit) {
+        atomicExch(halo.err, 2);
+        break;
+      }
+      __nanosleep(32);
+    }
+    for (int w = 0; w < tail.nwaits; ++w)
+      spin_until_geq(tail.waits[w].my_ready, halo.epoch * (unsigned long long)tail.waits[w].nchunk, halo.err);
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+  for (int64_t q = blockIdx.x * (int64_t)kThreads + tid; q < tail.n_ro; q += (int64_t)gridDim.x * kThreads) {
+    double sacc = 0.0;
+    for (int e = tail.rowptr[q]; e < tail.rowptr[q + 1]; ++e)
+      sacc = __dadd_rn(sacc, __dmul_rn(tail.val[e], __ldcg(tail.lvec + tail.col[e])));
+    const int r = tail.rows[q];
+    y[r] = __dadd_rn(__ldcg(y + r), sacc);
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(tail.ctr + 1, 1u) == gridDim.x - 1) {
+      atomicExch(tail.ctr, 0u);
+      atomicExch(tail.ctr + 1, 0u);
+      __threadfence();
+      for (int w = 0; w < tail.nwaits; ++w) st_release_sys(tail.waits[w].peer_done, halo.epoch);
+    }
   }
 }
 
@@ -464,6 +529,30 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
     SP_CUDA(cudaMemcpyAsync(A->longrows.get(), longrows.get(), (size_t)nlong * 4, cudaMemcpyDeviceToDevice, st));
   SP_TRY(A->sched.alloc(2));
   SP_CUDA(cudaMemsetAsync(A->sched.get(), 0, 8, st));
+  SP_TRY(A->tail_ctr.alloc(2));
+  SP_CUDA(cudaMemsetAsync(A->tail_ctr.get(), 0, 8, st));
+  A->n_bblocks = 0;
+  if (A->n_ro > 0) {  // claim order for the fused off-diagonal tail: boundary blocks first
+    const int64_t nbk = A->n_rowblocks;
+    DevBuf<uint32_t> f1, f0;
+    DevBuf<int> dn2;
+    SP_TRY(f1.alloc(nbk));
+    SP_TRY(f0.alloc(nbk));
+    SP_TRY(dn2.alloc(2));
+    SP_TRY(A->block_order.alloc(nbk));
+    k_boundary_blocks<<<nblk(nbk), 256, 0, st>>>(A->rbp.get(), nbk, A->rows_o.get(), A->n_ro, f1.get(), f0.get());
+    SP_LAUNCH();
+    CUB_CALL(tmp, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes,
+                                             cub::CountingInputIterator<int32_t>(0), f1.get(),
+                                             A->block_order.get(), dn2.get(), (int)nbk, st));
+    int nbb = 0;
+    SP_CUDA(cudaMemcpyAsync(&nbb, dn2.get(), 4, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    CUB_CALL(tmp, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes,
+                                             cub::CountingInputIterator<int32_t>(0), f0.get(),
+                                             A->block_order.get() + nbb, dn2.get() + 1, (int)nbk, st));
+    A->n_bblocks = nbb;
+  }
   switch (A->lanes) {
     case 1: SP_TRY(tma_setup<1>(A)); break;
     case 2: SP_TRY(tma_setup<2>(A)); break;
@@ -477,11 +566,28 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
 }
 
 template <int W>
-static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put) {
+static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put,
+                       bool fuse_tail) {
+  SpmvHalo h{A->halo_puts.get(), A->n_puts, fuse_put ? A->put_chunks_total : 0,
+             (unsigned long long)A->epoch, A->halo_err.get()};
+  SpmvTail t{};
+  if (fuse_tail) {
+    t.order = A->block_order.get();
+    t.n_bblocks = (int)A->n_bblocks;
+    t.enabled = 1;
+    t.rows = A->rows_o.get();
+    t.rowptr = A->rowptr_o.get();
+    t.col = A->col_o.get();
+    t.val = A->val_o.get();
+    t.lvec = A->lvec.get() + (A->epoch & 1) * A->lvec_stride;
+    t.n_ro = A->n_ro;
+    t.waits = A->halo_waits.get();
+    t.nwaits = A->n_waits;
+    t.ctr = A->tail_ctr.get();
+  }
   k_spmv_tma<W><<<(unsigned)A->tma_grid, kCtaThreads, kTmaSmem, s>>>(
       A->rbp.get(), (int)A->n_rowblocks, A->rowptr_d.get(), A->col_d.get(), A->val_d.get(), x, y,
-      A->sched.get(), A->halo_puts.get(), A->n_puts, fuse_put ? A->put_chunks_total : 0,
-      (unsigned long long)A->epoch, A->halo_err.get());
+      A->sched.get(), h, t);
 }
 
 template <int W>
@@ -490,7 +596,7 @@ static void launch_vector(spmat_s *A, const double *x, double *y, cudaStream_t s
                                                   x, y, A->m);
 }
 
-int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put) {
+int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put, bool fuse_tail) {
   if (A->m == 0) return SPMAT_OK;
   if (A->kernel_id == KERNEL_VECTOR) {
     switch (std::max(A->lanes, 4)) {
@@ -504,12 +610,12 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_
   }
   if (A->kernel_id == KERNEL_TMA) {
     switch (A->lanes) {
-      case 1: launch_tma<1>(A, x, y, s, fuse_put); break;
-      case 2: launch_tma<2>(A, x, y, s, fuse_put); break;
-      case 4: launch_tma<4>(A, x, y, s, fuse_put); break;
-      case 8: launch_tma<8>(A, x, y, s, fuse_put); break;
-      case 16: launch_tma<16>(A, x, y, s, fuse_put); break;
-      default: launch_tma<32>(A, x, y, s, fuse_put); break;
+      case 1: launch_tma<1>(A, x, y, s, fuse_put, fuse_tail); break;
+      case 2: launch_tma<2>(A, x, y, s, fuse_put, fuse_tail); break;
+      case 4: launch_tma<4>(A, x, y, s, fuse_put, fuse_tail); break;
+      case 8: launch_tma<8>(A, x, y, s, fuse_put, fuse_tail); break;
+      case 16: launch_tma<16>(A, x, y, s, fuse_put, fuse_tail); break;
+      default: launch_tma<32>(A, x, y, s, fuse_put, fuse_tail); break;
     }
   } else {
     k_spmv_stream<<<(unsigned)A->n_rowblocks, kThreads, 0, s>>>(A->rbp.get(), A->rowptr_d.get(),
