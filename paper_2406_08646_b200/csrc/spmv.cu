@@ -205,7 +205,10 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     if (lane32 != 0) return;
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    // claims run two ahead: the atomic for block it+2 is in flight while block it is issued,
+    // so only the (order, bounds) loads of the next block sit on the producer's path
     int b = (int)atomicAdd(sched, 1u);
+    int b_next = (int)atomicAdd(sched, 1u);
     int2 A = make_int2(0, 0), B = make_int2(0, 0);
     if (b < n_blocks) {
       const int blk = tail.order ? tail.order[b] : b;
@@ -239,8 +242,9 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
         if (ce > ca) bulk_g2s(st[s].col, col + ca, (ce - ca) * 4, &full[s], policy);
         bulk_g2s(st[s].rp, rowptr + ra, (re - ra) * 4, &full[s], policy);
       }
-      b = (int)atomicAdd(sched, 1u);  // claim the next block while the consumers work
+      b = b_next;
       if (b < n_blocks) {
+        b_next = (int)atomicAdd(sched, 1u);
         const int blk = tail.order ? tail.order[b] : b;
         A = rb[blk];
         B = rb[blk + 1];
