@@ -195,15 +195,16 @@ struct SpmvHalo {                      // fused NVLink halo puts (comm warps)
   unsigned long long epoch;
   int *err;
 };
-struct SpmvTail {                      // fused off-diagonal SpMV-add (kernel tail)
-  const int32_t *order;                // claim index -> row block, boundary blocks first
+struct SpmvTail {                      // fused off-diagonal SpMV-add (work items in the claim order)
+  const int32_t *order;                // row-block order, boundary blocks first
   int n_bblocks, enabled;
+  int t0, n_items;                     // claim indices [t0, t0+n_items) are off-diagonal items
   const int32_t *rows, *rowptr, *col;  // compressed off-diagonal block
   const double *val, *lvec;            // lvec: this epoch's ghost buffer
   int64_t n_ro;
   const HaloWait *waits;
   int nwaits, pad;
-  unsigned int *ctr;                   // [0] boundary-block warps done, [1] CTAs done with the tail
+  unsigned int *ctr;                   // [0] boundary-block warps done, [1] off-diagonal items done
 };
 
 // ------------------------------------------------------------------ matrix

@@ -206,19 +206,25 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
     // claims run two ahead: the atomic for block it+2 is in flight while block it is issued,
-    // so only the (order, bounds) loads of the next block sit on the producer's path
+    // so only the (order, bounds) loads of the next block sit on the producer's path.
+    // Claim index c maps to: an off-diagonal work item if c in [t0, t0+n_items), else a row
+    // block (through the boundary-first order when the tail is fused).
+    const int n_total = n_blocks + tail.n_items;
+    auto bounds = [&](int c, int2 &A, int2 &B) {
+      if (c >= tail.t0 && c < tail.t0 + tail.n_items) return;
+      const int k = c < tail.t0 ? c : c - tail.n_items;
+      const int blk = tail.order ? tail.order[k] : k;
+      A = rb[blk];
+      B = rb[blk + 1];
+    };
     int b = (int)atomicAdd(sched, 1u);
     int b_next = (int)atomicAdd(sched, 1u);
     int2 A = make_int2(0, 0), B = make_int2(0, 0);
-    if (b < n_blocks) {
-      const int blk = tail.order ? tail.order[b] : b;
-      A = rb[blk];
-      B = rb[blk + 1];
-    }
+    if (b < n_total) bounds(b, A, B);
     for (int it = 0;; ++it) {
       const int s = it % kStages;
       if (it >= kStages) mbar_wait(&empty[s], (uint32_t)(((it / kStages) - 1) & 1));
-      if (b >= n_blocks) {  // out of work: terminal header, then hand the counter back
+      if (b >= n_total) {  // out of work: terminal header, then hand the counter back
         st[s].hdr = make_int4(-1, 0, 0, 0);
         mbar_arrive_tx(&full[s], 0);
         __threadfence();
@@ -228,26 +234,29 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
         }
         return;
       }
-      const int r0 = A.x, r1 = B.x, p0 = A.y, p1 = B.y;
-      st[s].hdr = make_int4(r0, r1, p0, p1);
-      st[s].flags.x = (tail.enabled && b < tail.n_bblocks) ? 1 : 0;
-      if (p1 - p0 > kCap) {  // a single long row: k_spmv_long computes it
+      if (b >= tail.t0 && b < tail.t0 + tail.n_items) {  // off-diagonal work item
+        st[s].hdr = make_int4(-2, b - tail.t0, 0, 0);
         mbar_arrive_tx(&full[s], 0);
       } else {
-        const int va = p0 & ~1, ve = (p1 + 1) & ~1;
-        const int ca = p0 & ~3, ce = (p1 + 3) & ~3;
-        const int ra = r0 & ~3, re = (r1 + 4) & ~3;
-        mbar_arrive_tx(&full[s], (uint32_t)((ve - va) * 8 + (ce - ca) * 4 + (re - ra) * 4));
-        if (ve > va) bulk_g2s(st[s].val, val + va, (ve - va) * 8, &full[s], policy);
-        if (ce > ca) bulk_g2s(st[s].col, col + ca, (ce - ca) * 4, &full[s], policy);
-        bulk_g2s(st[s].rp, rowptr + ra, (re - ra) * 4, &full[s], policy);
+        const int r0 = A.x, r1 = B.x, p0 = A.y, p1 = B.y;
+        st[s].hdr = make_int4(r0, r1, p0, p1);
+        st[s].flags.x = (tail.enabled && b < tail.n_bblocks) ? 1 : 0;
+        if (p1 - p0 > kCap) {  // a single long row: k_spmv_long computes it
+          mbar_arrive_tx(&full[s], 0);
+        } else {
+          const int va = p0 & ~1, ve = (p1 + 1) & ~1;
+          const int ca = p0 & ~3, ce = (p1 + 3) & ~3;
+          const int ra = r0 & ~3, re = (r1 + 4) & ~3;
+          mbar_arrive_tx(&full[s], (uint32_t)((ve - va) * 8 + (ce - ca) * 4 + (re - ra) * 4));
+          if (ve > va) bulk_g2s(st[s].val, val + va, (ve - va) * 8, &full[s], policy);
+          if (ce > ca) bulk_g2s(st[s].col, col + ca, (ce - ca) * 4, &full[s], policy);
+          bulk_g2s(st[s].rp, rowptr + ra, (re - ra) * 4, &full[s], policy);
+        }
       }
       b = b_next;
-      if (b < n_blocks) {
+      if (b < n_total) {
         b_next = (int)atomicAdd(sched, 1u);
-        const int blk = tail.order ? tail.order[b] : b;
-        A = rb[blk];
-        B = rb[blk + 1];
+        bounds(b, A, B);
       }
     }
   }
@@ -260,7 +269,44 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
     const int4 h = st[s].hdr;
     const int r0 = h.x, r1 = h.y, p0 = h.z, p1 = h.w;
-    if (r0 < 0) break;
+    if (r0 == -1) break;
+    if (r0 == -2) {  // ---- off-diagonal work item: y[rows_o] += A_o lvec for kThreads rows
+      if (tid == 0) {  // every boundary block written and every sender's epoch data landed
+        const unsigned target = (unsigned)(kConsumerWarps * tail.n_bblocks);
+        const long long t0 = clock64();
+        while (ld_acquire_gpu(tail.ctr) < target) {
+          if (clock64() - t0 > kSpinLimit) {
+            atomicExch(halo.err, 2);
+            break;
+          }
+          __nanosleep(32);
+        }
+        for (int w = 0; w < tail.nwaits; ++w)
+          spin_until_geq(tail.waits[w].my_ready, halo.epoch * (unsigned long long)tail.waits[w].nchunk, halo.err);
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+      const int64_t q = (int64_t)r1 * kThreads + tid;
+      if (q < tail.n_ro) {
+        double sacc = 0.0;
+        for (int e = tail.rowptr[q]; e < tail.rowptr[q + 1]; ++e)
+          sacc = __dadd_rn(sacc, __dmul_rn(tail.val[e], __ldcg(tail.lvec + tail.col[e])));
+        const int r = tail.rows[q];
+        y[r] = __dadd_rn(__ldcg(y + r), sacc);
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+      if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(tail.ctr + 1, 1u) == (unsigned)tail.n_items - 1) {  // last item: release lvec
+          atomicExch(tail.ctr, 0u);
+          atomicExch(tail.ctr + 1, 0u);
+          __threadfence();
+          for (int w = 0; w < tail.nwaits; ++w) st_release_sys(tail.waits[w].peer_done, halo.epoch);
+        }
+      }
+      __syncwarp();
+      if (lane32 == 0) mbar_arrive(&empty[s]);
+      continue;
+    }
     const int boundary = st[s].flags.x;
     if (p1 - p0 <= kCap) {
       const double *sv = st[s].val + (p0 & 1);  // sv[e - p0] = val[e]
@@ -299,40 +345,6 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
         __threadfence();
         atomicAdd(tail.ctr, 1u);
       }
-    }
-  }
-  if (!tail.enabled) return;
-  // ---------------- fused off-diagonal tail: y[rows_o] += A_o lvec once every boundary block
-  // is written and every sender's epoch data has landed; then release the ghost buffer
-  if (tid == 0) {
-    const unsigned target = (unsigned)(kConsumerWarps * tail.n_bblocks);
-    const long long t0 = clock64();
-    while (ld_acquire_gpu(tail.ctr) < target) {
-      if (clock64() - t0 > kSpinLimit) {
-        atomicExch(halo.err, 2);
-        break;
-      }
-      __nanosleep(32);
-    }
-    for (int w = 0; w < tail.nwaits; ++w)
-      spin_until_geq(tail.waits[w].my_ready, halo.epoch * (unsigned long long)tail.waits[w].nchunk, halo.err);
-  }
-  asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
-  for (int64_t q = blockIdx.x * (int64_t)kThreads + tid; q < tail.n_ro; q += (int64_t)gridDim.x * kThreads) {
-    double sacc = 0.0;
-    for (int e = tail.rowptr[q]; e < tail.rowptr[q + 1]; ++e)
-      sacc = __dadd_rn(sacc, __dmul_rn(tail.val[e], __ldcg(tail.lvec + tail.col[e])));
-    const int r = tail.rows[q];
-    y[r] = __dadd_rn(__ldcg(y + r), sacc);
-  }
-  asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(tail.ctr + 1, 1u) == gridDim.x - 1) {
-      atomicExch(tail.ctr, 0u);
-      atomicExch(tail.ctr + 1, 0u);
-      __threadfence();
-      for (int w = 0; w < tail.nwaits; ++w) st_release_sys(tail.waits[w].peer_done, halo.epoch);
     }
   }
 }
@@ -575,10 +587,15 @@ static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, b
   SpmvHalo h{A->halo_puts.get(), A->n_puts, fuse_put ? A->put_chunks_total : 0,
              (unsigned long long)A->epoch, A->halo_err.get()};
   SpmvTail t{};
+  t.t0 = (int)A->n_rowblocks;  // no items: every claim index is a row block
   if (fuse_tail) {
     t.order = A->block_order.get();
     t.n_bblocks = (int)A->n_bblocks;
     t.enabled = 1;
+    // items go a quarter of the way through the sweep: by then the boundary blocks (claimed
+    // first) are written and the halo puts (issued at kernel start) have landed
+    t.n_items = (int)((A->n_ro + kThreads - 1) / kThreads);
+    t.t0 = (int)std::max<int64_t>(A->n_bblocks, A->n_rowblocks / 4);
     t.rows = A->rows_o.get();
     t.rowptr = A->rowptr_o.get();
     t.col = A->col_o.get();
