@@ -185,6 +185,11 @@ int spmat_check(spmat_t A);
    environment forces 1. */
 int spmat_halo_mode(spmat_t A);
 
+/* Device trace of the last fused MatMult kernel (created with SPMAT_TRACE=1 in the
+   environment, else *len = 0): globaltimer nanoseconds, per CTA [start, -, last block done,
+   end] then per off-diagonal work item [start, halo ready, done].  Copies min(cap, len). */
+int spmat_trace_read(spmat_t A, int64_t *host_buf, int64_t cap, int64_t *len);
+
 int spmat_destroy(spmat_t A);
 
 #ifdef __cplusplus

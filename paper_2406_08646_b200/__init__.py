@@ -53,7 +53,8 @@ ABI_SYMBOLS = (
     "spmat_comm_check", "spmat_comm_destroy", "sf_create", "sf_bcast_begin", "sf_bcast_end",
     "sf_get_info", "sf_export", "sf_destroy", "spmat_create_coo", "spmat_set_values_coo",
     "spmat_mult", "spmat_mult_part", "spmat_get_info", "spmat_export", "spmat_get_halo_sf",
-    "spmat_profile", "spmat_profile_read", "spmat_check", "spmat_halo_mode", "spmat_destroy")
+    "spmat_profile", "spmat_profile_read", "spmat_check", "spmat_halo_mode", "spmat_trace_read",
+    "spmat_destroy")
 
 
 class SpmatError(RuntimeError):
@@ -101,6 +102,7 @@ def load(path: str = LIB_PATH):
         "spmat_profile_read": ([p, p, p], i32),
         "spmat_check": ([p], i32),
         "spmat_halo_mode": ([p], i32),
+        "spmat_trace_read": ([p, p, i64, P(i64)], i32),
         "spmat_destroy": ([p], i32),
     }
     for name, (args, res) in sig.items():
@@ -255,6 +257,14 @@ def spmat_check(A_h):
 
 def spmat_halo_mode(A_h) -> int:
     return int(load().spmat_halo_mode(A_h))
+
+
+def spmat_trace_read(A_h) -> np.ndarray:
+    n = ctypes.c_int64()
+    _check(load().spmat_trace_read(A_h, None, 0, ctypes.byref(n)), "spmat_trace_read")
+    out = np.zeros(n.value, dtype=np.int64)
+    _check(load().spmat_trace_read(A_h, _ptr(out), n.value, ctypes.byref(n)), "spmat_trace_read")
+    return out
 
 
 def spmat_destroy(A_h):

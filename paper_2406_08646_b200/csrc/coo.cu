@@ -718,6 +718,16 @@ int spmat_check(spmat_t A) {
   return spmat_comm_check(A->comm);
 }
 
+int spmat_trace_read(spmat_t A, int64_t *host_buf, int64_t cap, int64_t *len) {
+  if (!A || !len) return fail(SPMAT_ERR_ARG, "spmat_trace_read: null argument");
+  DeviceGuard g(A->comm->device);
+  SP_CUDA(cudaDeviceSynchronize());
+  *len = (int64_t)A->trace.n;
+  if (host_buf && cap > 0 && A->trace.n)
+    SP_CUDA(cudaMemcpy(host_buf, A->trace.get(), 8 * std::min<int64_t>(cap, *len), cudaMemcpyDeviceToHost));
+  return SPMAT_OK;
+}
+
 int spmat_halo_mode(spmat_t A) {
   if (!A) return -1;
   return A->comm->nranks == 1 ? 0 : (A->peer ? 2 : 1);
@@ -831,7 +841,7 @@ int spmat_destroy(spmat_t A) {
     A->rows_o.release(); A->rowptr_o.release(); A->col_o.release(); A->val_o.release();
     A->colmap.release(); A->lvec.release(); A->jmap.release(); A->perm.release();
     A->mixed.release(); A->sendperm.release(); A->sendbuf.release(); A->recvbuf.release();
-    A->rbp.release(); A->sched.release(); A->block_order.release(); A->tail_ctr.release(); A->halo_flags.release(); A->halo_puts.release(); A->halo_waits.release(); A->halo_counter.release(); A->halo_err.release(); A->longrows.release(); A->xstage.release(); A->ystage.release();
+    A->rbp.release(); A->sched.release(); A->block_order.release(); A->tail_ctr.release(); A->trace.release(); A->halo_flags.release(); A->halo_puts.release(); A->halo_waits.release(); A->halo_counter.release(); A->halo_err.release(); A->longrows.release(); A->xstage.release(); A->ystage.release();
   }
   delete A;
   return SPMAT_OK;

@@ -205,6 +205,7 @@ struct SpmvTail {                      // fused off-diagonal SpMV-add (work item
   const HaloWait *waits;
   int nwaits, pad;
   unsigned int *ctr;                   // [0] boundary-block warps done, [1] off-diagonal items done
+  unsigned long long *trace;           // SPMAT_TRACE=1: globaltimer stamps (nullptr = off)
 };
 
 // ------------------------------------------------------------------ matrix
@@ -249,6 +250,7 @@ struct spmat_s {
   spmat::DevBuf<int32_t> block_order;  // boundary row blocks first (fused off-diagonal tail)
   int64_t n_bblocks = 0;
   spmat::DevBuf<unsigned int> tail_ctr;
+  spmat::DevBuf<unsigned long long> trace;  // [cta][4] + [item][3] globaltimer stamps
   spmat::DevBuf<unsigned int> sched; // its block counter + finished-CTA counter
   // host staging for host x / y
   spmat::DevBuf<double> xstage, ystage;

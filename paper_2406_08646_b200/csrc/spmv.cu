@@ -261,6 +261,8 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     }
   }
   // ---------------- consumer warps
+  unsigned long long *trc = tail.trace ? tail.trace + 4 * (size_t)blockIdx.x : nullptr;
+  if (trc && tid == 0) trc[0] = gtimer();
   constexpr int RPP = kThreads / W;  // rows per pass
   constexpr int U = W == 1 ? 8 : 4;  // elements per lane in flight
   const int lane = tid % W;
@@ -269,8 +271,13 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
     const int4 h = st[s].hdr;
     const int r0 = h.x, r1 = h.y, p0 = h.z, p1 = h.w;
-    if (r0 == -1) break;
+    if (r0 == -1) {
+      if (trc && tid == 0) trc[2] = gtimer();
+      break;
+    }
     if (r0 == -2) {  // ---- off-diagonal work item: y[rows_o] += A_o lvec for kThreads rows
+      unsigned long long *itr = tail.trace ? tail.trace + 4 * (size_t)gridDim.x + 3 * (size_t)r1 : nullptr;
+      if (itr && tid == 0) itr[0] = gtimer();
       if (tid == 0) {  // every boundary block written and every sender's epoch data landed
         const unsigned target = (unsigned)(kConsumerWarps * tail.n_bblocks);
         const long long t0 = clock64();
@@ -285,6 +292,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
           spin_until_geq(tail.waits[w].my_ready, halo.epoch * (unsigned long long)tail.waits[w].nchunk, halo.err);
       }
       asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+      if (itr && tid == 0) itr[1] = gtimer();
       const int64_t q = (int64_t)r1 * kThreads + tid;
       if (q < tail.n_ro) {
         double sacc = 0.0;
@@ -294,6 +302,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
         y[r] = __dadd_rn(__ldcg(y + r), sacc);
       }
       asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+      if (itr && tid == 0) itr[2] = gtimer();
       if (tid == 0) {
         __threadfence();
         if (atomicAdd(tail.ctr + 1, 1u) == (unsigned)tail.n_items - 1) {  // last item: release lvec
@@ -346,6 +355,10 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
         atomicAdd(tail.ctr, 1u);
       }
     }
+  }
+  if (trc) {
+    asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+    if (tid == 0) trc[3] = gtimer();
   }
 }
 
@@ -547,6 +560,7 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   SP_CUDA(cudaMemsetAsync(A->sched.get(), 0, 8, st));
   SP_TRY(A->tail_ctr.alloc(2));
   SP_CUDA(cudaMemsetAsync(A->tail_ctr.get(), 0, 8, st));
+
   A->n_bblocks = 0;
   if (A->n_ro > 0) {  // claim order for the fused off-diagonal tail: boundary blocks first
     const int64_t nbk = A->n_rowblocks;
@@ -577,6 +591,13 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
     case 16: SP_TRY(tma_setup<16>(A)); break;
     default: SP_TRY(tma_setup<32>(A)); break;
   }
+  if (const char *tr = getenv("SPMAT_TRACE")) {  // device trace of the fused MatMult kernel
+    if (atoi(tr)) {
+      const int64_t nitems = (A->n_ro + kThreads - 1) / kThreads;
+      SP_TRY(A->trace.alloc(4 * (size_t)A->tma_grid + 3 * (size_t)nitems + 16));
+      SP_CUDA(cudaMemsetAsync(A->trace.get(), 0, A->trace.n * 8, st));
+    }
+  }
   SP_CUDA(cudaStreamSynchronize(st));
   return SPMAT_OK;
 }
@@ -595,7 +616,10 @@ static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, b
     // items go a quarter of the way through the sweep: by then the boundary blocks (claimed
     // first) are written and the halo puts (issued at kernel start) have landed
     t.n_items = (int)((A->n_ro + kThreads - 1) / kThreads);
-    t.t0 = (int)std::max<int64_t>(A->n_bblocks, A->n_rowblocks / 4);
+    const char *f = getenv("SPMAT_TAIL_AT");  // fraction of the sweep before the items
+    const double at = f ? atof(f) : 0.5;
+    t.t0 = (int)std::max<int64_t>(A->n_bblocks, (int64_t)(A->n_rowblocks * at));
+    t.trace = A->trace.get();
     t.rows = A->rows_o.get();
     t.rowptr = A->rowptr_o.get();
     t.col = A->col_o.get();
