@@ -196,8 +196,7 @@ struct SpmvHalo {                      // fused NVLink halo puts (comm warps)
   int *err;
 };
 struct SpmvTail {                      // fused off-diagonal SpMV-add (work items in the claim order)
-  const int32_t *order;                // row-block order, boundary blocks first
-  int n_bblocks, enabled;
+  int n_bblocks, enabled;              // boundary blocks are the first n_bblocks in claim order
   int t0, n_items;                     // claim indices [t0, t0+n_items) are off-diagonal items
   const int32_t *rows, *rowptr, *col;  // compressed off-diagonal block
   const double *val, *lvec;            // lvec: this epoch's ghost buffer
@@ -248,6 +247,7 @@ struct spmat_s {
   int64_t n_long = 0;
   int tma_grid = 0;                  // persistent grid of the bulk-copy SpMV
   spmat::DevBuf<int32_t> block_order;  // boundary row blocks first (fused off-diagonal tail)
+  spmat::DevBuf<int4> blocks4;         // (r0, r1, p0, p1) per row block in claim order
   int64_t n_bblocks = 0;
   spmat::DevBuf<unsigned int> tail_ctr;
   spmat::DevBuf<unsigned long long> trace;  // [cta][4] + [item][3] globaltimer stamps

@@ -108,6 +108,16 @@ __global__ void k_boundary_blocks(const int2 *__restrict__ rb, int64_t nb, const
   }
 }
 
+// blocks4[c] = (r0, r1, p0, p1) of the row block claimed c-th (order == nullptr: identity)
+__global__ void k_blocks4(const int2 *__restrict__ rb, const int32_t *__restrict__ order, int64_t nb,
+                          int4 *__restrict__ out) {
+  GRID_STRIDE(c, nb) {
+    const int b = order ? order[c] : (int)c;
+    const int2 A = rb[b], B = rb[b + 1];
+    out[c] = make_int4(A.x, B.x, A.y, B.y);
+  }
+}
+
 __global__ void k_rb_pairs(const int32_t *__restrict__ rows, const int32_t *__restrict__ rowptr,
                            int64_t n, int2 *__restrict__ out) {
   GRID_STRIDE(t, n) out[t] = make_int2(rows[t], rowptr[rows[t]]);
@@ -179,7 +189,7 @@ constexpr int kCtaThreads = kThreads + 64;  // + producer warp + comm warp
 
 template <int W>
 __global__ void __launch_bounds__(kCtaThreads, 3)
-    k_spmv_tma(const int2 *__restrict__ rb, int n_blocks, const int32_t *__restrict__ rowptr,
+    k_spmv_tma(const int4 *__restrict__ blocks, int n_blocks, const int32_t *__restrict__ rowptr,
                const int32_t *__restrict__ col, const double *__restrict__ val,
                const double *__restrict__ x, double *__restrict__ y,
                unsigned int *__restrict__ sched, const SpmvHalo halo, const SpmvTail tail) {
@@ -210,17 +220,14 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     // Claim index c maps to: an off-diagonal work item if c in [t0, t0+n_items), else a row
     // block (through the boundary-first order when the tail is fused).
     const int n_total = n_blocks + tail.n_items;
-    auto bounds = [&](int c, int2 &A, int2 &B) {
+    auto bounds = [&](int c, int4 &H) {  // one 16-byte load: (r0, r1, p0, p1) in claim order
       if (c >= tail.t0 && c < tail.t0 + tail.n_items) return;
-      const int k = c < tail.t0 ? c : c - tail.n_items;
-      const int blk = tail.order ? tail.order[k] : k;
-      A = rb[blk];
-      B = rb[blk + 1];
+      H = blocks[c < tail.t0 ? c : c - tail.n_items];
     };
     int b = (int)atomicAdd(sched, 1u);
     int b_next = (int)atomicAdd(sched, 1u);
-    int2 A = make_int2(0, 0), B = make_int2(0, 0);
-    if (b < n_total) bounds(b, A, B);
+    int4 H = make_int4(0, 0, 0, 0);
+    if (b < n_total) bounds(b, H);
     for (int it = 0;; ++it) {
       const int s = it % kStages;
       if (it >= kStages) mbar_wait(&empty[s], (uint32_t)(((it / kStages) - 1) & 1));
@@ -238,8 +245,8 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
         st[s].hdr = make_int4(-2, b - tail.t0, 0, 0);
         mbar_arrive_tx(&full[s], 0);
       } else {
-        const int r0 = A.x, r1 = B.x, p0 = A.y, p1 = B.y;
-        st[s].hdr = make_int4(r0, r1, p0, p1);
+        const int r0 = H.x, r1 = H.y, p0 = H.z, p1 = H.w;
+        st[s].hdr = H;
         st[s].flags.x = (tail.enabled && b < tail.n_bblocks) ? 1 : 0;
         if (p1 - p0 > kCap) {  // a single long row: k_spmv_long computes it
           mbar_arrive_tx(&full[s], 0);
@@ -256,7 +263,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
       b = b_next;
       if (b < n_total) {
         b_next = (int)atomicAdd(sched, 1u);
-        bounds(b, A, B);
+        bounds(b, H);
       }
     }
   }
@@ -583,6 +590,10 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
                                              A->block_order.get() + nbb, dn2.get() + 1, (int)nbk, st));
     A->n_bblocks = nbb;
   }
+  SP_TRY(A->blocks4.alloc(A->n_rowblocks));
+  k_blocks4<<<nblk(A->n_rowblocks), 256, 0, st>>>(A->rbp.get(), A->n_ro > 0 ? A->block_order.get() : nullptr,
+                                                  A->n_rowblocks, A->blocks4.get());
+  SP_LAUNCH();
   switch (A->lanes) {
     case 1: SP_TRY(tma_setup<1>(A)); break;
     case 2: SP_TRY(tma_setup<2>(A)); break;
@@ -610,7 +621,6 @@ static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, b
   SpmvTail t{};
   t.t0 = (int)A->n_rowblocks;  // no items: every claim index is a row block
   if (fuse_tail) {
-    t.order = A->block_order.get();
     t.n_bblocks = (int)A->n_bblocks;
     t.enabled = 1;
     // items go a quarter of the way through the sweep: by then the boundary blocks (claimed
@@ -631,7 +641,7 @@ static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, b
     t.ctr = A->tail_ctr.get();
   }
   k_spmv_tma<W><<<(unsigned)A->tma_grid, kCtaThreads, kTmaSmem, s>>>(
-      A->rbp.get(), (int)A->n_rowblocks, A->rowptr_d.get(), A->col_d.get(), A->val_d.get(), x, y,
+      A->blocks4.get(), (int)A->n_rowblocks, A->rowptr_d.get(), A->col_d.get(), A->val_d.get(), x, y,
       A->sched.get(), h, t);
 }
 

@@ -36,6 +36,15 @@ def main():
     for _ in range(a.reps):
         A.mult(x, y)
     torch.cuda.synchronize()
+    # per-call device time with events around every call (launch gaps show as e[k+1]-e[k] > d)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * a.reps)]
+    for k in range(a.reps):
+        ev[2 * k].record()
+        A.mult(x, y)
+        ev[2 * k + 1].record()
+    torch.cuda.synchronize()
+    dur = [ev[2 * k].elapsed_time(ev[2 * k + 1]) * 1e3 for k in range(a.reps)]
+    per = ev[0].elapsed_time(ev[-1]) * 1e3 / a.reps
     t = sp.spmat_trace_read(A.h)
     info = A.info()
     G = (t.size - 16) // 4  # upper bound; trailing item records follow the CTA records
@@ -46,7 +55,8 @@ def main():
     t0 = cta[:, 0].min()
     span = cta[:, 3].max() - t0
     term = cta[:, 2] - t0
-    msg = [f"rank {r}: kernel span {span / 1e3:.1f} us, CTAs {G}, mode {A.halo_mode()}",
+    msg = [f"rank {r}: kernel span {span / 1e3:.1f} us, CTAs {G}, mode {A.halo_mode()}; per call "
+           f"{per:.1f} us, call duration median {np.median(dur):.1f} us",
            f"  CTA start spread {np.ptp(cta[:, 0]) / 1e3:.1f} us; last-block done: min {term.min() / 1e3:.1f} "
            f"median {np.median(term) / 1e3:.1f} max {term.max() / 1e3:.1f} us; end max {(cta[:, 3].max() - t0) / 1e3:.1f}"]
     if nitems:
