@@ -8,8 +8,9 @@
 // the val, col and row-pointer slices of a block land in a shared-memory stage through
 // cp.async.bulk (the TMA engine's 1-D copy) tracked by an mbarrier, kStages blocks in
 // flight per CTA, so DRAM requests never wait for the arithmetic.  The arithmetic then walks
-// rows straight out of shared memory with W lanes per row (W from the mean row length, the
-// "row statistics" selector): with W = 1 (3D 7-point stencils) lane l owns row r0 + l, so a
+// rows straight out of shared memory with W lanes per row (W per row block from its row count
+// -- the row-statistics selector -- so every block is done in one pass): with W = 1 (3D
+// 7-point stencils) lane l owns row r0 + l, so a
 // warp's x gathers hit consecutive x entries (coalesced), and each row is summed left to
 // right from +0.0 with separately rounded products -- bit-identical to a serial CSR loop.
 //
@@ -187,7 +188,6 @@ __device__ __forceinline__ int ld_stream(const int *p) {
 constexpr int kConsumerWarps = kThreads / 32;
 constexpr int kCtaThreads = kThreads + 64;  // + producer warp + comm warp
 
-template <int W>
 __global__ void __launch_bounds__(kCtaThreads, 3)
     k_spmv_tma(const int4 *__restrict__ blocks, int n_blocks, const int32_t *__restrict__ rowptr,
                const int32_t *__restrict__ col, const double *__restrict__ val,
@@ -270,9 +270,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
   // ---------------- consumer warps
   unsigned long long *trc = tail.trace ? tail.trace + 4 * (size_t)blockIdx.x : nullptr;
   if (trc && tid == 0) trc[0] = gtimer();
-  constexpr int RPP = kThreads / W;  // rows per pass
-  constexpr int U = W == 1 ? 8 : 4;  // elements per lane in flight
-  const int lane = tid % W;
+  constexpr int U = 8;  // elements per lane in flight
   for (int it = 0;; ++it) {
     const int s = it % kStages;
     mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
@@ -328,7 +326,12 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
       const double *sv = st[s].val + (p0 & 1);  // sv[e - p0] = val[e]
       const int *sc = st[s].col + (p0 & 3);
       const int *rp = st[s].rp - (r0 & ~3);     // rp[r] = rowptr[r]
-      for (int r = r0 + tid / W; r < r1; r += RPP) {
+      // lanes per row, per block: the largest power of two that still covers every row of
+      // the block in one pass (W = 1 for stencil-like blocks: left-to-right row sums)
+      int W = 1;
+      while (W < 32 && (r1 - r0) * W * 2 <= kThreads) W <<= 1;
+      const int lane = tid & (W - 1);
+      for (int r = r0 + tid / W; r < r1; r += kThreads / W) {
         const int a = rp[r] - p0, z = rp[r + 1] - p0;
         double acc = 0.0;
         for (int e0 = a + lane; e0 < z; e0 += U * W) {
@@ -348,7 +351,6 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
         }
         if (W > 1) {
           const unsigned mask = __activemask();
-#pragma unroll
           for (int o = W >> 1; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(mask, acc, o, W));
         }
         if (lane == 0) y[r] = acc;
@@ -487,15 +489,14 @@ static int lanes_for(double mean) {  // W lanes per row from the mean row length
   return 32;
 }
 
-template <int W>
 static int tma_setup(spmat_s *A) {
   static bool attr_set = false;
   if (!attr_set) {
-    SP_CUDA(cudaFuncSetAttribute(k_spmv_tma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+    SP_CUDA(cudaFuncSetAttribute(k_spmv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
     attr_set = true;
   }
   int per_sm = 0;
-  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_tma<W>, kCtaThreads, kTmaSmem));
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_tma, kCtaThreads, kTmaSmem));
   // SPMAT_RESERVE_SMS leaves SMs free for concurrently running kernels (e.g. NCCL's)
   int reserve = 0;
   if (const char *e = getenv("SPMAT_RESERVE_SMS")) reserve = std::max(0, atoi(e));
@@ -594,14 +595,7 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   k_blocks4<<<nblk(A->n_rowblocks), 256, 0, st>>>(A->rbp.get(), A->n_ro > 0 ? A->block_order.get() : nullptr,
                                                   A->n_rowblocks, A->blocks4.get());
   SP_LAUNCH();
-  switch (A->lanes) {
-    case 1: SP_TRY(tma_setup<1>(A)); break;
-    case 2: SP_TRY(tma_setup<2>(A)); break;
-    case 4: SP_TRY(tma_setup<4>(A)); break;
-    case 8: SP_TRY(tma_setup<8>(A)); break;
-    case 16: SP_TRY(tma_setup<16>(A)); break;
-    default: SP_TRY(tma_setup<32>(A)); break;
-  }
+  SP_TRY(tma_setup(A));
   if (const char *tr = getenv("SPMAT_TRACE")) {  // device trace of the fused MatMult kernel
     if (atoi(tr)) {
       const int64_t nitems = (A->n_ro + kThreads - 1) / kThreads;
@@ -613,7 +607,6 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   return SPMAT_OK;
 }
 
-template <int W>
 static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put,
                        bool fuse_tail) {
   SpmvHalo h{A->halo_puts.get(), A->n_puts, fuse_put ? A->put_chunks_total : 0,
@@ -640,7 +633,7 @@ static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, b
     t.nwaits = A->n_waits;
     t.ctr = A->tail_ctr.get();
   }
-  k_spmv_tma<W><<<(unsigned)A->tma_grid, kCtaThreads, kTmaSmem, s>>>(
+  k_spmv_tma<<<(unsigned)A->tma_grid, kCtaThreads, kTmaSmem, s>>>(
       A->blocks4.get(), (int)A->n_rowblocks, A->rowptr_d.get(), A->col_d.get(), A->val_d.get(), x, y,
       A->sched.get(), h, t);
 }
@@ -664,14 +657,7 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_
     return SPMAT_OK;
   }
   if (A->kernel_id == KERNEL_TMA) {
-    switch (A->lanes) {
-      case 1: launch_tma<1>(A, x, y, s, fuse_put, fuse_tail); break;
-      case 2: launch_tma<2>(A, x, y, s, fuse_put, fuse_tail); break;
-      case 4: launch_tma<4>(A, x, y, s, fuse_put, fuse_tail); break;
-      case 8: launch_tma<8>(A, x, y, s, fuse_put, fuse_tail); break;
-      case 16: launch_tma<16>(A, x, y, s, fuse_put, fuse_tail); break;
-      default: launch_tma<32>(A, x, y, s, fuse_put, fuse_tail); break;
-    }
+    launch_tma(A, x, y, s, fuse_put, fuse_tail);
   } else {
     k_spmv_stream<<<(unsigned)A->n_rowblocks, kThreads, 0, s>>>(A->rbp.get(), A->rowptr_d.get(),
                                                                A->col_d.get(), A->val_d.get(), x, y);
