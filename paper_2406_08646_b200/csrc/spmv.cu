@@ -185,6 +185,41 @@ __device__ __forceinline__ int ld_stream(const int *p) {
 // and release the stage on its `empty` mbarrier (one arrive per consumer warp).  A stage
 // header with r0 = -1 ends the loop.  The last CTA to run out of blocks resets the counter
 // for the next launch (stream order makes that safe; CUDA-graph safe too).
+// W lanes per row: lane l of a row's group sums elements a+l, a+l+W, ... (8 in flight), then
+// a shuffle reduction; W = 1 is a plain left-to-right sum (the oracle's order)
+template <int W>
+__device__ __forceinline__ void rows_w(int r0, int r1, int p0, const int *__restrict__ rp,
+                                       const int *__restrict__ sc, const double *__restrict__ sv,
+                                       const double *__restrict__ x, double *__restrict__ y, int tid) {
+  constexpr int U = 8;
+  const int lane = tid & (W - 1);
+  for (int r = r0 + tid / W; r < r1; r += kThreads / W) {
+    const int a = rp[r] - p0, z = rp[r + 1] - p0;
+    double acc = 0.0;
+    for (int e0 = a + lane; e0 < z; e0 += U * W) {
+      int cc[U];
+      double vv[U], xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * W;
+        cc[u] = e < z ? sc[e] : 0;
+        vv[u] = e < z ? sv[e] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = __ldg(x + cc[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (e0 + u * W < z) acc = __dadd_rn(acc, __dmul_rn(vv[u], xv[u]));
+    }
+    if (W > 1) {
+      const unsigned mask = __activemask();
+#pragma unroll
+      for (int o = W >> 1; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(mask, acc, o, W));
+    }
+    if (lane == 0) y[r] = acc;
+  }
+}
+
 constexpr int kConsumerWarps = kThreads / 32;
 constexpr int kCtaThreads = kThreads + 64;  // + producer warp + comm warp
 
@@ -270,7 +305,6 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
   // ---------------- consumer warps
   unsigned long long *trc = tail.trace ? tail.trace + 4 * (size_t)blockIdx.x : nullptr;
   if (trc && tid == 0) trc[0] = gtimer();
-  constexpr int U = 8;  // elements per lane in flight
   for (int it = 0;; ++it) {
     const int s = it % kStages;
     mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
@@ -328,33 +362,13 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
       const int *rp = st[s].rp - (r0 & ~3);     // rp[r] = rowptr[r]
       // lanes per row, per block: the largest power of two that still covers every row of
       // the block in one pass (W = 1 for stencil-like blocks: left-to-right row sums)
-      int W = 1;
-      while (W < 32 && (r1 - r0) * W * 2 <= kThreads) W <<= 1;
-      const int lane = tid & (W - 1);
-      for (int r = r0 + tid / W; r < r1; r += kThreads / W) {
-        const int a = rp[r] - p0, z = rp[r + 1] - p0;
-        double acc = 0.0;
-        for (int e0 = a + lane; e0 < z; e0 += U * W) {
-          int cc[U];
-          double vv[U], xv[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int e = e0 + u * W;
-            cc[u] = e < z ? sc[e] : 0;
-            vv[u] = e < z ? sv[e] : 0.0;
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) xv[u] = __ldg(x + cc[u]);
-#pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (e0 + u * W < z) acc = __dadd_rn(acc, __dmul_rn(vv[u], xv[u]));
-        }
-        if (W > 1) {
-          const unsigned mask = __activemask();
-          for (int o = W >> 1; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(mask, acc, o, W));
-        }
-        if (lane == 0) y[r] = acc;
-      }
+      const int nrows = r1 - r0;
+      if (nrows * 2 > kThreads) rows_w<1>(r0, r1, p0, rp, sc, sv, x, y, tid);
+      else if (nrows * 4 > kThreads) rows_w<2>(r0, r1, p0, rp, sc, sv, x, y, tid);
+      else if (nrows * 8 > kThreads) rows_w<4>(r0, r1, p0, rp, sc, sv, x, y, tid);
+      else if (nrows * 16 > kThreads) rows_w<8>(r0, r1, p0, rp, sc, sv, x, y, tid);
+      else if (nrows * 32 > kThreads) rows_w<16>(r0, r1, p0, rp, sc, sv, x, y, tid);
+      else rows_w<32>(r0, r1, p0, rp, sc, sv, x, y, tid);
     }
     __syncwarp();
     if (lane32 == 0) {
