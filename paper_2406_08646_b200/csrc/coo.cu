@@ -253,6 +253,77 @@ __global__ void k_numeric_local(const uint32_t *__restrict__ jmap, const uint32_
   }
 }
 
+// Tiled variant (default): CTA c owns nonzeros [c*kNumTile, (c+1)*kNumTile); their
+// contributions [jmap[z0], jmap[z1]) are contiguous in perm, so the CTA first streams that
+// range -- perm coalesced, v[perm] gathered, kNumU loads in flight per thread -- into shared
+// memory, then one thread per nonzero sums its segment from shared memory in canonical order.
+// A tile whose range exceeds kNumCap falls back to the per-nonzero loop.
+constexpr int kNumTile = 1024, kNumCap = 4096, kNumThreads = 256, kNumU = 8;
+__global__ void __launch_bounds__(kNumThreads) k_numeric_tile(
+    const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm, const double *__restrict__ v,
+    uint64_t ncoo, int64_t nnz_d, int64_t nnz, double *__restrict__ val_d, double *__restrict__ val_o,
+    int mode) {
+  __shared__ double cv[kNumCap];
+  __shared__ unsigned char remote[kNumCap];
+  const int64_t z0 = (int64_t)blockIdx.x * kNumTile, z1 = min(nnz, z0 + kNumTile);
+  const uint32_t t0 = jmap[z0], t1 = jmap[z1];
+  const int n = (int)(t1 - t0);
+  const int tid = threadIdx.x;
+  if (n <= kNumCap) {
+    for (int base = 0; base < n; base += kNumThreads * kNumU) {
+      uint32_t p[kNumU];
+#pragma unroll
+      for (int u = 0; u < kNumU; ++u) {
+        const int e = base + u * kNumThreads + tid;
+        p[u] = e < n ? __ldg(perm + t0 + e) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < kNumU; ++u) {
+        const int e = base + u * kNumThreads + tid;
+        if (e < n) {  // received contributions are finished by k_numeric_mixed
+          cv[e] = p[u] < ncoo ? __ldg(v + p[u]) : 0.0;
+          remote[e] = p[u] < ncoo ? 0 : 1;
+        }
+      }
+    }
+    __syncthreads();
+    for (int64_t z = z0 + tid; z < z1; z += kNumThreads) {
+      const uint32_t a = jmap[z], b = jmap[z + 1];
+      double s = 0.0;
+      bool local = true;
+      for (uint32_t t = a; t < b; ++t) {
+        if (remote[t - t0]) {
+          local = false;
+          break;
+        }
+        s = __dadd_rn(s, cv[t - t0]);
+      }
+      if (local) {
+        double *dst = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
+        *dst = mode == SPMAT_INSERT ? __dadd_rn(0.0, s) : __dadd_rn(*dst, s);
+      }
+    }
+    return;
+  }
+  for (int64_t z = z0 + tid; z < z1; z += kNumThreads) {  // oversized tile: plain loop
+    const uint32_t a = jmap[z], b = jmap[z + 1];
+    double s = 0.0;
+    bool local = true;
+    for (uint32_t t = a; t < b; ++t) {
+      const uint32_t q = perm[t];
+      if (q >= ncoo) {
+        local = false;
+        break;
+      }
+      s = __dadd_rn(s, v[q]);
+    }
+    if (local) {
+      double *dst = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
+      *dst = mode == SPMAT_INSERT ? __dadd_rn(0.0, s) : __dadd_rn(*dst, s);
+    }
+  }
+}
+
 __global__ void k_numeric_mixed(const uint32_t *__restrict__ mixed, int64_t nmixed,
                                 const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm,
                                 const double *__restrict__ v, const double *__restrict__ recv,
@@ -679,8 +750,15 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
     SP_CUDA(cudaEventRecord(A->ev_recv_done, c->comm_stream));
   }
   if (nnz > 0) {
-    k_numeric_local<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
-                                              A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
+    const char *nk = getenv("SPMAT_NUMERIC_KERNEL");
+    if (nk && !strcmp(nk, "plain")) {
+      k_numeric_local<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
+                                                A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
+    } else {
+      k_numeric_tile<<<(unsigned)((nnz + kNumTile - 1) / kNumTile), kNumThreads, 0, s>>>(
+          A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo, A->nnz_d, nnz, A->val_d.get(),
+          A->val_o.get(), mode);
+    }
     SP_LAUNCH();
   }
   if (exchange) {

@@ -375,3 +375,20 @@ def test_kernel_variants(sp, comm, kernel, case, monkeypatch):
     O.set_values([vi])
     assert np.array_equal(canon(yd.cpu().numpy()), canon(O.mult(xi.numpy())))
     A.close()
+
+
+@pytest.mark.parametrize("numeric", ["tile", "plain"])
+def test_numeric_kernels(sp, comm, numeric, monkeypatch):
+    """Both COO numeric kernels give the oracle's values bit for bit (Z1 order)."""
+    monkeypatch.setenv("SPMAT_NUMERIC_KERNEL", numeric)
+    for M, i, j, v in [(9 ** 3, *synth.q1_coo(9, values="real")),
+                       (50, *synth.random_coo(50, 50, 3000, dup_frac=0.9, neg_frac=0.1, values="real"))]:
+        O = oracle.OracleMat(M, M, [M], [M], [i], [j])
+        O.set_values([v])
+        A = sp.Mat(comm, M, M, M, M, dev(i), dev(j))
+        A.set_values(dev(v))
+        assert np.array_equal(canon(A.export("val_d")), canon(O.export(0, "val_d")))
+        A.set_values(dev(v), sp.ADD)
+        O.set_values([v], oracle.ADD)
+        assert np.array_equal(canon(A.export("val_d")), canon(O.export(0, "val_d")))
+        A.close()
