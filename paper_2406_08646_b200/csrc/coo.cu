@@ -253,73 +253,61 @@ __global__ void k_numeric_local(const uint32_t *__restrict__ jmap, const uint32_
   }
 }
 
-// Tiled variant (default): CTA c owns nonzeros [c*kNumTile, (c+1)*kNumTile); their
-// contributions [jmap[z0], jmap[z1]) are contiguous in perm, so the CTA first streams that
-// range -- perm coalesced, v[perm] gathered, kNumU loads in flight per thread -- into shared
-// memory, then one thread per nonzero sums its segment from shared memory in canonical order.
-// A tile whose range exceeds kNumCap falls back to the per-nonzero loop.
-constexpr int kNumTile = 1024, kNumCap = 4096, kNumThreads = 256, kNumU = 8;
-__global__ void __launch_bounds__(kNumThreads) k_numeric_tile(
+// Default numeric kernel: each thread finishes kNumU nonzeros z = base + u*blockDim + tid
+// (coalesced across the warp), advancing all of them one contribution per round so every
+// level of the jmap -> perm -> v chain has kNumU loads in flight.  Each nonzero is still
+// summed in canonical order by one thread; a nonzero meeting a received contribution is left
+// for k_numeric_mixed.
+constexpr int kNumU = 4;
+__global__ void __launch_bounds__(256) k_numeric_ilp(
     const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm, const double *__restrict__ v,
     uint64_t ncoo, int64_t nnz_d, int64_t nnz, double *__restrict__ val_d, double *__restrict__ val_o,
     int mode) {
-  __shared__ double cv[kNumCap];
-  __shared__ unsigned char remote[kNumCap];
-  const int64_t z0 = (int64_t)blockIdx.x * kNumTile, z1 = min(nnz, z0 + kNumTile);
-  const uint32_t t0 = jmap[z0], t1 = jmap[z1];
-  const int n = (int)(t1 - t0);
-  const int tid = threadIdx.x;
-  if (n <= kNumCap) {
-    for (int base = 0; base < n; base += kNumThreads * kNumU) {
-      uint32_t p[kNumU];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * kNumU;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kNumU + threadIdx.x; base < nnz; base += stride) {
+    uint32_t a[kNumU], b[kNumU];
+    double s[kNumU];
+    bool ok[kNumU];
+#pragma unroll
+    for (int u = 0; u < kNumU; ++u) {
+      const int64_t z = base + (int64_t)u * blockDim.x;
+      a[u] = z < nnz ? __ldg(jmap + z) : 0u;
+      b[u] = z < nnz ? __ldg(jmap + z + 1) : 0u;
+      s[u] = 0.0;
+      ok[u] = z < nnz;
+    }
+    for (;;) {  // one contribution of every unfinished nonzero per round
+      uint32_t q[kNumU];
+      bool any = false;
 #pragma unroll
       for (int u = 0; u < kNumU; ++u) {
-        const int e = base + u * kNumThreads + tid;
-        p[u] = e < n ? __ldg(perm + t0 + e) : 0u;
+        const bool live = ok[u] && a[u] < b[u];
+        q[u] = live ? __ldg(perm + a[u]) : 0u;
+        any |= live;
+      }
+      if (!any) break;
+      double vv[kNumU];
+#pragma unroll
+      for (int u = 0; u < kNumU; ++u) {
+        const bool live = ok[u] && a[u] < b[u];
+        if (live && q[u] >= ncoo) ok[u] = false;  // received contribution: mixed nonzero
+        vv[u] = (live && q[u] < ncoo) ? __ldg(v + q[u]) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < kNumU; ++u) {
-        const int e = base + u * kNumThreads + tid;
-        if (e < n) {  // received contributions are finished by k_numeric_mixed
-          cv[e] = p[u] < ncoo ? __ldg(v + p[u]) : 0.0;
-          remote[e] = p[u] < ncoo ? 0 : 1;
+        if (ok[u] && a[u] < b[u]) {
+          s[u] = __dadd_rn(s[u], vv[u]);
+          ++a[u];
         }
       }
     }
-    __syncthreads();
-    for (int64_t z = z0 + tid; z < z1; z += kNumThreads) {
-      const uint32_t a = jmap[z], b = jmap[z + 1];
-      double s = 0.0;
-      bool local = true;
-      for (uint32_t t = a; t < b; ++t) {
-        if (remote[t - t0]) {
-          local = false;
-          break;
-        }
-        s = __dadd_rn(s, cv[t - t0]);
-      }
-      if (local) {
+#pragma unroll
+    for (int u = 0; u < kNumU; ++u) {
+      const int64_t z = base + (int64_t)u * blockDim.x;
+      if (ok[u]) {
         double *dst = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
-        *dst = mode == SPMAT_INSERT ? __dadd_rn(0.0, s) : __dadd_rn(*dst, s);
+        *dst = mode == SPMAT_INSERT ? __dadd_rn(0.0, s[u]) : __dadd_rn(*dst, s[u]);
       }
-    }
-    return;
-  }
-  for (int64_t z = z0 + tid; z < z1; z += kNumThreads) {  // oversized tile: plain loop
-    const uint32_t a = jmap[z], b = jmap[z + 1];
-    double s = 0.0;
-    bool local = true;
-    for (uint32_t t = a; t < b; ++t) {
-      const uint32_t q = perm[t];
-      if (q >= ncoo) {
-        local = false;
-        break;
-      }
-      s = __dadd_rn(s, v[q]);
-    }
-    if (local) {
-      double *dst = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
-      *dst = mode == SPMAT_INSERT ? __dadd_rn(0.0, s) : __dadd_rn(*dst, s);
     }
   }
 }
@@ -755,9 +743,10 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
       k_numeric_local<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
                                                 A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
     } else {
-      k_numeric_tile<<<(unsigned)((nnz + kNumTile - 1) / kNumTile), kNumThreads, 0, s>>>(
-          A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo, A->nnz_d, nnz, A->val_d.get(),
-          A->val_o.get(), mode);
+      const int64_t blocks = std::min<int64_t>((nnz + 256 * kNumU - 1) / (256 * kNumU),
+                                               (int64_t)A->comm->num_sms * 32);
+      k_numeric_ilp<<<(unsigned)blocks, 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
+                                                     A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
     }
     SP_LAUNCH();
   }

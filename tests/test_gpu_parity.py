@@ -377,7 +377,7 @@ def test_kernel_variants(sp, comm, kernel, case, monkeypatch):
     A.close()
 
 
-@pytest.mark.parametrize("numeric", ["tile", "plain"])
+@pytest.mark.parametrize("numeric", ["ilp", "plain"])
 def test_numeric_kernels(sp, comm, numeric, monkeypatch):
     """Both COO numeric kernels give the oracle's values bit for bit (Z1 order)."""
     monkeypatch.setenv("SPMAT_NUMERIC_KERNEL", numeric)
