@@ -738,8 +738,12 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
     SP_CUDA(cudaEventRecord(A->ev_recv_done, c->comm_stream));
   }
   if (nnz > 0) {
+    // ILP kernel when nonzeros have ~1 contribution (stencil COO); with many duplicates of
+    // varying count (element COO) one nonzero per thread keeps more threads busy
     const char *nk = getenv("SPMAT_NUMERIC_KERNEL");
-    if (nk && !strcmp(nk, "plain")) {
+    bool plain = (double)A->ncontrib > 1.5 * (double)nnz;
+    if (nk) plain = !strcmp(nk, "plain");
+    if (plain) {
       k_numeric_local<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
                                                 A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
     } else {
