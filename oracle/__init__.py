@@ -65,6 +65,7 @@ def lib():
             L.orc_export.restype = i64
             L.orc_destroy.argtypes = [p]
             L.orc_sf_bcast.argtypes = [ctypes.c_int, p, p, p, p, p, p, p, p, ctypes.c_int]
+            L.orc_sf_reduce.argtypes = [ctypes.c_int, p, p, p, p, p, p, p, p, ctypes.c_int]
             L.orc_sample_rows.argtypes = [i64, p, p, p, i64, p, p, p]
             L.orc_dense_coo.argtypes = [i64, i64, i64, p, p, p, p]
             _lib = L
@@ -197,6 +198,38 @@ def sf_bcast(nroots, leaves, rootdata, leafdata, op=REPLACE):
     if st != ORC_OK:
         raise ValueError(f"oracle sf_bcast failed: {st}")
     return [Lg[ldoff[p]:ldoff[p + 1]].copy() for p in range(P)]
+
+
+def sf_reduce(nroots, leaves, leafdata, rootdata, op=SUM):
+    """Graph-walk SF reduce (leaf -> root) over P simulated ranks; returns new rootdata.
+    leaves[p] = (ilocal or None, remote_rank, remote_offset)."""
+    P = len(nroots)
+    lv = [len(l[1]) for l in leaves]
+    lvoff = _np(np.concatenate([[0], np.cumsum(lv)]), np.int64)
+    il = None
+    if any(l[0] is not None for l in leaves):
+        il = _np(np.concatenate([_np(l[0] if l[0] is not None else np.arange(len(l[1])),
+                                     np.int64) for l in leaves]), np.int64)
+    rr = _np(np.concatenate([_np(l[1], np.int64) for l in leaves]), np.int64)
+    ro = _np(np.concatenate([_np(l[2], np.int64) for l in leaves]), np.int64)
+    ld = [_np(a, np.float64) for a in leafdata]
+    rd = [_np(a, np.float64).copy() for a in rootdata]
+    ldoff = _np(np.concatenate([[0], np.cumsum([a.size for a in ld])]), np.int64)
+    rdoff = _np(np.concatenate([[0], np.cumsum(nroots)]), np.int64)
+    L = _np(np.concatenate(ld) if ld else np.zeros(0), np.float64)
+    R = np.zeros(int(rdoff[-1]))
+    for p in range(P):
+        R[rdoff[p]:rdoff[p + 1]] = rd[p][:nroots[p]]
+    st = lib().orc_sf_reduce(P, _ptr(lvoff), _ptr(il) if il is not None else ctypes.c_void_p(0),
+                             _ptr(rr), _ptr(ro), _ptr(rdoff), _ptr(ldoff), _ptr(L), _ptr(R), int(op))
+    if st != ORC_OK:
+        raise ValueError(f"oracle sf_reduce failed: {st}")
+    out = []
+    for p in range(P):
+        a = rd[p].copy()
+        a[:nroots[p]] = R[rdoff[p]:rdoff[p + 1]]
+        out.append(a)
+    return out
 
 
 def sample_rows(coo_i, coo_j, coo_v, rows, x_global):

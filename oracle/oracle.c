@@ -484,6 +484,39 @@ int orc_sf_bcast(int P, const int64_t *lvoff, const int64_t *ilocal, const int64
 }
 
 /*
+ * orc_sf_reduce: brute-force walk of PetscSFReduce ("the latter reduces leaf
+ * values into roots"), same array conventions as orc_sf_bcast.  Contributions to a root are
+ * applied in ascending (source rank, leaf index) order (SPEC.md L139-141 reading):
+ *   op 1 SUM:     root = root + leaf, one contribution at a time in that order
+ *   op 0 REPLACE: root = the last contribution in that order
+ * Leaf index = ilocal(l).  Roots nobody references are untouched.
+ */
+int orc_sf_reduce(int P, const int64_t *lvoff, const int64_t *ilocal, const int64_t *rrank,
+                  const int64_t *roffset, const int64_t *rdoff, const int64_t *ldoff,
+                  const double *leafdata, double *rootdata, int op) {
+  for (int q = 0; q < P; ++q)        /* every root, in rank order */
+    for (int64_t r = 0; r < rdoff[q + 1] - rdoff[q]; ++r)
+      for (int p = 0; p < P; ++p) {  /* sources ascending */
+        /* leaves of p on root (q, r), ascending leaf index: selection by repeated minimum */
+        int64_t last = -1;
+        for (;;) {
+          int64_t best = -1, bestl = -1;
+          for (int64_t l = lvoff[p]; l < lvoff[p + 1]; ++l) {
+            if (rrank[l] != q || roffset[l] != r) continue;
+            int64_t li = ilocal ? ilocal[l] : l - lvoff[p];
+            if (li > last && (best < 0 || li < bestl)) { best = l; bestl = li; }
+          }
+          if (best < 0) break;
+          double c = leafdata[ldoff[p] + bestl];
+          double *root = &rootdata[rdoff[q] + r];
+          *root = op == 0 ? c : *root + c;
+          last = bestl;
+        }
+      }
+  return ORC_OK;
+}
+
+/*
  * orc_sample_rows: y_i for a sorted list of sampled rows straight from the COO definition
  * A_ij = sum_k v[k] over entries with i[k]=i, j[k]=j, i,j >= 0,
  * for full-size parity checks where assembling the whole matrix on the host is too slow.

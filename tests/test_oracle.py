@@ -461,3 +461,49 @@ def test_sample_rows_matches_full_p1():
     x = synth.x_vector(0, 125, "real").numpy()
     rows = np.arange(0, 125, 7)
     assert np.array_equal(oracle.sample_rows(i, j, v, rows, x), A.mult(x)[rows])
+
+
+def test_spec_sf_reduce_examples():
+    g = _parse_golden("spec_sf_examples.txt")
+    t = g["reduce_pingpong_sum"].split()
+    leaf = [float(v) for v in t[1:4]]
+    root0 = [float(v) for v in t[5:8]]
+    want = [float(v) for v in t[9:12]]
+    leaves = [(None, [], []), (None, [0, 0, 0], [0, 1, 2])]
+    out = oracle.sf_reduce([3, 0], leaves, [[], leaf], [root0, []], oracle.SUM)
+    assert out[0].tolist() == want
+    t = g["reduce_fanin"].split()
+    lv = [float(t[1]), float(t[2])]
+    for op, key in ((oracle.SUM, "sum"), (oracle.REPLACE, "replace")):
+        out = oracle.sf_reduce([1], [(None, [0, 0], [0, 0])], [lv], [[0.0]], op)
+        assert out[0].tolist() == [float(t[t.index(key) + 1])]
+
+
+def test_sf_reduce_random_vs_python_walk():
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        P = int(rng.integers(1, 5))
+        nroots = [int(rng.integers(0, 10)) for _ in range(P)]
+        owners = [q for q in range(P) if nroots[q] > 0]
+        leaves, leafdata, rootdata = [], [], []
+        for p in range(P):
+            nl = int(rng.integers(0, 12)) if owners else 0
+            space = nl + int(rng.integers(0, 3))
+            il = rng.permutation(space)[:nl] if nl else np.zeros(0, np.int64)
+            rr = rng.choice(owners, nl) if nl else np.zeros(0, np.int64)
+            ro = np.array([rng.integers(0, nroots[q]) for q in rr], dtype=np.int64)
+            leaves.append((il, rr, ro))
+            leafdata.append(rng.integers(-50, 50, space).astype(float))
+            rootdata.append(rng.integers(-50, 50, nroots[p]).astype(float))
+        for op in (oracle.REPLACE, oracle.SUM):
+            out = oracle.sf_reduce(nroots, leaves, leafdata, rootdata, op)
+            want = [r.copy() for r in rootdata]
+            # independent walk: contributions in ascending (source rank, leaf index)
+            for p in range(P):
+                il, rr, ro = leaves[p]
+                for l in np.argsort(il, kind="stable"):
+                    q, off = rr[l], ro[l]
+                    c = leafdata[p][il[l]]
+                    want[q][off] = c if op == oracle.REPLACE else want[q][off] + c
+            for q in range(P):
+                assert np.array_equal(out[q], want[q])
