@@ -97,6 +97,15 @@ int sf_create(spmat_comm_t comm, int64_t nroots, int64_t nleaves, const int64_t 
 int sf_bcast_begin(sf_t sf, const double *rootdata, double *leafdata, int op, void *stream);
 int sf_bcast_end(sf_t sf, const double *rootdata, double *leafdata, int op, void *stream);
 
+/* Split-phase reduce leaf -> root ("reduces leaf values into roots").  leafdata
+   and rootdata are DEVICE arrays.  Contributions to one root are applied in ascending
+   (source rank, leaf index) order (reading of SPEC.md L139-141): SUM adds them one at a time
+   to the root's value; REPLACE stores the last one.  Roots nobody references are untouched.
+   Same split-phase and stream rules as sf_bcast_*; begin must not be issued while another
+   operation of this SF is pending (SPMAT_ERR_STATE). */
+int sf_reduce_begin(sf_t sf, const double *leafdata, double *rootdata, int op, void *stream);
+int sf_reduce_end(sf_t sf, const double *leafdata, double *rootdata, int op, void *stream);
+
 /* info[0..7] = nroots, nleaves, n_send_neighbours, n_recv_neighbours, n_send_values,
    n_recv_values, n_self_edges, packed (1 if any pack or unpack kernel is needed) */
 int sf_get_info(sf_t sf, int64_t info[8]);

@@ -51,6 +51,7 @@ SF_EXPORT = dict(recv_ranks=0, recv_counts=1, leaf_idx=2, send_ranks=3, send_cou
 ABI_SYMBOLS = (
     "spmat_version", "spmat_last_error", "spmat_comm_unique_id", "spmat_comm_create",
     "spmat_comm_check", "spmat_comm_destroy", "sf_create", "sf_bcast_begin", "sf_bcast_end",
+    "sf_reduce_begin", "sf_reduce_end",
     "sf_get_info", "sf_export", "sf_destroy", "spmat_create_coo", "spmat_set_values_coo",
     "spmat_mult", "spmat_mult_part", "spmat_get_info", "spmat_export", "spmat_get_halo_sf",
     "spmat_profile", "spmat_profile_read", "spmat_check", "spmat_halo_mode", "spmat_trace_read",
@@ -88,6 +89,8 @@ def load(path: str = LIB_PATH):
         "sf_create": ([p, i64, i64, p, p, p, P(p)], i32),
         "sf_bcast_begin": ([p, p, p, i32, p], i32),
         "sf_bcast_end": ([p, p, p, i32, p], i32),
+        "sf_reduce_begin": ([p, p, p, i32, p], i32),
+        "sf_reduce_end": ([p, p, p, i32, p], i32),
         "sf_get_info": ([p, p], i32),
         "sf_export": ([p, i32, p, i64, P(i64)], i32),
         "sf_destroy": ([p], i32),
@@ -176,6 +179,16 @@ def sf_bcast_begin(sf_h, rootdata, leafdata, op=REPLACE, stream=None):
 def sf_bcast_end(sf_h, rootdata, leafdata, op=REPLACE, stream=None):
     _check(load().sf_bcast_end(sf_h, _ptr(rootdata), _ptr(leafdata), op, _stream(stream)),
            "sf_bcast_end")
+
+
+def sf_reduce_begin(sf_h, leafdata, rootdata, op=SUM, stream=None):
+    _check(load().sf_reduce_begin(sf_h, _ptr(leafdata), _ptr(rootdata), op, _stream(stream)),
+           "sf_reduce_begin")
+
+
+def sf_reduce_end(sf_h, leafdata, rootdata, op=SUM, stream=None):
+    _check(load().sf_reduce_end(sf_h, _ptr(leafdata), _ptr(rootdata), op, _stream(stream)),
+           "sf_reduce_end")
 
 
 def sf_get_info(sf_h) -> dict:
@@ -321,6 +334,12 @@ class StarForest:
 
     def bcast_end(self, root, leaf, op=REPLACE, stream=None):
         sf_bcast_end(self.h, root, leaf, op, stream)
+
+    def reduce_begin(self, leaf, root, op=SUM, stream=None):
+        sf_reduce_begin(self.h, leaf, root, op, stream)
+
+    def reduce_end(self, leaf, root, op=SUM, stream=None):
+        sf_reduce_end(self.h, leaf, root, op, stream)
 
     def info(self):
         return sf_get_info(self.h)

@@ -160,6 +160,12 @@ struct sf_s {
   const double *p_root = nullptr;
   double *p_leaf = nullptr;
   int p_op = -1;
+  int p_kind = 0;                        // pending op: 1 = bcast, 2 = reduce
+  // reduce (leaf -> root) plan: touched roots, their contributions in (source rank, leaf)
+  // order; code >= 0 -> received value redbuf[code], code < 0 -> own leaf self_leaf[-code-1]
+  int64_t n_touched = 0;
+  spmat::DevBuf<int64_t> d_red_roots, d_red_ptr, d_red_code;
+  spmat::DevBuf<double> d_redbuf;        // received leaf values, requester-major (soff layout)
 };
 
 namespace spmat {
@@ -170,6 +176,8 @@ int sf_begin(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t st
              cudaEvent_t *prof /* optional pair recorded on the comm stream */);
 int sf_end(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stream);
 void sf_free(sf_s *sf);
+int sf_reduce_begin_impl(sf_s *sf, const double *leaf, double *root, int op, cudaStream_t stream);
+int sf_reduce_end_impl(sf_s *sf, const double *leaf, double *root, int op, cudaStream_t stream);
 }  // namespace spmat
 
 // ------------------------------------------------------------------ device-initiated halo

@@ -229,6 +229,39 @@ int sf_build(spmat_comm_s *comm, int64_t nroots, int64_t nleaves, const int64_t 
     sf_free(sf);
     return s;
   }
+  // ---- reduce plan: every contribution (root, source rank, sequence) sorted; the sequence
+  // within one source follows that source's leaf order (its leaves are sorted by
+  // (owner, root offset, leaf index)), so a root sees ascending (source rank, leaf index)
+  {
+    struct Con { int64_t root, src, seq, code; };
+    std::vector<Con> cons;
+    cons.reserve(sf->nsend + self_root.size());
+    for (size_t a = 0; a < sf->snbr.size(); ++a)
+      for (int64_t t = 0; t < sf->scount[a]; ++t)
+        cons.push_back({sf->h_root_idx[sf->soff[a] + t], sf->snbr[a], t, sf->soff[a] + t});
+    for (size_t t = 0; t < self_root.size(); ++t)
+      cons.push_back({self_root[t], me, (int64_t)t, -(int64_t)t - 1});
+    std::sort(cons.begin(), cons.end(), [](const Con &x, const Con &y) {
+      if (x.root != y.root) return x.root < y.root;
+      if (x.src != y.src) return x.src < y.src;
+      return x.seq < y.seq;
+    });
+    std::vector<int64_t> roots, ptr(1, 0), code;
+    for (size_t t = 0; t < cons.size(); ++t) {
+      if (t == 0 || cons[t].root != cons[t - 1].root) {
+        if (t) ptr.push_back((int64_t)t);
+        roots.push_back(cons[t].root);
+      }
+      code.push_back(cons[t].code);
+    }
+    if (!cons.empty()) ptr.push_back((int64_t)cons.size());
+    sf->n_touched = (int64_t)roots.size();
+    if ((s = up(sf->d_red_roots, roots)) || (s = up(sf->d_red_ptr, ptr)) ||
+        (s = up(sf->d_red_code, code)) || (s = sf->d_redbuf.alloc(sf->nsend))) {
+      sf_free(sf);
+      return s;
+    }
+  }
   if (cudaEventCreateWithFlags(&sf->ev_begin, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&sf->ev_done, cudaEventDisableTiming) != cudaSuccess) {
     sf_free(sf);
@@ -238,9 +271,83 @@ int sf_build(spmat_comm_s *comm, int64_t nroots, int64_t nleaves, const int64_t 
   return SPMAT_OK;
 }
 
+// PetscSFReduce root side: one thread per touched root applies its contributions in
+// ascending (source rank, leaf index) order -- REPLACE keeps the last, SUM adds one at a time.
+__global__ void k_reduce_combine(const int64_t *__restrict__ roots, const int64_t *__restrict__ ptr,
+                                 const int64_t *__restrict__ code, int64_t n,
+                                 const double *__restrict__ redbuf, const double *__restrict__ leaf,
+                                 const int64_t *__restrict__ self_leaf, double *__restrict__ root,
+                                 int op) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = roots[t];
+    double s = root[r];
+    for (int64_t k = ptr[t]; k < ptr[t + 1]; ++k) {
+      const int64_t c = code[k];
+      const double v = c >= 0 ? redbuf[c] : leaf[self_leaf[-c - 1]];
+      s = op == SF_REPLACE ? v : __dadd_rn(s, v);
+    }
+    root[r] = s;
+  }
+}
+
+// leaf -> root: pack leaves per owner (unless contiguous), NCCL send to owners / receive from
+// requesters, combine on the owners -- all on the comm stream after the work on `stream`
+int sf_reduce_begin_impl(sf_s *sf, const double *leaf, double *root, int op, cudaStream_t stream) {
+  if (sf->pending) return fail(SPMAT_ERR_STATE, "sf_reduce_begin: an operation is already pending");
+  if (op != SF_REPLACE && op != SF_SUM) return fail(SPMAT_ERR_ARG, "sf_reduce: bad op %d", op);
+  spmat_comm_s *c = sf->comm;
+  cudaStream_t cs = c->comm_stream;
+  SP_CUDA(cudaEventRecord(sf->ev_begin, stream));
+  SP_CUDA(cudaStreamWaitEvent(cs, sf->ev_begin, 0));
+  const int T = 256;
+  if (sf->need_unpack_any && sf->nrecv > 0) {  // non-contiguous leaves: pack into d_recvbuf
+    k_gather<<<grid_for(sf->nrecv, T, c->num_sms), T, 0, cs>>>(leaf, sf->d_leaf_idx.get(),
+                                                              sf->d_recvbuf.get(), sf->nrecv);
+    SP_LAUNCH();
+  }
+  if (c->nranks > 1 && (!sf->rnbr.empty() || !sf->snbr.empty())) {
+    NcclApi *api = c->api;
+    SP_NCCL(api, api->GroupStart());
+    for (size_t a = 0; a < sf->snbr.size(); ++a)
+      SP_NCCL(api, api->Recv(sf->d_redbuf.get() + sf->soff[a], sf->scount[a], ncclFloat64,
+                             sf->snbr[a], c->nccl, cs));
+    for (size_t a = 0; a < sf->rnbr.size(); ++a) {
+      const double *src = sf->leaf_start[a] >= 0 ? leaf + sf->leaf_start[a]
+                                                 : sf->d_recvbuf.get() + sf->roff[a];
+      SP_NCCL(api, api->Send(src, sf->rcount[a], ncclFloat64, sf->rnbr[a], c->nccl, cs));
+    }
+    SP_NCCL(api, api->GroupEnd());
+  }
+  if (sf->n_touched > 0) {
+    k_reduce_combine<<<grid_for(sf->n_touched, T, c->num_sms), T, 0, cs>>>(
+        sf->d_red_roots.get(), sf->d_red_ptr.get(), sf->d_red_code.get(), sf->n_touched,
+        sf->d_redbuf.get(), leaf, sf->d_self_leaf.get(), root, op);
+    SP_LAUNCH();
+  }
+  SP_CUDA(cudaEventRecord(sf->ev_done, cs));
+  sf->pending = true;
+  sf->p_kind = 2;
+  sf->p_root = root;
+  sf->p_leaf = const_cast<double *>(leaf);
+  sf->p_op = op;
+  return SPMAT_OK;
+}
+
+int sf_reduce_end_impl(sf_s *sf, const double *leaf, double *root, int op, cudaStream_t stream) {
+  if (!sf->pending || sf->p_kind != 2)
+    return fail(SPMAT_ERR_STATE, "sf_reduce_end without sf_reduce_begin");
+  if (root != sf->p_root || leaf != sf->p_leaf || op != sf->p_op)
+    return fail(SPMAT_ERR_STATE, "sf_reduce_end: buffers or op differ from sf_reduce_begin");
+  SP_CUDA(cudaStreamWaitEvent(stream, sf->ev_done, 0));
+  sf->pending = false;
+  sf->p_kind = 0;
+  return SPMAT_OK;
+}
+
 int sf_begin(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stream,
              cudaEvent_t *prof) {
-  if (sf->pending) return fail(SPMAT_ERR_STATE, "sf_bcast_begin: a bcast is already pending");
+  if (sf->pending) return fail(SPMAT_ERR_STATE, "sf_bcast_begin: an operation is already pending");
   if (op != SF_REPLACE && op != SF_SUM) return fail(SPMAT_ERR_ARG, "sf_bcast: bad op %d", op);
   spmat_comm_s *c = sf->comm;
   cudaStream_t cs = c->comm_stream;
@@ -284,6 +391,7 @@ int sf_begin(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t st
   if (prof) SP_CUDA(cudaEventRecord(prof[1], cs));
   SP_CUDA(cudaEventRecord(sf->ev_done, cs));
   sf->pending = true;
+  sf->p_kind = 1;
   sf->p_root = root;
   sf->p_leaf = leaf;
   sf->p_op = op;
@@ -291,11 +399,12 @@ int sf_begin(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t st
 }
 
 int sf_end(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stream) {
-  if (!sf->pending) return fail(SPMAT_ERR_STATE, "sf_bcast_end without sf_bcast_begin");
+  if (!sf->pending || sf->p_kind != 1) return fail(SPMAT_ERR_STATE, "sf_bcast_end without sf_bcast_begin");
   if (root != sf->p_root || leaf != sf->p_leaf || op != sf->p_op)
     return fail(SPMAT_ERR_STATE, "sf_bcast_end: buffers or op differ from sf_bcast_begin");
   SP_CUDA(cudaStreamWaitEvent(stream, sf->ev_done, 0));
   sf->pending = false;
+  sf->p_kind = 0;
   return SPMAT_OK;
 }
 
@@ -352,6 +461,21 @@ int sf_bcast_end(sf_t sf, const double *rootdata, double *leafdata, int op, void
   if (!sf) return fail(SPMAT_ERR_ARG, "sf_bcast_end: null sf");
   DeviceGuard g(sf->comm->device);
   return sf_end(sf, rootdata, leafdata, op, (cudaStream_t)stream);
+}
+
+int sf_reduce_begin(sf_t sf, const double *leafdata, double *rootdata, int op, void *stream) {
+  if (!sf) return fail(SPMAT_ERR_ARG, "sf_reduce_begin: null sf");
+  if ((sf->nrecv > 0 || sf->nself > 0) && !leafdata)
+    return fail(SPMAT_ERR_ARG, "sf_reduce_begin: null leafdata");
+  if (sf->n_touched > 0 && !rootdata) return fail(SPMAT_ERR_ARG, "sf_reduce_begin: null rootdata");
+  DeviceGuard g(sf->comm->device);
+  return sf_reduce_begin_impl(sf, leafdata, rootdata, op, (cudaStream_t)stream);
+}
+
+int sf_reduce_end(sf_t sf, const double *leafdata, double *rootdata, int op, void *stream) {
+  if (!sf) return fail(SPMAT_ERR_ARG, "sf_reduce_end: null sf");
+  DeviceGuard g(sf->comm->device);
+  return sf_reduce_end_impl(sf, leafdata, rootdata, op, (cudaStream_t)stream);
 }
 
 int sf_get_info(sf_t sf, int64_t info[8]) {

@@ -220,6 +220,13 @@ def case_sf(c, seed):
         sf.bcast_begin(root, leaf, op)
         sf.bcast_end(root, leaf, op)
         assert np.array_equal(leaf.cpu().numpy(), want), f"sf seed {seed} op {op} rank {r}"
+        # reduce leaf -> root, (source rank, leaf index) order (oracle.sf_reduce)
+        want = oracle.sf_reduce(nroots, leaves, leafdata, rootdata, op)[r]
+        root = torch.from_numpy(rootdata[r]).cuda()
+        leaf = torch.from_numpy(leafdata[r]).cuda()
+        sf.reduce_begin(leaf, root, op)
+        sf.reduce_end(leaf, root, op)
+        assert np.array_equal(root.cpu().numpy(), want), f"sf reduce seed {seed} op {op} rank {r}"
     sf.close()
 
 

@@ -282,6 +282,14 @@ def test_sf_single_rank(sp, comm):
         sf.bcast_begin(rd, leaf, op)
         sf.bcast_end(rd, leaf, op)
         assert np.array_equal(leaf.cpu().numpy(), want)
+        # reduce leaf -> root in (rank, leaf index) order
+        wantr = oracle.sf_reduce([nroots], [(il, np.zeros(nleaves), ro)], [leaf0.numpy()],
+                                 [root.numpy()], op)[0]
+        rd = dev(root)
+        leaf = dev(leaf0)
+        sf.reduce_begin(leaf, rd, op)
+        sf.reduce_end(leaf, rd, op)
+        assert np.array_equal(rd.cpu().numpy(), wantr)
     sf.close()
     with pytest.raises(sp.SpmatError):
         sp.StarForest(comm, 3, None, [0], [3])  # offset >= nroots
