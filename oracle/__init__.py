@@ -67,6 +67,7 @@ def lib():
             L.orc_sf_bcast.argtypes = [ctypes.c_int, p, p, p, p, p, p, p, p, ctypes.c_int]
             L.orc_sf_reduce.argtypes = [ctypes.c_int, p, p, p, p, p, p, p, p, ctypes.c_int]
             L.orc_sample_rows.argtypes = [i64, p, p, p, i64, p, p, p]
+            L.orc_cg.argtypes = [p, p, p, ctypes.c_int, p]
             L.orc_dense_coo.argtypes = [i64, i64, i64, p, p, p, p]
             _lib = L
     return _lib
@@ -135,6 +136,16 @@ class OracleMat:
         if st != ORC_OK:
             raise ValueError(f"oracle mult failed: {st}")
         return y
+
+    def cg(self, b_global, x0_global, maxit):
+        """Unpreconditioned CG (oracle.c orc_cg); returns (x, rr_hist)."""
+        b = _np(b_global, np.float64)
+        x = _np(x0_global, np.float64).copy()
+        hist = np.zeros(maxit + 1)
+        st = lib().orc_cg(self._h, _ptr(b), _ptr(x), int(maxit), _ptr(hist))
+        if st != ORC_OK:
+            raise ValueError(f"oracle cg failed: {st}")
+        return x, hist
 
     def info(self, r, key):
         return int(lib().orc_info(self._h, r, INFO[key]))

@@ -594,3 +594,70 @@ int orc_dense_coo(int64_t M, int64_t N, int64_t ncoo, const int64_t *gi, const i
   }
   return ORC_OK;
 }
+
+/* dot product, left to right from +0.0 (VecDot) */
+static double orc_dot(int64_t n, const double *a, const double *b) {
+  double s = +0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double p = a[i] * b[i];
+    s = s + p;
+  }
+  return s;
+}
+
+/*
+ * orc_cg: unpreconditioned conjugate gradients, the MatMult consumer of the paper's
+ * CG/CGAsync experiment.  The paper fixes the structure -- MatMult, vector dot
+ * products and AXPYs per iteration, a user-given maximum iteration count and no convergence
+ * test inside the loop -- and leaves the iteration itself to the textbook
+ * (Hestenes & Stiefel 1952), written out here step by step:
+ *   r = b - A x;  p = r;  rr = r.r
+ *   repeat maxit times:  q = A p;  alpha = rr / p.q;  x = x + alpha p;  r = r - alpha q;
+ *                        rrn = r.r;  beta = rrn / rr;  p = r + beta p;  rr = rrn
+ * A x uses orc_mult (the distributed MatMult of the simulated ranks).  rr_hist[k] = r_k.r_k
+ * for k = 0..maxit.  If p.q or rr becomes exactly 0 the iteration stops (x, r unchanged) and
+ * the remaining history repeats the last rr.  Requires a square matrix (M == N).
+ */
+int orc_cg(const orc_sys *S, const double *b, double *x, int maxit, double *rr_hist) {
+  if (!S || S->M != S->N || maxit < 0) return ORC_ERR_ARG;
+  const int64_t n = S->M;
+  double *r = (double *)xcalloc(n, sizeof(double));
+  double *p = (double *)xcalloc(n, sizeof(double));
+  double *q = (double *)xcalloc(n, sizeof(double));
+  int st = orc_mult(S, x, q);
+  if (st != ORC_OK) { free(r); free(p); free(q); return st; }
+  for (int64_t i = 0; i < n; ++i) {
+    r[i] = b[i] - q[i];
+    p[i] = r[i];
+  }
+  double rr = orc_dot(n, r, r);
+  if (rr_hist) rr_hist[0] = rr;
+  int stopped = 0;
+  for (int k = 0; k < maxit; ++k) {
+    if (!stopped) {
+      orc_mult(S, p, q);
+      double pq = orc_dot(n, p, q);
+      if (pq == 0.0 || rr == 0.0) {
+        stopped = 1;
+      } else {
+        double alpha = rr / pq;
+        for (int64_t i = 0; i < n; ++i) {
+          double t = alpha * p[i];
+          x[i] = x[i] + t;
+          double u = alpha * q[i];
+          r[i] = r[i] - u;
+        }
+        double rrn = orc_dot(n, r, r);
+        double beta = rrn / rr;
+        for (int64_t i = 0; i < n; ++i) {
+          double t = beta * p[i];
+          p[i] = r[i] + t;
+        }
+        rr = rrn;
+      }
+    }
+    if (rr_hist) rr_hist[k + 1] = rr;
+  }
+  free(r); free(p); free(q);
+  return ORC_OK;
+}

@@ -507,3 +507,70 @@ def test_sf_reduce_random_vs_python_walk():
                     want[q][off] = c if op == oracle.REPLACE else want[q][off] + c
             for q in range(P):
                 assert np.array_equal(out[q], want[q])
+
+
+# ---------------------------------------------------------------- CG (NEXT #1) pins
+def _spd_system(n=5, values="int", P=1):
+    shape = (n, n)
+    M = n * n
+    A, *_ = build_stencil(shape, 5, P=P, values=values)
+    return A, M
+
+
+def test_cg_solves_spd_system():
+    """After enough iterations CG's iterate solves A x = b (numpy.linalg.solve, independent)."""
+    A, M = _spd_system(6)
+    D = A.dense()
+    b = synth.x_vector(0, M, "real", seed=3).numpy()
+    x, hist = A.cg(b, np.zeros(M), 60)
+    xs = np.linalg.solve(D, b)
+    assert np.max(np.abs(x - xs)) <= 1e-10 * np.max(np.abs(xs))
+    assert hist[-1] <= 1e-20 * hist[0]
+
+
+def test_cg_first_step_closed_form():
+    """x1 = x0 + (r0.r0 / r0.A r0) r0 with r0 = b - A x0, computed with numpy's dense matrix."""
+    A, M = _spd_system(5)
+    D = A.dense()
+    b = synth.x_vector(0, M, "real", seed=4).numpy()
+    x0 = synth.x_vector(0, M, "real", seed=5).numpy()
+    r0 = b - D @ x0
+    alpha = (r0 @ r0) / (r0 @ (D @ r0))
+    x1, hist = A.cg(b, x0, 1)
+    assert np.max(np.abs(x1 - (x0 + alpha * r0))) <= 1e-13 * np.max(np.abs(x1))
+    assert abs(hist[0] - r0 @ r0) <= 1e-13 * (r0 @ r0)
+
+
+def test_cg_energy_error_monotone():
+    """||x - x_k||_A is non-increasing along CG iterations (textbook property)."""
+    A, M = _spd_system(7)
+    D = A.dense()
+    b = synth.x_vector(0, M, "real", seed=6).numpy()
+    xs = np.linalg.solve(D, b)
+    prev = None
+    for k in range(0, 25, 3):
+        x, _ = A.cg(b, np.zeros(M), k)
+        e = x - xs
+        en = e @ (D @ e)
+        if prev is not None:
+            assert en <= prev * (1 + 1e-12)
+        prev = en
+
+
+def test_cg_partition_independent():
+    """CG on the same global matrix simulated on 1 and 3 ranks: only the diag/off-diagonal
+    split of MatMult's row sums differs (O5), so iterates agree to rounding."""
+    A1, M = _spd_system(6, P=1)
+    A3, _ = _spd_system(6, P=3)
+    b = synth.x_vector(0, M, "int", seed=7).numpy()
+    x1, h1 = A1.cg(b, np.zeros(M), 12)
+    x3, h3 = A3.cg(b, np.zeros(M), 12)
+    assert np.max(np.abs(x1 - x3)) <= 1e-12 * np.max(np.abs(x1))
+    assert np.max(np.abs(h1 - h3) / h1) <= 1e-10
+    assert h1[0] == h3[0]  # r0 = b - A*0 = b exactly
+
+
+def test_cg_zero_rhs_stops():
+    A, M = _spd_system(4)
+    x, hist = A.cg(np.zeros(M), np.zeros(M), 5)
+    assert np.all(x == 0) and np.all(hist == 0)
