@@ -184,6 +184,23 @@ int spmat_get_halo_sf(spmat_t A, sf_t *borrowed);
 int spmat_profile(spmat_t A, int enable);
 int spmat_profile_read(spmat_t A, double ms[4], int64_t n[4]);
 
+/* ------------------------------------------------------ Krylov (CGAsync) --- */
+
+/* VecDotAsync: *result (DEVICE scalar) = sum over all ranks of a.b, a and b
+   DEVICE arrays of m_local doubles in this matrix's row layout.  Enqueue-only, collective.
+   Deterministic: fixed per-rank reduction tree, ranks summed in rank order through a scalar
+   board in IPC-mapped device memory (NVLink); identical result on every rank. */
+int spmat_vec_dot(spmat_t A, const double *a, const double *b, double *result, void *stream);
+
+/* Unpreconditioned conjugate gradients for a square A, maxit iterations, all scalars on the
+   device and no host synchronisation (CGAsync; no convergence test inside the
+   loop).  Per iteration: q = A p (spmat_mult), alpha = rr / p.q, x += alpha p,
+   r -= alpha q, rr' = r.r, beta = rr'/rr, p = r + beta p.  b (in), x (in: initial guess,
+   out: iterate) are DEVICE arrays of m_local doubles; rr_hist (DEVICE, maxit+1 doubles, or
+   NULL) receives r_k.r_k.  If p.q or rr becomes 0 the iterate stops changing.
+   Enqueue-only, collective; workspace is allocated on first use. */
+int spmat_cg(spmat_t A, const double *b, double *x, int maxit, double *rr_hist, void *stream);
+
 /* Synchronise the device and report asynchronous failures of this matrix's work: CUDA
    errors, NCCL async errors, and a device-initiated halo whose peer never answered. */
 int spmat_check(spmat_t A);

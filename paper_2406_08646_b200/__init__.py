@@ -55,6 +55,7 @@ ABI_SYMBOLS = (
     "sf_get_info", "sf_export", "sf_destroy", "spmat_create_coo", "spmat_set_values_coo",
     "spmat_mult", "spmat_mult_part", "spmat_get_info", "spmat_export", "spmat_get_halo_sf",
     "spmat_profile", "spmat_profile_read", "spmat_check", "spmat_halo_mode", "spmat_trace_read",
+    "spmat_vec_dot", "spmat_cg",
     "spmat_destroy")
 
 
@@ -106,6 +107,8 @@ def load(path: str = LIB_PATH):
         "spmat_check": ([p], i32),
         "spmat_halo_mode": ([p], i32),
         "spmat_trace_read": ([p, p, i64, P(i64)], i32),
+        "spmat_vec_dot": ([p, p, p, p, p], i32),
+        "spmat_cg": ([p, p, p, i32, p, p], i32),
         "spmat_destroy": ([p], i32),
     }
     for name, (args, res) in sig.items():
@@ -280,6 +283,16 @@ def spmat_trace_read(A_h) -> np.ndarray:
     return out
 
 
+def spmat_vec_dot(A_h, a, b, result, stream=None):
+    _check(load().spmat_vec_dot(A_h, _ptr(a), _ptr(b), _ptr(result), _stream(stream)),
+           "spmat_vec_dot")
+
+
+def spmat_cg(A_h, b, x, maxit, rr_hist=None, stream=None):
+    _check(load().spmat_cg(A_h, _ptr(b), _ptr(x), int(maxit), _ptr(rr_hist), _stream(stream)),
+           "spmat_cg")
+
+
 def spmat_destroy(A_h):
     _check(load().spmat_destroy(A_h), "spmat_destroy")
 
@@ -387,6 +400,12 @@ class Mat:
 
     def check(self):
         spmat_check(self.h)
+
+    def dot(self, a, b, result, stream=None):
+        spmat_vec_dot(self.h, a, b, result, stream)
+
+    def cg(self, b, x, maxit, rr_hist=None, stream=None):
+        spmat_cg(self.h, b, x, maxit, rr_hist, stream)
 
     def halo_mode(self):
         return spmat_halo_mode(self.h)

@@ -189,6 +189,12 @@ int spmat_comm_create(const unsigned char *id, int nranks, int rank, int device,
       delete c;
       return fail(SPMAT_ERR_NCCL, "ncclCommInitRank: %s", msg);
     }
+    int bs = board_setup(c);
+    if (bs != SPMAT_OK) {
+      c->api->CommDestroy(c->nccl);
+      delete c;
+      return bs;
+    }
   }
   *out = c;
   return SPMAT_OK;
@@ -216,6 +222,7 @@ int spmat_comm_destroy(spmat_comm_t c) {
   {
     DeviceGuard g(c->device);
     if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
+    board_release(c);
     if (c->nccl) c->api->CommDestroy(c->nccl);
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->setup_stream) cudaStreamDestroy(c->setup_stream);

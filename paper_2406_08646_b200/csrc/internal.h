@@ -123,7 +123,22 @@ struct Comm {
   int exchange_dev(const void *d_send, const int64_t *soff, const int64_t *scount,
                    void *d_recv, const int64_t *roff, const int64_t *rcount,
                    size_t elem_bytes, cudaStream_t stream);
+
+  // Scalar board (krylov.cu): every rank's small device array, mapped into every other rank
+  // through CUDA IPC, for device-side all-reductions of a few scalars over NVLink.
+  // val[parity][src][kBoardWidth] doubles, flag[parity][src] epochs.
+  static constexpr int kBoardWidth = 4;
+  bool board_ok = false;
+  DevBuf<double> board_val;
+  DevBuf<unsigned long long> board_flag;
+  std::vector<void *> board_peer_mem;               // opened IPC mappings (to close)
+  DevBuf<double *> d_peer_val;                      // per rank: its val array (self included)
+  DevBuf<unsigned long long *> d_peer_flag;
+  DevBuf<int> board_err;
+  int64_t board_epoch = 0;
 };
+int board_setup(Comm *c);      // collective; leaves board_ok false when IPC is unavailable
+void board_release(Comm *c);
 
 }  // namespace spmat
 
@@ -279,6 +294,8 @@ struct spmat_s {
   int n_puts = 0, n_waits = 0, put_chunks_total = 0;
   int64_t epoch = 0;
   int64_t lvec_stride = 0;          // peer mode: lvec holds two epochs' ghost buffers
+  // CG / dot workspace (krylov.cu), allocated on first use
+  spmat::DevBuf<double> cg_r, cg_p, cg_q, cg_partial, cg_scalars, cg_reduced;
 };
 
 namespace spmat {

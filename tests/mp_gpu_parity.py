@@ -230,6 +230,46 @@ def case_sf(c, seed):
     sf.close()
 
 
+def case_cg(c):
+    """CGAsync analogue across ranks: iterate vs the oracle's P-rank CG; the residual history
+    (device scalars from the scalar board) is bit-identical on every rank."""
+    P, r = c.P, c.r
+    shape = (10, 9, 4 * P)
+    M = int(np.prod(shape))
+    sizes = synth.slab_sizes(shape, P)
+    off = synth.offsets_from_sizes(sizes)
+    coo = [synth.stencil_coo(shape, 7, rows=(off[q], off[q + 1]), values="int") for q in range(P)]
+    O = oracle.OracleMat(M, M, sizes, sizes, [t[0] for t in coo], [t[1] for t in coo])
+    O.set_values([t[2] for t in coo])
+    i, j, v = coo[r]
+    A = sp.Mat(c.comm, sizes[r], sizes[r], M, M, i.cuda(), j.cuda())
+    A.set_values(v.cuda())
+    rhs = synth.x_vector(0, M, "real", seed=9).numpy()
+    b = torch.from_numpy(np.ascontiguousarray(rhs[off[r]:off[r + 1]])).cuda()
+    iters = 25
+    x = torch.zeros(sizes[r], dtype=torch.float64, device="cuda")
+    hist = torch.zeros(iters + 1, dtype=torch.float64, device="cuda")
+    A.cg(b, x, iters, hist)
+    xo, ho = O.cg(rhs, np.zeros(M), iters)
+    assert rel_err(x.cpu().numpy(), xo[off[r]:off[r + 1]]) <= 1e-10
+    h = hist.cpu()
+    allh = [torch.zeros_like(h) for _ in range(P)]
+    dist.all_gather_object(allh, h)
+    for q in range(P):
+        assert torch.equal(allh[q], h), "residual history differs between ranks"
+    assert np.max(np.abs(h.numpy() - ho) / ho[0]) <= 1e-10
+    # dot product of integer vectors: exact
+    a = synth.x_vector(off[r], off[r + 1], "int", seed=4).cuda()
+    bb = synth.x_vector(off[r], off[r + 1], "int", seed=5).cuda()
+    res = torch.zeros(1, dtype=torch.float64, device="cuda")
+    A.dot(a, bb, res)
+    ga = synth.x_vector(0, M, "int", seed=4).numpy()
+    gb = synth.x_vector(0, M, "int", seed=5).numpy()
+    assert res.item() == float(np.dot(ga, gb))
+    A.check()
+    A.close()
+
+
 def case_errors(c):
     P, r = c.P, c.r
     # only the last rank has an out-of-range index: every rank must report it
@@ -260,6 +300,7 @@ def main():
              ("elasticity", lambda: case_elasticity(c))]
     cases += [(f"random{s}", (lambda s=s: case_random(c, s))) for s in range(6)]
     cases += [(f"sf{s}", (lambda s=s: case_sf(c, s))) for s in range(6)]
+    cases += [("cg", lambda: case_cg(c))]
     cases += [("errors", lambda: case_errors(c))]
     for name, fn in cases:
         try:

@@ -400,3 +400,39 @@ def test_numeric_kernels(sp, comm, numeric, monkeypatch):
         O.set_values([v], oracle.ADD)
         assert np.array_equal(canon(A.export("val_d")), canon(O.export(0, "val_d")))
         A.close()
+
+
+def test_vec_dot_and_cg_single_rank(sp, comm):
+    """VecDotAsync and CGAsync analogues vs the oracle."""
+    n = 24
+    M = n * n
+    i, j, v = synth.stencil_coo((n, n), 5, values="int")
+    A = sp.Mat(comm, M, M, M, M, dev(i), dev(j))
+    A.set_values(dev(v))
+    a = synth.x_vector(0, M, "int", seed=1)
+    b = synth.x_vector(0, M, "int", seed=2)
+    res = torch.zeros(1, dtype=torch.float64, device="cuda")
+    A.dot(dev(a), dev(b), res)
+    assert res.item() == float(np.dot(a.numpy(), b.numpy()))  # integer products: exact
+    O = oracle.OracleMat(M, M, [M], [M], [i], [j])
+    O.set_values([v])
+    rhs = synth.x_vector(0, M, "real", seed=3)
+    for iters in (1, 5, 40):
+        x = torch.zeros(M, dtype=torch.float64, device="cuda")
+        hist = torch.zeros(iters + 1, dtype=torch.float64, device="cuda")
+        A.cg(dev(rhs), x, iters, hist)
+        xo, ho = O.cg(rhs.numpy(), np.zeros(M), iters)
+        assert rel_err(x.cpu().numpy(), xo) <= 1e-10
+        assert np.max(np.abs(hist.cpu().numpy() - ho) / ho[0]) <= 1e-10
+    # deterministic: the same call twice is bit-identical
+    x1 = torch.zeros(M, dtype=torch.float64, device="cuda")
+    x2 = torch.zeros(M, dtype=torch.float64, device="cuda")
+    A.cg(dev(rhs), x1, 30)
+    A.cg(dev(rhs), x2, 30)
+    assert torch.equal(x1, x2)
+    # converged: the GPU iterate solves the system (numpy, independent)
+    xs = np.linalg.solve(O.dense(), rhs.numpy())
+    x = torch.zeros(M, dtype=torch.float64, device="cuda")
+    A.cg(dev(rhs), x, 200)
+    assert rel_err(x.cpu().numpy(), xs) <= 1e-9
+    A.close()
