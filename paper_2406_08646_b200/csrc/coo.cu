@@ -903,6 +903,9 @@ int spmat_destroy(spmat_t A) {
     cudaDeviceSynchronize();
     halo_peer_release(A);
     if (A->halo) sf_free(A->halo);
+    for (cudaEvent_t e : A->pipe_ev) cudaEventDestroy(e);
+    if (A->pipe_in) cudaStreamDestroy(A->pipe_in);
+    if (A->pipe_out) cudaStreamDestroy(A->pipe_out);
     if (A->ev_send_ready) cudaEventDestroy(A->ev_send_ready);
     if (A->ev_recv_done) cudaEventDestroy(A->ev_recv_done);
     for (auto &v : A->prof_ev)

@@ -294,6 +294,11 @@ struct spmat_s {
   int n_puts = 0, n_waits = 0, put_chunks_total = 0;
   int64_t epoch = 0;
   int64_t lvec_stride = 0;          // peer mode: lvec holds two epochs' ghost buffers
+  // host-buffer MatMult pipeline (mult.cu / spmv.cu), built on first use
+  int pipe_chunks = 0;
+  std::vector<int64_t> pipe_block, pipe_row, pipe_xneed;  // claim range, row range, last x row
+  cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;                        // 2 * chunks + 2
   // CG / dot workspace (krylov.cu), allocated on first use
   spmat::DevBuf<double> cg_r, cg_p, cg_q, cg_partial, cg_scalars, cg_reduced;
 };
@@ -305,6 +310,9 @@ int spmv_prepare(spmat_s *A, cudaStream_t stream);  // row blocks + kernel choic
 int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream, bool fuse_put = false,
               bool fuse_tail = false);
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
+// host-buffer pipeline (single rank): row chunks of the diagonal SpMV
+int spmv_pipe_prepare(spmat_s *A, int chunks);  // chunk rows + the x columns each chunk reads
+int spmv_diag_chunk(spmat_s *A, const double *x, double *y, int k, cudaStream_t s);
 int halo_peer_setup(spmat_s *A);                  // collective; leaves A->peer false on NCCL
 void halo_peer_release(spmat_s *A);
 int halo_peer_put(spmat_s *A, const double *x, cudaStream_t s);  // standalone put kernel

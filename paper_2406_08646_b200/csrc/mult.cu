@@ -4,6 +4,10 @@
 // The halo exchange is issued first on the high-priority comm stream (NCCL), the diagonal
 // SpMV runs on the caller's stream meanwhile, and the off-diagonal SpMV-add waits on the
 // halo event on the device: the host never blocks (contrast the MPI path of P:492-509).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
 #include "internal.h"
 
 namespace spmat {
@@ -77,6 +81,59 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
   return SPMAT_OK;
 }
 
+// Host x and y on one rank: copy x in row chunks on one stream, run the SpMV chunk k as soon
+// as every x row it reads has arrived, and copy y chunk k back on a third stream -- PCIe is
+// full duplex, so the x upload, the SpMV and the y download overlap chunk by chunk.
+static bool pipeline_ok(spmat_s *A) {
+  const char *e = getenv("SPMAT_HOST_PIPELINE");
+  if (e && !strcmp(e, "0")) return false;
+  return A->comm->nranks == 1 && A->kernel_id == 3 && A->n_long == 0 && A->m == A->n &&
+         A->m >= (1 << 20) && A->n_rowblocks >= 64;
+}
+
+static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStream_t s) {
+  const int C = 8;
+  SP_TRY(spmv_pipe_prepare(A, C));
+  const int nc = A->pipe_chunks;
+  if (!A->pipe_in) {
+    SP_CUDA(cudaStreamCreateWithFlags(&A->pipe_in, cudaStreamNonBlocking));
+    SP_CUDA(cudaStreamCreateWithFlags(&A->pipe_out, cudaStreamNonBlocking));
+  }
+  while (A->pipe_ev.size() < (size_t)(2 * nc + 2)) {
+    cudaEvent_t e;
+    SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    A->pipe_ev.push_back(e);
+  }
+  if (A->xstage.n < (size_t)A->n) SP_TRY(A->xstage.alloc(A->n));
+  if (A->ystage.n < (size_t)A->m) SP_TRY(A->ystage.alloc(A->m));
+  double *dx = A->xstage.get(), *dy = A->ystage.get();
+  cudaEvent_t *ev = A->pipe_ev.data();  // [0,nc) x chunk in, [nc,2nc) y chunk done, 2nc start, 2nc+1 end
+  SP_CUDA(cudaEventRecord(ev[2 * nc], s));  // earlier work on s (users of the staging buffers)
+  SP_CUDA(cudaStreamWaitEvent(A->pipe_in, ev[2 * nc], 0));
+  SP_CUDA(cudaStreamWaitEvent(A->pipe_out, ev[2 * nc], 0));
+  for (int k = 0; k < nc; ++k) {
+    const int64_t r0 = A->pipe_row[k], r1 = A->pipe_row[k + 1];
+    SP_CUDA(cudaMemcpyAsync(dx + r0, x + r0, (r1 - r0) * 8, cudaMemcpyHostToDevice, A->pipe_in));
+    SP_CUDA(cudaEventRecord(ev[k], A->pipe_in));
+  }
+  for (int k = 0; k < nc; ++k) {
+    // the x chunk holding the last column this row chunk reads (uploads complete in order)
+    int need = 0;
+    while (need + 1 < nc && A->pipe_row[need + 1] <= A->pipe_xneed[k]) ++need;
+    need = std::max(need, k);
+    SP_CUDA(cudaStreamWaitEvent(s, ev[need], 0));
+    SP_TRY(spmv_diag_chunk(A, dx, dy, k, s));
+    SP_CUDA(cudaEventRecord(ev[nc + k], s));
+    SP_CUDA(cudaStreamWaitEvent(A->pipe_out, ev[nc + k], 0));
+    const int64_t r0 = A->pipe_row[k], r1 = A->pipe_row[k + 1];
+    SP_CUDA(cudaMemcpyAsync(y + r0, dy + r0, (r1 - r0) * 8, cudaMemcpyDeviceToHost, A->pipe_out));
+  }
+  SP_CUDA(cudaEventRecord(ev[2 * nc + 1], A->pipe_out));
+  SP_CUDA(cudaStreamWaitEvent(s, ev[2 * nc + 1], 0));
+  SP_CUDA(cudaStreamSynchronize(s));
+  return SPMAT_OK;
+}
+
 }  // namespace spmat
 
 using namespace spmat;
@@ -94,6 +151,7 @@ int spmat_mult(spmat_t A, const double *x, double *y, void *stream) {
   const bool hx = A->n > 0 && !is_device_ptr(x);
   const bool hy = A->m > 0 && !is_device_ptr(y);
   if (!hx && !hy) return mult_impl(A, x, y, 7, s);
+  if (hx && hy && pipeline_ok(A)) return mult_host_pipelined(A, x, y, s);
   // host buffers: stage through device copies inside the stream order
   const double *dx = x;
   double *dy = y;

@@ -695,3 +695,63 @@ int spmv_offdiag(spmat_s *A, double *y, cudaStream_t s) {
 }
 
 }  // namespace spmat
+
+namespace spmat {
+
+// ------------------------------------------------------------------ host-buffer pipeline
+// last column read by each chunk of rows (max over its rows of the last column index)
+__global__ void k_chunk_maxcol(const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+                               int64_t r0, int64_t r1, int *__restrict__ out) {
+  int best = -1;
+  for (int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r1;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int a = rowptr[r], z = rowptr[r + 1];
+    if (z > a) best = max(best, col[z - 1]);  // columns ascend within a row
+  }
+  atomicMax(out, best);
+}
+
+int spmv_pipe_prepare(spmat_s *A, int chunks) {
+  if (A->pipe_chunks == chunks) return SPMAT_OK;
+  const int64_t nb = A->n_rowblocks;
+  if (nb < chunks) chunks = (int)std::max<int64_t>(1, nb);
+  A->pipe_block.assign(chunks + 1, 0);
+  A->pipe_row.assign(chunks + 1, 0);
+  A->pipe_xneed.assign(chunks, 0);
+  std::vector<int4> edge(chunks + 1);
+  for (int k = 0; k <= chunks; ++k) A->pipe_block[k] = nb * k / chunks;
+  for (int k = 0; k < chunks; ++k)
+    SP_CUDA(cudaMemcpy(&edge[k], A->blocks4.get() + A->pipe_block[k], sizeof(int4), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < chunks; ++k) A->pipe_row[k] = edge[k].x;
+  A->pipe_row[chunks] = A->m;
+  DevBuf<int> mx;
+  SP_TRY(mx.alloc(chunks));
+  SP_CUDA(cudaMemset(mx.get(), 0xff, chunks * sizeof(int)));
+  for (int k = 0; k < chunks; ++k) {
+    k_chunk_maxcol<<<nblk(A->pipe_row[k + 1] - A->pipe_row[k]), 256>>>(
+        A->rowptr_d.get(), A->col_d.get(), A->pipe_row[k], A->pipe_row[k + 1], mx.get() + k);
+    SP_LAUNCH();
+  }
+  std::vector<int> h(chunks);
+  SP_CUDA(cudaMemcpy(h.data(), mx.get(), chunks * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < chunks; ++k) A->pipe_xneed[k] = h[k];
+  A->pipe_chunks = chunks;
+  return SPMAT_OK;
+}
+
+// the bulk-copy SpMV over claim range [pipe_block[k], pipe_block[k+1]) (single rank: the
+// claim order is the row order, so that is the chunk's rows)
+int spmv_diag_chunk(spmat_s *A, const double *x, double *y, int k, cudaStream_t s) {
+  const int64_t c0 = A->pipe_block[k], c1 = A->pipe_block[k + 1];
+  if (c1 <= c0) return SPMAT_OK;
+  SpmvHalo h{A->halo_puts.get(), 0, 0, 0ull, A->halo_err.get()};
+  SpmvTail t{};
+  t.t0 = (int)(c1 - c0);
+  const unsigned grid = (unsigned)std::min<int64_t>(A->tma_grid, c1 - c0);
+  k_spmv_tma<<<grid, kCtaThreads, kTmaSmem, s>>>(A->blocks4.get() + c0, (int)(c1 - c0), A->rowptr_d.get(),
+                                                A->col_d.get(), A->val_d.get(), x, y, A->sched.get(), h, t);
+  SP_LAUNCH();
+  return SPMAT_OK;
+}
+
+}  // namespace spmat
