@@ -117,8 +117,11 @@ class OracleMat:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            lib().orc_destroy(h)
+        if h is not None and h.value and _lib is not None:
+            try:
+                _lib.orc_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
             self._h = None
 
     def set_values(self, coo_v, mode=INSERT):

@@ -127,6 +127,9 @@ def stencil_offsets(ndim: int, npts: int):
     if npts == 3 ** ndim:
         import itertools
         return [tuple(t) for t in itertools.product((-1, 0, 1), repeat=ndim)]
+    if npts == 5 ** ndim:  # Q2-like: every node within distance 2 per axis
+        import itertools
+        return [tuple(t) for t in itertools.product((-2, -1, 0, 1, 2), repeat=ndim)]
     raise ValueError(f"unsupported stencil: ndim={ndim} npts={npts}")
 
 
@@ -355,6 +358,9 @@ CONFIGS = {
     "c3": dict(kind="q1", n=160, per_gpu=False),
     "c4": dict(kind="stencil", shape=(256, 256, 256), npts=7, per_gpu=True),
     "c5": dict(kind="elasticity", n=200, per_gpu=False),
+    # variants: C4 per-GPU cubes in a box decomposition; Q2-like 125-point
+    "c4b": dict(kind="box", local=(256, 256, 256), npts=7, per_gpu=True),
+    "q2": dict(kind="stencil", shape=(96, 96, 96), npts=125, per_gpu=False),
 }
 
 CONFIG_TEXT = {
@@ -363,6 +369,8 @@ CONFIG_TEXT = {
     "c3": "3D Q1 27-point stencil 160^3 nodes, COO from per-element duplicates",
     "c4": "3D 7-point Laplacian 256^3 per GPU, z-slab MPIAIJ, weak scaling",
     "c5": "3D 3-dof 27-point elasticity-like 200^3, strong scaling",
+    "c4b": "3D 7-point Laplacian 256^3 per GPU, box (cube) decomposition with renumbering",
+    "q2": "3D 125-point (Q2-like) stencil 96^3",
 }
 
 
@@ -375,11 +383,19 @@ def config_rows(name: str, P: int = 1) -> int:
         return n * (P if c["per_gpu"] else 1)
     if c["kind"] == "q1":
         return c["n"] ** 3
+    if c["kind"] == "box":
+        n = 1
+        for sdim in config_shape(name, P):
+            n *= sdim
+        return n
     return 3 * c["n"] ** 3
 
 
 def config_shape(name: str, P: int = 1):
     c = CONFIGS[name]
+    if c["kind"] == "box":
+        procs = box_procs(P)
+        return tuple(l * p for l, p in zip(c["local"], procs))
     if c["kind"] != "stencil":
         raise ValueError(name)
     shape = list(c["shape"])
@@ -402,6 +418,10 @@ def config_rank_coo(name: str, P: int, r: int, values: str = "int", seed: int = 
         i, j, v = stencil_coo(shape, c["npts"], rows=(off[r], off[r + 1]), values=values,
                               seed=seed, device=device)
         return i, j, v, sizes
+    if c["kind"] == "box":
+        shape, procs = config_shape(name, P), box_procs(P)
+        i, j, v = stencil_coo_box(shape, c["npts"], procs, r, values=values, seed=seed, device=device)
+        return i, j, v, box_sizes(shape, procs)
     if c["kind"] == "q1":
         n = c["n"]
         sizes = slab_sizes((n, n, n), P)
@@ -414,3 +434,95 @@ def config_rank_coo(name: str, P: int, r: int, values: str = "int", seed: int = 
     i, j, v = elasticity_coo(n, nodes=(r * nodes, (r + 1) * nodes), values=values, seed=seed,
                              device=device)
     return i, j, v, sizes
+
+
+# ----------------------------------------------------------------------------------------
+# box (cube) decomposition with per-rank renumbering ("a cube of cells per
+# rank"); SURVEY §8(e) variant.  Rank r = bx + px*(by + py*bz) owns the box of nodes
+# [bx*nx/px, (bx+1)*nx/px) x ... and its nodes are numbered contiguously, lexicographically
+# inside the box, after all nodes of ranks < r.  Halo faces are strided in the owner's
+# numbering, so the owner must gather them (the SF pack path).
+# ----------------------------------------------------------------------------------------
+
+
+def box_procs(P: int):
+    """px, py, pz for P ranks: 1 -> 1x1x1, 2 -> 2x1x1, 4 -> 2x2x1, 8 -> 2x2x2, else Px1x1."""
+    return {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}.get(P, (P, 1, 1))
+
+
+def _box_bounds(n, p, b):
+    return (b * n) // p, ((b + 1) * n) // p
+
+
+def box_sizes(shape, procs):
+    px, py, pz = procs
+    nx, ny, nz = shape
+    sizes = []
+    for bz in range(pz):
+        for by in range(py):
+            for bx in range(px):
+                x0, x1 = _box_bounds(nx, px, bx)
+                y0, y1 = _box_bounds(ny, py, by)
+                z0, z1 = _box_bounds(nz, pz, bz)
+                sizes.append((x1 - x0) * (y1 - y0) * (z1 - z0))
+    return sizes
+
+
+def _box_of(i, n, p):
+    """Box index of coordinate i when [0, n) is cut at floor(k*n/p), k = 0..p."""
+    bounds = torch.tensor([(k * n) // p for k in range(1, p)], dtype=I64, device=i.device)
+    return torch.searchsorted(bounds, i, right=True) if p > 1 else torch.zeros_like(i)
+
+
+def box_global_id(ix, iy, iz, shape, procs):
+    """Natural coordinates -> global id under the box numbering (int64 tensors)."""
+    px, py, pz = procs
+    nx, ny, nz = shape
+    sizes = box_sizes(shape, procs)
+    offs = torch.tensor(offsets_from_sizes(sizes)[:-1], dtype=I64, device=ix.device)
+    bx, by, bz = _box_of(ix, nx, px), _box_of(iy, ny, py), _box_of(iz, nz, pz)
+    x0, y0, z0 = (bx * nx) // px, (by * ny) // py, (bz * nz) // pz
+    lx = ((bx + 1) * nx) // px - x0
+    ly = ((by + 1) * ny) // py - y0
+    rank = bx + px * (by + py * bz)
+    return offs[rank] + (ix - x0) + lx * ((iy - y0) + ly * (iz - z0))
+
+
+def stencil_coo_box(shape, npts: int, procs, rank: int, values: str = "int",
+                    seed: int = DEFAULT_SEED, device="cpu"):
+    """Stencil COO of rank `rank` under the box decomposition (rows = its box's nodes in the
+    box numbering; entry k = local_node * S + s).  Values: "int" Laplacian weights, or
+    "real" hashed on the NATURAL (i, j) so every P sees the same operator."""
+    px, py, pz = procs
+    nx, ny, nz = shape
+    bx, by, bz = rank % px, (rank // px) % py, rank // (px * py)
+    x0, x1 = _box_bounds(nx, px, bx)
+    y0, y1 = _box_bounds(ny, py, by)
+    z0, z1 = _box_bounds(nz, pz, bz)
+    lx, ly, lz = x1 - x0, y1 - y0, z1 - z0
+    loc = torch.arange(lx * ly * lz, dtype=I64, device=device)
+    ix = x0 + loc % lx
+    iy = y0 + (loc // lx) % ly
+    iz = z0 + loc // (lx * ly)
+    offs = stencil_offsets(3, npts)
+    S = len(offs)
+    gi = box_global_id(ix, iy, iz, shape, procs)
+    nat_i = ix + nx * (iy + ny * iz)
+    i = gi.repeat_interleave(S)
+    jcols, nat_j = [], []
+    for off in offs:
+        dz, dy, dx = off
+        jx, jy, jz = ix + dx, iy + dy, iz + dz
+        inside = (jx >= 0) & (jx < nx) & (jy >= 0) & (jy < ny) & (jz >= 0) & (jz < nz)
+        g = box_global_id(jx.clamp(0, nx - 1), jy.clamp(0, ny - 1), jz.clamp(0, nz - 1), shape, procs)
+        jcols.append(torch.where(inside, g, torch.full_like(g, -1)))
+        nat_j.append(jx + nx * (jy + ny * jz))
+    j = torch.stack(jcols, dim=1).reshape(-1)
+    if values == "int":
+        w = torch.full((S,), -1.0, dtype=F64, device=device)
+        w[offs.index((0, 0, 0))] = float(npts - 1)
+        v = w.repeat(loc.numel())
+    else:
+        nj = torch.stack(nat_j, dim=1).reshape(-1)
+        v = uniform_pm1(hash_ids(seed, nat_i.repeat_interleave(S), nj))
+    return i, j, v

@@ -169,6 +169,21 @@ def case_q1(c, values):
         assert info["n_mixed"] > 0
 
 
+def case_box(c, npts, values):
+    """Box (cube) decomposition with per-rank renumbering: strided owner
+    faces (gathered by the halo puts / SF pack kernel), up to 26 neighbours."""
+    P = c.P
+    procs = synth.box_procs(P)
+    shape = (8 * procs[0] + 1, 6 * procs[1], 5 * procs[2])
+    sizes = synth.box_sizes(shape, procs)
+    M = sum(sizes)
+    coo = [synth.stencil_coo_box(shape, npts, procs, q, values=values) for q in range(P)]
+    x = synth.x_vector(0, M, values).numpy()
+    info, _ = check_matrix(c, f"box{npts}-{values}", M, M, sizes, sizes, coo, values, x,
+                           exact_y=(values == "int"))
+    assert info["n_ghost"] > 0
+
+
 def case_elasticity(c):
     P = c.P
     n = 2 * P
@@ -300,6 +315,8 @@ def main():
              ("elasticity", lambda: case_elasticity(c))]
     cases += [(f"random{s}", (lambda s=s: case_random(c, s))) for s in range(6)]
     cases += [(f"sf{s}", (lambda s=s: case_sf(c, s))) for s in range(6)]
+    cases += [("box7-int", lambda: case_box(c, 7, "int")), ("box7-real", lambda: case_box(c, 7, "real")),
+              ("box27-real", lambda: case_box(c, 27, "real"))]
     cases += [("cg", lambda: case_cg(c))]
     cases += [("errors", lambda: case_errors(c))]
     for name, fn in cases:

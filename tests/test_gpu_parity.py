@@ -79,6 +79,7 @@ CASES = {
     "q1mass_7": lambda values: (7 ** 3,) * 2 + synth.q1_coo(7, variant="mass", values=values),
     "el_6": lambda values: (3 * 6 ** 3,) * 2 + synth.elasticity_coo(6, values=values),
     "27pt_2d9": lambda values: (81, 81) + synth.stencil_coo((9, 9), 9, values=values),
+    "q2_125pt": lambda values: (9 ** 3,) * 2 + synth.stencil_coo((9, 9, 9), 125, values=values),
 }
 
 

@@ -574,3 +574,37 @@ def test_cg_zero_rhs_stops():
     A, M = _spd_system(4)
     x, hist = A.cg(np.zeros(M), np.zeros(M), 5)
     assert np.all(x == 0) and np.all(hist == 0)
+
+
+# ---------------------------------------------------------------- variants (NEXT #4)
+@pytest.mark.parametrize("P,npts", [(2, 7), (4, 7), (8, 27), (3, 7)])
+def test_box_decomposition_is_a_renumbering(P, npts):
+    """Box (cube) partition with per-rank renumbering: permuting the
+    assembled matrix back to natural order gives exactly the natural stencil matrix."""
+    shape = (6, 4, 5) if P != 8 else (4, 4, 4)
+    procs = synth.box_procs(P)
+    sizes = synth.box_sizes(shape, procs)
+    M = int(np.prod(shape))
+    assert sum(sizes) == M
+    ii, jj, vv = [], [], []
+    for r in range(P):
+        i, j, v = synth.stencil_coo_box(shape, npts, procs, r, values="real")
+        ii.append(i); jj.append(j); vv.append(v)
+    O = oracle.OracleMat(M, M, sizes, sizes, ii, jj)
+    O.set_values(vv)
+    g = torch.arange(M)
+    nx, ny = shape[0], shape[1]
+    perm = synth.box_global_id(g % nx, (g // nx) % ny, g // (nx * ny), shape, procs).numpy()
+    assert sorted(perm.tolist()) == list(range(M))
+    i1, j1, v1 = synth.stencil_coo(shape, npts, values="real")
+    O1 = oracle.OracleMat(M, M, [M], [M], [i1], [j1])
+    O1.set_values([v1])
+    assert np.array_equal(O.dense()[np.ix_(perm, perm)], O1.dense())
+
+
+def test_q2_125pt_nnz():
+    """125-point (Q2-like) stencil: nnz = (5n - 6)^3 for an n^3 grid (closed form)."""
+    for n in (3, 5, 6):
+        i, j, v = synth.stencil_coo((n, n, n), 125)
+        A = oracle.OracleMat(n ** 3, n ** 3, [n ** 3], [n ** 3], [i], [j])
+        assert A.info(0, "nnz_d") == (5 * n - 6) ** 3
