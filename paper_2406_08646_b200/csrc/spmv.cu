@@ -305,11 +305,25 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
   // ---------------- consumer warps
   unsigned long long *trc = tail.trace ? tail.trace + 4 * (size_t)blockIdx.x : nullptr;
   if (trc && tid == 0) trc[0] = gtimer();
+  // boundary blocks are claimed before everything else, so a warp publishes how many it
+  // wrote (one fence + one atomic per warp) when it meets its first other claim
+  unsigned bdone = 0;
+  bool published = !tail.enabled;
+  auto publish = [&]() {
+    if (published) return;
+    published = true;
+    __syncwarp();
+    if (lane32 == 0 && bdone) {
+      __threadfence();
+      atomicAdd(tail.ctr, bdone);
+    }
+  };
   for (int it = 0;; ++it) {
     const int s = it % kStages;
     mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
     const int4 h = st[s].hdr;
     const int r0 = h.x, r1 = h.y, p0 = h.z, p1 = h.w;
+    if (r0 < 0 || !st[s].flags.x) publish();
     if (r0 == -1) {
       if (trc && tid == 0) trc[2] = gtimer();
       break;
@@ -371,13 +385,8 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
       else rows_w<32>(r0, r1, p0, rp, sc, sv, x, y, tid);
     }
     __syncwarp();
-    if (lane32 == 0) {
-      mbar_arrive(&empty[s]);
-      if (boundary) {  // publish this warp's y rows of a boundary block to the tail
-        __threadfence();
-        atomicAdd(tail.ctr, 1u);
-      }
-    }
+    if (lane32 == 0) mbar_arrive(&empty[s]);
+    bdone += boundary ? 1u : 0u;
   }
   if (trc) {
     asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
