@@ -152,6 +152,14 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream);
    written.  Collective. */
 int spmat_mult(spmat_t A, const double *x, double *y, void *stream);
 
+/* MatSetBlockSize analogue for the SpMV storage (block-CSR on GPU): bs = 3 checks that
+   the assembled diagonal block consists of dense, aligned 3x3 blocks (node-block matrices with
+   3 dofs per node) and from then on multiplies it from a 3x3 block-CSR copy (8.44 instead of
+   12 bytes per nonzero), refreshed after every spmat_set_values_coo; bs = 1 returns to CSR.
+   SPMAT_ERR_ARG if the structure is not blocked (the matrix keeps CSR).  Local, host-
+   synchronising. */
+int spmat_set_block_size(spmat_t A, int bs);
+
 /* Parts of MatMult for isolated timing: part bit 1 = diagonal SpMV (y = A_d x), bit 2 =
    halo exchange (x -> ghost vector), bit 4 = off-diagonal SpMV-add (y += A_o ghosts).
    part 7 == spmat_mult on device pointers. */

@@ -55,7 +55,7 @@ ABI_SYMBOLS = (
     "sf_get_info", "sf_export", "sf_destroy", "spmat_create_coo", "spmat_set_values_coo",
     "spmat_mult", "spmat_mult_part", "spmat_get_info", "spmat_export", "spmat_get_halo_sf",
     "spmat_profile", "spmat_profile_read", "spmat_check", "spmat_halo_mode", "spmat_trace_read",
-    "spmat_vec_dot", "spmat_cg",
+    "spmat_vec_dot", "spmat_cg", "spmat_set_block_size",
     "spmat_destroy")
 
 
@@ -109,6 +109,7 @@ def load(path: str = LIB_PATH):
         "spmat_trace_read": ([p, p, i64, P(i64)], i32),
         "spmat_vec_dot": ([p, p, p, p, p], i32),
         "spmat_cg": ([p, p, p, i32, p, p], i32),
+        "spmat_set_block_size": ([p, i32], i32),
         "spmat_destroy": ([p], i32),
     }
     for name, (args, res) in sig.items():
@@ -400,6 +401,9 @@ class Mat:
 
     def check(self):
         spmat_check(self.h)
+
+    def set_block_size(self, bs):
+        _check(load().spmat_set_block_size(self.h, int(bs)), "spmat_set_block_size")
 
     def dot(self, a, b, result, stream=None):
         spmat_vec_dot(self.h, a, b, result, stream)

@@ -1,0 +1,363 @@
+// bsr.cu -- 3x3 block-CSR diagonal block for multi-dof matrices (the paper's planned
+// "block-CSR on GPU").
+//
+// spmat_set_block_size(A, 3) checks that the assembled diagonal CSR block is made of dense,
+// aligned 3x3 blocks (true for node-block COO such as the 3-dof elasticity config C5) and keeps
+// a block copy: browptr (block rows), bcol (one column index per block), bval (9 values per
+// block, row-major).  Bytes per nonzero drop from 12 (8 value + 4 column) to 8.44 (8 value +
+// 4/9 column), so the HBM-bound SpMV moves ~30 % fewer bytes.  bval is refreshed from the CSR
+// values after every spmat_set_values_coo (the assembly plan stays the CSR one).
+//
+// k_spmv_bsr3 mirrors k_spmv_tma: persistent warp-specialised CTAs, a producer warp staging
+// (bval, bcol, browptr) slices of a "row block" of block rows through cp.async.bulk into a
+// 2-stage mbarrier ring, 8 consumer warps computing W lanes per block row.  A lane walks its
+// blocks in ascending column order and adds v_i0*x_0, v_i1*x_1, v_i2*x_2 for each block row i,
+// which with W = 1 is exactly the CSR row's left-to-right order.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace spmat {
+
+namespace {
+
+constexpr int kT = 256;                    // consumer threads
+constexpr int kCtaT = kT + 32;             // + producer warp
+constexpr int kBudgetD = 2048;             // doubles per row block (9*blocks + 6*block rows)
+constexpr int kCapD = kBudgetD + 576;      // stage capacity in doubles (a 64-block row fits)
+constexpr int kMaxBR = kBudgetD / 6;       // block rows per row block
+constexpr int kStagesB = 2;
+
+struct __align__(16) BsrStage {
+  double val[kCapD + 2];
+  int col[(kCapD / 9 + 11) & ~3];  // multiples of 4 ints keep every array 16-byte aligned
+  int rp[(kMaxBR + 11) & ~3];
+  int4 hdr;  // br0, br1, bp0, bp1
+};
+constexpr size_t kBsrSmem = kStagesB * sizeof(BsrStage) + 2 * kStagesB * sizeof(unsigned long long);
+
+#define GSTRIDE(t, n) \
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (n); t += (int64_t)gridDim.x * blockDim.x)
+
+inline unsigned nb(int64_t n, int t = 256) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + t - 1) / t, (int64_t)1 << 30));
+}
+
+// warp per block row: rows 3br..3br+2 share one column list made of aligned triples
+__global__ void k_bsr_check(const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+                            int64_t mb, int *__restrict__ bad) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= mb) return;
+  const int64_t r = 3 * warp;
+  const int a0 = rowptr[r], a1 = rowptr[r + 1], a2 = rowptr[r + 2], a3 = rowptr[r + 3];
+  const int len = a1 - a0;
+  if (a2 - a1 != len || a3 - a2 != len || len % 3) {
+    if (lane == 0) atomicOr(bad, 1);
+    return;
+  }
+  for (int p = lane; p < len; p += 32) {
+    const int c0 = col[a0 + p];
+    bool ok = c0 == col[a1 + p] && c0 == col[a2 + p];
+    ok = ok && ((p % 3 == 0) ? (c0 % 3 == 0) : (c0 == col[a0 + p - 1] + 1));
+    if (!ok) atomicOr(bad, 1);
+  }
+}
+
+__global__ void k_bsr_build(const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+                            int64_t mb, int32_t *__restrict__ browptr, int32_t *__restrict__ bcol) {
+  GSTRIDE(br, mb + 1) {
+    const int a = rowptr[3 * br];
+    browptr[br] = a / 9;
+    if (br < mb) {
+      const int nblk_row = (rowptr[3 * br + 1] - a) / 3;
+      for (int q = 0; q < nblk_row; ++q) bcol[a / 9 + q] = col[a + 3 * q] / 3;
+    }
+  }
+}
+
+// warp per block row: bval[9*(bp0+q) + 3i + j] = val[rowptr[3br+i] + 3q + j]
+__global__ void k_bsr_refresh(const int32_t *__restrict__ rowptr, const double *__restrict__ val,
+                              const int32_t *__restrict__ browptr, int64_t mb, double *__restrict__ bval) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t br = warp; br < mb; br += nwarps) {
+    const int bp0 = browptr[br], nbr = browptr[br + 1] - bp0;
+    const int r0 = rowptr[3 * br], r1 = rowptr[3 * br + 1], r2 = rowptr[3 * br + 2];
+    for (int v = lane; v < 9 * nbr; v += 32) {
+      const int q = v / 9, i = (v % 9) / 3, j = v % 3;
+      const int base = i == 0 ? r0 : (i == 1 ? r1 : r2);
+      bval[9 * (int64_t)bp0 + v] = val[base + 3 * q + j];
+    }
+  }
+}
+
+// row-block boundaries over block rows: cost(br) = 9*browptr[br] + 6*br
+__global__ void k_bsr_candidates(const int32_t *__restrict__ browptr, int64_t mb, int64_t ncost,
+                                 int32_t *__restrict__ cand) {
+  GSTRIDE(t, ncost) {
+    const int64_t target = t * (int64_t)kBudgetD;
+    int64_t lo = 0, hi = mb;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (9 * (int64_t)browptr[mid] + 6 * mid < target) lo = mid + 1; else hi = mid;
+    }
+    cand[t] = (int32_t)lo;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cand[ncost] = (int32_t)mb;
+}
+
+__global__ void k_bsr_blocks4(const int32_t *__restrict__ bounds, const int32_t *__restrict__ browptr,
+                              int64_t n, int4 *__restrict__ out) {
+  GSTRIDE(t, n) {
+    const int a = bounds[t], b = bounds[t + 1];
+    out[t] = make_int4(a, b, browptr[a], browptr[b]);
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void brows_w(int br0, int br1, int bp0, const int *__restrict__ rp,
+                                        const int *__restrict__ sc, const double *__restrict__ sv,
+                                        const double *__restrict__ x, double *__restrict__ y, int tid) {
+  constexpr int U = 4;  // blocks per lane in flight
+  const int lane = tid & (W - 1);
+  for (int br = br0 + tid / W; br < br1; br += kT / W) {
+    const int a = rp[br] - bp0, z = rp[br + 1] - bp0;
+    double y0 = 0.0, y1 = 0.0, y2 = 0.0;
+    for (int e0 = a + lane; e0 < z; e0 += U * W) {
+      double xv[U][3];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * W;
+        const int c = e < z ? sc[e] : 0;
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) xv[u][jj] = __ldg(x + 3 * c + jj);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * W;
+        if (e < z) {
+          const double *v = sv + 9 * e;
+#pragma unroll
+          for (int jj = 0; jj < 3; ++jj) {
+            y0 = __dadd_rn(y0, __dmul_rn(v[jj], xv[u][jj]));
+            y1 = __dadd_rn(y1, __dmul_rn(v[3 + jj], xv[u][jj]));
+            y2 = __dadd_rn(y2, __dmul_rn(v[6 + jj], xv[u][jj]));
+          }
+        }
+      }
+    }
+    if (W > 1) {
+      const unsigned mask = __activemask();
+#pragma unroll
+      for (int o = W >> 1; o > 0; o >>= 1) {
+        y0 = __dadd_rn(y0, __shfl_down_sync(mask, y0, o, W));
+        y1 = __dadd_rn(y1, __shfl_down_sync(mask, y1, o, W));
+        y2 = __dadd_rn(y2, __shfl_down_sync(mask, y2, o, W));
+      }
+    }
+    if (lane == 0) {
+      y[3 * (int64_t)br] = y0;
+      y[3 * (int64_t)br + 1] = y1;
+      y[3 * (int64_t)br + 2] = y2;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCtaT, 3)
+    k_spmv_bsr3(const int4 *__restrict__ blocks, int n_blocks, const int32_t *__restrict__ browptr,
+                const int32_t *__restrict__ bcol, const double *__restrict__ bval,
+                const double *__restrict__ x, double *__restrict__ y, unsigned int *__restrict__ sched) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  BsrStage *st = reinterpret_cast<BsrStage *>(smem);
+  unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + kStagesB * sizeof(BsrStage));
+  unsigned long long *empty = full + kStagesB;
+  const int tid = threadIdx.x, warp = tid >> 5, lane32 = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < kStagesB; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == kT / 32) {  // producer
+    if (lane32 != 0) return;
+    uint64_t policy;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    int b = (int)atomicAdd(sched, 1u);
+    int b_next = (int)atomicAdd(sched, 1u);
+    int4 H = b < n_blocks ? blocks[b] : make_int4(0, 0, 0, 0);
+    for (int it = 0;; ++it) {
+      const int s = it % kStagesB;
+      if (it >= kStagesB) mbar_wait(&empty[s], (uint32_t)(((it / kStagesB) - 1) & 1));
+      if (b >= n_blocks) {
+        st[s].hdr = make_int4(-1, 0, 0, 0);
+        mbar_arrive_tx(&full[s], 0);
+        __threadfence();
+        if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+          atomicExch(sched, 0u);
+          atomicExch(sched + 1, 0u);
+        }
+        return;
+      }
+      st[s].hdr = H;
+      const int64_t v0 = 9 * (int64_t)H.z, v1 = 9 * (int64_t)H.w;
+      const int64_t va = v0 & ~1ll, ve = (v1 + 1) & ~1ll;
+      const int ca = H.z & ~3, ce = (H.w + 3) & ~3;
+      const int ra = H.x & ~3, re = (H.y + 4) & ~3;
+      mbar_arrive_tx(&full[s], (uint32_t)((ve - va) * 8 + (ce - ca) * 4 + (re - ra) * 4));
+      if (ve > va) bulk_g2s(st[s].val, bval + va, (uint32_t)((ve - va) * 8), &full[s], policy);
+      if (ce > ca) bulk_g2s(st[s].col, bcol + ca, (ce - ca) * 4, &full[s], policy);
+      bulk_g2s(st[s].rp, browptr + ra, (re - ra) * 4, &full[s], policy);
+      b = b_next;
+      if (b < n_blocks) {
+        b_next = (int)atomicAdd(sched, 1u);
+        H = blocks[b];
+      }
+    }
+  }
+  for (int it = 0;; ++it) {  // consumers
+    const int s = it % kStagesB;
+    mbar_wait(&full[s], (uint32_t)((it / kStagesB) & 1));
+    const int4 h = st[s].hdr;
+    if (h.x < 0) break;
+    const int br0 = h.x, br1 = h.y, bp0 = h.z;
+    const double *sv = st[s].val + ((9 * (int64_t)bp0) & 1);
+    const int *sc = st[s].col + (bp0 & 3);
+    const int *rp = st[s].rp - (br0 & ~3);
+    const int nbr = br1 - br0;
+    if (nbr * 2 > kT) brows_w<1>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 4 > kT) brows_w<2>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 8 > kT) brows_w<4>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 16 > kT) brows_w<8>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 32 > kT) brows_w<16>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else brows_w<32>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    __syncwarp();
+    if (lane32 == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+#define CUB_CALL2(tmp, call_with_tmp)                                          \
+  do {                                                                         \
+    size_t temp_storage_bytes = 0;                                             \
+    void *d_temp_storage = nullptr;                                            \
+    SP_CUDA(call_with_tmp);                                                    \
+    if (temp_storage_bytes > (tmp).n) SP_TRY((tmp).alloc(temp_storage_bytes)); \
+    d_temp_storage = (tmp).get();                                              \
+    SP_CUDA(call_with_tmp);                                                    \
+  } while (0)
+
+}  // namespace
+
+int bsr_refresh(spmat_s *A, cudaStream_t s) {
+  if (A->bs != 3 || A->mb == 0) return SPMAT_OK;
+  k_bsr_refresh<<<nb(A->mb * 32), 256, 0, s>>>(A->rowptr_d.get(), A->val_d.get(), A->browptr.get(),
+                                                A->mb, A->bval.get());
+  SP_LAUNCH();
+  return SPMAT_OK;
+}
+
+int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s) {
+  k_spmv_bsr3<<<(unsigned)A->bsr_grid, kCtaT, kBsrSmem, s>>>(A->bblocks4.get(), (int)A->n_brblocks,
+                                                           A->browptr.get(), A->bcol.get(), A->bval.get(),
+                                                           x, y, A->bsched.get());
+  SP_LAUNCH();
+  return SPMAT_OK;
+}
+
+static int bsr_setup(spmat_s *A) {
+  cudaStream_t st = A->comm->setup_stream;
+  const int64_t mb = A->m / 3;
+  DevBuf<int> bad;
+  SP_TRY(bad.alloc(1));
+  SP_CUDA(cudaMemsetAsync(bad.get(), 0, 4, st));
+  if (mb > 0) {
+    k_bsr_check<<<nb(mb * 32), 256, 0, st>>>(A->rowptr_d.get(), A->col_d.get(), mb, bad.get());
+    SP_LAUNCH();
+  }
+  int hbad = 0;
+  SP_CUDA(cudaMemcpyAsync(&hbad, bad.get(), 4, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  if (hbad) return fail(SPMAT_ERR_ARG, "spmat_set_block_size: the diagonal block is not made of aligned 3x3 blocks");
+  const int64_t nnzb = A->nnz_d / 9;
+  A->mb = mb;
+  A->nnzb = nnzb;
+  SP_TRY(A->browptr.alloc(mb + 1 + 8));
+  SP_TRY(A->bcol.alloc(nnzb + 8));
+  SP_TRY(A->bval.alloc(9 * nnzb + 8));
+  k_bsr_build<<<nb(mb + 1), 256, 0, st>>>(A->rowptr_d.get(), A->col_d.get(), mb, A->browptr.get(), A->bcol.get());
+  SP_LAUNCH();
+  // longest block row must fit one stage
+  std::vector<int32_t> h(mb + 1);
+  SP_CUDA(cudaMemcpyAsync(h.data(), A->browptr.get(), (mb + 1) * 4, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  for (int64_t br = 0; br < mb; ++br)
+    if (9 * (int64_t)(h[br + 1] - h[br]) > kCapD - kBudgetD)
+      return fail(SPMAT_ERR_ARG, "spmat_set_block_size: a block row has more than %d blocks", (kCapD - kBudgetD) / 9);
+  // row blocks over block rows
+  const int64_t total = 9 * nnzb + 6 * mb;
+  const int64_t ncost = (total + kBudgetD - 1) / kBudgetD;
+  DevBuf<int32_t> cand, uniq;
+  DevBuf<int> dn;
+  DevBuf<char> tmp;
+  SP_TRY(cand.alloc(ncost + 1));
+  SP_TRY(uniq.alloc(ncost + 1));
+  SP_TRY(dn.alloc(1));
+  k_bsr_candidates<<<nb(ncost), 256, 0, st>>>(A->browptr.get(), mb, ncost, cand.get());
+  SP_LAUNCH();
+  CUB_CALL2(tmp, cub::DeviceSelect::Unique(d_temp_storage, temp_storage_bytes, cand.get(), uniq.get(),
+                                           dn.get(), (int)(ncost + 1), st));
+  int nu = 0;
+  SP_CUDA(cudaMemcpyAsync(&nu, dn.get(), 4, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  A->n_brblocks = nu - 1;
+  SP_TRY(A->bblocks4.alloc(std::max(nu - 1, 1)));
+  if (nu > 1) {
+    k_bsr_blocks4<<<nb(nu - 1), 256, 0, st>>>(uniq.get(), A->browptr.get(), nu - 1, A->bblocks4.get());
+    SP_LAUNCH();
+  }
+  SP_TRY(A->bsched.alloc(2));
+  SP_CUDA(cudaMemsetAsync(A->bsched.get(), 0, 8, st));
+  static bool attr = false;
+  if (!attr) {
+    SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
+    attr = true;
+  }
+  int per_sm = 0;
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_bsr3, kCtaT, kBsrSmem));
+  A->bsr_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * A->comm->num_sms,
+                                                           std::max<int64_t>(A->n_brblocks, 1)));
+  A->bs = 3;
+  A->kernel_id = 4;
+  if (A->values_set) SP_TRY(bsr_refresh(A, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  return SPMAT_OK;
+}
+
+}  // namespace spmat
+
+using namespace spmat;
+
+extern "C" {
+
+int spmat_set_block_size(spmat_t A, int bs) {
+  if (!A) return fail(SPMAT_ERR_ARG, "spmat_set_block_size: null matrix");
+  DeviceGuard g(A->comm->device);
+  if (bs == 1) {
+    A->bs = 1;
+    A->kernel_id = 3;
+    return SPMAT_OK;
+  }
+  if (bs != 3) return fail(SPMAT_ERR_ARG, "spmat_set_block_size: only 1 and 3 are supported");
+  if (A->m % 3 || A->n % 3) return fail(SPMAT_ERR_ARG, "spmat_set_block_size: local sizes not multiples of 3");
+  if (A->bs == 3) return SPMAT_OK;
+  return bsr_setup(A);
+}
+
+}  // extern "C"

@@ -764,6 +764,7 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
       SP_LAUNCH();
     }
   }
+  SP_TRY(bsr_refresh(A, s));  // block copy of the diagonal values, if any
   A->values_set = true;
   return SPMAT_OK;
 }

@@ -294,6 +294,14 @@ struct spmat_s {
   int n_puts = 0, n_waits = 0, put_chunks_total = 0;
   int64_t epoch = 0;
   int64_t lvec_stride = 0;          // peer mode: lvec holds two epochs' ghost buffers
+  // 3x3 block-CSR copy of the diagonal block (bsr.cu), after spmat_set_block_size(A, 3)
+  int bs = 1;
+  int64_t mb = 0, nnzb = 0, n_brblocks = 0;
+  int bsr_grid = 0;
+  spmat::DevBuf<int32_t> browptr, bcol;
+  spmat::DevBuf<double> bval;
+  spmat::DevBuf<int4> bblocks4;
+  spmat::DevBuf<unsigned int> bsched;
   // host-buffer MatMult pipeline (mult.cu / spmv.cu), built on first use
   int pipe_chunks = 0;
   std::vector<int64_t> pipe_block, pipe_row, pipe_xneed;  // claim range, row range, last x row
@@ -310,6 +318,8 @@ int spmv_prepare(spmat_s *A, cudaStream_t stream);  // row blocks + kernel choic
 int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream, bool fuse_put = false,
               bool fuse_tail = false);
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
+int bsr_refresh(spmat_s *A, cudaStream_t s);  // bval from the CSR values
+int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s);
 // host-buffer pipeline (single rank): row chunks of the diagonal SpMV
 int spmv_pipe_prepare(spmat_s *A, int chunks);  // chunk rows + the x columns each chunk reads
 int spmv_diag_chunk(spmat_s *A, const double *x, double *y, int k, cudaStream_t s);

@@ -69,7 +69,7 @@ def oracle_positions(O, r):
     return csrc, pos
 
 
-def check_matrix(c, name, M, N, row_sizes, col_sizes, coo, values, x_global, exact_y):
+def check_matrix(c, name, M, N, row_sizes, col_sizes, coo, values, x_global, exact_y, bs=1):
     """coo: list over ranks of (i, j, v) CPU tensors (every rank has all of them)."""
     P, r = c.P, c.r
     O = oracle.OracleMat(M, N, row_sizes, col_sizes, [t[0] for t in coo], [t[1] for t in coo])
@@ -77,6 +77,8 @@ def check_matrix(c, name, M, N, row_sizes, col_sizes, coo, values, x_global, exa
     i, j, v = coo[r]
     A = sp.Mat(c.comm, row_sizes[r], col_sizes[r], M, N, i.cuda(), j.cuda())
     A.set_values(v.cuda())
+    if bs > 1:
+        A.set_block_size(bs)
     c.halo_mode = A.halo_mode()
     info = A.info()
     assert info["rstart"] == O.info(r, "rstart") and info["cstart"] == O.info(r, "cstart")
@@ -193,6 +195,7 @@ def case_elasticity(c):
     coo = [synth.elasticity_coo(n, nodes=(q * nodes, (q + 1) * nodes), values="real") for q in range(P)]
     x = synth.x_vector(0, M, "real").numpy()
     check_matrix(c, "elasticity", M, M, sizes, sizes, coo, "real", x, exact_y=False)
+    check_matrix(c, "elasticity-bsr", M, M, sizes, sizes, coo, "real", x, exact_y=False, bs=3)
 
 
 def case_random(c, seed):

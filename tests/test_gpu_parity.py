@@ -455,3 +455,40 @@ def test_host_pipeline_matches_device(sp, comm):
         A.mult(xh, yh)
         assert torch.equal(yh, yd.cpu())
     A.close()
+
+
+@pytest.mark.parametrize("values", ["int", "real"])
+def test_block_csr_3x3(sp, comm, values):
+    """3x3 block-CSR SpMV (spmat_set_block_size) on the node-block elasticity matrix vs the
+    oracle; values refreshed after set_values (INSERT and ADD); unblocked matrices refuse."""
+    n = 7
+    M = 3 * n ** 3
+    i, j, v = synth.elasticity_coo(n, values=values)
+    O = oracle.OracleMat(M, M, [M], [M], [i], [j])
+    O.set_values([v])
+    A = sp.Mat(comm, M, M, M, M, dev(i), dev(j))
+    A.set_values(dev(v))
+    x = synth.x_vector(0, M, values)
+    y_csr = torch.empty(M, dtype=torch.float64, device="cuda")
+    A.mult(dev(x), y_csr)
+    A.set_block_size(3)
+    assert A.info()["spmv_kernel_id"] == 4
+    y = torch.empty(M, dtype=torch.float64, device="cuda")
+    A.mult(dev(x), y)
+    yo = O.mult(x.numpy())
+    if values == "int":
+        assert np.array_equal(canon(y.cpu().numpy()), canon(yo))
+    else:
+        assert rel_err(y.cpu().numpy(), yo) <= TOL
+    A.set_values(dev(v), sp.ADD)  # the block copy follows the assembly
+    O.set_values([v], oracle.ADD)
+    A.mult(dev(x), y)
+    assert rel_err(y.cpu().numpy(), O.mult(x.numpy())) <= TOL
+    A.set_block_size(1)
+    A.close()
+    i, j, v = synth.stencil_coo((9, 9, 9), 7)
+    B = sp.Mat(comm, 729, 729, 729, 729, dev(i), dev(j))
+    with pytest.raises(sp.SpmatError) as e:
+        B.set_block_size(3)
+    assert e.value.status == sp.SPMAT_ERR_ARG
+    B.close()
