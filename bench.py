@@ -35,7 +35,8 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 
 KERNEL_NAMES = {1: "k_spmv_stream (diagonal-block SpMV)", 2: "k_spmv_vector (diagonal-block SpMV)",
-                3: "k_spmv_tma<W> (diagonal-block SpMV, bulk-copy staged)"}
+                3: "k_spmv_tma (diagonal-block SpMV, bulk-copy staged)",
+                4: "k_spmv_bsr3 (diagonal-block 3x3 block-CSR SpMV, bulk-copy staged)"}
 METRIC = "MatMult GFLOP/s & HBM GB/s (% roofline), fp64, at 1/2/4/8 B200"
 UNIT = "GFLOP/s"
 FALLBACK_HBM = 6650.0
@@ -52,6 +53,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--kernel", default=None, help="SPMAT_SPMV_KERNEL override")
+    ap.add_argument("--block-size", type=int, default=None,
+                    help="spmat_set_block_size (default: 3 for the 3-dof config c5, else 1)")
     return ap.parse_args()
 
 
@@ -124,9 +127,13 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ byte / flop model
-def byte_model(info, m, n):
-    """Algorithmic bytes per MatMult (int32 indices, fp64 values)."""
-    diag = 12 * info["nnz_d"] + 4 * (m + 1) + 8 * n + 8 * m
+def byte_model(info, m, n, bs=1):
+    """Algorithmic bytes per MatMult (int32 indices, fp64 values); with 3x3
+    block-CSR one column index per 9 values and one row pointer per block row."""
+    if bs == 3:
+        diag = 8 * info["nnz_d"] + 4 * (info["nnz_d"] // 9) + 4 * (m // 3 + 1) + 8 * n + 8 * m
+    else:
+        diag = 12 * info["nnz_d"] + 4 * (m + 1) + 8 * n + 8 * m
     nro = info["n_offdiag_rows"]
     off = (12 * info["nnz_o"] + 4 * (nro + 1) + 4 * nro + 8 * info["n_ghost"] + 16 * nro
            if nro else 0)
@@ -250,6 +257,9 @@ def main():
     t0 = time.perf_counter()
     A = sp.Mat(comm, m, m, M, M, i, j)
     t_create = max_over_ranks(time.perf_counter() - t0)
+    bs = a.block_size if a.block_size is not None else (3 if cfg == "c5" else 1)
+    if bs != 1:
+        A.set_block_size(bs)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     A.set_values(v)
     torch.cuda.synchronize()
@@ -349,7 +359,7 @@ def main():
                "h2d_bytes_per_step": 8 * m * P, "d2h_bytes_per_step": 8 * m * P, "steps": ke}
 
     # ---- report
-    diag_bytes, off_bytes = byte_model(info, m, m)
+    diag_bytes, off_bytes = byte_model(info, m, m, bs)
     hinfo = sp.sf_get_info(A.halo_sf())
     halo_bytes = 8 * (hinfo["n_recv"] + hinfo["n_send"])
     hbm_peak, peak_src, peakd = peaks()
