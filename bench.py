@@ -368,9 +368,20 @@ def main():
     fused = info["n_offdiag_rows"] > 0 and t_off == 0.0
     kernel_bytes = diag_bytes + (off_bytes if fused else 0)
     achieved = kernel_bytes / t_diag / 1e9 if t_diag > 0 else None
-    per_step_kernels = 1 + (1 if info["n_offdiag_rows"] > 0 else 0)
-    if P > 1 and hinfo["packed"]:
-        per_step_kernels += 1
+    # our kernels per MatMult: the fused kernel alone (NVLink halo + off-diagonal items inside);
+    # otherwise diag + off-diagonal (+ the SF pack/unpack kernels, or the standalone put) --
+    # NCCL's own kernels are not counted
+    halo_mode = A.halo_mode()
+    if fused:
+        per_step_kernels = 1
+    else:
+        per_step_kernels = 1 + (1 if info["n_offdiag_rows"] > 0 else 0)
+        if halo_mode == 1 and hinfo["packed"]:
+            per_step_kernels += 1
+        if halo_mode == 2:
+            per_step_kernels += 1 if info["spmv_kernel_id"] != 3 else 0
+    if info["spmv_kernel_id"] == 3 and info["max_row_nnz"] > 2560:
+        per_step_kernels += 1  # k_spmv_long
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):

@@ -27,7 +27,7 @@ namespace {
 
 constexpr int kT = 256;                    // consumer threads
 constexpr int kCtaT = kT + 32;             // + producer warp
-constexpr int kBudgetD = 2048;             // doubles per row block (9*blocks + 6*block rows)
+constexpr int kBudgetD = 2880;             // doubles per row block (9*blocks + 6*block rows): ~24 KB
 constexpr int kCapD = kBudgetD + 576;      // stage capacity in doubles (a 64-block row fits)
 constexpr int kMaxBR = kBudgetD / 6;       // block rows per row block
 constexpr int kStagesB = 2;
