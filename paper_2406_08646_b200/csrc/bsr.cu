@@ -349,6 +349,7 @@ extern "C" {
 int spmat_set_block_size(spmat_t A, int bs) {
   if (!A) return fail(SPMAT_ERR_ARG, "spmat_set_block_size: null matrix");
   DeviceGuard g(A->comm->device);
+  cg_graph_release(A);  // a captured CG iteration would still launch the old kernel
   if (bs == 1) {
     A->bs = 1;
     A->kernel_id = 3;

@@ -902,6 +902,7 @@ int spmat_destroy(spmat_t A) {
   {
     DeviceGuard g(A->comm->device);
     cudaDeviceSynchronize();
+    cg_graph_release(A);
     halo_peer_release(A);
     if (A->halo) sf_free(A->halo);
     for (cudaEvent_t e : A->pipe_ev) cudaEventDestroy(e);

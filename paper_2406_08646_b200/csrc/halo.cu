@@ -36,9 +36,9 @@ static inline int put_chunks(int64_t count) {
 // standalone put (halo-only MatMult parts, or a diagonal kernel without comm warps)
 __global__ void __launch_bounds__(32 * kPutWarps) k_halo_put(const HaloPut *__restrict__ puts, int nputs,
                                                              int total, const double *__restrict__ x,
-                                                             unsigned long long epoch, int *err) {
+                                                             const unsigned long long *epoch_ctr, int *err) {
   const int c = blockIdx.x * kPutWarps + (threadIdx.x >> 5);
-  if (c < total) halo_put_warp(puts, nputs, c, x, epoch, err);
+  if (c < total) halo_put_warp(puts, nputs, c, x, *epoch_ctr + 1ull, err);
 }
 
 // y[rows[q]] += A_o lvec, after the senders' epoch-e data has landed; the last CTA releases lvec
@@ -46,8 +46,11 @@ __global__ void __launch_bounds__(256) k_spmv_offdiag_peer(
     const int32_t *__restrict__ rows, const int32_t *__restrict__ rowptr,
     const int32_t *__restrict__ col, const double *__restrict__ val, const double *lvec_base,
     int64_t lvec_stride, double *__restrict__ y, int64_t nro, const HaloWait *__restrict__ waits, int nwaits,
-    unsigned long long epoch, unsigned int *counter, int *err, int signal) {
+    unsigned long long *epoch_ctr, unsigned int *counter, int *err, int signal) {
   __shared__ int ok;
+  // this MatMult's epoch; every CTA reads it before its arrival on `counter`, so before the
+  // last CTA stores it back
+  const unsigned long long epoch = *epoch_ctr + 1ull;
   if (threadIdx.x == 0) {
     int good = 1;
     for (int w = 0; w < nwaits && good; ++w)
@@ -72,6 +75,7 @@ __global__ void __launch_bounds__(256) k_spmv_offdiag_peer(
     if (atomicAdd(counter, 1u) == gridDim.x - 1) {
       atomicExch(counter, 0u);
       for (int w = 0; w < nwaits; ++w) st_release_sys(waits[w].peer_done, epoch);
+      *epoch_ctr = epoch;  // this MatMult is done
     }
   }
 }
@@ -188,7 +192,8 @@ int halo_peer_setup(spmat_s *A) {
   A->n_puts = (int)puts.size();
   A->n_waits = (int)waits.size();
   A->put_chunks_total = total_chunks;
-  A->epoch = 0;
+  SP_TRY(A->d_epoch.alloc(1));
+  SP_CUDA(cudaMemset(A->d_epoch.get(), 0, sizeof(unsigned long long)));
   A->peer = true;
   // every rank's flags are zero and every handle is open before the first put
   int64_t sync[1] = {0};
@@ -211,21 +216,20 @@ int halo_peer_put(spmat_s *A, const double *x, cudaStream_t s) {
   if (A->n_puts == 0) return SPMAT_OK;
   const int grid = (A->put_chunks_total + kPutWarps - 1) / kPutWarps;
   k_halo_put<<<grid, 32 * kPutWarps, 0, s>>>(A->halo_puts.get(), A->n_puts, A->put_chunks_total, x,
-                                            (unsigned long long)A->epoch, A->halo_err.get());
+                                            A->d_epoch.get(), A->halo_err.get());
   SP_LAUNCH();
   return SPMAT_OK;
 }
 
 // off-diagonal SpMV-add gated on the epoch's halo; with compute == false it only waits and
-// releases (halo-only timing)
+// releases (halo-only timing).  Always launched: it also ends the MatMult's epoch.
 int halo_peer_offdiag(spmat_s *A, double *y, cudaStream_t s, bool compute) {
-  if (A->n_waits == 0 && (!compute || A->n_ro == 0)) return SPMAT_OK;
   const int64_t nro = compute ? A->n_ro : 0;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nro + 255) / 256, 4L * A->comm->num_sms));
   k_spmv_offdiag_peer<<<grid, 256, 0, s>>>(A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(),
                                            A->val_o.get(), A->lvec.get(), A->lvec_stride, y, nro,
                                            A->halo_waits.get(), A->n_waits,
-                                           (unsigned long long)A->epoch, A->halo_counter.get(),
+                                           A->d_epoch.get(), A->halo_counter.get(),
                                            A->halo_err.get(), 1);
   SP_LAUNCH();
   return SPMAT_OK;

@@ -135,7 +135,7 @@ struct Comm {
   DevBuf<double *> d_peer_val;                      // per rank: its val array (self included)
   DevBuf<unsigned long long *> d_peer_flag;
   DevBuf<int> board_err;
-  int64_t board_epoch = 0;
+  DevBuf<unsigned long long> d_board_epoch;  // completed board reductions (device, graph-safe)
 };
 int board_setup(Comm *c);      // collective; leaves board_ok false when IPC is unavailable
 void board_release(Comm *c);
@@ -215,14 +215,19 @@ struct HaloWait {                      // one sender of my ghost entries
 struct SpmvHalo {                      // fused NVLink halo puts (comm warps)
   const HaloPut *puts;
   int nputs, put_chunks;
-  unsigned long long epoch;
+  // device epoch counter (NVLink mode, else nullptr): this MatMult is epoch *epoch_ctr + 1;
+  // with bump, the kernel's last CTA stores it back (the MatMult ends in this kernel).
+  // Device-side so that MatMults can be captured in CUDA graphs and replayed.
+  unsigned long long *epoch_ctr;
+  int bump;
   int *err;
 };
 struct SpmvTail {                      // fused off-diagonal SpMV-add (work items in the claim order)
   int n_bblocks, enabled;              // boundary blocks are the first n_bblocks in claim order
   int t0, n_items;                     // claim indices [t0, t0+n_items) are off-diagonal items
   const int32_t *rows, *rowptr, *col;  // compressed off-diagonal block
-  const double *val, *lvec;            // lvec: this epoch's ghost buffer
+  const double *val, *lvec;            // lvec: ghost buffers, buffer (epoch & 1) at lvec_stride
+  int64_t lvec_stride;
   int64_t n_ro;
   const HaloWait *waits;
   int nwaits, pad;
@@ -292,8 +297,13 @@ struct spmat_s {
   spmat::DevBuf<unsigned int> halo_counter;
   spmat::DevBuf<int> halo_err;
   int n_puts = 0, n_waits = 0, put_chunks_total = 0;
-  int64_t epoch = 0;
+  spmat::DevBuf<unsigned long long> d_epoch;  // completed NVLink-halo MatMults (device)
   int64_t lvec_stride = 0;          // peer mode: lvec holds two epochs' ghost buffers
+  // CUDA graph of one CG iteration (krylov.cu), keyed by the caller's x / history pointers
+  cudaGraphExec_t cg_exec = nullptr;
+  const void *cg_key_x = nullptr, *cg_key_h = nullptr;
+  cudaStream_t cg_stream = nullptr;
+  cudaEvent_t cg_ev[2] = {nullptr, nullptr};
   // 3x3 block-CSR copy of the diagonal block (bsr.cu), after spmat_set_block_size(A, 3)
   int bs = 1;
   int64_t mb = 0, nnzb = 0, n_brblocks = 0;
@@ -318,6 +328,7 @@ int spmv_prepare(spmat_s *A, cudaStream_t stream);  // row blocks + kernel choic
 int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream, bool fuse_put = false,
               bool fuse_tail = false);
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
+void cg_graph_release(spmat_s *A);            // drop the captured CG iteration
 int bsr_refresh(spmat_s *A, cudaStream_t s);  // bval from the CSR values
 int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s);
 // host-buffer pipeline (single rank): row chunks of the diagonal SpMV

@@ -12,6 +12,10 @@
 //
 // Local dot products use a fixed decomposition (kDotBlocks CTAs x 256 threads, fixed strides,
 // fixed reduction trees), so results are deterministic run to run.
+//
+// Every epoch (halo, board) and the residual-history index live in device memory, so one CG
+// iteration is captured once as a CUDA graph and replayed maxit times (SPMAT_GRAPH=0 turns the
+// graph off): the launch cost of ~6 kernels per iteration becomes one graph launch.
 #include <algorithm>
 #include <cstring>
 
@@ -31,9 +35,11 @@ int board_setup(Comm *c) {
   SP_TRY(c->board_val.alloc(2 * (size_t)P * W));
   SP_TRY(c->board_flag.alloc(2 * (size_t)P));
   SP_TRY(c->board_err.alloc(1));
+  SP_TRY(c->d_board_epoch.alloc(1));
   SP_CUDA(cudaMemset(c->board_val.get(), 0, 2 * P * W * sizeof(double)));
   SP_CUDA(cudaMemset(c->board_flag.get(), 0, 2 * P * sizeof(unsigned long long)));
   SP_CUDA(cudaMemset(c->board_err.get(), 0, sizeof(int)));
+  SP_CUDA(cudaMemset(c->d_board_epoch.get(), 0, sizeof(unsigned long long)));
   cudaIpcMemHandle_t hv, hf;
   memset(&hv, 0, sizeof hv);
   memset(&hf, 0, sizeof hf);
@@ -81,7 +87,6 @@ int board_setup(Comm *c) {
   SP_CUDA(cudaMemcpy(c->d_peer_val.get(), pv.data(), P * sizeof(double *), cudaMemcpyHostToDevice));
   SP_CUDA(cudaMemcpy(c->d_peer_flag.get(), pf.data(), P * sizeof(void *), cudaMemcpyHostToDevice));
   c->board_ok = true;
-  c->board_epoch = 0;
   return SPMAT_OK;
 }
 
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(kDotThreads) k_cg_init(const double *__restric
 
 struct CgScalars {
   double rr, pq, alpha, beta;
-  int stopped, pad;
+  int stopped, iter;  // iter: index of the last residual-history entry written
 };
 
 // x = x + alpha p; r = r - alpha q; partial of r.r (products rounded separately, no FMA)
@@ -181,13 +186,12 @@ __global__ void k_cg_pupdate(double *__restrict__ p, const double *__restrict__ 
 enum { OP_DOT = 0, OP_CG_INIT = 1, OP_CG_ALPHA = 2, OP_CG_BETA = 3 };
 
 // One CTA: local sum of the partials (fixed order), the cross-rank sum through the scalar
-// board (or the value already all-reduced by NCCL when board == nullptr and P > 1), then
-// the scalar step of CG.
+// board (or the value already all-reduced by NCCL when preduced != nullptr), then the scalar
+// step of CG.  The board epoch is read from and written back to device memory.
 __global__ void __launch_bounds__(kDotThreads) k_finalize(
     const double *__restrict__ partial, int np, int op, CgScalars *sc, double *result,
-    double *__restrict__ hist, int hist_k, double *const *peer_val,
-    unsigned long long *const *peer_flag, int P, int me, unsigned long long epoch, int *err,
-    const double *preduced) {
+    double *__restrict__ hist, double *const *peer_val, unsigned long long *const *peer_flag, int P,
+    int me, unsigned long long *board_epoch, int *err, const double *preduced) {
   __shared__ double red[kDotThreads / 32];
   __shared__ double total;
   double s = 0.0;
@@ -198,6 +202,7 @@ __global__ void __launch_bounds__(kDotThreads) k_finalize(
   if (preduced) {  // NCCL already summed the local values over ranks
     if (threadIdx.x == 0) total = *preduced;
   } else if (peer_val) {
+    const unsigned long long epoch = *board_epoch + 1ull;
     const int par = (int)(epoch & 1);
     const int W = Comm::kBoardWidth;
     if (threadIdx.x < P) {  // my partial into every rank's board, then its flag
@@ -215,6 +220,7 @@ __global__ void __launch_bounds__(kDotThreads) k_finalize(
       const double *v = peer_val[me] + (size_t)par * P * W;
       for (int q = 0; q < P; ++q) t = __dadd_rn(t, __ldcg(v + (size_t)q * W));  // rank order
       total = t;
+      *board_epoch = epoch;
     }
     __syncthreads();
   }
@@ -225,6 +231,7 @@ __global__ void __launch_bounds__(kDotThreads) k_finalize(
   } else if (op == OP_CG_INIT) {
     sc->rr = g;
     sc->stopped = g == 0.0 ? 1 : 0;
+    sc->iter = 0;
     if (hist) hist[0] = g;
   } else if (op == OP_CG_ALPHA) {
     sc->pq = g;
@@ -235,7 +242,8 @@ __global__ void __launch_bounds__(kDotThreads) k_finalize(
       sc->beta = g / sc->rr;
       sc->rr = g;
     }
-    if (hist) hist[hist_k] = sc->rr;
+    sc->iter += 1;
+    if (hist) hist[sc->iter] = sc->rr;
   }
 }
 
@@ -251,30 +259,66 @@ static int ensure_ws(spmat_s *A) {
 }
 
 // global sum of partials -> op; cross-rank through the board or ncclAllReduce
-static int finalize(spmat_s *A, int op, double *result, double *hist, int hist_k, cudaStream_t s) {
+static int finalize(spmat_s *A, int op, double *result, double *hist, cudaStream_t s) {
   Comm *c = A->comm;
   const int np = dot_blocks(A);
   CgScalars *sc = (CgScalars *)A->cg_scalars.get();
   if (c->nranks > 1 && !c->board_ok) {
     // local sum first, then NCCL all-reduce of the scalar, then the scalar step
     k_finalize<<<1, kDotThreads, 0, s>>>(A->cg_partial.get(), np, OP_DOT, sc, A->cg_reduced.get(),
-                                         nullptr, 0, nullptr, nullptr, 1, 0, 0, nullptr, nullptr);
+                                         nullptr, nullptr, nullptr, 1, 0, nullptr, nullptr, nullptr);
     SP_LAUNCH();
     SP_NCCL(c->api, c->api->AllReduce(A->cg_reduced.get(), A->cg_reduced.get() + 1, 1, ncclFloat64,
                                       ncclSum, c->nccl, s));
-    k_finalize<<<1, kDotThreads, 0, s>>>(A->cg_partial.get(), 0, op, sc, result, hist, hist_k,
-                                         nullptr, nullptr, 1, 0, 0, nullptr, A->cg_reduced.get() + 1);
+    k_finalize<<<1, kDotThreads, 0, s>>>(A->cg_partial.get(), 0, op, sc, result, hist, nullptr, nullptr,
+                                         1, 0, nullptr, nullptr, A->cg_reduced.get() + 1);
     SP_LAUNCH();
     return SPMAT_OK;
   }
   const bool board = c->nranks > 1;
-  unsigned long long epoch = board ? (unsigned long long)(++c->board_epoch) : 0ull;
-  k_finalize<<<1, kDotThreads, 0, s>>>(A->cg_partial.get(), np, op, sc, result, hist, hist_k,
+  k_finalize<<<1, kDotThreads, 0, s>>>(A->cg_partial.get(), np, op, sc, result, hist,
                                        board ? c->d_peer_val.get() : nullptr,
                                        board ? c->d_peer_flag.get() : nullptr, c->nranks, c->rank,
-                                       epoch, board ? c->board_err.get() : nullptr, nullptr);
+                                       board ? c->d_board_epoch.get() : nullptr,
+                                       board ? c->board_err.get() : nullptr, nullptr);
   SP_LAUNCH();
   return SPMAT_OK;
+}
+
+// one CG iteration on stream s (captured into a graph, or launched directly)
+static int cg_iteration(spmat_s *A, double *x, double *rr_hist, cudaStream_t s) {
+  const int64_t m = A->m;
+  double *r = A->cg_r.get(), *p = A->cg_p.get(), *q = A->cg_q.get();
+  CgScalars *sc = (CgScalars *)A->cg_scalars.get();
+  const int nb = dot_blocks(A);
+  const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)A->comm->num_sms * 8));
+  SP_TRY(spmat_mult_part(A, p, q, 7, s));                            // q = A p
+  k_dot_partial<<<nb, kDotThreads, 0, s>>>(p, q, m, A->cg_partial.get());
+  SP_LAUNCH();
+  SP_TRY(finalize(A, OP_CG_ALPHA, nullptr, nullptr, s));            // alpha = rr / p.q
+  k_cg_update<<<nb, kDotThreads, 0, s>>>(x, r, p, q, m, sc, A->cg_partial.get());
+  SP_LAUNCH();
+  SP_TRY(finalize(A, OP_CG_BETA, nullptr, rr_hist, s));             // beta, rr = r.r
+  k_cg_pupdate<<<gv, 256, 0, s>>>(p, r, m, sc);                     // p = r + beta p
+  SP_LAUNCH();
+  return SPMAT_OK;
+}
+
+static bool graph_ok(spmat_s *A) {
+  const char *e = getenv("SPMAT_GRAPH");
+  if (e && !strcmp(e, "0")) return false;
+  if (A->profile) return false;
+  if (A->comm->nranks == 1) return true;
+  return A->peer && A->comm->board_ok;  // NCCL stays out of captured graphs
+}
+
+void cg_graph_release(spmat_s *A) {
+  if (A->cg_exec) cudaGraphExecDestroy(A->cg_exec);
+  A->cg_exec = nullptr;
+  if (A->cg_stream) cudaStreamDestroy(A->cg_stream);
+  A->cg_stream = nullptr;
+  for (auto &e : A->cg_ev)
+    if (e) cudaEventDestroy(e), e = nullptr;
 }
 
 }  // namespace spmat
@@ -290,7 +334,7 @@ int spmat_vec_dot(spmat_t A, const double *a, const double *b, double *result, v
   SP_TRY(ensure_ws(A));
   k_dot_partial<<<dot_blocks(A), kDotThreads, 0, s>>>(a, b, A->m, A->cg_partial.get());
   SP_LAUNCH();
-  return finalize(A, OP_DOT, result, nullptr, 0, s);
+  return finalize(A, OP_DOT, result, nullptr, s);
 }
 
 int spmat_cg(spmat_t A, const double *b, double *x, int maxit, double *rr_hist, void *stream) {
@@ -303,31 +347,52 @@ int spmat_cg(spmat_t A, const double *b, double *x, int maxit, double *rr_hist, 
   cudaStream_t s = (cudaStream_t)stream;
   SP_TRY(ensure_ws(A));
   const int64_t m = A->m;
-  if (A->cg_r.n < (size_t)m) {
+  if (A->cg_r.n < (size_t)m || A->cg_r.n == 0) {
     SP_TRY(A->cg_r.alloc(std::max<int64_t>(m, 1)));
     SP_TRY(A->cg_p.alloc(std::max<int64_t>(m, 1)));
     SP_TRY(A->cg_q.alloc(std::max<int64_t>(m, 1)));
   }
   double *r = A->cg_r.get(), *p = A->cg_p.get(), *q = A->cg_q.get();
-  CgScalars *sc = (CgScalars *)A->cg_scalars.get();
   const int nb = dot_blocks(A);
-  const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)A->comm->num_sms * 8));
-  // r = b - A x; p = r; rr = r.r
-  SP_TRY(spmat_mult_part(A, x, q, 7, stream));
-  k_cg_init<<<nb, kDotThreads, 0, s>>>(b, q, r, p, m, A->cg_partial.get());
-  SP_LAUNCH();
-  SP_TRY(finalize(A, OP_CG_INIT, nullptr, rr_hist, 0, s));
-  for (int k = 0; k < maxit; ++k) {
-    SP_TRY(spmat_mult_part(A, p, q, 7, stream));                       // q = A p
-    k_dot_partial<<<nb, kDotThreads, 0, s>>>(p, q, m, A->cg_partial.get());
-    SP_LAUNCH();
-    SP_TRY(finalize(A, OP_CG_ALPHA, nullptr, nullptr, 0, s));          // alpha = rr / p.q
-    k_cg_update<<<nb, kDotThreads, 0, s>>>(x, r, p, q, m, sc, A->cg_partial.get());
-    SP_LAUNCH();
-    SP_TRY(finalize(A, OP_CG_BETA, nullptr, rr_hist, k + 1, s));      // beta, rr = r.r
-    k_cg_pupdate<<<gv, 256, 0, s>>>(p, r, m, sc);                      // p = r + beta p
-    SP_LAUNCH();
+  const bool use_graph = graph_ok(A) && maxit > 0;
+  cudaStream_t cs = s;
+  if (use_graph) {  // our own stream (capturable even when the caller uses the legacy stream)
+    if (!A->cg_stream) {
+      SP_CUDA(cudaStreamCreateWithFlags(&A->cg_stream, cudaStreamNonBlocking));
+      SP_CUDA(cudaEventCreateWithFlags(&A->cg_ev[0], cudaEventDisableTiming));
+      SP_CUDA(cudaEventCreateWithFlags(&A->cg_ev[1], cudaEventDisableTiming));
+    }
+    cs = A->cg_stream;
+    SP_CUDA(cudaEventRecord(A->cg_ev[0], s));
+    SP_CUDA(cudaStreamWaitEvent(cs, A->cg_ev[0], 0));
   }
+  // r = b - A x; p = r; rr = r.r
+  SP_TRY(spmat_mult_part(A, x, q, 7, cs));
+  k_cg_init<<<nb, kDotThreads, 0, cs>>>(b, q, r, p, m, A->cg_partial.get());
+  SP_LAUNCH();
+  SP_TRY(finalize(A, OP_CG_INIT, nullptr, rr_hist, cs));
+  if (!use_graph) {
+    for (int k = 0; k < maxit; ++k) SP_TRY(cg_iteration(A, x, rr_hist, s));
+    return SPMAT_OK;
+  }
+  if (!A->cg_exec || A->cg_key_x != x || A->cg_key_h != rr_hist) {
+    if (A->cg_exec) cudaGraphExecDestroy(A->cg_exec);
+    A->cg_exec = nullptr;
+    cudaGraph_t graph;
+    SP_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    int st = cg_iteration(A, x, rr_hist, cs);
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
+    if (st != SPMAT_OK) return st;
+    if (e != cudaSuccess) return fail(SPMAT_ERR_CUDA, "spmat_cg: graph capture: %s", cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&A->cg_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(SPMAT_ERR_CUDA, "spmat_cg: graph instantiate: %s", cudaGetErrorString(e));
+    A->cg_key_x = x;
+    A->cg_key_h = rr_hist;
+  }
+  for (int k = 0; k < maxit; ++k) SP_CUDA(cudaGraphLaunch(A->cg_exec, cs));
+  SP_CUDA(cudaEventRecord(A->cg_ev[1], cs));
+  SP_CUDA(cudaStreamWaitEvent(s, A->cg_ev[1], 0));
   return SPMAT_OK;
 }
 

@@ -31,7 +31,8 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
   if (multi && A->peer) {  // device-initiated halo over NVLink (halo.cu)
     bool fused = false;
     if (part & 2) {
-      ++A->epoch;
+      // the epoch lives on the device (A->d_epoch): kernels read it, the MatMult's last kernel
+      // advances it -- so MatMults can be captured in CUDA graphs.
       // the bulk-copy SpMV's comm warps do the puts; otherwise a standalone put kernel
       fused = (part & 1) && A->kernel_id == 3 && A->m > 0 && A->n_rowblocks > 0;
       if (!fused) {

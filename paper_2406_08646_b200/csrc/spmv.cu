@@ -180,10 +180,13 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // this MatMult's halo epoch: read by every CTA before any claim, so before the last CTA
+  // (which only exists once every CTA has claimed) stores it back
+  const unsigned long long epoch = halo.epoch_ctr ? *halo.epoch_ctr + 1ull : 0ull;
   __syncthreads();
   if (warp == kConsumerWarps + 1) {  // ---------------- comm warp: fused halo puts (halo.cu)
     for (int c = blockIdx.x; c < halo.put_chunks; c += gridDim.x)
-      halo_put_warp(halo.puts, halo.nputs, c, x, halo.epoch, halo.err);
+      halo_put_warp(halo.puts, halo.nputs, c, x, epoch, halo.err);
     return;
   }
   if (warp == kConsumerWarps) {  // ---------------- producer warp
@@ -213,6 +216,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
         if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
           atomicExch(sched, 0u);
           atomicExch(sched + 1, 0u);
+          if (halo.bump && halo.epoch_ctr) *halo.epoch_ctr = epoch;  // this MatMult is done
         }
         return;
       }
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
           __nanosleep(32);
         }
         for (int w = 0; w < tail.nwaits; ++w)
-          spin_until_geq(tail.waits[w].my_ready, halo.epoch * (unsigned long long)tail.waits[w].nchunk, halo.err);
+          spin_until_geq(tail.waits[w].my_ready, epoch * (unsigned long long)tail.waits[w].nchunk, halo.err);
       }
       asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
       if (itr && tid == 0) itr[1] = gtimer();
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
       if (q < tail.n_ro) {
         double sacc = 0.0;
         for (int e = tail.rowptr[q]; e < tail.rowptr[q + 1]; ++e)
-          sacc = __dadd_rn(sacc, __dmul_rn(tail.val[e], __ldcg(tail.lvec + tail.col[e])));
+          sacc = __dadd_rn(sacc, __dmul_rn(tail.val[e], __ldcg(tail.lvec + (epoch & 1) * tail.lvec_stride + tail.col[e])));
         const int r = tail.rows[q];
         y[r] = __dadd_rn(__ldcg(y + r), sacc);
       }
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
           atomicExch(tail.ctr, 0u);
           atomicExch(tail.ctr + 1, 0u);
           __threadfence();
-          for (int w = 0; w < tail.nwaits; ++w) st_release_sys(tail.waits[w].peer_done, halo.epoch);
+          for (int w = 0; w < tail.nwaits; ++w) st_release_sys(tail.waits[w].peer_done, epoch);
         }
       }
       __syncwarp();
@@ -421,8 +425,12 @@ __global__ void __launch_bounds__(256) k_spmv_offdiag(const int32_t *__restrict_
                                                       const int32_t *__restrict__ rowptr,
                                                       const int32_t *__restrict__ col,
                                                       const double *__restrict__ val,
-                                                      const double *__restrict__ lvec,
+                                                      const double *__restrict__ lvec_base,
+                                                      int64_t lvec_stride,
+                                                      const unsigned long long *__restrict__ epoch_ctr,
                                                       double *__restrict__ y, int64_t nro) {
+  // ghost buffer of the last completed epoch (NVLink mode) or the single buffer (NCCL)
+  const double *lvec = lvec_base + (epoch_ctr ? (int64_t)(*epoch_ctr & 1ull) * lvec_stride : 0);
   GRID_STRIDE(q, nro) {
     double s = 0.0;
     for (int e = rowptr[q]; e < rowptr[q + 1]; ++e)
@@ -572,8 +580,10 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
 
 static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put,
                        bool fuse_tail) {
+  // the kernel ends the MatMult (bumps the device epoch) when it also runs the off-diagonal
+  // items; otherwise k_spmv_offdiag_peer does
   SpmvHalo h{A->halo_puts.get(), A->n_puts, fuse_put ? A->put_chunks_total : 0,
-             (unsigned long long)A->epoch, A->halo_err.get()};
+             A->peer ? A->d_epoch.get() : nullptr, (fuse_put && fuse_tail) ? 1 : 0, A->halo_err.get()};
   SpmvTail t{};
   t.t0 = (int)A->n_rowblocks;  // no items: every claim index is a row block
   if (fuse_tail) {
@@ -590,7 +600,8 @@ static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, b
     t.rowptr = A->rowptr_o.get();
     t.col = A->col_o.get();
     t.val = A->val_o.get();
-    t.lvec = A->lvec.get() + (A->epoch & 1) * A->lvec_stride;
+    t.lvec = A->lvec.get();
+    t.lvec_stride = A->lvec_stride;
     t.n_ro = A->n_ro;
     t.waits = A->halo_waits.get();
     t.nwaits = A->n_waits;
@@ -637,9 +648,9 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_
 
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t s) {
   if (A->n_ro == 0) return SPMAT_OK;
-  const double *lvec = A->lvec.get() + (A->peer ? (A->epoch & 1) * A->lvec_stride : 0);
   k_spmv_offdiag<<<nblk(A->n_ro), 256, 0, s>>>(A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(),
-                                              A->val_o.get(), lvec, y, A->n_ro);
+                                              A->val_o.get(), A->lvec.get(), A->lvec_stride,
+                                              A->peer ? A->d_epoch.get() : nullptr, y, A->n_ro);
   SP_LAUNCH();
   return SPMAT_OK;
 }
@@ -694,7 +705,7 @@ int spmv_pipe_prepare(spmat_s *A, int chunks) {
 int spmv_diag_chunk(spmat_s *A, const double *x, double *y, int k, cudaStream_t s) {
   const int64_t c0 = A->pipe_block[k], c1 = A->pipe_block[k + 1];
   if (c1 <= c0) return SPMAT_OK;
-  SpmvHalo h{A->halo_puts.get(), 0, 0, 0ull, A->halo_err.get()};
+  SpmvHalo h{A->halo_puts.get(), 0, 0, nullptr, 0, A->halo_err.get()};
   SpmvTail t{};
   t.t0 = (int)(c1 - c0);
   const unsigned grid = (unsigned)std::min<int64_t>(A->tma_grid, c1 - c0);

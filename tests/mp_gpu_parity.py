@@ -284,6 +284,16 @@ def case_cg(c):
     ga = synth.x_vector(0, M, "int", seed=4).numpy()
     gb = synth.x_vector(0, M, "int", seed=5).numpy()
     assert res.item() == float(np.dot(ga, gb))
+    # the CUDA-graph CG (device-side epochs) equals the eagerly launched one bit for bit
+    outs = []
+    for g in ("1", "0"):
+        os.environ["SPMAT_GRAPH"] = g
+        xg = torch.zeros(sizes[r], dtype=torch.float64, device="cuda")
+        A.cg(b, xg, iters)
+        A.cg(b, xg, 3)  # a second call replays the cached graph
+        outs.append(xg.cpu())
+    os.environ.pop("SPMAT_GRAPH")
+    assert torch.equal(outs[0], outs[1])
     A.check()
     A.close()
 

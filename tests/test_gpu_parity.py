@@ -492,3 +492,40 @@ def test_block_csr_3x3(sp, comm, values):
         B.set_block_size(3)
     assert e.value.status == sp.SPMAT_ERR_ARG
     B.close()
+
+
+def test_cuda_graphs(sp, comm, monkeypatch):
+    """MatMult is capturable in a (torch) CUDA graph, and the graph-replayed CG iteration
+    equals the eagerly launched one bit for bit."""
+    n = 40
+    M = n ** 3
+    i, j, v = synth.stencil_coo((n, n, n), 7, values="real")
+    A = sp.Mat(comm, M, M, M, M, dev(i), dev(j))
+    A.set_values(dev(v))
+    x = synth.x_vector(0, M, "real", device="cuda")
+    y0 = torch.empty(M, dtype=torch.float64, device="cuda")
+    A.mult(x, y0)
+    y = torch.zeros(M, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        A.mult(x, y, s)  # warm-up on the capture stream
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        A.mult(x, y, s)
+    y.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, y0)
+    b = synth.x_vector(0, M, "real", seed=2, device="cuda")
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SPMAT_GRAPH", flag)
+        xg = torch.zeros(M, dtype=torch.float64, device="cuda")
+        hist = torch.zeros(21, dtype=torch.float64, device="cuda")
+        A.cg(b, xg, 20, hist)
+        outs.append((xg.cpu(), hist.cpu()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    A.close()
