@@ -35,6 +35,14 @@ int fail(int status, const char *fmt, ...) {
   return status;
 }
 
+bool pdl_on() {
+  static const bool on = [] {
+    const char *e = getenv("SPMAT_PDL");
+    return !(e && !strcmp(e, "0"));
+  }();
+  return on;
+}
+
 bool is_device_ptr(const void *p) {
   if (!p) return false;
   cudaPointerAttributes attr;

@@ -6,24 +6,26 @@
 // as measured here on B200, an NCCL p2p kernel whose handshakes crawl while the SpMV keeps
 // HBM saturated (the 17 us transfer then completes only after the SpMV).
 //
-// B200 design: at create time every rank exports its ghost vector (lvec) and a small flag
-// array through CUDA IPC; each owner opens the lvec of the ranks that need its rows and
-// learns where in their lvec its values go (the halo SF leaves are contiguous per owner).
-// Per MatMult (epoch e):
-//   k_halo_put (high-priority comm stream, a few CTAs per destination): wait until the
-//     destination has finished reading epoch e-1 (done flag), store the owned x entries
-//     straight into the destination's lvec over NVLink, fence, then bump the destination's
-//     ready counter (release, system scope);
-//   k_spmv_offdiag_peer (caller's stream, after the diagonal SpMV): wait until every
-//     sender's ready counter shows epoch e (acquire), add A_o lvec into y, and the last CTA
-//     tells each sender that lvec may be overwritten (done = e).
-// The transfer (0.5-1 MB) overlaps the diagonal SpMV completely; no NCCL kernel, no host
+// B200 design: at create time every rank exports its ghost buffer and a small flag array
+// through CUDA IPC; each owner opens the ghost buffer of the ranks that need its rows and
+// learns where its values go (the halo SF leaves are contiguous per owner).  Ghost values
+// travel as flagged 16-byte lines {value, epoch} (halo_dev.cuh): the flag in the line is the
+// readiness signal, so a put is stores only and a reader waits per value.
+// Per MatMult (epoch e, kept on the device):
+//   put (comm warps of the diagonal SpMV, or k_halo_put): wait until the destination has
+//     finished reading epoch e-2 (done flag; two buffers by epoch parity), store the owned x
+//     entries as lines flagged e straight into the destination's buffer over NVLink;
+//   off-diagonal SpMV-add (the fused kernel's tail items, or k_spmv_offdiag_peer): read each
+//     ghost line until it carries flag e, add A_o lvec into y; the last CTA tells every sender
+//     that the buffer may be overwritten (done = e) and advances the epoch.
+// The transfer (0.5-2 MB of lines) overlaps the diagonal SpMV; no NCCL kernel, no host
 // synchronisation.  Spins are bounded (a stuck peer sets an error word instead of hanging).
 #include <algorithm>
 #include <cstring>
 
 #include "halo_dev.cuh"
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace spmat {
 
@@ -37,38 +39,36 @@ static inline int put_chunks(int64_t count) {
 __global__ void __launch_bounds__(32 * kPutWarps) k_halo_put(const HaloPut *__restrict__ puts, int nputs,
                                                              int total, const double *__restrict__ x,
                                                              const unsigned long long *epoch_ctr, int *err) {
+  pdl_wait();
   const int c = blockIdx.x * kPutWarps + (threadIdx.x >> 5);
   if (c < total) halo_put_warp(puts, nputs, c, x, *epoch_ctr + 1ull, err);
 }
 
-// y[rows[q]] += A_o lvec, after the senders' epoch-e data has landed; the last CTA releases lvec
+// y[rows[q]] += A_o lvec with this MatMult's ghost lines (each read waits for its flag); with
+// nro == 0 it only waits until all n_ghost lines have landed (halo-only timing).  The last
+// CTA releases the buffer to the senders and advances the epoch.
 __global__ void __launch_bounds__(256) k_spmv_offdiag_peer(
     const int32_t *__restrict__ rows, const int32_t *__restrict__ rowptr,
-    const int32_t *__restrict__ col, const double *__restrict__ val, const double *lvec_base,
-    int64_t lvec_stride, double *__restrict__ y, int64_t nro, const HaloWait *__restrict__ waits, int nwaits,
-    unsigned long long *epoch_ctr, unsigned int *counter, int *err, int signal) {
-  __shared__ int ok;
+    const int32_t *__restrict__ col, const double *__restrict__ val, const uint4 *ghost_base,
+    int64_t ghost_stride, int64_t n_ghost, double *__restrict__ y, int64_t nro, int W,
+    const HaloWait *__restrict__ waits, int nwaits, unsigned long long *epoch_ctr,
+    unsigned int *counter, int *err) {
+  pdl_wait();
   // this MatMult's epoch; every CTA reads it before its arrival on `counter`, so before the
   // last CTA stores it back
   const unsigned long long epoch = *epoch_ctr + 1ull;
-  if (threadIdx.x == 0) {
-    int good = 1;
-    for (int w = 0; w < nwaits && good; ++w)
-      good = spin_until_geq(waits[w].my_ready, epoch * (unsigned long long)waits[w].nchunk, err);
-    ok = good;
-  }
-  __syncthreads();
-  const double *lvec = lvec_base + (int64_t)(epoch & 1) * lvec_stride;
-  if (ok) {
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nro;
-         q += (int64_t)gridDim.x * blockDim.x) {
-      double s = 0.0;
-      for (int e = rowptr[q]; e < rowptr[q + 1]; ++e) s = __dadd_rn(s, __dmul_rn(val[e], __ldcg(lvec + col[e])));
-      const int r = rows[q];
-      y[r] = __dadd_rn(y[r], s);
+  const uint32_t flag = ll_flag(epoch);
+  const uint4 *gl = ghost_base + (int64_t)(epoch & 1) * ghost_stride;
+  if (nro > 0) {  // block-uniform loop bound: every lane reaches the shuffles in offdiag_row_w
+    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < nro * W; t0 += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t q = (t0 + threadIdx.x) / W;
+      offdiag_row_w(q, q < nro, W, rows, rowptr, col, val,
+                    [&](int c) { return ll_load(gl + c, flag, err); }, y);
     }
+  } else {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_ghost; g += (int64_t)gridDim.x * blockDim.x)
+      (void)ll_load(gl + g, flag, err);
   }
-  if (!signal) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -98,16 +98,18 @@ int halo_peer_setup(spmat_s *A) {
     SP_TRY(c->allreduce_max_i64(vote0, 2));
     if (vote0[0] || vote0[1]) return SPMAT_OK;  // NCCL halo on every rank
   }
-  SP_TRY(A->halo_flags.alloc(2 * (size_t)P));  // [0,P): ready from sender q; [P,2P): done from receiver q
-  SP_CUDA(cudaMemset(A->halo_flags.get(), 0, 2 * P * sizeof(unsigned long long)));
-  // two ghost buffers (epoch parity) so an owner never waits for the previous epoch's reads
-  A->lvec_stride = std::max<int64_t>(A->n_ghost, 1);
-  SP_TRY(A->lvec.alloc(2 * (size_t)A->lvec_stride));
+  SP_TRY(A->halo_flags.alloc(P));  // [q]: done flag from receiver q
+  SP_CUDA(cudaMemset(A->halo_flags.get(), 0, P * sizeof(unsigned long long)));
+  // two ghost buffers (epoch parity) so an owner never waits for the previous epoch's reads;
+  // zeroed lines carry flag 0, which no epoch (>= 1) matches
+  A->ghost_stride = std::max<int64_t>(A->n_ghost, 1);
+  SP_TRY(A->ghost.alloc(2 * (size_t)A->ghost_stride));
+  SP_CUDA(cudaMemset(A->ghost.get(), 0, A->ghost.n * sizeof(uint4)));
   cudaIpcMemHandle_t hl, hf;
   memset(&hl, 0, sizeof hl);
   memset(&hf, 0, sizeof hf);
   if (want && !fail) {
-    if (cudaIpcGetMemHandle(&hl, A->lvec.get()) != cudaSuccess ||
+    if (cudaIpcGetMemHandle(&hl, A->ghost.get()) != cudaSuccess ||
         cudaIpcGetMemHandle(&hf, A->halo_flags.get()) != cudaSuccess) {
       cudaGetLastError();
       fail = 1;
@@ -122,10 +124,10 @@ int halo_peer_setup(spmat_s *A) {
   std::vector<int64_t> mine(17 + P, -1), all((size_t)(17 + P) * P);
   memcpy(mine.data(), &hl, 64);
   memcpy(mine.data() + 8, &hf, 64);
-  mine[16] = A->lvec_stride;
+  mine[16] = A->ghost_stride;
   for (size_t a = 0; a < sf->rnbr.size(); ++a) mine[17 + sf->rnbr[a]] = sf->leaf_start[a];
   SP_TRY(c->allgather_i64(mine.data(), 17 + P, all.data()));
-  A->peer_lvec.assign(P, nullptr);
+  A->peer_ghost.assign(P, nullptr);
   A->peer_flags.assign(P, nullptr);
   int64_t open_fail = 0;
   auto open_rank = [&](int q) {
@@ -141,7 +143,7 @@ int halo_peer_setup(spmat_s *A) {
       if (p1) cudaIpcCloseMemHandle(p1);
       return;
     }
-    A->peer_lvec[q] = (double *)p1;
+    A->peer_ghost[q] = (uint4 *)p1;
     A->peer_flags[q] = (unsigned long long *)p2;
   };
   for (int q : sf->snbr) open_rank(q);
@@ -159,13 +161,12 @@ int halo_peer_setup(spmat_s *A) {
     const int q = sf->snbr[a];
     const int64_t lstart = all[(size_t)(17 + P) * q + 17 + me];
     HaloPut p;
-    p.dst = A->peer_lvec[q] + lstart;
+    p.dst = A->peer_ghost[q] + lstart;
     p.dst_stride = all[(size_t)(17 + P) * q + 16];
     p.count = sf->scount[a];
     p.root_start = sf->root_start[a] >= 0 ? sf->root_start[a] : 0;
     p.root_idx = sf->root_start[a] >= 0 ? nullptr : sf->d_root_idx.get() + sf->soff[a];
-    p.peer_ready = A->peer_flags[q] + me;
-    p.my_done = A->halo_flags.get() + P + q;
+    p.my_done = A->halo_flags.get() + q;
     p.nchunk = put_chunks(p.count);
     total_chunks += p.nchunk;
     puts.push_back(p);
@@ -174,9 +175,7 @@ int halo_peer_setup(spmat_s *A) {
   for (size_t a = 0; a < sf->rnbr.size(); ++a) {
     const int q = sf->rnbr[a];
     HaloWait w;
-    w.my_ready = A->halo_flags.get() + q;
-    w.nchunk = put_chunks(sf->rcount[a]);
-    w.peer_done = A->peer_flags[q] + P + me;
+    w.peer_done = A->peer_flags[q] + me;
     waits.push_back(w);
   }
   SP_TRY(A->halo_puts.alloc(puts.size()));
@@ -202,11 +201,11 @@ int halo_peer_setup(spmat_s *A) {
 }
 
 void halo_peer_release(spmat_s *A) {
-  for (size_t q = 0; q < A->peer_lvec.size(); ++q) {
-    if (A->peer_lvec[q]) cudaIpcCloseMemHandle(A->peer_lvec[q]);
+  for (size_t q = 0; q < A->peer_ghost.size(); ++q) {
+    if (A->peer_ghost[q]) cudaIpcCloseMemHandle(A->peer_ghost[q]);
     if (A->peer_flags[q]) cudaIpcCloseMemHandle(A->peer_flags[q]);
   }
-  A->peer_lvec.clear();
+  A->peer_ghost.clear();
   A->peer_flags.clear();
   A->peer = false;
 }
@@ -221,17 +220,17 @@ int halo_peer_put(spmat_s *A, const double *x, cudaStream_t s) {
   return SPMAT_OK;
 }
 
-// off-diagonal SpMV-add gated on the epoch's halo; with compute == false it only waits and
-// releases (halo-only timing).  Always launched: it also ends the MatMult's epoch.
+// off-diagonal SpMV-add on the epoch's ghost lines; with compute == false it only waits for
+// them and releases (halo-only timing).  Always launched: it also ends the MatMult's epoch.
 int halo_peer_offdiag(spmat_s *A, double *y, cudaStream_t s, bool compute) {
   const int64_t nro = compute ? A->n_ro : 0;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nro + 255) / 256, 4L * A->comm->num_sms));
-  k_spmv_offdiag_peer<<<grid, 256, 0, s>>>(A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(),
-                                           A->val_o.get(), A->lvec.get(), A->lvec_stride, y, nro,
-                                           A->halo_waits.get(), A->n_waits,
-                                           A->d_epoch.get(), A->halo_counter.get(),
-                                           A->halo_err.get(), 1);
-  SP_LAUNCH();
+  const int64_t work = nro > 0 ? nro * A->ro_w : A->n_ghost;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 4L * A->comm->num_sms));
+  SP_CUDA(launch_pdl(k_spmv_offdiag_peer, grid, 256, 0, s, (const int32_t *)A->rows_o.get(),
+                     (const int32_t *)A->rowptr_o.get(), (const int32_t *)A->col_o.get(),
+                     (const double *)A->val_o.get(), (const uint4 *)A->ghost.get(), A->ghost_stride,
+                     A->n_ghost, y, nro, A->ro_w, (const HaloWait *)A->halo_waits.get(), A->n_waits,
+                     A->d_epoch.get(), A->halo_counter.get(), A->halo_err.get()));
   return SPMAT_OK;
 }
 

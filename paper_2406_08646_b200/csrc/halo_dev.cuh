@@ -4,7 +4,7 @@
 
 namespace spmat {
 
-constexpr int64_t kPutChunk = 1024;  // values per put warp
+constexpr int64_t kPutChunk = 256;  // values per put warp
 constexpr long long kSpinLimit = 20LL * 2000 * 1000 * 1000;  // ~20 s of SM clocks
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -19,9 +19,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 }
 __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void red_release_sys_add(unsigned long long *p, unsigned long long v) {
-  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // bounded spin; returns false on timeout (and records it in *err)
@@ -38,10 +35,46 @@ __device__ __forceinline__ bool spin_until_geq(const unsigned long long *flag,
   return true;
 }
 
+// ---- flagged lines ("LL" lines, as in NCCL's low-latency protocol)
+// A double travels with its epoch: one 16-byte line {lo32, flag, hi32, flag}, written by a
+// single 16-byte store and read by a single 16-byte load.  Each 8-byte half arrives whole, so
+// a reader that sees both flags equal to the epoch it expects has the complete value -- no
+// fence, no separate ready counter, no second NVLink round trip on the critical path.
+__device__ __forceinline__ void ll_store(uint4 *p, double v, uint32_t flag) {
+  const long long b = __double_as_longlong(v);
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"((uint32_t)b),
+               "r"(flag), "r"((uint32_t)(b >> 32)), "r"(flag)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ll_load_raw(const uint4 *p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+// the value of line p once it carries `flag` (bounded spin; 0.0 and *err = 1 on timeout)
+__device__ __forceinline__ double ll_load(const uint4 *p, uint32_t flag, int *err) {
+  uint4 v = ll_load_raw(p);
+  if (v.y != flag || v.w != flag) {
+    const long long t0 = clock64();
+    do {
+      if (clock64() - t0 > kSpinLimit) {
+        atomicExch(err, 1);
+        return 0.0;
+      }
+      v = ll_load_raw(p);
+    } while (v.y != flag || v.w != flag);
+  }
+  return __longlong_as_double((long long)(((unsigned long long)v.z << 32) | v.x));
+}
+__device__ __forceinline__ uint32_t ll_flag(unsigned long long epoch) { return (uint32_t)epoch; }
+
 // One warp moves put chunk c (global numbering over all destinations) of epoch `epoch`:
 // wait until the destination has released the ghost buffer of epoch-2 (double buffering),
-// store the owned x entries into the destination's lvec buffer (epoch & 1) over NVLink,
-// fence at system scope, then bump the destination's ready counter.
+// then store the owned x entries as flagged lines into the destination's ghost buffer
+// (epoch & 1) over NVLink.  Nothing else: the flags are the readiness signal.
 __device__ __forceinline__ void halo_put_warp(const HaloPut *__restrict__ puts, int nputs, int c,
                                               const double *__restrict__ x,
                                               unsigned long long epoch, int *err) {
@@ -54,7 +87,8 @@ __device__ __forceinline__ void halo_put_warp(const HaloPut *__restrict__ puts, 
   if (lane == 0 && epoch > 2) ok = spin_until_geq(p.my_done, epoch - 2, err) ? 1 : 0;
   ok = __shfl_sync(0xffffffffu, ok, 0);
   if (!ok) return;
-  double *dst = p.dst + (int64_t)(epoch & 1) * p.dst_stride;
+  uint4 *dst = p.dst + (int64_t)(epoch & 1) * p.dst_stride;
+  const uint32_t flag = ll_flag(epoch);
   const int64_t per = (p.count + p.nchunk - 1) / p.nchunk;
   const int64_t lo = c * per, hi = min(p.count, lo + per);
   constexpr int U = 8;
@@ -68,12 +102,31 @@ __device__ __forceinline__ void halo_put_warp(const HaloPut *__restrict__ puts, 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t t = t0 + 32 * u;
-      if (t < hi) dst[t] = v[u];
+      if (t < hi) ll_store(dst + t, v[u], flag);
     }
   }
-  __threadfence_system();
-  __syncwarp();
-  if (lane == 0) red_release_sys_add(p.peer_ready, 1ull);
+}
+
+// Off-diagonal SpMV-add with W lanes per row (W a power of two <= 32): thread t of a group
+// handles row q's entries rowptr[q]+t, +W, ... and the group sums by a shuffle tree.  Every
+// lane of the warp must call it (the shuffles); lanes with valid == false contribute nothing.
+// W = 1 is the plain left-to-right row sum.  ghost(c) returns ghost value c.
+template <class Ghost>
+__device__ __forceinline__ void offdiag_row_w(int64_t q, bool valid, int W,
+                                              const int32_t *__restrict__ rows,
+                                              const int32_t *__restrict__ rowptr,
+                                              const int32_t *__restrict__ col,
+                                              const double *__restrict__ val, Ghost ghost,
+                                              double *y) {
+  const int sub = threadIdx.x & (W - 1);
+  double s = 0.0;
+  if (valid)
+    for (int e = rowptr[q] + sub; e < rowptr[q + 1]; e += W) s = __dadd_rn(s, __dmul_rn(val[e], ghost(col[e])));
+  for (int o = W >> 1; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o, W));
+  if (valid && sub == 0) {
+    const int r = rows[q];
+    y[r] = __dadd_rn(__ldcg(y + r), s);
+  }
 }
 
 }  // namespace spmat

@@ -103,6 +103,25 @@ struct DevBuf {
   T *get() const { return p; }
 };
 
+// Launch with programmatic stream serialization (PDL, ptx.cuh) unless SPMAT_PDL=0: the
+// kernel's CTAs may start while the previous kernel of the stream drains.
+bool pdl_on();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // is `p` a device (or managed) pointer?
 bool is_device_ptr(const void *p);
 
@@ -125,15 +144,12 @@ struct Comm {
                    size_t elem_bytes, cudaStream_t stream);
 
   // Scalar board (krylov.cu): every rank's small device array, mapped into every other rank
-  // through CUDA IPC, for device-side all-reductions of a few scalars over NVLink.
-  // val[parity][src][kBoardWidth] doubles, flag[parity][src] epochs.
-  static constexpr int kBoardWidth = 4;
+  // through CUDA IPC, for device-side all-reductions of a scalar over NVLink.
+  // line[parity][src]: src's partial as a flagged 16-byte line (halo_dev.cuh).
   bool board_ok = false;
-  DevBuf<double> board_val;
-  DevBuf<unsigned long long> board_flag;
+  DevBuf<uint4> board_line;
   std::vector<void *> board_peer_mem;               // opened IPC mappings (to close)
-  DevBuf<double *> d_peer_val;                      // per rank: its val array (self included)
-  DevBuf<unsigned long long *> d_peer_flag;
+  DevBuf<uint4 *> d_peer_line;                      // per rank: its line array (self included)
   DevBuf<int> board_err;
   DevBuf<unsigned long long> d_board_epoch;  // completed board reductions (device, graph-safe)
 };
@@ -197,18 +213,15 @@ int sf_reduce_end_impl(sf_s *sf, const double *leaf, double *root, int op, cudaS
 
 // ------------------------------------------------------------------ device-initiated halo
 struct HaloPut {                       // one destination rank of my owned x entries
-  double *dst;                         // peer lvec + first leaf for me (IPC mapping)
-  int64_t dst_stride;                  // peer lvec buffer stride (double-buffered by epoch)
+  uint4 *dst;                          // peer ghost lines + first leaf for me (IPC mapping)
+  int64_t dst_stride;                  // peer ghost buffer stride in lines (double-buffered by epoch)
   int64_t count, root_start;           // contiguous x slice, or...
   const int64_t *root_idx;             // ...gather indices (device), nullptr if contiguous
-  unsigned long long *peer_ready;      // destination's ready counter for me (IPC mapping)
-  unsigned long long *my_done;         // destination -> me: "lvec free" epoch (local)
+  unsigned long long *my_done;         // destination -> me: "ghost buffer free" epoch (local)
   int nchunk, pad;
 };
 struct HaloWait {                      // one sender of my ghost entries
-  unsigned long long *my_ready;        // local counter the sender bumps once per chunk
-  unsigned long long *peer_done;       // sender's "lvec free" flag for me (IPC mapping)
-  int nchunk, pad;
+  unsigned long long *peer_done;       // sender's "ghost buffer free" flag for me (IPC mapping)
 };
 
 // kernel-parameter bundles of the bulk-copy SpMV
@@ -226,11 +239,12 @@ struct SpmvTail {                      // fused off-diagonal SpMV-add (work item
   int n_bblocks, enabled;              // boundary blocks are the first n_bblocks in claim order
   int t0, n_items;                     // claim indices [t0, t0+n_items) are off-diagonal items
   const int32_t *rows, *rowptr, *col;  // compressed off-diagonal block
-  const double *val, *lvec;            // lvec: ghost buffers, buffer (epoch & 1) at lvec_stride
-  int64_t lvec_stride;
+  const double *val;
+  const uint4 *ghost;                  // flagged ghost lines, buffer (epoch & 1) at ghost_stride
+  int64_t ghost_stride;
   int64_t n_ro;
   const HaloWait *waits;
-  int nwaits, pad;
+  int nwaits, w;                       // w: lanes per off-diagonal row (power of two <= 32)
   unsigned int *ctr;                   // [0] boundary-block warps done, [1] off-diagonal items done
   unsigned long long *trace;           // SPMAT_TRACE=1: globaltimer stamps (nullptr = off)
 };
@@ -247,6 +261,7 @@ struct spmat_s {
   spmat::DevBuf<double> val_d;
   // off-diagonal block: compressed rows
   int64_t nnz_o = 0, n_ro = 0;
+  int ro_w = 1;  // lanes per off-diagonal row in the SpMV-add kernels (offdiag_rows_w)
   spmat::DevBuf<int32_t> rows_o, rowptr_o, col_o;
   spmat::DevBuf<double> val_o;
   int64_t n_ghost = 0;
@@ -278,7 +293,7 @@ struct spmat_s {
   spmat::DevBuf<int4> blocks4;         // (r0, r1, p0, p1) per row block in claim order
   int64_t n_bblocks = 0;
   spmat::DevBuf<unsigned int> tail_ctr;
-  spmat::DevBuf<unsigned long long> trace;  // [cta][4] + [item][3] globaltimer stamps
+  spmat::DevBuf<unsigned long long> trace;  // [cta][4] + [item][4] globaltimer stamps
   spmat::DevBuf<unsigned int> sched; // its block counter + finished-CTA counter
   // host staging for host x / y
   spmat::DevBuf<double> xstage, ystage;
@@ -289,8 +304,9 @@ struct spmat_s {
   int64_t plan_builds = 0;
   // device-initiated halo over NVLink peer memory (halo.cu)
   bool peer = false;
-  spmat::DevBuf<unsigned long long> halo_flags;  // [0,P) ready counters, [P,2P) done flags
-  std::vector<double *> peer_lvec;
+  spmat::DevBuf<unsigned long long> halo_flags;  // [q]: done flag from receiver q
+  spmat::DevBuf<uint4> ghost;    // flagged ghost lines (halo_dev.cuh), two epochs' buffers
+  std::vector<uint4 *> peer_ghost;
   std::vector<unsigned long long *> peer_flags;
   spmat::DevBuf<HaloPut> halo_puts;
   spmat::DevBuf<HaloWait> halo_waits;
@@ -298,7 +314,7 @@ struct spmat_s {
   spmat::DevBuf<int> halo_err;
   int n_puts = 0, n_waits = 0, put_chunks_total = 0;
   spmat::DevBuf<unsigned long long> d_epoch;  // completed NVLink-halo MatMults (device)
-  int64_t lvec_stride = 0;          // peer mode: lvec holds two epochs' ghost buffers
+  int64_t ghost_stride = 0;         // lines per epoch buffer of `ghost`
   // CUDA graph of one CG iteration (krylov.cu), keyed by the caller's x / history pointers
   cudaGraphExec_t cg_exec = nullptr;
   const void *cg_key_x = nullptr, *cg_key_h = nullptr;
@@ -319,6 +335,7 @@ struct spmat_s {
   std::vector<cudaEvent_t> pipe_ev;                        // 2 * chunks + 2
   // CG / dot workspace (krylov.cu), allocated on first use
   spmat::DevBuf<double> cg_r, cg_p, cg_q, cg_partial, cg_scalars, cg_reduced;
+  spmat::DevBuf<unsigned> cg_count;  // CTA arrival counter of the dot kernels (last CTA finalizes)
 };
 
 namespace spmat {

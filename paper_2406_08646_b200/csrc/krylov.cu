@@ -7,20 +7,23 @@
 // number of iterations without a host-side convergence test.  The paper reduced
 // the partial dots with NVSHMEM; here the cross-rank reduction goes through a "scalar board":
 // each rank's small device array is IPC-mapped into every other rank (NVLink), a rank stores
-// its partial into every board and raises an epoch flag, then sums the P partials of its own
-// board in rank order -- the same bit-identical value on every rank, no NCCL kernel, no host.
+// its partial into every board as a line flagged with the reduction's epoch (halo_dev.cuh),
+// then sums the P partials of its own board in rank order once they carry the epoch -- the
+// same bit-identical value on every rank, no NCCL kernel, no host, no fence.
 //
-// Local dot products use a fixed decomposition (kDotBlocks CTAs x 256 threads, fixed strides,
+// Local dot products use a fixed decomposition (a function of m only: CTAs x 256 threads, fixed strides,
 // fixed reduction trees), so results are deterministic run to run.
 //
 // Every epoch (halo, board) and the residual-history index live in device memory, so one CG
 // iteration is captured once as a CUDA graph and replayed maxit times (SPMAT_GRAPH=0 turns the
-// graph off): the launch cost of ~6 kernels per iteration becomes one graph launch.
+// graph off): the launch cost of the iteration's kernels becomes one graph launch.  Each dot is
+// one kernel: the last CTA to finish sums the partials and does the cross-rank step.
 #include <algorithm>
 #include <cstring>
 
 #include "halo_dev.cuh"
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace spmat {
 
@@ -31,50 +34,37 @@ int board_setup(Comm *c) {
   const int P = c->nranks, me = c->rank;
   c->board_ok = false;
   if (P == 1) return SPMAT_OK;
-  const int W = Comm::kBoardWidth;
-  SP_TRY(c->board_val.alloc(2 * (size_t)P * W));
-  SP_TRY(c->board_flag.alloc(2 * (size_t)P));
+  SP_TRY(c->board_line.alloc(2 * (size_t)P));
   SP_TRY(c->board_err.alloc(1));
   SP_TRY(c->d_board_epoch.alloc(1));
-  SP_CUDA(cudaMemset(c->board_val.get(), 0, 2 * P * W * sizeof(double)));
-  SP_CUDA(cudaMemset(c->board_flag.get(), 0, 2 * P * sizeof(unsigned long long)));
+  SP_CUDA(cudaMemset(c->board_line.get(), 0, 2 * P * sizeof(uint4)));  // flag 0: no epoch
   SP_CUDA(cudaMemset(c->board_err.get(), 0, sizeof(int)));
   SP_CUDA(cudaMemset(c->d_board_epoch.get(), 0, sizeof(unsigned long long)));
-  cudaIpcMemHandle_t hv, hf;
+  cudaIpcMemHandle_t hv;
   memset(&hv, 0, sizeof hv);
-  memset(&hf, 0, sizeof hf);
   int64_t fail = 0;
   if (getenv("SPMAT_BOARD") && !strcmp(getenv("SPMAT_BOARD"), "nccl")) fail = 1;
-  if (!fail && (cudaIpcGetMemHandle(&hv, c->board_val.get()) != cudaSuccess ||
-                cudaIpcGetMemHandle(&hf, c->board_flag.get()) != cudaSuccess)) {
+  if (!fail && cudaIpcGetMemHandle(&hv, c->board_line.get()) != cudaSuccess) {
     cudaGetLastError();
     fail = 1;
   }
-  std::vector<int64_t> mine(16), all(16 * (size_t)P);
+  std::vector<int64_t> mine(8), all(8 * (size_t)P);
   memcpy(mine.data(), &hv, 64);
-  memcpy(mine.data() + 8, &hf, 64);
-  SP_TRY(c->allgather_i64(mine.data(), 16, all.data()));
-  std::vector<double *> pv(P, nullptr);
-  std::vector<unsigned long long *> pf(P, nullptr);
-  pv[me] = c->board_val.get();
-  pf[me] = c->board_flag.get();
+  SP_TRY(c->allgather_i64(mine.data(), 8, all.data()));
+  std::vector<uint4 *> pl(P, nullptr);
+  pl[me] = c->board_line.get();
   for (int q = 0; q < P && !fail; ++q) {
     if (q == me) continue;
-    cudaIpcMemHandle_t h1, h2;
-    memcpy(&h1, all.data() + 16 * (size_t)q, 64);
-    memcpy(&h2, all.data() + 16 * (size_t)q + 8, 64);
-    void *a = nullptr, *b = nullptr;
-    if (cudaIpcOpenMemHandle(&a, h1, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
-        cudaIpcOpenMemHandle(&b, h2, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, all.data() + 8 * (size_t)q, 64);
+    void *a = nullptr;
+    if (cudaIpcOpenMemHandle(&a, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
       cudaGetLastError();
-      if (a) cudaIpcCloseMemHandle(a);
       fail = 1;
       break;
     }
     c->board_peer_mem.push_back(a);
-    c->board_peer_mem.push_back(b);
-    pv[q] = (double *)a;
-    pf[q] = (unsigned long long *)b;
+    pl[q] = (uint4 *)a;
   }
   int64_t vote[1] = {fail};
   SP_TRY(c->allreduce_max_i64(vote, 1));
@@ -82,10 +72,8 @@ int board_setup(Comm *c) {
     board_release(c);
     return SPMAT_OK;  // reductions fall back to ncclAllReduce
   }
-  SP_TRY(c->d_peer_val.alloc(P));
-  SP_TRY(c->d_peer_flag.alloc(P));
-  SP_CUDA(cudaMemcpy(c->d_peer_val.get(), pv.data(), P * sizeof(double *), cudaMemcpyHostToDevice));
-  SP_CUDA(cudaMemcpy(c->d_peer_flag.get(), pf.data(), P * sizeof(void *), cudaMemcpyHostToDevice));
+  SP_TRY(c->d_peer_line.alloc(P));
+  SP_CUDA(cudaMemcpy(c->d_peer_line.get(), pl.data(), P * sizeof(uint4 *), cudaMemcpyHostToDevice));
   c->board_ok = true;
   return SPMAT_OK;
 }
@@ -109,28 +97,129 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o));
   }
+  __syncthreads();  // red may be reused
   return s;  // valid in thread 0
+}
+
+struct CgScalars {
+  double rr, pq, alpha, beta;
+  int stopped, iter;  // iter: index of the last residual-history entry written
+};
+
+enum { OP_DOT = 0, OP_CG_INIT = 1, OP_CG_ALPHA = 2, OP_CG_BETA = 3 };
+
+// What the CTA that finishes a dot does with the partial sums.
+struct FinArgs {
+  double *partial;  // one partial per CTA of the dot kernel
+  int op;
+  CgScalars *sc;
+  double *result, *hist;
+  uint4 *const *peer_line;  // scalar board (nullptr: single rank, or NCCL path)
+  int P, me;
+  unsigned long long *board_epoch;
+  int *err;
+  const double *preduced;  // NCCL path: the value already all-reduced over ranks
+  unsigned *count;         // non-null: the last CTA of the dot kernel finalizes in place
+};
+
+// One CTA: local sum of the np partials (fixed order), the cross-rank sum through the scalar
+// board (or the NCCL-reduced value), then the scalar step of CG.  The board epoch is read from
+// and written back to device memory.
+__device__ void finalize_cta(const FinArgs &f, int np) {
+  __shared__ double red[kDotThreads / 32];
+  __shared__ double total;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += kDotThreads) s = __dadd_rn(s, __ldcg(f.partial + i));
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) total = s;
+  __syncthreads();
+  if (f.preduced) {  // NCCL already summed the local values over ranks
+    if (threadIdx.x == 0) total = *f.preduced;
+  } else if (f.peer_line) {
+    // my partial, flagged with this reduction's epoch, into every rank's board (one 16-byte
+    // store each, no fence); then the P lines of my board, summed in rank order once each
+    // carries the epoch -- the same value on every rank
+    const unsigned long long epoch = *f.board_epoch + 1ull;
+    const int par = (int)(epoch & 1);
+    const int P = f.P;
+    const uint32_t flag = ll_flag(epoch);
+    if (threadIdx.x < P) ll_store(f.peer_line[threadIdx.x] + (size_t)par * P + f.me, total, flag);
+    if (threadIdx.x == 0) {
+      const uint4 *mine = f.peer_line[f.me] + (size_t)par * P;
+      double t = 0.0;
+      for (int q = 0; q < P; ++q) t = __dadd_rn(t, ll_load(mine + q, flag, f.err));  // rank order
+      total = t;
+      *f.board_epoch = epoch;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  const double g = total;
+  CgScalars *sc = f.sc;
+  if (f.op == OP_DOT) {
+    *f.result = g;
+  } else if (f.op == OP_CG_INIT) {
+    sc->rr = g;
+    sc->stopped = g == 0.0 ? 1 : 0;
+    sc->iter = 0;
+    if (f.hist) f.hist[0] = g;
+  } else if (f.op == OP_CG_ALPHA) {
+    sc->pq = g;
+    if (g == 0.0 || sc->rr == 0.0) sc->stopped = 1;
+    sc->alpha = sc->stopped ? 0.0 : sc->rr / g;
+  } else {  // OP_CG_BETA
+    if (!sc->stopped) {
+      sc->beta = g / sc->rr;
+      sc->rr = g;
+    }
+    sc->iter += 1;
+    if (f.hist) f.hist[sc->iter] = sc->rr;
+  }
+}
+
+// Each CTA stores its partial; with f.count the last CTA to arrive finalizes (one kernel per
+// dot instead of two).  Called by every thread of the CTA.
+__device__ __forceinline__ void partial_done(double s, const FinArgs &f) {
+  __shared__ int last;
+  if (threadIdx.x == 0) {
+    f.partial[blockIdx.x] = s;
+    if (f.count) {
+      __threadfence();
+      last = atomicAdd(f.count, 1u) == gridDim.x - 1 ? 1 : 0;
+    }
+  }
+  if (!f.count) return;
+  __syncthreads();
+  if (!last) return;
+  if (threadIdx.x == 0) *f.count = 0u;  // ready for the next dot
+  __threadfence();
+  finalize_cta(f, gridDim.x);
+}
+
+__global__ void __launch_bounds__(kDotThreads) k_finalize(FinArgs f, int np) {
+  pdl_wait();
+  finalize_cta(f, np);
 }
 
 // CTA c owns [c*chunk, (c+1)*chunk); partial[c] = sum of a*b there
 __global__ void __launch_bounds__(kDotThreads) k_dot_partial(const double *__restrict__ a,
                                                              const double *__restrict__ b, int64_t n,
-                                                             double *__restrict__ partial) {
+                                                             FinArgs f) {
   __shared__ double red[kDotThreads / 32];
+  pdl_wait();
   const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
   double s = 0.0;
   for (int64_t i = lo + threadIdx.x; i < hi; i += kDotThreads) s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
-  s = block_sum(s, red);
-  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+  partial_done(block_sum(s, red), f);
 }
 
 // r = b - q; p = r; partial of r.r
 __global__ void __launch_bounds__(kDotThreads) k_cg_init(const double *__restrict__ b,
                                                          const double *__restrict__ q, double *__restrict__ r,
-                                                         double *__restrict__ p, int64_t n,
-                                                         double *__restrict__ partial) {
+                                                         double *__restrict__ p, int64_t n, FinArgs f) {
   __shared__ double red[kDotThreads / 32];
+  pdl_wait();
   const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
   double s = 0.0;
@@ -140,24 +229,18 @@ __global__ void __launch_bounds__(kDotThreads) k_cg_init(const double *__restric
     p[i] = ri;
     s = __dadd_rn(s, __dmul_rn(ri, ri));
   }
-  s = block_sum(s, red);
-  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+  partial_done(block_sum(s, red), f);
 }
-
-struct CgScalars {
-  double rr, pq, alpha, beta;
-  int stopped, iter;  // iter: index of the last residual-history entry written
-};
 
 // x = x + alpha p; r = r - alpha q; partial of r.r (products rounded separately, no FMA)
 __global__ void __launch_bounds__(kDotThreads) k_cg_update(double *__restrict__ x, double *__restrict__ r,
                                                            const double *__restrict__ p,
                                                            const double *__restrict__ q, int64_t n,
-                                                           const CgScalars *__restrict__ sc,
-                                                           double *__restrict__ partial) {
+                                                           FinArgs f) {
   __shared__ double red[kDotThreads / 32];
-  const double alpha = sc->alpha;
-  const bool go = !sc->stopped;
+  pdl_wait();
+  const double alpha = f.sc->alpha;
+  const bool go = !f.sc->stopped;
   const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
   double s = 0.0;
@@ -170,117 +253,85 @@ __global__ void __launch_bounds__(kDotThreads) k_cg_update(double *__restrict__ 
     }
     s = __dadd_rn(s, __dmul_rn(ri, ri));
   }
-  s = block_sum(s, red);
-  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+  // every CTA has read sc->alpha/stopped before the last one (which rewrites sc) gets here
+  partial_done(block_sum(s, red), f);
 }
 
 // p = r + beta p
 __global__ void k_cg_pupdate(double *__restrict__ p, const double *__restrict__ r, int64_t n,
                              const CgScalars *__restrict__ sc) {
+  pdl_wait();
   if (sc->stopped) return;
   const double beta = sc->beta;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
 }
 
-enum { OP_DOT = 0, OP_CG_INIT = 1, OP_CG_ALPHA = 2, OP_CG_BETA = 3 };
-
-// One CTA: local sum of the partials (fixed order), the cross-rank sum through the scalar
-// board (or the value already all-reduced by NCCL when preduced != nullptr), then the scalar
-// step of CG.  The board epoch is read from and written back to device memory.
-__global__ void __launch_bounds__(kDotThreads) k_finalize(
-    const double *__restrict__ partial, int np, int op, CgScalars *sc, double *result,
-    double *__restrict__ hist, double *const *peer_val, unsigned long long *const *peer_flag, int P,
-    int me, unsigned long long *board_epoch, int *err, const double *preduced) {
-  __shared__ double red[kDotThreads / 32];
-  __shared__ double total;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < np; i += kDotThreads) s = __dadd_rn(s, partial[i]);
-  s = block_sum(s, red);
-  if (threadIdx.x == 0) total = s;
-  __syncthreads();
-  if (preduced) {  // NCCL already summed the local values over ranks
-    if (threadIdx.x == 0) total = *preduced;
-  } else if (peer_val) {
-    const unsigned long long epoch = *board_epoch + 1ull;
-    const int par = (int)(epoch & 1);
-    const int W = Comm::kBoardWidth;
-    if (threadIdx.x < P) {  // my partial into every rank's board, then its flag
-      const int q = threadIdx.x;
-      peer_val[q][((size_t)par * P + me) * W] = total;
-      __threadfence_system();
-      st_release_sys(peer_flag[q] + (size_t)par * P + me, epoch);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long *mine = peer_flag[me] + (size_t)par * P;
-      bool ok = true;
-      for (int q = 0; q < P && ok; ++q) ok = spin_until_geq(mine + q, epoch, err);
-      double t = 0.0;
-      const double *v = peer_val[me] + (size_t)par * P * W;
-      for (int q = 0; q < P; ++q) t = __dadd_rn(t, __ldcg(v + (size_t)q * W));  // rank order
-      total = t;
-      *board_epoch = epoch;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x != 0) return;
-  const double g = total;
-  if (op == OP_DOT) {
-    *result = g;
-  } else if (op == OP_CG_INIT) {
-    sc->rr = g;
-    sc->stopped = g == 0.0 ? 1 : 0;
-    sc->iter = 0;
-    if (hist) hist[0] = g;
-  } else if (op == OP_CG_ALPHA) {
-    sc->pq = g;
-    if (g == 0.0 || sc->rr == 0.0) sc->stopped = 1;
-    sc->alpha = sc->stopped ? 0.0 : sc->rr / g;
-  } else {  // OP_CG_BETA
-    if (!sc->stopped) {
-      sc->beta = g / sc->rr;
-      sc->rr = g;
-    }
-    sc->iter += 1;
-    if (hist) hist[sc->iter] = sc->rr;
-  }
-}
-
 // ------------------------------------------------------------------ host side
-static int dot_blocks(spmat_s *A) { return A->comm->num_sms * 4; }
+static int max_dot_blocks(spmat_s *A) { return A->comm->num_sms * 4; }
+
+// CTAs of a dot over the local rows: ~8 elements per thread, at most 4 per SM -- a function of
+// m only, so every dot of a matrix reduces in the same fixed order
+static int dot_blocks(spmat_s *A) {
+  const int64_t want = (A->m + 8 * kDotThreads - 1) / (8 * kDotThreads);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, max_dot_blocks(A)));
+}
 
 static int ensure_ws(spmat_s *A) {
   if (A->cg_partial.n) return SPMAT_OK;
-  SP_TRY(A->cg_partial.alloc(dot_blocks(A)));
+  SP_TRY(A->cg_partial.alloc(max_dot_blocks(A)));
   SP_TRY(A->cg_scalars.alloc(sizeof(CgScalars) / sizeof(double) + 2));
   SP_TRY(A->cg_reduced.alloc(2));
+  SP_TRY(A->cg_count.alloc(1));
+  SP_CUDA(cudaMemset(A->cg_count.get(), 0, sizeof(unsigned)));
   return SPMAT_OK;
 }
 
-// global sum of partials -> op; cross-rank through the board or ncclAllReduce
-static int finalize(spmat_s *A, int op, double *result, double *hist, cudaStream_t s) {
+// the NCCL path (several ranks without the scalar board) cannot finalize inside the dot kernel
+static bool nccl_reduce(spmat_s *A) { return A->comm->nranks > 1 && !A->comm->board_ok; }
+
+static FinArgs fin_args(spmat_s *A, int op, double *result, double *hist) {
   Comm *c = A->comm;
-  const int np = dot_blocks(A);
-  CgScalars *sc = (CgScalars *)A->cg_scalars.get();
-  if (c->nranks > 1 && !c->board_ok) {
-    // local sum first, then NCCL all-reduce of the scalar, then the scalar step
-    k_finalize<<<1, kDotThreads, 0, s>>>(A->cg_partial.get(), np, OP_DOT, sc, A->cg_reduced.get(),
-                                         nullptr, nullptr, nullptr, 1, 0, nullptr, nullptr, nullptr);
-    SP_LAUNCH();
-    SP_NCCL(c->api, c->api->AllReduce(A->cg_reduced.get(), A->cg_reduced.get() + 1, 1, ncclFloat64,
-                                      ncclSum, c->nccl, s));
-    k_finalize<<<1, kDotThreads, 0, s>>>(A->cg_partial.get(), 0, op, sc, result, hist, nullptr, nullptr,
-                                         1, 0, nullptr, nullptr, A->cg_reduced.get() + 1);
-    SP_LAUNCH();
-    return SPMAT_OK;
+  FinArgs f{};
+  f.partial = A->cg_partial.get();
+  f.op = op;
+  f.sc = (CgScalars *)A->cg_scalars.get();
+  f.result = result;
+  f.hist = hist;
+  f.P = c->nranks;
+  f.me = c->rank;
+  if (nccl_reduce(A)) {  // the dot kernel only stores partials; finish_nccl does the rest
+    f.op = OP_DOT;
+    f.result = A->cg_reduced.get();
+    return f;
   }
-  const bool board = c->nranks > 1;
-  k_finalize<<<1, kDotThreads, 0, s>>>(A->cg_partial.get(), np, op, sc, result, hist,
-                                       board ? c->d_peer_val.get() : nullptr,
-                                       board ? c->d_peer_flag.get() : nullptr, c->nranks, c->rank,
-                                       board ? c->d_board_epoch.get() : nullptr,
-                                       board ? c->board_err.get() : nullptr, nullptr);
+  f.count = A->cg_count.get();
+  if (c->nranks > 1) {
+    f.peer_line = c->d_peer_line.get();
+    f.board_epoch = c->d_board_epoch.get();
+    f.err = c->board_err.get();
+  }
+  return f;
+}
+
+// NCCL path: local sum of the partials, ncclAllReduce of the scalar, then the scalar step
+static int finish_nccl(spmat_s *A, int op, double *result, double *hist, cudaStream_t s) {
+  if (!nccl_reduce(A)) return SPMAT_OK;
+  Comm *c = A->comm;
+  FinArgs f = fin_args(A, OP_DOT, nullptr, nullptr);
+  k_finalize<<<1, kDotThreads, 0, s>>>(f, dot_blocks(A));
+  SP_LAUNCH();
+  SP_NCCL(c->api, c->api->AllReduce(A->cg_reduced.get(), A->cg_reduced.get() + 1, 1, ncclFloat64,
+                                    ncclSum, c->nccl, s));
+  FinArgs g{};
+  g.partial = A->cg_partial.get();
+  g.op = op;
+  g.sc = (CgScalars *)A->cg_scalars.get();
+  g.result = result;
+  g.hist = hist;
+  g.P = 1;
+  g.preduced = A->cg_reduced.get() + 1;
+  k_finalize<<<1, kDotThreads, 0, s>>>(g, 0);
   SP_LAUNCH();
   return SPMAT_OK;
 }
@@ -293,14 +344,13 @@ static int cg_iteration(spmat_s *A, double *x, double *rr_hist, cudaStream_t s) 
   const int nb = dot_blocks(A);
   const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)A->comm->num_sms * 8));
   SP_TRY(spmat_mult_part(A, p, q, 7, s));                            // q = A p
-  k_dot_partial<<<nb, kDotThreads, 0, s>>>(p, q, m, A->cg_partial.get());
-  SP_LAUNCH();
-  SP_TRY(finalize(A, OP_CG_ALPHA, nullptr, nullptr, s));            // alpha = rr / p.q
-  k_cg_update<<<nb, kDotThreads, 0, s>>>(x, r, p, q, m, sc, A->cg_partial.get());
-  SP_LAUNCH();
-  SP_TRY(finalize(A, OP_CG_BETA, nullptr, rr_hist, s));             // beta, rr = r.r
-  k_cg_pupdate<<<gv, 256, 0, s>>>(p, r, m, sc);                     // p = r + beta p
-  SP_LAUNCH();
+  SP_CUDA(launch_pdl(k_dot_partial, nb, kDotThreads, 0, s, (const double *)p, (const double *)q, m,
+                     fin_args(A, OP_CG_ALPHA, nullptr, nullptr)));
+  SP_TRY(finish_nccl(A, OP_CG_ALPHA, nullptr, nullptr, s));         // alpha = rr / p.q
+  SP_CUDA(launch_pdl(k_cg_update, nb, kDotThreads, 0, s, x, r, (const double *)p, (const double *)q, m,
+                     fin_args(A, OP_CG_BETA, nullptr, rr_hist)));
+  SP_TRY(finish_nccl(A, OP_CG_BETA, nullptr, rr_hist, s));          // beta, rr = r.r
+  SP_CUDA(launch_pdl(k_cg_pupdate, gv, 256, 0, s, p, (const double *)r, m, (const CgScalars *)sc));  // p = r + beta p
   return SPMAT_OK;
 }
 
@@ -332,9 +382,9 @@ int spmat_vec_dot(spmat_t A, const double *a, const double *b, double *result, v
   DeviceGuard g(A->comm->device);
   cudaStream_t s = (cudaStream_t)stream;
   SP_TRY(ensure_ws(A));
-  k_dot_partial<<<dot_blocks(A), kDotThreads, 0, s>>>(a, b, A->m, A->cg_partial.get());
-  SP_LAUNCH();
-  return finalize(A, OP_DOT, result, nullptr, s);
+  SP_CUDA(launch_pdl(k_dot_partial, dot_blocks(A), kDotThreads, 0, s, a, b, A->m,
+                     fin_args(A, OP_DOT, result, nullptr)));
+  return finish_nccl(A, OP_DOT, result, nullptr, s);
 }
 
 int spmat_cg(spmat_t A, const double *b, double *x, int maxit, double *rr_hist, void *stream) {
@@ -368,9 +418,9 @@ int spmat_cg(spmat_t A, const double *b, double *x, int maxit, double *rr_hist, 
   }
   // r = b - A x; p = r; rr = r.r
   SP_TRY(spmat_mult_part(A, x, q, 7, cs));
-  k_cg_init<<<nb, kDotThreads, 0, cs>>>(b, q, r, p, m, A->cg_partial.get());
-  SP_LAUNCH();
-  SP_TRY(finalize(A, OP_CG_INIT, nullptr, rr_hist, cs));
+  SP_CUDA(launch_pdl(k_cg_init, nb, kDotThreads, 0, cs, b, (const double *)q, r, p, m,
+                     fin_args(A, OP_CG_INIT, nullptr, rr_hist)));
+  SP_TRY(finish_nccl(A, OP_CG_INIT, nullptr, rr_hist, cs));
   if (!use_graph) {
     for (int k = 0; k < maxit; ++k) SP_TRY(cg_iteration(A, x, rr_hist, s));
     return SPMAT_OK;

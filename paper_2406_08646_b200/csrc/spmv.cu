@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  pdl_wait();  // (launch_pdl) the barrier set-up above may overlap the previous kernel
   // this MatMult's halo epoch: read by every CTA before any claim, so before the last CTA
   // (which only exists once every CTA has claimed) stores it back
   const unsigned long long epoch = halo.epoch_ctr ? *halo.epoch_ctr + 1ull : 0ull;
@@ -187,6 +188,8 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
   if (warp == kConsumerWarps + 1) {  // ---------------- comm warp: fused halo puts (halo.cu)
     for (int c = blockIdx.x; c < halo.put_chunks; c += gridDim.x)
       halo_put_warp(halo.puts, halo.nputs, c, x, epoch, halo.err);
+    if (tail.trace && lane32 == 0 && blockIdx.x < halo.put_chunks)
+      tail.trace[4 * (size_t)blockIdx.x + 1] = gtimer();  // this CTA's puts are out
     return;
   }
   if (warp == kConsumerWarps) {  // ---------------- producer warp
@@ -273,9 +276,9 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
       break;
     }
     if (r0 == -2) {  // ---- off-diagonal work item: y[rows_o] += A_o lvec for kThreads rows
-      unsigned long long *itr = tail.trace ? tail.trace + 4 * (size_t)gridDim.x + 3 * (size_t)r1 : nullptr;
+      unsigned long long *itr = tail.trace ? tail.trace + 4 * (size_t)gridDim.x + 4 * (size_t)r1 : nullptr;
       if (itr && tid == 0) itr[0] = gtimer();
-      if (tid == 0) {  // every boundary block written and every sender's epoch data landed
+      if (tid == 0) {  // every boundary block written (the ghost lines are waited for one by one)
         const unsigned target = (unsigned)(kConsumerWarps * tail.n_bblocks);
         const long long t0 = clock64();
         while (ld_acquire_gpu(tail.ctr) < target) {
@@ -285,19 +288,15 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
           }
           __nanosleep(32);
         }
-        for (int w = 0; w < tail.nwaits; ++w)
-          spin_until_geq(tail.waits[w].my_ready, epoch * (unsigned long long)tail.waits[w].nchunk, halo.err);
+        if (itr) itr[3] = gtimer();  // boundary blocks written
       }
       asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
       if (itr && tid == 0) itr[1] = gtimer();
-      const int64_t q = (int64_t)r1 * kThreads + tid;
-      if (q < tail.n_ro) {
-        double sacc = 0.0;
-        for (int e = tail.rowptr[q]; e < tail.rowptr[q + 1]; ++e)
-          sacc = __dadd_rn(sacc, __dmul_rn(tail.val[e], __ldcg(tail.lvec + (epoch & 1) * tail.lvec_stride + tail.col[e])));
-        const int r = tail.rows[q];
-        y[r] = __dadd_rn(__ldcg(y + r), sacc);
-      }
+      const int64_t q = ((int64_t)r1 * kThreads + tid) / tail.w;  // item r1: kThreads / w rows
+      const uint4 *gl = tail.ghost + (int64_t)(epoch & 1) * tail.ghost_stride;
+      const uint32_t flag = ll_flag(epoch);
+      offdiag_row_w(q, q < tail.n_ro, tail.w, tail.rows, tail.rowptr, tail.col, tail.val,
+                    [&](int c) { return ll_load(gl + c, flag, halo.err); }, y);
       asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
       if (itr && tid == 0) itr[2] = gtimer();
       if (tid == 0) {
@@ -425,18 +424,24 @@ __global__ void __launch_bounds__(256) k_spmv_offdiag(const int32_t *__restrict_
                                                       const int32_t *__restrict__ rowptr,
                                                       const int32_t *__restrict__ col,
                                                       const double *__restrict__ val,
-                                                      const double *__restrict__ lvec_base,
-                                                      int64_t lvec_stride,
+                                                      const double *__restrict__ lvec,
+                                                      const uint4 *__restrict__ ghost,
+                                                      int64_t ghost_stride,
                                                       const unsigned long long *__restrict__ epoch_ctr,
-                                                      double *__restrict__ y, int64_t nro) {
-  // ghost buffer of the last completed epoch (NVLink mode) or the single buffer (NCCL)
-  const double *lvec = lvec_base + (epoch_ctr ? (int64_t)(*epoch_ctr & 1ull) * lvec_stride : 0);
-  GRID_STRIDE(q, nro) {
-    double s = 0.0;
-    for (int e = rowptr[q]; e < rowptr[q + 1]; ++e)
-      s = __dadd_rn(s, __dmul_rn(val[e], lvec[col[e]]));
-    const int r = rows[q];
-    y[r] = __dadd_rn(y[r], s);
+                                                      double *__restrict__ y, int64_t nro, int W,
+                                                      int *err) {
+  pdl_wait();
+  // NCCL mode: lvec.  NVLink mode: the ghost lines of the last completed epoch (already landed).
+  const unsigned long long epoch = ghost ? *epoch_ctr : 0ull;
+  const uint4 *gl = ghost ? ghost + (int64_t)(epoch & 1) * ghost_stride : nullptr;
+  // block-uniform loop bound: every lane reaches the shuffles in offdiag_row_w
+  for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < nro * W; t0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = (t0 + threadIdx.x) / W;
+    if (gl)
+      offdiag_row_w(q, q < nro, W, rows, rowptr, col, val,
+                    [&](int c) { return ll_load(gl + c, ll_flag(epoch), err); }, y);
+    else
+      offdiag_row_w(q, q < nro, W, rows, rowptr, col, val, [&](int c) { return __ldcg(lvec + c); }, y);
   }
 }
 
@@ -486,6 +491,16 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   A->max_row_nnz = 0;
   A->n_rowblocks = 0;
   A->lanes = lanes_for(m ? (double)nnz / (double)m : 0.0);
+  // off-diagonal rows: the largest power of two w <= 32 with >= 2 entries per lane on average
+  // (stencil slabs: 1 entry per row -> w = 1, the plain row sum).  The SpMV-add is latency-
+  // bound (a dependent ghost read per entry), so short lane loops matter more than lanes.
+  A->ro_w = 1;
+  if (A->n_ro > 0)
+    while (A->ro_w < 32 && 4 * A->ro_w * A->n_ro <= A->nnz_o) A->ro_w *= 2;
+  if (const char *w = getenv("SPMAT_RO_W")) {
+    const int v = atoi(w);
+    if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) A->ro_w = v;
+  }
   if (m == 0) return SPMAT_OK;
   DevBuf<char> tmp;
   DevBuf<uint32_t> flag;
@@ -569,17 +584,19 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   SP_TRY(tma_setup(A));
   if (const char *tr = getenv("SPMAT_TRACE")) {  // device trace of the fused MatMult kernel
     if (atoi(tr)) {
-      const int64_t nitems = (A->n_ro + kThreads - 1) / kThreads;
-      SP_TRY(A->trace.alloc(4 * (size_t)A->tma_grid + 3 * (size_t)nitems + 16));
+      const int64_t nitems = (A->n_ro * A->ro_w + kThreads - 1) / kThreads;
+      SP_TRY(A->trace.alloc(4 * (size_t)A->tma_grid + 4 * (size_t)nitems + 16));
       SP_CUDA(cudaMemsetAsync(A->trace.get(), 0, A->trace.n * 8, st));
+      const unsigned long long hdr[2] = {(unsigned long long)A->tma_grid, (unsigned long long)nitems};
+      SP_CUDA(cudaMemcpyAsync(A->trace.get() + A->trace.n - 2, hdr, sizeof hdr, cudaMemcpyHostToDevice, st));
     }
   }
   SP_CUDA(cudaStreamSynchronize(st));
   return SPMAT_OK;
 }
 
-static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put,
-                       bool fuse_tail) {
+static cudaError_t launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put,
+                              bool fuse_tail) {
   // the kernel ends the MatMult (bumps the device epoch) when it also runs the off-diagonal
   // items; otherwise k_spmv_offdiag_peer does
   SpmvHalo h{A->halo_puts.get(), A->n_puts, fuse_put ? A->put_chunks_total : 0,
@@ -591,7 +608,8 @@ static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, b
     t.enabled = 1;
     // items go a quarter of the way through the sweep: by then the boundary blocks (claimed
     // first) are written and the halo puts (issued at kernel start) have landed
-    t.n_items = (int)((A->n_ro + kThreads - 1) / kThreads);
+    t.w = A->ro_w;
+    t.n_items = (int)((A->n_ro * A->ro_w + kThreads - 1) / kThreads);
     const char *f = getenv("SPMAT_TAIL_AT");  // fraction of the sweep before the items
     const double at = f ? atof(f) : 0.5;
     t.t0 = (int)std::max<int64_t>(A->n_bblocks, (int64_t)(A->n_rowblocks * at));
@@ -600,16 +618,16 @@ static void launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, b
     t.rowptr = A->rowptr_o.get();
     t.col = A->col_o.get();
     t.val = A->val_o.get();
-    t.lvec = A->lvec.get();
-    t.lvec_stride = A->lvec_stride;
+    t.ghost = A->ghost.get();
+    t.ghost_stride = A->ghost_stride;
     t.n_ro = A->n_ro;
     t.waits = A->halo_waits.get();
     t.nwaits = A->n_waits;
     t.ctr = A->tail_ctr.get();
   }
-  k_spmv_tma<<<(unsigned)A->tma_grid, kCtaThreads, kTmaSmem, s>>>(
-      A->blocks4.get(), (int)A->n_rowblocks, A->rowptr_d.get(), A->col_d.get(), A->val_d.get(), x, y,
-      A->sched.get(), h, t);
+  return launch_pdl(k_spmv_tma, (unsigned)A->tma_grid, kCtaThreads, kTmaSmem, s, (const int4 *)A->blocks4.get(),
+                    (int)A->n_rowblocks, (const int32_t *)A->rowptr_d.get(), (const int32_t *)A->col_d.get(),
+                    (const double *)A->val_d.get(), x, y, A->sched.get(), h, t);
 }
 
 template <int W>
@@ -632,7 +650,7 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_
     return SPMAT_OK;
   }
   if (A->kernel_id == KERNEL_TMA) {
-    launch_tma(A, x, y, s, fuse_put, fuse_tail);
+    SP_CUDA(launch_tma(A, x, y, s, fuse_put, fuse_tail));
   } else {
     k_spmv_stream<<<(unsigned)A->n_rowblocks, kThreads, 0, s>>>(A->rbp.get(), A->rowptr_d.get(),
                                                                A->col_d.get(), A->val_d.get(), x, y);
@@ -648,9 +666,10 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_
 
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t s) {
   if (A->n_ro == 0) return SPMAT_OK;
-  k_spmv_offdiag<<<nblk(A->n_ro), 256, 0, s>>>(A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(),
-                                              A->val_o.get(), A->lvec.get(), A->lvec_stride,
-                                              A->peer ? A->d_epoch.get() : nullptr, y, A->n_ro);
+  k_spmv_offdiag<<<nblk(A->n_ro * A->ro_w), 256, 0, s>>>(
+      A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(), A->val_o.get(), A->lvec.get(),
+      A->peer ? A->ghost.get() : nullptr, A->ghost_stride, A->peer ? A->d_epoch.get() : nullptr, y,
+      A->n_ro, A->ro_w, A->peer ? A->halo_err.get() : nullptr);
   SP_LAUNCH();
   return SPMAT_OK;
 }

@@ -29,3 +29,22 @@ def test_multirank_parity(P, halo):
     assert f"MULTIRANK P={P} failures=0" in r.stdout
     want = 2 if halo == "peer" else 1
     assert f"halo_mode={want}" in r.stdout
+
+
+@pytest.mark.parametrize("ro_w", ["1", "32"])
+def test_multirank_offdiag_lanes(ro_w):
+    """The off-diagonal SpMV-add with forced lanes per row (1: plain row sums, 32: one warp per
+    row) in the fused NVLink kernel, the standalone kernels and the NCCL path."""
+    P = 2
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    env = dict(os.environ)
+    env["SPMAT_RO_W"] = ro_w
+    port = 29661 + int(ro_w)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(HERE, "mp_gpu_parity.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    sys.stdout.write(r.stdout[-6000:])
+    sys.stderr.write(r.stderr[-6000:])
+    assert r.returncode == 0
+    assert f"MULTIRANK P={P} failures=0" in r.stdout

@@ -44,6 +44,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="kuu,bump,c4")
     ap.add_argument("--iters", type=int, default=50)
+    ap.add_argument("--breakdown", action="store_true",
+                    help="also time MatMult alone and the dot alone (us per call)")
     a = ap.parse_args()
     P, r = int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("RANK", 0))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -70,15 +72,44 @@ def main():
         e1.record(s)
         torch.cuda.synchronize()
         us = sd.max_over_ranks(e0.elapsed_time(e1) * 1e3 / a.iters)
+        parts = {}
+        if a.breakdown:
+            y = torch.empty_like(x)
+            res = torch.empty(1, dtype=torch.float64, device="cuda")
+            def fn_s(key, st):
+                if key == "mult":
+                    A.mult(b, y, st)
+                else:
+                    A.dot(b, x, res, st)
+
+            for key in ("mult", "dot"):
+                fn = lambda: fn_s(key, s)  # noqa: E731
+                for _ in range(5):
+                    fn()
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()  # device time, not the Python launch rate
+                gs = torch.cuda.Stream()
+                with torch.cuda.graph(g, stream=gs):
+                    with torch.cuda.stream(gs):
+                        for _ in range(a.iters):
+                            fn_s(key, gs)
+                torch.cuda.synchronize()
+                sd.barrier()
+                e0.record(s)
+                g.replay()
+                e1.record(s)
+                torch.cuda.synchronize()
+                parts[key] = sd.max_over_ranks(e0.elapsed_time(e1) * 1e3 / a.iters)
         nnz = sd.sum_over_ranks(A.info()["nnz_d"] + A.info()["nnz_o"])
         out.append({"config": name, "rows": M, "nnz": nnz, "P": P, "us_per_iteration": us,
-                    "halo_mode": A.halo_mode()})
+                    "halo_mode": A.halo_mode(), **{f"us_{k}": v for k, v in parts.items()}})
         A.close()
     if r == 0:
         print(json.dumps({"bench": "cg_async", "rows": out}), flush=True)
         for o in out:
             print(f"{o['config']:6s} P={o['P']} rows={o['rows']:>10d} nnz={o['nnz']:>11d} "
-                  f"{o['us_per_iteration']:9.1f} us/iteration")
+                  f"{o['us_per_iteration']:9.1f} us/iteration"
+                  + "".join(f"  {k[3:]} {o[k]:.1f}" for k in o if k.startswith("us_") and k != "us_per_iteration"))
     comm.close()
     if P > 1:
         torch.distributed.destroy_process_group()
