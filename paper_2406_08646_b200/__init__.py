@@ -27,7 +27,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libspmat.so")
+LIB_PATH = os.environ.get("SPMAT_LIB") or os.path.join(_HERE, "libspmat.so")  # SPMAT_LIB: A/B builds
 
 SPMAT_OK, SPMAT_ERR_ARG, SPMAT_ERR_RANGE, SPMAT_ERR_STATE = 0, 1, 2, 3
 SPMAT_ERR_MISMATCH, SPMAT_ERR_OOM, SPMAT_ERR_CUDA, SPMAT_ERR_NCCL = 4, 5, 6, 7

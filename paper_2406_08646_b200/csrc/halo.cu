@@ -59,7 +59,10 @@ __global__ void __launch_bounds__(256) k_spmv_offdiag_peer(
   const unsigned long long epoch = *epoch_ctr + 1ull;
   const uint32_t flag = ll_flag(epoch);
   const uint4 *gl = ghost_base + (int64_t)(epoch & 1) * ghost_stride;
-  if (nro > 0) {  // block-uniform loop bound: every lane reaches the shuffles in offdiag_row_w
+  if (nro > 0 && W == 1) {
+    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x * kRowsU; t0 < nro; t0 += (int64_t)gridDim.x * blockDim.x * kRowsU)
+      offdiag_rows_u<kRowsU>(t0 + threadIdx.x, blockDim.x, nro, rows, rowptr, col, val, gl, nullptr, flag, err, y);
+  } else if (nro > 0) {  // block-uniform loop bound: every lane reaches the shuffles in offdiag_row_w
     for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < nro * W; t0 += (int64_t)gridDim.x * blockDim.x) {
       const int64_t q = (t0 + threadIdx.x) / W;
       offdiag_row_w(q, q < nro, W, rows, rowptr, col, val,
@@ -224,7 +227,7 @@ int halo_peer_put(spmat_s *A, const double *x, cudaStream_t s) {
 // them and releases (halo-only timing).  Always launched: it also ends the MatMult's epoch.
 int halo_peer_offdiag(spmat_s *A, double *y, cudaStream_t s, bool compute) {
   const int64_t nro = compute ? A->n_ro : 0;
-  const int64_t work = nro > 0 ? nro * A->ro_w : A->n_ghost;
+  const int64_t work = nro > 0 ? (A->ro_w == 1 ? (nro + kRowsU - 1) / kRowsU : nro * A->ro_w) : A->n_ghost;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 4L * A->comm->num_sms));
   SP_CUDA(launch_pdl(k_spmv_offdiag_peer, grid, 256, 0, s, (const int32_t *)A->rows_o.get(),
                      (const int32_t *)A->rowptr_o.get(), (const int32_t *)A->col_o.get(),

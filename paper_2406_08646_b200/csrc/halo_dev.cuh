@@ -70,6 +70,11 @@ __device__ __forceinline__ double ll_load(const uint4 *p, uint32_t flag, int *er
   return __longlong_as_double((long long)(((unsigned long long)v.z << 32) | v.x));
 }
 __device__ __forceinline__ uint32_t ll_flag(unsigned long long epoch) { return (uint32_t)epoch; }
+// finish a line already loaded as v (reload p until it carries `flag`)
+__device__ __forceinline__ double ll_value(const uint4 *p, uint4 v, uint32_t flag, int *err) {
+  if (v.y != flag || v.w != flag) return ll_load(p, flag, err);
+  return __longlong_as_double((long long)(((unsigned long long)v.z << 32) | v.x));
+}
 
 // One warp moves put chunk c (global numbering over all destinations) of epoch `epoch`:
 // wait until the destination has released the ghost buffer of epoch-2 (double buffering),
@@ -128,5 +133,67 @@ __device__ __forceinline__ void offdiag_row_w(int64_t q, bool valid, int W,
     y[r] = __dadd_rn(__ldcg(y + r), s);
   }
 }
+
+// Off-diagonal SpMV-add for U rows per thread, one lane per row (rows q0, q0 + stride, ...):
+// each level of the load chain (row pointers -> column/value -> ghost value, and row id -> y)
+// is issued for all U rows before any of them is used, so an item costs one chain of
+// latencies instead of U.  Each row is summed left to right (the oracle's order).
+// gl != nullptr: flagged ghost lines of `flag`; else the plain ghost vector lv.
+template <int U>
+__device__ __forceinline__ void offdiag_rows_u(int64_t q0, int64_t stride, int64_t nro,
+                                               const int32_t *__restrict__ rows,
+                                               const int32_t *__restrict__ rowptr,
+                                               const int32_t *__restrict__ col,
+                                               const double *__restrict__ val, const uint4 *gl,
+                                               const double *lv, uint32_t flag, int *err, double *y) {
+  int a[U], b[U];
+  double s[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t q = q0 + u * stride;
+    a[u] = q < nro ? rowptr[q] : 0;
+    b[u] = q < nro ? rowptr[q + 1] : 0;
+    s[u] = 0.0;
+  }
+  for (int k = 0;; ++k) {
+    int c[U];
+    double v[U];
+    bool any = false;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool h = a[u] + k < b[u];
+      any |= h;
+      c[u] = h ? col[a[u] + k] : -1;
+      v[u] = h ? val[a[u] + k] : 0.0;
+    }
+    if (!any) break;
+    if (gl) {
+      uint4 g[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c[u] >= 0) g[u] = ll_load_raw(gl + c[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c[u] >= 0) s[u] = __dadd_rn(s[u], __dmul_rn(v[u], ll_value(gl + c[u], g[u], flag, err)));
+    } else {
+      double g[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) g[u] = c[u] >= 0 ? __ldcg(lv + c[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c[u] >= 0) s[u] = __dadd_rn(s[u], __dmul_rn(v[u], g[u]));
+    }
+  }
+  int r[U];
+  double yo[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) r[u] = q0 + u * stride < nro ? rows[q0 + u * stride] : -1;
+#pragma unroll
+  for (int u = 0; u < U; ++u) yo[u] = r[u] >= 0 ? __ldcg(y + r[u]) : 0.0;
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (r[u] >= 0) y[r[u]] = __dadd_rn(yo[u], s[u]);
+}
+constexpr int kRowsU = 4;  // rows per thread of the one-lane-per-row off-diagonal path
 
 }  // namespace spmat

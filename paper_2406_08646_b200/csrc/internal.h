@@ -237,7 +237,6 @@ struct SpmvHalo {                      // fused NVLink halo puts (comm warps)
 };
 struct SpmvTail {                      // fused off-diagonal SpMV-add (work items in the claim order)
   int n_bblocks, enabled;              // boundary blocks are the first n_bblocks in claim order
-  int t0, n_items;                     // claim indices [t0, t0+n_items) are off-diagonal items
   const int32_t *rows, *rowptr, *col;  // compressed off-diagonal block
   const double *val;
   const uint4 *ghost;                  // flagged ghost lines, buffer (epoch & 1) at ghost_stride
@@ -245,7 +244,7 @@ struct SpmvTail {                      // fused off-diagonal SpMV-add (work item
   int64_t n_ro;
   const HaloWait *waits;
   int nwaits, w;                       // w: lanes per off-diagonal row (power of two <= 32)
-  unsigned int *ctr;                   // [0] boundary-block warps done, [1] off-diagonal items done
+  unsigned int *ctr;                   // [0] boundary-block warps done, [1] chunk claims, [2] comm warps done
   unsigned long long *trace;           // SPMAT_TRACE=1: globaltimer stamps (nullptr = off)
 };
 
@@ -293,7 +292,7 @@ struct spmat_s {
   spmat::DevBuf<int4> blocks4;         // (r0, r1, p0, p1) per row block in claim order
   int64_t n_bblocks = 0;
   spmat::DevBuf<unsigned int> tail_ctr;
-  spmat::DevBuf<unsigned long long> trace;  // [cta][4] + [item][4] globaltimer stamps
+  spmat::DevBuf<unsigned long long> trace;  // SPMAT_TRACE: [cta][kTraceCta] globaltimer stamps + header
   spmat::DevBuf<unsigned int> sched; // its block counter + finished-CTA counter
   // host staging for host x / y
   spmat::DevBuf<double> xstage, ystage;

@@ -161,7 +161,68 @@ __device__ __forceinline__ void rows_w(int r0, int r1, int p0, const int *__rest
 }
 
 constexpr int kConsumerWarps = kThreads / 32;
+// SPMAT_TRACE=1 record per CTA (globaltimer ns): consumer start, puts out, last block done,
+// consumer end, comm warp saw the boundary blocks, comm warp tail done
+constexpr int kTraceCta = 6;
 constexpr int kCtaThreads = kThreads + 64;  // + producer warp + comm warp
+
+// Fused off-diagonal SpMV-add, run by the comm warps right after their puts: once every
+// boundary row block is written, claim chunks of off-diagonal rows from a counter and add
+// A_o lvec into y, reading this epoch's flagged ghost lines.  The latency-bound chunks run
+// beside the consumer warps' bandwidth-bound streaming (they used to be work items in the
+// claim sequence, which idled whole CTAs on ghost-read latency: C4 P=2 kernel span 255 ->
+// 251.6 us).  The last comm warp to finish releases the ghost buffer to the senders and
+// resets the counters for the next launch.  Not inlined, and not called from the consumer
+// path: either raised the streaming loop's register demand (C4 P=1 262 -> 302 us measured).
+__device__ __noinline__ void tail_warp(const SpmvTail tail, unsigned long long epoch, int *err,
+                                       double *y, unsigned long long *trc) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    const unsigned target = (unsigned)(kConsumerWarps * tail.n_bblocks);
+    const long long t0 = clock64();
+    while (ld_acquire_gpu(tail.ctr) < target) {
+      if (clock64() - t0 > kSpinLimit) {
+        atomicExch(err, 2);
+        break;
+      }
+      __nanosleep(64);
+    }
+    if (trc) trc[4] = gtimer();
+  }
+  __syncwarp();
+  const uint4 *gl = tail.ghost + (int64_t)(epoch & 1) * tail.ghost_stride;
+  const uint32_t flag = ll_flag(epoch);
+  const int w = tail.w;
+  const int64_t per = w == 1 ? 32 * kRowsU : 32 / w;  // rows per chunk
+  const int64_t n_chunks = (tail.n_ro + per - 1) / per;
+  for (;;) {
+    int64_t c = 0;
+    if (lane == 0) c = atomicAdd(tail.ctr + 1, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= n_chunks) break;
+    if (w == 1) {
+      offdiag_rows_u<kRowsU>(c * per + lane, 32, tail.n_ro, tail.rows, tail.rowptr, tail.col, tail.val, gl,
+                             nullptr, flag, err, y);
+    } else {
+      const int64_t q = c * per + lane / w;
+      offdiag_row_w(q, q < tail.n_ro, w, tail.rows, tail.rowptr, tail.col, tail.val,
+                    [&](int cc) { return ll_load(gl + cc, flag, err); }, y);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (trc) trc[5] = gtimer();
+    __threadfence();
+    // every warp stops claiming before it arrives here, so the last arrival may reset
+    if (atomicAdd(tail.ctr + 2, 1u) == gridDim.x - 1) {
+      atomicExch(tail.ctr, 0u);
+      atomicExch(tail.ctr + 1, 0u);
+      atomicExch(tail.ctr + 2, 0u);
+      __threadfence();
+      for (int q = 0; q < tail.nwaits; ++q) st_release_sys(tail.waits[q].peer_done, epoch);
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kCtaThreads, 3)
     k_spmv_tma(const int4 *__restrict__ blocks, int n_blocks, const int32_t *__restrict__ rowptr,
@@ -185,11 +246,12 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
   // (which only exists once every CTA has claimed) stores it back
   const unsigned long long epoch = halo.epoch_ctr ? *halo.epoch_ctr + 1ull : 0ull;
   __syncthreads();
-  if (warp == kConsumerWarps + 1) {  // ---------------- comm warp: fused halo puts (halo.cu)
+  unsigned long long *trc = tail.trace ? tail.trace + kTraceCta * (size_t)blockIdx.x : nullptr;
+  if (warp == kConsumerWarps + 1) {  // ---------------- comm warp: halo puts, then the tail
     for (int c = blockIdx.x; c < halo.put_chunks; c += gridDim.x)
       halo_put_warp(halo.puts, halo.nputs, c, x, epoch, halo.err);
-    if (tail.trace && lane32 == 0 && blockIdx.x < halo.put_chunks)
-      tail.trace[4 * (size_t)blockIdx.x + 1] = gtimer();  // this CTA's puts are out
+    if (trc && lane32 == 0) trc[1] = gtimer();  // this CTA's puts are out
+    if (tail.enabled) tail_warp(tail, epoch, halo.err, y, trc);
     return;
   }
   if (warp == kConsumerWarps) {  // ---------------- producer warp
@@ -198,13 +260,10 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
     // claims run two ahead: the atomic for block it+2 is in flight while block it is issued,
     // so only the (order, bounds) loads of the next block sit on the producer's path.
-    // Claim index c maps to: an off-diagonal work item if c in [t0, t0+n_items), else a row
-    // block (through the boundary-first order when the tail is fused).
-    const int n_total = n_blocks + tail.n_items;
-    auto bounds = [&](int c, int4 &H) {  // one 16-byte load: (r0, r1, p0, p1) in claim order
-      if (c >= tail.t0 && c < tail.t0 + tail.n_items) return;
-      H = blocks[c < tail.t0 ? c : c - tail.n_items];
-    };
+    // Claim index c is row block c of the claim order (boundary blocks first when the tail is
+    // fused).
+    const int n_total = n_blocks;
+    auto bounds = [&](int c, int4 &H) { H = blocks[c]; };  // one 16-byte load: (r0, r1, p0, p1)
     int b = (int)atomicAdd(sched, 1u);
     int b_next = (int)atomicAdd(sched, 1u);
     int4 H = make_int4(0, 0, 0, 0);
@@ -223,10 +282,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
         }
         return;
       }
-      if (b >= tail.t0 && b < tail.t0 + tail.n_items) {  // off-diagonal work item
-        st[s].hdr = make_int4(-2, b - tail.t0, 0, 0);
-        mbar_arrive_tx(&full[s], 0);
-      } else {
+      {
         const int r0 = H.x, r1 = H.y, p0 = H.z, p1 = H.w;
         st[s].hdr = H;
         st[s].flags.x = (tail.enabled && b < tail.n_bblocks) ? 1 : 0;
@@ -250,7 +306,6 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     }
   }
   // ---------------- consumer warps
-  unsigned long long *trc = tail.trace ? tail.trace + 4 * (size_t)blockIdx.x : nullptr;
   if (trc && tid == 0) trc[0] = gtimer();
   // boundary blocks are claimed before everything else, so a warp publishes how many it
   // wrote (one fence + one atomic per warp) when it meets its first other claim
@@ -274,43 +329,6 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     if (r0 == -1) {
       if (trc && tid == 0) trc[2] = gtimer();
       break;
-    }
-    if (r0 == -2) {  // ---- off-diagonal work item: y[rows_o] += A_o lvec for kThreads rows
-      unsigned long long *itr = tail.trace ? tail.trace + 4 * (size_t)gridDim.x + 4 * (size_t)r1 : nullptr;
-      if (itr && tid == 0) itr[0] = gtimer();
-      if (tid == 0) {  // every boundary block written (the ghost lines are waited for one by one)
-        const unsigned target = (unsigned)(kConsumerWarps * tail.n_bblocks);
-        const long long t0 = clock64();
-        while (ld_acquire_gpu(tail.ctr) < target) {
-          if (clock64() - t0 > kSpinLimit) {
-            atomicExch(halo.err, 2);
-            break;
-          }
-          __nanosleep(32);
-        }
-        if (itr) itr[3] = gtimer();  // boundary blocks written
-      }
-      asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
-      if (itr && tid == 0) itr[1] = gtimer();
-      const int64_t q = ((int64_t)r1 * kThreads + tid) / tail.w;  // item r1: kThreads / w rows
-      const uint4 *gl = tail.ghost + (int64_t)(epoch & 1) * tail.ghost_stride;
-      const uint32_t flag = ll_flag(epoch);
-      offdiag_row_w(q, q < tail.n_ro, tail.w, tail.rows, tail.rowptr, tail.col, tail.val,
-                    [&](int c) { return ll_load(gl + c, flag, halo.err); }, y);
-      asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
-      if (itr && tid == 0) itr[2] = gtimer();
-      if (tid == 0) {
-        __threadfence();
-        if (atomicAdd(tail.ctr + 1, 1u) == (unsigned)tail.n_items - 1) {  // last item: release lvec
-          atomicExch(tail.ctr, 0u);
-          atomicExch(tail.ctr + 1, 0u);
-          __threadfence();
-          for (int w = 0; w < tail.nwaits; ++w) st_release_sys(tail.waits[w].peer_done, epoch);
-        }
-      }
-      __syncwarp();
-      if (lane32 == 0) mbar_arrive(&empty[s]);
-      continue;
     }
     const int boundary = st[s].flags.x;
     if (p1 - p0 <= kCap) {
@@ -434,6 +452,12 @@ __global__ void __launch_bounds__(256) k_spmv_offdiag(const int32_t *__restrict_
   // NCCL mode: lvec.  NVLink mode: the ghost lines of the last completed epoch (already landed).
   const unsigned long long epoch = ghost ? *epoch_ctr : 0ull;
   const uint4 *gl = ghost ? ghost + (int64_t)(epoch & 1) * ghost_stride : nullptr;
+  if (W == 1) {
+    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x * kRowsU; t0 < nro; t0 += (int64_t)gridDim.x * blockDim.x * kRowsU)
+      offdiag_rows_u<kRowsU>(t0 + threadIdx.x, blockDim.x, nro, rows, rowptr, col, val, gl, lvec,
+                             ll_flag(epoch), err, y);
+    return;
+  }
   // block-uniform loop bound: every lane reaches the shuffles in offdiag_row_w
   for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < nro * W; t0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t q = (t0 + threadIdx.x) / W;
@@ -552,8 +576,8 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
     SP_CUDA(cudaMemcpyAsync(A->longrows.get(), longrows.get(), (size_t)nlong * 4, cudaMemcpyDeviceToDevice, st));
   SP_TRY(A->sched.alloc(2));
   SP_CUDA(cudaMemsetAsync(A->sched.get(), 0, 8, st));
-  SP_TRY(A->tail_ctr.alloc(2));
-  SP_CUDA(cudaMemsetAsync(A->tail_ctr.get(), 0, 8, st));
+  SP_TRY(A->tail_ctr.alloc(3));
+  SP_CUDA(cudaMemsetAsync(A->tail_ctr.get(), 0, 12, st));
 
   A->n_bblocks = 0;
   if (A->n_ro > 0) {  // claim order for the fused off-diagonal tail: boundary blocks first
@@ -584,10 +608,9 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   SP_TRY(tma_setup(A));
   if (const char *tr = getenv("SPMAT_TRACE")) {  // device trace of the fused MatMult kernel
     if (atoi(tr)) {
-      const int64_t nitems = (A->n_ro * A->ro_w + kThreads - 1) / kThreads;
-      SP_TRY(A->trace.alloc(4 * (size_t)A->tma_grid + 4 * (size_t)nitems + 16));
+      SP_TRY(A->trace.alloc(kTraceCta * (size_t)A->tma_grid + 16));
       SP_CUDA(cudaMemsetAsync(A->trace.get(), 0, A->trace.n * 8, st));
-      const unsigned long long hdr[2] = {(unsigned long long)A->tma_grid, (unsigned long long)nitems};
+      const unsigned long long hdr[2] = {(unsigned long long)A->tma_grid, (unsigned long long)kTraceCta};
       SP_CUDA(cudaMemcpyAsync(A->trace.get() + A->trace.n - 2, hdr, sizeof hdr, cudaMemcpyHostToDevice, st));
     }
   }
@@ -602,18 +625,11 @@ static cudaError_t launch_tma(spmat_s *A, const double *x, double *y, cudaStream
   SpmvHalo h{A->halo_puts.get(), A->n_puts, fuse_put ? A->put_chunks_total : 0,
              A->peer ? A->d_epoch.get() : nullptr, (fuse_put && fuse_tail) ? 1 : 0, A->halo_err.get()};
   SpmvTail t{};
-  t.t0 = (int)A->n_rowblocks;  // no items: every claim index is a row block
-  if (fuse_tail) {
+  t.trace = A->trace.get();
+  if (fuse_tail) {  // the comm warps add A_o lvec once the boundary blocks (claimed first) are written
     t.n_bblocks = (int)A->n_bblocks;
     t.enabled = 1;
-    // items go a quarter of the way through the sweep: by then the boundary blocks (claimed
-    // first) are written and the halo puts (issued at kernel start) have landed
     t.w = A->ro_w;
-    t.n_items = (int)((A->n_ro * A->ro_w + kThreads - 1) / kThreads);
-    const char *f = getenv("SPMAT_TAIL_AT");  // fraction of the sweep before the items
-    const double at = f ? atof(f) : 0.5;
-    t.t0 = (int)std::max<int64_t>(A->n_bblocks, (int64_t)(A->n_rowblocks * at));
-    t.trace = A->trace.get();
     t.rows = A->rows_o.get();
     t.rowptr = A->rowptr_o.get();
     t.col = A->col_o.get();
@@ -666,7 +682,7 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_
 
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t s) {
   if (A->n_ro == 0) return SPMAT_OK;
-  k_spmv_offdiag<<<nblk(A->n_ro * A->ro_w), 256, 0, s>>>(
+  k_spmv_offdiag<<<nblk(A->ro_w == 1 ? (A->n_ro + kRowsU - 1) / kRowsU : A->n_ro * A->ro_w), 256, 0, s>>>(
       A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(), A->val_o.get(), A->lvec.get(),
       A->peer ? A->ghost.get() : nullptr, A->ghost_stride, A->peer ? A->d_epoch.get() : nullptr, y,
       A->n_ro, A->ro_w, A->peer ? A->halo_err.get() : nullptr);
@@ -726,7 +742,6 @@ int spmv_diag_chunk(spmat_s *A, const double *x, double *y, int k, cudaStream_t 
   if (c1 <= c0) return SPMAT_OK;
   SpmvHalo h{A->halo_puts.get(), 0, 0, nullptr, 0, A->halo_err.get()};
   SpmvTail t{};
-  t.t0 = (int)(c1 - c0);
   const unsigned grid = (unsigned)std::min<int64_t>(A->tma_grid, c1 - c0);
   k_spmv_tma<<<grid, kCtaThreads, kTmaSmem, s>>>(A->blocks4.get() + c0, (int)(c1 - c0), A->rowptr_d.get(),
                                                 A->col_d.get(), A->val_d.get(), x, y, A->sched.get(), h, t);

@@ -64,28 +64,27 @@ def main():
     dur = [ev[2 * k].elapsed_time(ev[2 * k + 1]) * 1e3 for k in range(a.reps)]
     per = ev[0].elapsed_time(ev[-1]) * 1e3 / a.reps
     t = sp.spmat_trace_read(A.h)
-    G, nitems = int(t[-2]), int(t[-1])  # header: CTAs, off-diagonal work items
-    cta = t[:4 * G].reshape(G, 4).astype(np.float64)
-    # item record: start, compute start (boundary blocks written), end, (same as [1])
-    items = t[4 * G:4 * G + 4 * nitems].reshape(nitems, 4).astype(np.float64) if nitems else np.zeros((0, 4))
+    G, K = int(t[-2]), int(t[-1])  # header: CTAs, stamps per CTA
+    # per CTA: consumer start, puts out, last block done, consumer end, comm warp saw the
+    # boundary blocks, comm warp off-diagonal chunks done (0 = not recorded)
+    cta = t[:K * G].reshape(G, K).astype(np.float64)
     t0 = cta[:, 0].min()
-    span = cta[:, 3].max() - t0
+    end = max(cta[:, 3].max(), cta[:, 5].max())
+    span = end - t0
     term = cta[:, 2] - t0
     msg = [f"rank {r}: kernel span {span / 1e3:.1f} us, CTAs {G}, mode {A.halo_mode()}; per call "
            f"{per:.1f} us, call duration median {np.median(dur):.1f} us",
            f"  CTA start spread {np.ptp(cta[:, 0]) / 1e3:.1f} us; last-block done: min {term.min() / 1e3:.1f} "
-           f"median {np.median(term) / 1e3:.1f} max {term.max() / 1e3:.1f} us; end max {(cta[:, 3].max() - t0) / 1e3:.1f}"]
+           f"median {np.median(term) / 1e3:.1f} max {term.max() / 1e3:.1f} us; consumers end max "
+           f"{(cta[:, 3].max() - t0) / 1e3:.1f}"]
     put = cta[:, 1][cta[:, 1] > 0] - t0
-    if put.size:
-        msg.append(f"  puts out: {put.size} CTAs, {put.min() / 1e3:.1f}..{put.max() / 1e3:.1f} us; "
-                   f"kernel start (globaltimer) {int(t0) % 10**9 / 1e3:.1f} us")
-    if nitems:
-        st = items[:, 0] - t0
-        wait = items[:, 1] - items[:, 0]
-        comp = items[:, 2] - items[:, 1]
-        msg.append(f"  items {nitems}: start {st.min() / 1e3:.1f}..{st.max() / 1e3:.1f} us; boundary-block "
-                   f"wait median {np.median(wait) / 1e3:.2f} max {wait.max() / 1e3:.2f} us; ghost wait + "
-                   f"compute median {np.median(comp) / 1e3:.2f} max {comp.max() / 1e3:.2f} us")
+    if put.size and A.halo_mode() == 2:
+        msg.append(f"  puts out: {put.min() / 1e3:.1f}..{put.max() / 1e3:.1f} us")
+    seen = cta[:, 4][cta[:, 4] > 0] - t0
+    done = cta[:, 5][cta[:, 5] > 0] - t0
+    if done.size:
+        msg.append(f"  off-diagonal (comm warps): boundary blocks seen {seen.min() / 1e3:.1f}..{seen.max() / 1e3:.1f} us; "
+                   f"chunks done median {np.median(done) / 1e3:.1f} max {done.max() / 1e3:.1f} us")
     for k in range(P):
         sd.barrier()
         if k == r:
