@@ -43,7 +43,8 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
       }
     }
     // full MatMult, no long rows: the off-diagonal SpMV-add runs in the same kernel's tail
-    const bool tail = fused && (part & 4) && A->n_ro > 0 && A->n_long == 0;
+    static const bool no_tail = getenv("SPMAT_FUSE_TAIL") && !strcmp(getenv("SPMAT_FUSE_TAIL"), "0");
+    const bool tail = fused && (part & 4) && A->n_ro > 0 && A->n_long == 0 && !no_tail;
     if (part & 1) {
       pe = A->profile ? prof_pair(A, 0) : nullptr;
       if (pe) SP_CUDA(cudaEventRecord(pe[0], s));

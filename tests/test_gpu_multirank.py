@@ -31,16 +31,18 @@ def test_multirank_parity(P, halo):
     assert f"halo_mode={want}" in r.stdout
 
 
-@pytest.mark.parametrize("ro_w", ["1", "32"])
-def test_multirank_offdiag_lanes(ro_w):
+@pytest.mark.parametrize("ro_w,fuse", [("1", "1"), ("32", "1"), ("1", "0"), ("8", "0")])
+def test_multirank_offdiag_lanes(ro_w, fuse):
     """The off-diagonal SpMV-add with forced lanes per row (1: plain row sums, 32: one warp per
-    row) in the fused NVLink kernel, the standalone kernels and the NCCL path."""
+    row), fused into the SpMV kernel's comm warps or (SPMAT_FUSE_TAIL=0) as the standalone
+    NVLink kernel."""
     P = 2
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
     env = dict(os.environ)
     env["SPMAT_RO_W"] = ro_w
-    port = 29661 + int(ro_w)
+    env["SPMAT_FUSE_TAIL"] = fuse
+    port = 29661 + int(ro_w) + 40 * int(fuse)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(HERE, "mp_gpu_parity.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
