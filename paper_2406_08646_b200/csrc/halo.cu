@@ -65,8 +65,7 @@ __global__ void __launch_bounds__(256) k_spmv_offdiag_peer(
   } else if (nro > 0) {  // block-uniform loop bound: every lane reaches the shuffles in offdiag_row_w
     for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < nro * W; t0 += (int64_t)gridDim.x * blockDim.x) {
       const int64_t q = (t0 + threadIdx.x) / W;
-      offdiag_row_w(q, q < nro, W, rows, rowptr, col, val,
-                    [&](int c) { return ll_load(gl + c, flag, err); }, y);
+      offdiag_row_w(q, q < nro, W, rows, rowptr, col, val, gl, nullptr, flag, err, y);
     }
   } else {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_ghost; g += (int64_t)gridDim.x * blockDim.x)

@@ -1,6 +1,7 @@
 // halo_dev.cuh -- device side of the NVLink halo (shared by halo.cu and spmv.cu).
 #pragma once
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace spmat {
 
@@ -115,18 +116,47 @@ __device__ __forceinline__ void halo_put_warp(const HaloPut *__restrict__ puts, 
 // Off-diagonal SpMV-add with W lanes per row (W a power of two <= 32): thread t of a group
 // handles row q's entries rowptr[q]+t, +W, ... and the group sums by a shuffle tree.  Every
 // lane of the warp must call it (the shuffles); lanes with valid == false contribute nothing.
-// W = 1 is the plain left-to-right row sum.  ghost(c) returns ghost value c.
-template <class Ghost>
+// W = 1 is the plain left-to-right row sum.  A lane loads the column/value of KB entries, then
+// their KB ghost values, before it uses any (the work is latency-bound: a dependent ghost read
+// per entry).  gl != nullptr: flagged ghost lines of `flag`; else the plain ghost vector lv.
 __device__ __forceinline__ void offdiag_row_w(int64_t q, bool valid, int W,
                                               const int32_t *__restrict__ rows,
                                               const int32_t *__restrict__ rowptr,
                                               const int32_t *__restrict__ col,
-                                              const double *__restrict__ val, Ghost ghost,
-                                              double *y) {
+                                              const double *__restrict__ val, const uint4 *gl,
+                                              const double *lv, uint32_t flag, int *err, double *y) {
+  constexpr int KB = 4;
   const int sub = threadIdx.x & (W - 1);
   double s = 0.0;
-  if (valid)
-    for (int e = rowptr[q] + sub; e < rowptr[q + 1]; e += W) s = __dadd_rn(s, __dmul_rn(val[e], ghost(col[e])));
+  if (valid) {
+    const int z = rowptr[q + 1];
+    for (int e0 = rowptr[q] + sub; e0 < z; e0 += KB * W) {
+      int c[KB];
+      double v[KB];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) {
+        const int e = e0 + k * W;
+        c[k] = e < z ? col[e] : -1;
+        v[k] = e < z ? val[e] : 0.0;
+      }
+      if (gl) {
+        uint4 g[KB];
+#pragma unroll
+        for (int k = 0; k < KB; ++k)
+          if (c[k] >= 0) g[k] = ll_load_raw(gl + c[k]);
+#pragma unroll
+        for (int k = 0; k < KB; ++k)
+          if (c[k] >= 0) s = __dadd_rn(s, __dmul_rn(v[k], ll_value(gl + c[k], g[k], flag, err)));
+      } else {
+        double g[KB];
+#pragma unroll
+        for (int k = 0; k < KB; ++k) g[k] = c[k] >= 0 ? __ldcg(lv + c[k]) : 0.0;
+#pragma unroll
+        for (int k = 0; k < KB; ++k)
+          if (c[k] >= 0) s = __dadd_rn(s, __dmul_rn(v[k], g[k]));
+      }
+    }
+  }
   for (int o = W >> 1; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o, W));
   if (valid && sub == 0) {
     const int r = rows[q];
@@ -195,5 +225,67 @@ __device__ __forceinline__ void offdiag_rows_u(int64_t q0, int64_t stride, int64
     if (r[u] >= 0) y[r[u]] = __dadd_rn(yo[u], s[u]);
 }
 constexpr int kRowsU = 4;  // rows per thread of the one-lane-per-row off-diagonal path
+
+// Fused off-diagonal SpMV-add (k_spmv_tma, k_spmv_bsr3), run by the comm warps right after
+// their puts: once every boundary row block is written (each of the consumer_warps consumer
+// warps of every CTA adds its count of boundary blocks to tail.ctr[0]), claim chunks of off-diagonal rows from a counter and add
+// A_o lvec into y, reading this epoch's flagged ghost lines.  The latency-bound chunks run
+// beside the consumer warps' bandwidth-bound streaming (they used to be work items in the
+// claim sequence, which idled whole CTAs on ghost-read latency: C4 P=2 kernel span 255 ->
+// 251.6 us).  The last comm warp to finish releases the ghost buffer to the senders and
+// resets the counters for the next launch.  Not inlined, and not called from the consumer
+// path: either raised the streaming loop's register demand (C4 P=1 262 -> 302 us measured).
+static __device__ __noinline__ void tail_warp(const SpmvTail tail, unsigned long long epoch, int *err,
+                                              double *y, unsigned long long *trc, int consumer_warps) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    // short backoff: with box partitions 444 warps may wait the whole sweep here
+    const unsigned target = (unsigned)(consumer_warps * tail.n_bblocks);
+    const long long t0 = clock64();
+    unsigned ns = 64;
+    while (ld_acquire_gpu(tail.ctr) < target) {
+      if (clock64() - t0 > kSpinLimit) {
+        atomicExch(err, 2);
+        break;
+      }
+      __nanosleep(ns);
+      ns = ns < 256 ? 2 * ns : ns;
+    }
+    if (trc) trc[4] = gtimer();
+  }
+  __syncwarp();
+  const uint4 *gl = tail.ghost + (int64_t)(epoch & 1) * tail.ghost_stride;
+  const uint32_t flag = ll_flag(epoch);
+  const int w = tail.w;
+  const int64_t per = w == 1 ? 32 * kRowsU : 32 / w;  // rows per chunk
+  const int64_t n_chunks = (tail.n_ro + per - 1) / per;
+  for (;;) {
+    int64_t c = 0;
+    if (lane == 0) c = atomicAdd(tail.ctr + 1, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= n_chunks) break;
+    if (w == 1) {
+      offdiag_rows_u<kRowsU>(c * per + lane, 32, tail.n_ro, tail.rows, tail.rowptr, tail.col, tail.val, gl,
+                             nullptr, flag, err, y);
+    } else {
+      const int64_t q = c * per + lane / w;
+      offdiag_row_w(q, q < tail.n_ro, w, tail.rows, tail.rowptr, tail.col, tail.val, gl, nullptr, flag, err, y);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (trc) trc[5] = gtimer();
+    __threadfence();
+    // every warp stops claiming before it arrives here, so the last arrival may reset
+    if (atomicAdd(tail.ctr + 2, 1u) == gridDim.x - 1) {
+      atomicExch(tail.ctr, 0u);
+      atomicExch(tail.ctr + 1, 0u);
+      atomicExch(tail.ctr + 2, 0u);
+      __threadfence();
+      for (int q = 0; q < tail.nwaits; ++q) st_release_sys(tail.waits[q].peer_done, epoch);
+    }
+  }
+}
+
 
 }  // namespace spmat

@@ -34,7 +34,11 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
       // the epoch lives on the device (A->d_epoch): kernels read it, the MatMult's last kernel
       // advances it -- so MatMults can be captured in CUDA graphs.
       // the bulk-copy SpMV's comm warps do the puts; otherwise a standalone put kernel
-      fused = (part & 1) && A->kernel_id == 3 && A->m > 0 && A->n_rowblocks > 0;
+      // (only k_spmv_tma has comm warps: a comm-warp variant of the 3x3 block kernel capped it
+      // at 64 registers and lost more on the stream than the overlap gained -- C5 P=2 1.43 ms
+      // either way, P=1 -2 %)
+      static const bool no_fuse = getenv("SPMAT_FUSE") && !strcmp(getenv("SPMAT_FUSE"), "0");
+      fused = !no_fuse && (part & 1) && A->kernel_id == 3 && A->m > 0 && A->n_rowblocks > 0;
       if (!fused) {
         pe = A->profile ? prof_pair(A, 2) : nullptr;
         if (pe) SP_CUDA(cudaEventRecord(pe[0], s));

@@ -166,67 +166,6 @@ constexpr int kConsumerWarps = kThreads / 32;
 constexpr int kTraceCta = 6;
 constexpr int kCtaThreads = kThreads + 64;  // + producer warp + comm warp
 
-// Fused off-diagonal SpMV-add, run by the comm warps right after their puts: once every
-// boundary row block is written, claim chunks of off-diagonal rows from a counter and add
-// A_o lvec into y, reading this epoch's flagged ghost lines.  The latency-bound chunks run
-// beside the consumer warps' bandwidth-bound streaming (they used to be work items in the
-// claim sequence, which idled whole CTAs on ghost-read latency: C4 P=2 kernel span 255 ->
-// 251.6 us).  The last comm warp to finish releases the ghost buffer to the senders and
-// resets the counters for the next launch.  Not inlined, and not called from the consumer
-// path: either raised the streaming loop's register demand (C4 P=1 262 -> 302 us measured).
-__device__ __noinline__ void tail_warp(const SpmvTail tail, unsigned long long epoch, int *err,
-                                       double *y, unsigned long long *trc) {
-  const int lane = threadIdx.x & 31;
-  if (lane == 0) {
-    // short backoff: with box partitions 444 warps may wait the whole sweep here
-    const unsigned target = (unsigned)(kConsumerWarps * tail.n_bblocks);
-    const long long t0 = clock64();
-    unsigned ns = 64;
-    while (ld_acquire_gpu(tail.ctr) < target) {
-      if (clock64() - t0 > kSpinLimit) {
-        atomicExch(err, 2);
-        break;
-      }
-      __nanosleep(ns);
-      ns = ns < 256 ? 2 * ns : ns;
-    }
-    if (trc) trc[4] = gtimer();
-  }
-  __syncwarp();
-  const uint4 *gl = tail.ghost + (int64_t)(epoch & 1) * tail.ghost_stride;
-  const uint32_t flag = ll_flag(epoch);
-  const int w = tail.w;
-  const int64_t per = w == 1 ? 32 * kRowsU : 32 / w;  // rows per chunk
-  const int64_t n_chunks = (tail.n_ro + per - 1) / per;
-  for (;;) {
-    int64_t c = 0;
-    if (lane == 0) c = atomicAdd(tail.ctr + 1, 1u);
-    c = __shfl_sync(0xffffffffu, c, 0);
-    if (c >= n_chunks) break;
-    if (w == 1) {
-      offdiag_rows_u<kRowsU>(c * per + lane, 32, tail.n_ro, tail.rows, tail.rowptr, tail.col, tail.val, gl,
-                             nullptr, flag, err, y);
-    } else {
-      const int64_t q = c * per + lane / w;
-      offdiag_row_w(q, q < tail.n_ro, w, tail.rows, tail.rowptr, tail.col, tail.val,
-                    [&](int cc) { return ll_load(gl + cc, flag, err); }, y);
-    }
-  }
-  __syncwarp();
-  if (lane == 0) {
-    if (trc) trc[5] = gtimer();
-    __threadfence();
-    // every warp stops claiming before it arrives here, so the last arrival may reset
-    if (atomicAdd(tail.ctr + 2, 1u) == gridDim.x - 1) {
-      atomicExch(tail.ctr, 0u);
-      atomicExch(tail.ctr + 1, 0u);
-      atomicExch(tail.ctr + 2, 0u);
-      __threadfence();
-      for (int q = 0; q < tail.nwaits; ++q) st_release_sys(tail.waits[q].peer_done, epoch);
-    }
-  }
-}
-
 __global__ void __launch_bounds__(kCtaThreads, 3)
     k_spmv_tma(const int4 *__restrict__ blocks, int n_blocks, const int32_t *__restrict__ rowptr,
                const int32_t *__restrict__ col, const double *__restrict__ val,
@@ -254,7 +193,7 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     for (int c = blockIdx.x; c < halo.put_chunks; c += gridDim.x)
       halo_put_warp(halo.puts, halo.nputs, c, x, epoch, halo.err);
     if (trc && lane32 == 0) trc[1] = gtimer();  // this CTA's puts are out
-    if (tail.enabled) tail_warp(tail, epoch, halo.err, y, trc);
+    if (tail.enabled) tail_warp(tail, epoch, halo.err, y, trc, kConsumerWarps);
     return;
   }
   if (warp == kConsumerWarps) {  // ---------------- producer warp
@@ -464,11 +403,7 @@ __global__ void __launch_bounds__(256) k_spmv_offdiag(const int32_t *__restrict_
   // block-uniform loop bound: every lane reaches the shuffles in offdiag_row_w
   for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < nro * W; t0 += (int64_t)gridDim.x * blockDim.x) {
     const int64_t q = (t0 + threadIdx.x) / W;
-    if (gl)
-      offdiag_row_w(q, q < nro, W, rows, rowptr, col, val,
-                    [&](int c) { return ll_load(gl + c, ll_flag(epoch), err); }, y);
-    else
-      offdiag_row_w(q, q < nro, W, rows, rowptr, col, val, [&](int c) { return __ldcg(lvec + c); }, y);
+    offdiag_row_w(q, q < nro, W, rows, rowptr, col, val, gl, lvec, ll_flag(epoch), err, y);
   }
 }
 
