@@ -908,6 +908,7 @@ int spmat_destroy(spmat_t A) {
     for (cudaEvent_t e : A->pipe_ev) cudaEventDestroy(e);
     if (A->pipe_in) cudaStreamDestroy(A->pipe_in);
     if (A->pipe_out) cudaStreamDestroy(A->pipe_out);
+    if (A->pipe_comm) cudaStreamDestroy(A->pipe_comm);
     if (A->ev_send_ready) cudaEventDestroy(A->ev_send_ready);
     if (A->ev_recv_done) cudaEventDestroy(A->ev_recv_done);
     for (auto &v : A->prof_ev)
@@ -917,7 +918,7 @@ int spmat_destroy(spmat_t A) {
     A->rows_o.release(); A->rowptr_o.release(); A->col_o.release(); A->val_o.release();
     A->colmap.release(); A->lvec.release(); A->jmap.release(); A->perm.release();
     A->mixed.release(); A->sendperm.release(); A->sendbuf.release(); A->recvbuf.release();
-    A->rbp.release(); A->sched.release(); A->block_order.release(); A->blocks4.release(); A->tail_ctr.release(); A->trace.release(); A->halo_flags.release(); A->ghost.release(); A->halo_puts.release(); A->halo_waits.release(); A->halo_counter.release(); A->halo_err.release(); A->longrows.release(); A->xstage.release(); A->ystage.release(); A->cg_r.release(); A->cg_p.release(); A->cg_q.release(); A->cg_partial.release(); A->cg_scalars.release(); A->cg_reduced.release();
+    A->rbp.release(); A->sched.release(); A->block_order.release(); A->blocks4.release(); A->tail_ctr.release(); A->trace.release(); A->halo_flags.release(); A->ghost.release(); A->halo_puts.release(); A->halo_waits.release(); A->halo_counter.release(); A->halo_err.release(); A->longrows.release(); A->xstage.release(); A->ystage.release(); A->pipe_blocks4.release(); A->cg_r.release(); A->cg_p.release(); A->cg_q.release(); A->cg_partial.release(); A->cg_scalars.release(); A->cg_reduced.release();
   }
   delete A;
   return SPMAT_OK;

@@ -82,6 +82,54 @@ __global__ void __launch_bounds__(256) k_spmv_offdiag_peer(
   }
 }
 
+// Host-buffer pipeline pieces (mult.cu): the off-diagonal SpMV-add of compressed rows [q0, q1)
+// with this MatMult's ghost lines (no epoch bookkeeping), and the epoch end: release the
+// ghost buffer to the senders and advance the epoch.
+__global__ void __launch_bounds__(256) k_offdiag_peer_range(
+    const int32_t *__restrict__ rows, const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+    const double *__restrict__ val, const uint4 *ghost_base, int64_t ghost_stride, double *__restrict__ y,
+    int64_t q0, int64_t q1, int W, const unsigned long long *epoch_ctr, int *err) {
+  pdl_wait();
+  const unsigned long long epoch = *epoch_ctr + 1ull;
+  const uint32_t flag = ll_flag(epoch);
+  const uint4 *gl = ghost_base + (int64_t)(epoch & 1) * ghost_stride;
+  const int64_t n = q1 - q0;
+  if (W == 1) {
+    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x * kRowsU; t0 < n; t0 += (int64_t)gridDim.x * blockDim.x * kRowsU)
+      offdiag_rows_u<kRowsU>(t0 + threadIdx.x, blockDim.x, n, rows + q0, rowptr + q0, col, val, gl, nullptr, flag,
+                             err, y);
+  } else {
+    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < n * W; t0 += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t q = (t0 + threadIdx.x) / W;
+      offdiag_row_w(q, q < n, W, rows + q0, rowptr + q0, col, val, gl, nullptr, flag, err, y);
+    }
+  }
+}
+
+__global__ void k_epoch_end(const HaloWait *__restrict__ waits, int nwaits, unsigned long long *epoch_ctr) {
+  pdl_wait();
+  const unsigned long long epoch = *epoch_ctr + 1ull;
+  for (int w = 0; w < nwaits; ++w) st_release_sys(waits[w].peer_done, epoch);
+  *epoch_ctr = epoch;
+}
+
+int halo_peer_offdiag_range(spmat_s *A, double *y, int64_t q0, int64_t q1, cudaStream_t s) {
+  if (q1 <= q0) return SPMAT_OK;
+  const int64_t work = A->ro_w == 1 ? (q1 - q0 + kRowsU - 1) / kRowsU : (q1 - q0) * A->ro_w;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 4L * A->comm->num_sms));
+  k_offdiag_peer_range<<<grid, 256, 0, s>>>(A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(), A->val_o.get(),
+                                            A->ghost.get(), A->ghost_stride, y, q0, q1, A->ro_w, A->d_epoch.get(),
+                                            A->halo_err.get());
+  SP_LAUNCH();
+  return SPMAT_OK;
+}
+
+int halo_peer_epoch_end(spmat_s *A, cudaStream_t s) {
+  k_epoch_end<<<1, 1, 0, s>>>(A->halo_waits.get(), A->n_waits, A->d_epoch.get());
+  SP_LAUNCH();
+  return SPMAT_OK;
+}
+
 int halo_peer_setup(spmat_s *A) {
   spmat_comm_s *c = A->comm;
   const int P = c->nranks, me = c->rank;

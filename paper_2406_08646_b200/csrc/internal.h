@@ -329,7 +329,11 @@ struct spmat_s {
   spmat::DevBuf<unsigned int> bsched;
   // host-buffer MatMult pipeline (mult.cu / spmv.cu), built on first use
   int pipe_chunks = 0;
-  std::vector<int64_t> pipe_block, pipe_row, pipe_xneed;  // claim range, row range, last x row
+  std::vector<int64_t> pipe_block, pipe_row, pipe_xmin, pipe_xneed;  // row-order block range, row range, x rows read
+  std::vector<int64_t> pipe_q;             // [chunks+1] first compressed off-diagonal row of each chunk
+  std::vector<char> pipe_put_chunk;        // chunk holds x rows the NVLink puts read
+  spmat::DevBuf<int4> pipe_blocks4;        // row-ordered block table (when the claim order differs)
+  cudaStream_t pipe_comm = nullptr;        // high-priority stream of the standalone put
   cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
   std::vector<cudaEvent_t> pipe_ev;                        // 2 * chunks + 2
   // CG / dot workspace (krylov.cu), allocated on first use
@@ -354,4 +358,6 @@ int halo_peer_setup(spmat_s *A);                  // collective; leaves A->peer 
 void halo_peer_release(spmat_s *A);
 int halo_peer_put(spmat_s *A, const double *x, cudaStream_t s);  // standalone put kernel
 int halo_peer_offdiag(spmat_s *A, double *y, cudaStream_t s, bool compute);
+int halo_peer_offdiag_range(spmat_s *A, double *y, int64_t q0, int64_t q1, cudaStream_t s);  // no epoch end
+int halo_peer_epoch_end(spmat_s *A, cudaStream_t s);   // release the ghost buffer, advance the epoch
 }  // namespace spmat

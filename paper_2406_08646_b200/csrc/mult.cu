@@ -87,25 +87,34 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
   return SPMAT_OK;
 }
 
-// Host x and y on one rank: copy x in row chunks on one stream, run the SpMV chunk k as soon
-// as every x row it reads has arrived, and copy y chunk k back on a third stream -- PCIe is
-// full duplex, so the x upload, the SpMV and the y download overlap chunk by chunk.
+// Host x and y: copy x in row chunks on one stream, run the SpMV of row chunk k as soon as
+// every x row it reads has arrived, and copy y chunk k back on a third stream -- PCIe is full
+// duplex, so the x upload, the SpMV and the y download overlap chunk by chunk.  Several ranks
+// (NVLink halo): the chunks holding the x rows the puts read go first, a standalone put kernel
+// on a high-priority stream sends them once they have landed, each row chunk's off-diagonal
+// rows are added right after its diagonal SpMV (reading the flagged ghost lines), and a last
+// one-thread kernel ends the epoch.
 static bool pipeline_ok(spmat_s *A) {
   const char *e = getenv("SPMAT_HOST_PIPELINE");
   if (e && !strcmp(e, "0")) return false;
-  return A->comm->nranks == 1 && A->kernel_id == 3 && A->n_long == 0 && A->m == A->n &&
-         A->m >= (1 << 20) && A->n_rowblocks >= 64;
+  if (!(A->kernel_id == 3 && A->n_long == 0 && A->m == A->n && A->m >= (1 << 20) && A->n_rowblocks >= 64))
+    return false;
+  return A->comm->nranks == 1 || A->peer;
 }
 
 static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStream_t s) {
   const int C = 8;
   SP_TRY(spmv_pipe_prepare(A, C));
   const int nc = A->pipe_chunks;
+  const bool multi = A->comm->nranks > 1;
   if (!A->pipe_in) {
+    int lo = 0, hi = 0;
+    SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     SP_CUDA(cudaStreamCreateWithFlags(&A->pipe_in, cudaStreamNonBlocking));
     SP_CUDA(cudaStreamCreateWithFlags(&A->pipe_out, cudaStreamNonBlocking));
+    SP_CUDA(cudaStreamCreateWithPriority(&A->pipe_comm, cudaStreamNonBlocking, hi));
   }
-  while (A->pipe_ev.size() < (size_t)(2 * nc + 2)) {
+  while (A->pipe_ev.size() < (size_t)(2 * nc + 3)) {
     cudaEvent_t e;
     SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     A->pipe_ev.push_back(e);
@@ -113,26 +122,48 @@ static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStrea
   if (A->xstage.n < (size_t)A->n) SP_TRY(A->xstage.alloc(A->n));
   if (A->ystage.n < (size_t)A->m) SP_TRY(A->ystage.alloc(A->m));
   double *dx = A->xstage.get(), *dy = A->ystage.get();
-  cudaEvent_t *ev = A->pipe_ev.data();  // [0,nc) x chunk in, [nc,2nc) y chunk done, 2nc start, 2nc+1 end
+  // [0,nc) x chunk in, [nc,2nc) y chunk done, 2nc start, 2nc+1 end, 2nc+2 puts done
+  cudaEvent_t *ev = A->pipe_ev.data();
   SP_CUDA(cudaEventRecord(ev[2 * nc], s));  // earlier work on s (users of the staging buffers)
   SP_CUDA(cudaStreamWaitEvent(A->pipe_in, ev[2 * nc], 0));
   SP_CUDA(cudaStreamWaitEvent(A->pipe_out, ev[2 * nc], 0));
-  for (int k = 0; k < nc; ++k) {
+  std::vector<int> order;
+  for (int pass = 0; pass < 2; ++pass)  // chunks the puts read first
+    for (int k = 0; k < nc; ++k)
+      if ((A->pipe_put_chunk[k] != 0) == (pass == 0)) order.push_back(k);
+  for (int k : order) {
     const int64_t r0 = A->pipe_row[k], r1 = A->pipe_row[k + 1];
     SP_CUDA(cudaMemcpyAsync(dx + r0, x + r0, (r1 - r0) * 8, cudaMemcpyHostToDevice, A->pipe_in));
     SP_CUDA(cudaEventRecord(ev[k], A->pipe_in));
   }
+  if (multi) {
+    SP_CUDA(cudaStreamWaitEvent(A->pipe_comm, ev[2 * nc], 0));
+    for (int k = 0; k < nc; ++k)
+      if (A->pipe_put_chunk[k]) SP_CUDA(cudaStreamWaitEvent(A->pipe_comm, ev[k], 0));
+    SP_TRY(halo_peer_put(A, dx, A->pipe_comm));
+    SP_CUDA(cudaEventRecord(ev[2 * nc + 2], A->pipe_comm));
+  }
+  bool put_waited = false;
   for (int k = 0; k < nc; ++k) {
-    // the x chunk holding the last column this row chunk reads (uploads complete in order)
-    int need = 0;
-    while (need + 1 < nc && A->pipe_row[need + 1] <= A->pipe_xneed[k]) ++need;
-    need = std::max(need, k);
-    SP_CUDA(cudaStreamWaitEvent(s, ev[need], 0));
+    for (int j = 0; j < nc; ++j)  // every x chunk holding a column this row chunk reads
+      if (A->pipe_row[j] <= A->pipe_xneed[k] && A->pipe_row[j + 1] > A->pipe_xmin[k])
+        SP_CUDA(cudaStreamWaitEvent(s, ev[j], 0));
     SP_TRY(spmv_diag_chunk(A, dx, dy, k, s));
+    if (multi && A->pipe_q[k + 1] > A->pipe_q[k]) {
+      // my puts are out before this stream spins on the neighbours' lines: no rank can hold
+      // every SM waiting while its own puts are still queued
+      if (!put_waited) SP_CUDA(cudaStreamWaitEvent(s, ev[2 * nc + 2], 0));
+      put_waited = true;
+      SP_TRY(halo_peer_offdiag_range(A, dy, A->pipe_q[k], A->pipe_q[k + 1], s));
+    }
     SP_CUDA(cudaEventRecord(ev[nc + k], s));
     SP_CUDA(cudaStreamWaitEvent(A->pipe_out, ev[nc + k], 0));
     const int64_t r0 = A->pipe_row[k], r1 = A->pipe_row[k + 1];
     SP_CUDA(cudaMemcpyAsync(y + r0, dy + r0, (r1 - r0) * 8, cudaMemcpyDeviceToHost, A->pipe_out));
+  }
+  if (multi) {  // the put read this epoch's number: it must be done before the epoch advances
+    if (!put_waited) SP_CUDA(cudaStreamWaitEvent(s, ev[2 * nc + 2], 0));
+    SP_TRY(halo_peer_epoch_end(A, s));
   }
   SP_CUDA(cudaEventRecord(ev[2 * nc + 1], A->pipe_out));
   SP_CUDA(cudaStreamWaitEvent(s, ev[2 * nc + 1], 0));

@@ -24,6 +24,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 
@@ -641,55 +642,98 @@ int spmv_offdiag(spmat_s *A, double *y, cudaStream_t s) {
 namespace spmat {
 
 // ------------------------------------------------------------------ host-buffer pipeline
-// last column read by each chunk of rows (max over its rows of the last column index)
-__global__ void k_chunk_maxcol(const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
-                               int64_t r0, int64_t r1, int *__restrict__ out) {
-  int best = -1;
+// first and last column read by each chunk of rows (columns ascend within a row)
+__global__ void k_chunk_cols(const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col,
+                             int64_t r0, int64_t r1, int *__restrict__ lo, int *__restrict__ hi) {
+  int a_min = INT_MAX, b_max = -1;
   for (int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r1;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int a = rowptr[r], z = rowptr[r + 1];
-    if (z > a) best = max(best, col[z - 1]);  // columns ascend within a row
+    if (z > a) {
+      a_min = min(a_min, col[a]);
+      b_max = max(b_max, col[z - 1]);
+    }
   }
-  atomicMax(out, best);
+  atomicMin(lo, a_min);
+  atomicMax(hi, b_max);
 }
 
+// Row chunks of the host-buffer pipeline (mult.cu): `chunks` ranges of whole row blocks in row
+// order, the x rows each reads, its compressed off-diagonal rows, and the chunks the NVLink
+// halo puts read (uploaded first).
 int spmv_pipe_prepare(spmat_s *A, int chunks) {
   if (A->pipe_chunks == chunks) return SPMAT_OK;
   const int64_t nb = A->n_rowblocks;
   if (nb < chunks) chunks = (int)std::max<int64_t>(1, nb);
+  // row-ordered block table (the claim order puts boundary blocks first when multi-rank)
+  if (A->block_order.get()) {
+    SP_TRY(A->pipe_blocks4.alloc(nb));
+    k_blocks4<<<nblk(nb), 256>>>(A->rbp.get(), nullptr, nb, A->pipe_blocks4.get());
+    SP_LAUNCH();
+  }
+  const int4 *rb4 = A->block_order.get() ? A->pipe_blocks4.get() : A->blocks4.get();
   A->pipe_block.assign(chunks + 1, 0);
   A->pipe_row.assign(chunks + 1, 0);
+  A->pipe_xmin.assign(chunks, 0);
   A->pipe_xneed.assign(chunks, 0);
+  A->pipe_q.assign(chunks + 1, 0);
   std::vector<int4> edge(chunks + 1);
   for (int k = 0; k <= chunks; ++k) A->pipe_block[k] = nb * k / chunks;
   for (int k = 0; k < chunks; ++k)
-    SP_CUDA(cudaMemcpy(&edge[k], A->blocks4.get() + A->pipe_block[k], sizeof(int4), cudaMemcpyDeviceToHost));
+    SP_CUDA(cudaMemcpy(&edge[k], rb4 + A->pipe_block[k], sizeof(int4), cudaMemcpyDeviceToHost));
   for (int k = 0; k < chunks; ++k) A->pipe_row[k] = edge[k].x;
   A->pipe_row[chunks] = A->m;
-  DevBuf<int> mx;
+  DevBuf<int> mn, mx;
+  SP_TRY(mn.alloc(chunks));
   SP_TRY(mx.alloc(chunks));
+  SP_CUDA(cudaMemset(mn.get(), 0x7f, chunks * sizeof(int)));
   SP_CUDA(cudaMemset(mx.get(), 0xff, chunks * sizeof(int)));
   for (int k = 0; k < chunks; ++k) {
-    k_chunk_maxcol<<<nblk(A->pipe_row[k + 1] - A->pipe_row[k]), 256>>>(
-        A->rowptr_d.get(), A->col_d.get(), A->pipe_row[k], A->pipe_row[k + 1], mx.get() + k);
+    k_chunk_cols<<<nblk(A->pipe_row[k + 1] - A->pipe_row[k]), 256>>>(
+        A->rowptr_d.get(), A->col_d.get(), A->pipe_row[k], A->pipe_row[k + 1], mn.get() + k, mx.get() + k);
     SP_LAUNCH();
   }
-  std::vector<int> h(chunks);
-  SP_CUDA(cudaMemcpy(h.data(), mx.get(), chunks * sizeof(int), cudaMemcpyDeviceToHost));
-  for (int k = 0; k < chunks; ++k) A->pipe_xneed[k] = h[k];
+  std::vector<int> h0(chunks), h1(chunks);
+  SP_CUDA(cudaMemcpy(h0.data(), mn.get(), chunks * sizeof(int), cudaMemcpyDeviceToHost));
+  SP_CUDA(cudaMemcpy(h1.data(), mx.get(), chunks * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < chunks; ++k) {
+    A->pipe_xmin[k] = h1[k] < 0 ? A->pipe_row[k] : h0[k];  // empty chunk: nothing to wait for
+    A->pipe_xneed[k] = h1[k] < 0 ? A->pipe_row[k] : h1[k];
+  }
+  // compressed off-diagonal rows of each chunk (rows_o ascending)
+  if (A->n_ro > 0) {
+    std::vector<int32_t> ro(A->n_ro);
+    SP_CUDA(cudaMemcpy(ro.data(), A->rows_o.get(), A->n_ro * 4, cudaMemcpyDeviceToHost));
+    for (int k = 0; k <= chunks; ++k)
+      A->pipe_q[k] = std::lower_bound(ro.begin(), ro.end(), (int32_t)A->pipe_row[k]) - ro.begin();
+  }
+  // x rows the NVLink puts read: contiguous root ranges, or everything when a put gathers
+  A->pipe_put_chunk.assign(chunks, 0);
+  if (A->peer && A->halo) {
+    const sf_s *sf = A->halo;
+    for (size_t a = 0; a < sf->snbr.size(); ++a) {
+      int64_t r0 = 0, r1 = A->n;
+      if (sf->root_start[a] >= 0) {
+        r0 = sf->root_start[a];
+        r1 = r0 + sf->scount[a];
+      }
+      for (int k = 0; k < chunks; ++k)
+        if (A->pipe_row[k] < r1 && A->pipe_row[k + 1] > r0) A->pipe_put_chunk[k] = 1;
+    }
+  }
   A->pipe_chunks = chunks;
   return SPMAT_OK;
 }
 
-// the bulk-copy SpMV over claim range [pipe_block[k], pipe_block[k+1]) (single rank: the
-// claim order is the row order, so that is the chunk's rows)
+// the bulk-copy SpMV over the row blocks [pipe_block[k], pipe_block[k+1]) of row order
 int spmv_diag_chunk(spmat_s *A, const double *x, double *y, int k, cudaStream_t s) {
   const int64_t c0 = A->pipe_block[k], c1 = A->pipe_block[k + 1];
   if (c1 <= c0) return SPMAT_OK;
   SpmvHalo h{A->halo_puts.get(), 0, 0, nullptr, 0, A->halo_err.get()};
   SpmvTail t{};
+  const int4 *rb4 = A->block_order.get() ? A->pipe_blocks4.get() : A->blocks4.get();
   const unsigned grid = (unsigned)std::min<int64_t>(A->tma_grid, c1 - c0);
-  k_spmv_tma<<<grid, kCtaThreads, kTmaSmem, s>>>(A->blocks4.get() + c0, (int)(c1 - c0), A->rowptr_d.get(),
+  k_spmv_tma<<<grid, kCtaThreads, kTmaSmem, s>>>(rb4 + c0, (int)(c1 - c0), A->rowptr_d.get(),
                                                 A->col_d.get(), A->val_d.get(), x, y, A->sched.get(), h, t);
   SP_LAUNCH();
   return SPMAT_OK;
