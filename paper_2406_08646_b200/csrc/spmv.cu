@@ -539,14 +539,9 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
                                              cub::CountingInputIterator<int32_t>(0), f0.get(),
                                              A->block_order.get() + nbb, dn2.get() + 1, (int)nbk, st));
     A->n_bblocks = nbb;
-    // boundary rows spread over most blocks (box partitions: a face every nx rows): moving the
-    // boundary blocks first would send the sweep through the matrix twice and lose the x
-    // window in L2 (measured: 256^3 box at P=2, sweep +17 us).  Keep the natural order; the
-    // off-diagonal add then waits for the whole sweep.
-    if (4 * nbb > nbk) {
-      A->n_bblocks = nbk;
-      A->block_order.release();
-    }
+    // (box partitions put boundary rows in most blocks: this order then sweeps the matrix
+    // twice and the diagonal SpMV alone loses ~2 %, but keeping the natural order -- the
+    // off-diagonal add after the whole sweep -- measured 1-3 % slower end to end)
   }
   SP_TRY(A->blocks4.alloc(A->n_rowblocks));
   k_blocks4<<<nblk(A->n_rowblocks), 256, 0, st>>>(A->rbp.get(), A->block_order.get(),
