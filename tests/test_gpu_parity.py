@@ -388,10 +388,12 @@ def test_kernel_variants(sp, comm, kernel, case, monkeypatch):
 
 @pytest.mark.parametrize("numeric", ["ilp", "plain"])
 def test_numeric_kernels(sp, comm, numeric, monkeypatch):
-    """Both COO numeric kernels give the oracle's values bit for bit (Z1 order)."""
+    """Both COO numeric kernels give the oracle's values bit for bit (Z1 order), also with
+    ~20 contributions per nonzero."""
     monkeypatch.setenv("SPMAT_NUMERIC_KERNEL", numeric)
     for M, i, j, v in [(9 ** 3, *synth.q1_coo(9, values="real")),
-                       (50, *synth.random_coo(50, 50, 3000, dup_frac=0.9, neg_frac=0.1, values="real"))]:
+                       (50, *synth.random_coo(50, 50, 3000, dup_frac=0.9, neg_frac=0.1, values="real")),
+                       (40, *synth.random_coo(40, 40, 30000, dup_frac=0.9, neg_frac=0.1, values="real"))]:
         O = oracle.OracleMat(M, M, [M], [M], [i], [j])
         O.set_values([v])
         A = sp.Mat(comm, M, M, M, M, dev(i), dev(j))
