@@ -15,7 +15,7 @@
 //   put (comm warps of the diagonal SpMV, or k_halo_put): wait until the destination has
 //     finished reading epoch e-2 (done flag; two buffers by epoch parity), store the owned x
 //     entries as lines flagged e straight into the destination's buffer over NVLink;
-//   off-diagonal SpMV-add (the fused kernel's tail items, or k_spmv_offdiag_peer): read each
+//   off-diagonal SpMV-add (the fused kernel's comm warps, or k_spmv_offdiag_peer): read each
 //     ghost line until it carries flag e, add A_o lvec into y; the last CTA tells every sender
 //     that the buffer may be overwritten (done = e) and advances the epoch.
 // The transfer (0.5-2 MB of lines) overlaps the diagonal SpMV; no NCCL kernel, no host

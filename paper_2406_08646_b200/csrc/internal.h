@@ -235,7 +235,7 @@ struct SpmvHalo {                      // fused NVLink halo puts (comm warps)
   int bump;
   int *err;
 };
-struct SpmvTail {                      // fused off-diagonal SpMV-add (work items in the claim order)
+struct SpmvTail {                      // fused off-diagonal SpMV-add (comm warps, halo_dev.cuh tail_warp)
   int n_bblocks, enabled;              // boundary blocks are the first n_bblocks in claim order
   const int32_t *rows, *rowptr, *col;  // compressed off-diagonal block
   const double *val;

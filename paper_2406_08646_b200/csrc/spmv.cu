@@ -563,7 +563,7 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
 static cudaError_t launch_tma(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put,
                               bool fuse_tail) {
   // the kernel ends the MatMult (bumps the device epoch) when it also runs the off-diagonal
-  // items; otherwise k_spmv_offdiag_peer does
+  // add; otherwise k_spmv_offdiag_peer does
   SpmvHalo h{A->halo_puts.get(), A->n_puts, fuse_put ? A->put_chunks_total : 0,
              A->peer ? A->d_epoch.get() : nullptr, (fuse_put && fuse_tail) ? 1 : 0, A->halo_err.get()};
   SpmvTail t{};
