@@ -88,12 +88,19 @@ int sf_create(spmat_comm_t comm, int64_t nroots, int64_t nleaves, const int64_t 
               const int32_t *remote_rank, const int64_t *remote_offset, sf_t *out);
 
 /* Split-phase broadcast root -> leaf.  rootdata (nroots doubles) and leafdata
-   (covering every ilocal) are DEVICE arrays.  Begin enqueues pack -> NCCL send/recv ->
-   unpack on the library's communication stream after the work already on `stream`; it
-   never blocks the host.  End makes `stream` wait for that work.  Between begin and end
-   the caller may enqueue independent work on `stream`; it must not write rootdata or read
-   leafdata.  Leaf entries not in the SF are untouched.  End must name the same buffers and
-   op as begin (else SPMAT_ERR_STATE). */
+   (covering every ilocal) are DEVICE arrays.  It never blocks the host.  Transport (chosen
+   collectively at sf_create, see sf_transport):
+     NVLink (default with several ranks, the paper's NVSHMEM SF P:533-562 with CUDA IPC):
+       begin enqueues on `stream` a put kernel that stores the root values as flagged 16-byte
+       lines straight into the leaf owners' staging buffers (it waits only for the owner to
+       have released the buffer it used two operations ago); end enqueues on `stream` the
+       kernel that reads each line once it has landed and writes leafdata.
+     NCCL (SPMAT_SF=nccl or SPMAT_HALO=nccl, or IPC unavailable): begin enqueues pack -> NCCL
+       send/recv -> unpack on the communication stream; end makes `stream` wait for it.
+   Between begin and end the caller may enqueue independent work on `stream`; it must not
+   write rootdata or read leafdata.  Leaf entries not in the SF are untouched.  End must
+   name the same buffers and op as begin (else SPMAT_ERR_STATE).  Collective: every rank
+   calls begin/end the same number of times. */
 int sf_bcast_begin(sf_t sf, const double *rootdata, double *leafdata, int op, void *stream);
 int sf_bcast_end(sf_t sf, const double *rootdata, double *leafdata, int op, void *stream);
 
@@ -114,6 +121,14 @@ int sf_get_info(sf_t sf, int64_t info[8]);
    order, 3 send neighbour ranks, 4 send counts, 5 root offsets in send order
    (all int64).  Copies min(cap, len) values into host_buf; *len = full length. */
 int sf_export(sf_t sf, int what, void *host_buf, int64_t cap, int64_t *len);
+
+/* 2 if this SF moves data as flagged lines over NVLink peer memory, 1 if over NCCL (0 with
+   one rank and no remote edges). */
+int sf_transport(sf_t sf);
+
+/* Synchronise the device and report a timed-out NVLink wait (a peer that never delivered
+   or released a buffer within ~20 s) as SPMAT_ERR_NCCL; else SPMAT_OK. */
+int sf_check(sf_t sf);
 
 int sf_destroy(sf_t sf);
 

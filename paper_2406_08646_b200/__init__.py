@@ -12,7 +12,8 @@ Names follow the C ABI (and through it the paper's MatSetPreallocationCOO /
 MatSetValuesCOO / MatMult / PetscSFBcastBegin/End):
 
     comm_unique_id, comm_create, comm_check, comm_destroy,
-    sf_create, sf_bcast_begin, sf_bcast_end, sf_get_info, sf_export, sf_destroy,
+    sf_create, sf_bcast_begin, sf_bcast_end, sf_reduce_begin, sf_reduce_end, sf_get_info, sf_export,
+    sf_transport, sf_check, sf_destroy,
     spmat_create_coo, spmat_set_values_coo, spmat_mult, spmat_mult_part,
     spmat_get_info, spmat_export, spmat_get_halo_sf, spmat_profile, spmat_profile_read,
     spmat_destroy
@@ -52,7 +53,7 @@ ABI_SYMBOLS = (
     "spmat_version", "spmat_last_error", "spmat_comm_unique_id", "spmat_comm_create",
     "spmat_comm_check", "spmat_comm_destroy", "sf_create", "sf_bcast_begin", "sf_bcast_end",
     "sf_reduce_begin", "sf_reduce_end",
-    "sf_get_info", "sf_export", "sf_destroy", "spmat_create_coo", "spmat_set_values_coo",
+    "sf_get_info", "sf_export", "sf_transport", "sf_check", "sf_destroy", "spmat_create_coo", "spmat_set_values_coo",
     "spmat_mult", "spmat_mult_part", "spmat_get_info", "spmat_export", "spmat_get_halo_sf",
     "spmat_profile", "spmat_profile_read", "spmat_check", "spmat_halo_mode", "spmat_trace_read",
     "spmat_vec_dot", "spmat_cg", "spmat_set_block_size",
@@ -95,6 +96,8 @@ def load(path: str = LIB_PATH):
         "sf_get_info": ([p, p], i32),
         "sf_export": ([p, i32, p, i64, P(i64)], i32),
         "sf_destroy": ([p], i32),
+        "sf_transport": ([p], i32),
+        "sf_check": ([p], i32),
         "spmat_create_coo": ([p, i64, i64, i64, i64, i64, p, p, P(p)], i32),
         "spmat_set_values_coo": ([p, p, i32, p], i32),
         "spmat_mult": ([p, p, p, p], i32),
@@ -208,6 +211,15 @@ def sf_export(sf_h, key) -> np.ndarray:
     out = np.zeros(n.value, dtype=np.int64)
     _check(load().sf_export(sf_h, what, _ptr(out), n.value, ctypes.byref(n)), "sf_export")
     return out
+
+
+def sf_transport(sf_h) -> int:
+    """2: flagged lines over NVLink peer memory, 1: NCCL, 0: single rank."""
+    return int(load().sf_transport(sf_h))
+
+
+def sf_check(sf_h):
+    _check(load().sf_check(sf_h), "sf_check")
 
 
 def sf_destroy(sf_h):
@@ -360,6 +372,12 @@ class StarForest:
 
     def export(self, key):
         return sf_export(self.h, key)
+
+    def transport(self):
+        return sf_transport(self.h)
+
+    def check(self):
+        sf_check(self.h)
 
     def close(self):
         if getattr(self, "h", None) is not None:

@@ -260,6 +260,17 @@ void halo_peer_release(spmat_s *A) {
   A->peer = false;
 }
 
+// flagged-line puts described by `puts` (chunks = sum of their nchunk) of epoch *epoch_ctr + 1
+int peer_put_launch(const HaloPut *puts, int nputs, int chunks, const double *src,
+                    const unsigned long long *epoch_ctr, int *err, cudaStream_t s) {
+  if (nputs == 0 || chunks == 0) return SPMAT_OK;
+  const int grid = (chunks + kPutWarps - 1) / kPutWarps;
+  SP_CUDA(launch_pdl(k_halo_put, grid, 32 * kPutWarps, 0, s, puts, nputs, chunks, src, epoch_ctr, err));
+  return SPMAT_OK;
+}
+
+int put_chunks_of(int64_t count) { return put_chunks(count); }
+
 // standalone put of the current epoch on stream s
 int halo_peer_put(spmat_s *A, const double *x, cudaStream_t s) {
   if (A->n_puts == 0) return SPMAT_OK;

@@ -160,6 +160,19 @@ void board_release(Comm *c);
 
 struct spmat_comm_s : spmat::Comm {};
 
+// ------------------------------------------------------------------ device-initiated halo
+struct HaloPut {                       // one destination rank of my owned x entries
+  uint4 *dst;                          // peer ghost lines + first leaf for me (IPC mapping)
+  int64_t dst_stride;                  // peer ghost buffer stride in lines (double-buffered by epoch)
+  int64_t count, root_start;           // contiguous x slice, or...
+  const int64_t *root_idx;             // ...gather indices (device), nullptr if contiguous
+  unsigned long long *my_done;         // destination -> me: "ghost buffer free" epoch (local)
+  int nchunk, pad;
+};
+struct HaloWait {                      // one sender of my ghost entries
+  unsigned long long *peer_done;       // sender's "ghost buffer free" flag for me (IPC mapping)
+};
+
 // ------------------------------------------------------------------ star forest
 struct sf_s {
   spmat_comm_s *comm = nullptr;
@@ -186,6 +199,8 @@ struct sf_s {
   std::vector<int64_t> h_leaf_idx, h_root_idx;
   // split-phase state
   cudaEvent_t ev_begin = nullptr, ev_done = nullptr;
+  cudaEvent_t ev_take = nullptr;         // NVLink transport: the last consuming kernel (epoch advanced)
+  bool take_captured = false;            // ev_take was recorded inside a stream capture
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;  // profiling (comm stream)
   bool pending = false;
   const double *p_root = nullptr;
@@ -197,6 +212,22 @@ struct sf_s {
   int64_t n_touched = 0;
   spmat::DevBuf<int64_t> d_red_roots, d_red_ptr, d_red_code;
   spmat::DevBuf<double> d_redbuf;        // received leaf values, requester-major (soff layout)
+  // NVLink transport (sf_peer_setup, the default with several ranks): values travel as
+  // flagged 16-byte lines (halo_dev.cuh) stored by the producer straight into the consumer's
+  // IPC-mapped staging buffer -- bcast: leaf side [2][nrecv] in recv order; reduce: root side
+  // [2][nsend] in requester-major order; two buffers by epoch parity, done flags back.
+  bool peer = false;
+  spmat::DevBuf<uint4> bline, rline;
+  int64_t bstride = 0, rstride = 0;
+  spmat::DevBuf<unsigned long long> pflags;  // [q] bcast done from receiver q, [P+q] reduce done from owner q
+  spmat::DevBuf<unsigned long long> d_ep;    // [0] completed bcasts, [1] completed reduces
+  std::vector<void *> peer_mem;              // opened IPC mappings
+  spmat::DevBuf<HaloPut> bputs, rputs;       // bcast: my roots -> leaf owners; reduce: my leaves -> root owners
+  int nbputs = 0, nrputs = 0, bchunks = 0, rchunks = 0;
+  spmat::DevBuf<HaloWait> bwaits, rwaits;    // producers to release after consuming
+  int nbwaits = 0, nrwaits = 0;
+  spmat::DevBuf<unsigned int> pcounter;      // last-CTA detection of the consuming kernels
+  spmat::DevBuf<int> perr;                   // bounded-spin timeouts
 };
 
 namespace spmat {
@@ -210,19 +241,6 @@ void sf_free(sf_s *sf);
 int sf_reduce_begin_impl(sf_s *sf, const double *leaf, double *root, int op, cudaStream_t stream);
 int sf_reduce_end_impl(sf_s *sf, const double *leaf, double *root, int op, cudaStream_t stream);
 }  // namespace spmat
-
-// ------------------------------------------------------------------ device-initiated halo
-struct HaloPut {                       // one destination rank of my owned x entries
-  uint4 *dst;                          // peer ghost lines + first leaf for me (IPC mapping)
-  int64_t dst_stride;                  // peer ghost buffer stride in lines (double-buffered by epoch)
-  int64_t count, root_start;           // contiguous x slice, or...
-  const int64_t *root_idx;             // ...gather indices (device), nullptr if contiguous
-  unsigned long long *my_done;         // destination -> me: "ghost buffer free" epoch (local)
-  int nchunk, pad;
-};
-struct HaloWait {                      // one sender of my ghost entries
-  unsigned long long *peer_done;       // sender's "ghost buffer free" flag for me (IPC mapping)
-};
 
 // kernel-parameter bundles of the bulk-copy SpMV
 struct SpmvHalo {                      // fused NVLink halo puts (comm warps)
@@ -354,6 +372,10 @@ int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s);
 // host-buffer pipeline (single rank): row chunks of the diagonal SpMV
 int spmv_pipe_prepare(spmat_s *A, int chunks);  // chunk rows + the x columns each chunk reads
 int spmv_diag_chunk(spmat_s *A, const double *x, double *y, int k, cudaStream_t s);
+int peer_put_launch(const HaloPut *puts, int nputs, int chunks, const double *src,
+                    const unsigned long long *epoch_ctr, int *err, cudaStream_t s);
+int put_chunks_of(int64_t count);  // put warps (chunks) for `count` values
+int sf_peer_setup(sf_s *sf);       // collective; leaves sf->peer false (NCCL) when unavailable
 int halo_peer_setup(spmat_s *A);                  // collective; leaves A->peer false on NCCL
 void halo_peer_release(spmat_s *A);
 int halo_peer_put(spmat_s *A, const double *x, cudaStream_t s);  // standalone put kernel

@@ -16,7 +16,9 @@
 #include <cstring>
 #include <numeric>
 
+#include "halo_dev.cuh"
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace spmat {
 
@@ -48,8 +50,11 @@ static inline unsigned grid_for(int64_t n, int threads, int sms) {
 
 void sf_free(sf_s *sf) {
   if (!sf) return;
+  for (void *p : sf->peer_mem) cudaIpcCloseMemHandle(p);
+  sf->peer_mem.clear();
   if (sf->ev_begin) cudaEventDestroy(sf->ev_begin);
   if (sf->ev_done) cudaEventDestroy(sf->ev_done);
+  if (sf->ev_take) cudaEventDestroy(sf->ev_take);
   delete sf;
 }
 
@@ -267,8 +272,219 @@ int sf_build(spmat_comm_s *comm, int64_t nroots, int64_t nleaves, const int64_t 
     sf_free(sf);
     return fail(SPMAT_ERR_CUDA, "sf_create: event creation failed");
   }
+  if ((s = sf_peer_setup(sf)) != SPMAT_OK) {
+    sf_free(sf);
+    return s;
+  }
   *out = sf;
   return SPMAT_OK;
+}
+
+// ------------------------------------------------------------------ NVLink transport
+// The paper's NVSHMEM PetscSF with CUDA IPC instead of NVSHMEM: at creation every
+// rank maps the staging buffers of the ranks it sends to; a Bcast/Reduce is then a put kernel
+// (flagged lines straight into the consumer's buffer over NVLink, after the consumer released
+// that buffer two epochs ago) and a consuming kernel that reads each line once it carries the
+// epoch, applies the op, and releases the buffer.  No NCCL kernel, no host synchronisation.
+int sf_peer_setup(sf_s *sf) {
+  spmat_comm_s *c = sf->comm;
+  const int P = c->nranks, me = c->rank;
+  sf->peer = false;
+  if (P == 1) return SPMAT_OK;
+  // SPMAT_SF=nccl (or SPMAT_HALO=nccl, which also covers the matrix halo's SF) keeps NCCL
+  const char *env = getenv("SPMAT_SF"), *henv = getenv("SPMAT_HALO");
+  int64_t vote0[1] = {((env && !strcmp(env, "nccl")) || (henv && !strcmp(henv, "nccl"))) ? 1 : 0};
+  SP_TRY(c->allreduce_max_i64(vote0, 1));
+  if (vote0[0]) return SPMAT_OK;
+  DeviceGuard g(c->device);
+  sf->bstride = std::max<int64_t>(sf->nrecv, 1);
+  sf->rstride = std::max<int64_t>(sf->nsend, 1);
+  SP_TRY(sf->bline.alloc(2 * (size_t)sf->bstride));
+  SP_TRY(sf->rline.alloc(2 * (size_t)sf->rstride));
+  SP_TRY(sf->pflags.alloc(2 * (size_t)P));
+  SP_TRY(sf->d_ep.alloc(2));
+  SP_TRY(sf->pcounter.alloc(1));
+  SP_TRY(sf->perr.alloc(1));
+  SP_CUDA(cudaEventCreateWithFlags(&sf->ev_take, cudaEventDisableTiming));
+  SP_CUDA(cudaMemset(sf->bline.get(), 0, sf->bline.n * sizeof(uint4)));  // flag 0: no epoch
+  SP_CUDA(cudaMemset(sf->rline.get(), 0, sf->rline.n * sizeof(uint4)));
+  SP_CUDA(cudaMemset(sf->pflags.get(), 0, 2 * P * sizeof(unsigned long long)));
+  SP_CUDA(cudaMemset(sf->d_ep.get(), 0, 2 * sizeof(unsigned long long)));
+  SP_CUDA(cudaMemset(sf->pcounter.get(), 0, sizeof(unsigned)));
+  SP_CUDA(cudaMemset(sf->perr.get(), 0, sizeof(int)));
+  cudaIpcMemHandle_t h[3];
+  memset(h, 0, sizeof h);
+  int64_t fail_ = 0;
+  if (cudaIpcGetMemHandle(&h[0], sf->bline.get()) != cudaSuccess ||
+      cudaIpcGetMemHandle(&h[1], sf->rline.get()) != cudaSuccess ||
+      cudaIpcGetMemHandle(&h[2], sf->pflags.get()) != cudaSuccess) {
+    cudaGetLastError();
+    fail_ = 1;
+  }
+  int64_t v1[1] = {fail_};
+  SP_TRY(c->allreduce_max_i64(v1, 1));
+  if (v1[0]) return SPMAT_OK;  // NCCL transport on every rank
+  // per rank: 3 handles, strides, and for every peer p the offset of p's data in my bline
+  // (p sends me roots) and in my rline (p sends me leaves)
+  const int W = 24 + 2 + 2 * P;
+  std::vector<int64_t> mine(W, -1), all((size_t)W * P);
+  memcpy(mine.data(), h, sizeof h);
+  mine[24] = sf->bstride;
+  mine[25] = sf->rstride;
+  for (size_t a = 0; a < sf->rnbr.size(); ++a) mine[26 + sf->rnbr[a]] = sf->roff[a];
+  for (size_t a = 0; a < sf->snbr.size(); ++a) mine[26 + P + sf->snbr[a]] = sf->soff[a];
+  SP_TRY(c->allgather_i64(mine.data(), W, all.data()));
+  std::vector<uint4 *> pb(P, nullptr), pr(P, nullptr);
+  std::vector<unsigned long long *> pf(P, nullptr);
+  int64_t open_fail = 0;
+  auto open = [&](int q) {
+    if (pf[q] || open_fail) return;
+    cudaIpcMemHandle_t hq[3];
+    memcpy(hq, all.data() + (size_t)W * q, sizeof hq);
+    void *m[3] = {nullptr, nullptr, nullptr};
+    for (int k = 0; k < 3 && !open_fail; ++k) {
+      if (cudaIpcOpenMemHandle(&m[k], hq[k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        open_fail = 1;
+      } else {
+        sf->peer_mem.push_back(m[k]);
+      }
+    }
+    pb[q] = (uint4 *)m[0];
+    pr[q] = (uint4 *)m[1];
+    pf[q] = (unsigned long long *)m[2];
+  };
+  for (int q : sf->snbr) open(q);
+  for (int q : sf->rnbr) open(q);
+  int64_t v2[1] = {open_fail};
+  SP_TRY(c->allreduce_max_i64(v2, 1));
+  if (v2[0]) {
+    for (void *m : sf->peer_mem) cudaIpcCloseMemHandle(m);
+    sf->peer_mem.clear();
+    return SPMAT_OK;
+  }
+  auto at = [&](int q, int k) { return all[(size_t)W * q + k]; };
+  std::vector<HaloPut> bp, rp;
+  std::vector<HaloWait> bw, rw;
+  sf->bchunks = sf->rchunks = 0;
+  for (size_t a = 0; a < sf->snbr.size(); ++a) {  // bcast: my roots -> q's leaves; reduce: q's leaves -> me
+    const int q = sf->snbr[a];
+    HaloPut p{};
+    p.dst = pb[q] + at(q, 26 + me);
+    p.dst_stride = at(q, 24);
+    p.count = sf->scount[a];
+    p.root_start = sf->root_start[a] >= 0 ? sf->root_start[a] : 0;
+    p.root_idx = sf->root_start[a] >= 0 ? nullptr : sf->d_root_idx.get() + sf->soff[a];
+    p.my_done = sf->pflags.get() + q;
+    p.nchunk = put_chunks_of(p.count);
+    sf->bchunks += p.nchunk;
+    bp.push_back(p);
+    HaloWait w{};
+    w.peer_done = pf[q] + P + me;  // I consumed q's leaves (reduce): release q's copy of them
+    rw.push_back(w);
+  }
+  for (size_t a = 0; a < sf->rnbr.size(); ++a) {  // bcast: q's roots -> my leaves; reduce: my leaves -> q
+    const int q = sf->rnbr[a];
+    HaloPut p{};
+    p.dst = pr[q] + at(q, 26 + P + me);
+    p.dst_stride = at(q, 25);
+    p.count = sf->rcount[a];
+    p.root_start = sf->leaf_start[a] >= 0 ? sf->leaf_start[a] : 0;
+    p.root_idx = sf->leaf_start[a] >= 0 ? nullptr : sf->d_leaf_idx.get() + sf->roff[a];
+    p.my_done = sf->pflags.get() + P + q;
+    p.nchunk = put_chunks_of(p.count);
+    sf->rchunks += p.nchunk;
+    rp.push_back(p);
+    HaloWait w{};
+    w.peer_done = pf[q] + me;  // I consumed q's roots (bcast): release q's copy of them
+    bw.push_back(w);
+  }
+  auto upload = [&](auto &dst, const auto &src) -> int {
+    SP_TRY(dst.alloc(src.size()));
+    if (!src.empty()) SP_CUDA(cudaMemcpy(dst.get(), src.data(), src.size() * sizeof(src[0]), cudaMemcpyHostToDevice));
+    return SPMAT_OK;
+  };
+  SP_TRY(upload(sf->bputs, bp));
+  SP_TRY(upload(sf->rputs, rp));
+  SP_TRY(upload(sf->bwaits, bw));
+  SP_TRY(upload(sf->rwaits, rw));
+  sf->nbputs = (int)bp.size();
+  sf->nrputs = (int)rp.size();
+  sf->nbwaits = (int)bw.size();
+  sf->nrwaits = (int)rw.size();
+  sf->peer = true;
+  int64_t sync[1] = {0};  // every buffer zeroed and mapped before the first put
+  SP_TRY(c->allreduce_max_i64(sync, 1));
+  return SPMAT_OK;
+}
+
+// The puts read the epoch the previous operation's consuming kernel advanced: order the
+// caller's stream after it (a no-op when that kernel ran on the same stream).  Inside a stream capture only an event recorded in the same capture can be
+// waited on; an operation ended before the capture began is the caller's to order (as any
+// work preceding a capture).
+static int sf_after_take(sf_s *sf, cudaStream_t stream) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  SP_CUDA(cudaStreamIsCapturing(stream, &st));
+  const bool capturing = st == cudaStreamCaptureStatusActive;
+  if (capturing != sf->take_captured) return SPMAT_OK;
+  SP_CUDA(cudaStreamWaitEvent(stream, sf->ev_take, 0));
+  return SPMAT_OK;
+}
+
+// Bcast consumer: leaf[leaf_idx[t]] (=|+=) the value of line t of this epoch; the last CTA
+// releases the staging buffer to the senders and advances the epoch.
+__global__ void k_sf_bcast_take(const uint4 *__restrict__ lines, int64_t stride, const int64_t *__restrict__ lidx,
+                                int64_t n, double *__restrict__ leaf, int op, const HaloWait *__restrict__ waits,
+                                int nwaits, unsigned long long *ep, unsigned int *counter, int *err) {
+  pdl_wait();
+  const unsigned long long epoch = *ep + 1ull;
+  const uint4 *gl = lines + (int64_t)(epoch & 1) * stride;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const double v = ll_load(gl + t, ll_flag(epoch), err);
+    const int64_t l = lidx[t];
+    leaf[l] = op == SF_REPLACE ? v : __dadd_rn(leaf[l], v);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(counter, 1u) == gridDim.x - 1) {
+      atomicExch(counter, 0u);
+      for (int w = 0; w < nwaits; ++w) st_release_sys(waits[w].peer_done, epoch);
+      *ep = epoch;
+    }
+  }
+}
+
+// Reduce consumer: k_reduce_combine's ordered combine with the received values read from this
+// epoch's lines; the last CTA releases the staging buffer and advances the epoch.
+__global__ void k_sf_reduce_take(const int64_t *__restrict__ roots, const int64_t *__restrict__ ptr,
+                                 const int64_t *__restrict__ code, int64_t n, const uint4 *__restrict__ lines,
+                                 int64_t stride, const double *__restrict__ leaf,
+                                 const int64_t *__restrict__ self_leaf, double *__restrict__ root, int op,
+                                 const HaloWait *__restrict__ waits, int nwaits, unsigned long long *ep,
+                                 unsigned int *counter, int *err) {
+  pdl_wait();
+  const unsigned long long epoch = *ep + 1ull;
+  const uint4 *gl = lines + (int64_t)(epoch & 1) * stride;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = roots[t];
+    double s = root[r];
+    for (int64_t k = ptr[t]; k < ptr[t + 1]; ++k) {
+      const int64_t cc = code[k];
+      const double v = cc >= 0 ? ll_load(gl + cc, ll_flag(epoch), err) : leaf[self_leaf[-cc - 1]];
+      s = op == SF_REPLACE ? v : __dadd_rn(s, v);
+    }
+    root[r] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(counter, 1u) == gridDim.x - 1) {
+      atomicExch(counter, 0u);
+      for (int w = 0; w < nwaits; ++w) st_release_sys(waits[w].peer_done, epoch);
+      *ep = epoch;
+    }
+  }
 }
 
 // PetscSFReduce root side: one thread per touched root applies its contributions in
@@ -297,6 +513,17 @@ int sf_reduce_begin_impl(sf_s *sf, const double *leaf, double *root, int op, cud
   if (sf->pending) return fail(SPMAT_ERR_STATE, "sf_reduce_begin: an operation is already pending");
   if (op != SF_REPLACE && op != SF_SUM) return fail(SPMAT_ERR_ARG, "sf_reduce: bad op %d", op);
   spmat_comm_s *c = sf->comm;
+  if (sf->peer) {  // flagged-line puts of my leaves on the caller's stream; sf_reduce_end combines
+    SP_TRY(sf_after_take(sf, stream));
+    SP_TRY(peer_put_launch(sf->rputs.get(), sf->nrputs, sf->rchunks, leaf, sf->d_ep.get() + 1, sf->perr.get(),
+                           stream));
+    sf->pending = true;
+    sf->p_kind = 2;
+    sf->p_root = root;
+    sf->p_leaf = const_cast<double *>(leaf);
+    sf->p_op = op;
+    return SPMAT_OK;
+  }
   cudaStream_t cs = c->comm_stream;
   SP_CUDA(cudaEventRecord(sf->ev_begin, stream));
   SP_CUDA(cudaStreamWaitEvent(cs, sf->ev_begin, 0));
@@ -339,7 +566,19 @@ int sf_reduce_end_impl(sf_s *sf, const double *leaf, double *root, int op, cudaS
     return fail(SPMAT_ERR_STATE, "sf_reduce_end without sf_reduce_begin");
   if (root != sf->p_root || leaf != sf->p_leaf || op != sf->p_op)
     return fail(SPMAT_ERR_STATE, "sf_reduce_end: buffers or op differ from sf_reduce_begin");
-  SP_CUDA(cudaStreamWaitEvent(stream, sf->ev_done, 0));
+  if (!sf->peer) SP_CUDA(cudaStreamWaitEvent(stream, sf->ev_done, 0));
+  if (sf->peer) {  // always launched: it also ends the epoch
+    const unsigned grid = grid_for(std::max<int64_t>(sf->n_touched, 1), 256, sf->comm->num_sms);
+    SP_CUDA(launch_pdl(k_sf_reduce_take, grid, 256, 0, stream, (const int64_t *)sf->d_red_roots.get(),
+                       (const int64_t *)sf->d_red_ptr.get(), (const int64_t *)sf->d_red_code.get(), sf->n_touched,
+                       (const uint4 *)sf->rline.get(), sf->rstride, (const double *)leaf,
+                       (const int64_t *)sf->d_self_leaf.get(), root, op, (const HaloWait *)sf->rwaits.get(),
+                       sf->nrwaits, sf->d_ep.get() + 1, sf->pcounter.get(), sf->perr.get()));
+    SP_CUDA(cudaEventRecord(sf->ev_take, stream));
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    SP_CUDA(cudaStreamIsCapturing(stream, &cst));
+    sf->take_captured = cst == cudaStreamCaptureStatusActive;
+  }
   sf->pending = false;
   sf->p_kind = 0;
   return SPMAT_OK;
@@ -350,11 +589,29 @@ int sf_begin(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t st
   if (sf->pending) return fail(SPMAT_ERR_STATE, "sf_bcast_begin: an operation is already pending");
   if (op != SF_REPLACE && op != SF_SUM) return fail(SPMAT_ERR_ARG, "sf_bcast: bad op %d", op);
   spmat_comm_s *c = sf->comm;
+  const int T = 256;
+  if (sf->peer) {  // flagged-line puts on the caller's stream; sf_end consumes them there too
+    if (prof) SP_CUDA(cudaEventRecord(prof[0], stream));
+    SP_TRY(sf_after_take(sf, stream));
+    SP_TRY(peer_put_launch(sf->bputs.get(), sf->nbputs, sf->bchunks, root, sf->d_ep.get(), sf->perr.get(),
+                           stream));
+    if (sf->nself > 0) {
+      k_scatter<<<grid_for(sf->nself, T, c->num_sms), T, 0, stream>>>(
+          root, sf->d_self_root.get(), leaf, sf->d_self_leaf.get(), sf->nself, op);
+      SP_LAUNCH();
+    }
+    if (prof) SP_CUDA(cudaEventRecord(prof[1], stream));
+    sf->pending = true;
+    sf->p_kind = 1;
+    sf->p_root = root;
+    sf->p_leaf = leaf;
+    sf->p_op = op;
+    return SPMAT_OK;
+  }
   cudaStream_t cs = c->comm_stream;
   SP_CUDA(cudaEventRecord(sf->ev_begin, stream));
   SP_CUDA(cudaStreamWaitEvent(cs, sf->ev_begin, 0));
   if (prof) SP_CUDA(cudaEventRecord(prof[0], cs));
-  const int T = 256;
   if (sf->need_pack && sf->nsend > 0) {
     k_gather<<<grid_for(sf->nsend, T, c->num_sms), T, 0, cs>>>(root, sf->d_root_idx.get(),
                                                               sf->d_sendbuf.get(), sf->nsend);
@@ -402,7 +659,18 @@ int sf_end(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stre
   if (!sf->pending || sf->p_kind != 1) return fail(SPMAT_ERR_STATE, "sf_bcast_end without sf_bcast_begin");
   if (root != sf->p_root || leaf != sf->p_leaf || op != sf->p_op)
     return fail(SPMAT_ERR_STATE, "sf_bcast_end: buffers or op differ from sf_bcast_begin");
-  SP_CUDA(cudaStreamWaitEvent(stream, sf->ev_done, 0));
+  if (!sf->peer) SP_CUDA(cudaStreamWaitEvent(stream, sf->ev_done, 0));
+  if (sf->peer) {  // always launched: it also ends the epoch
+    const unsigned grid = grid_for(std::max<int64_t>(sf->nrecv, 1), 256, sf->comm->num_sms);
+    SP_CUDA(launch_pdl(k_sf_bcast_take, grid, 256, 0, stream, (const uint4 *)sf->bline.get(), sf->bstride,
+                       (const int64_t *)sf->d_leaf_idx.get(), sf->nrecv, leaf, op,
+                       (const HaloWait *)sf->bwaits.get(), sf->nbwaits, sf->d_ep.get(), sf->pcounter.get(),
+                       sf->perr.get()));
+    SP_CUDA(cudaEventRecord(sf->ev_take, stream));
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    SP_CUDA(cudaStreamIsCapturing(stream, &cst));
+    sf->take_captured = cst == cudaStreamCaptureStatusActive;
+  }
   sf->pending = false;
   sf->p_kind = 0;
   return SPMAT_OK;
@@ -508,13 +776,32 @@ int sf_export(sf_t sf, int what, void *host_buf, int64_t cap, int64_t *len) {
   return SPMAT_OK;
 }
 
+int sf_transport(sf_t sf) {
+  if (!sf) return 0;
+  if (sf->peer) return 2;
+  return sf->comm->nranks > 1 ? 1 : 0;
+}
+
+int sf_check(sf_t sf) {
+  if (!sf) return fail(SPMAT_ERR_ARG, "sf_check: null sf");
+  DeviceGuard g(sf->comm->device);
+  SP_CUDA(cudaDeviceSynchronize());
+  if (sf->peer) {
+    int e = 0;
+    SP_CUDA(cudaMemcpy(&e, sf->perr.get(), sizeof(int), cudaMemcpyDeviceToHost));
+    if (e) return fail(SPMAT_ERR_NCCL, "star forest over NVLink: a peer did not answer (timeout)");
+  }
+  return SPMAT_OK;
+}
+
 int sf_destroy(sf_t sf) {
   if (!sf) return SPMAT_OK;
-  {
-    DeviceGuard g(sf->comm->device);
-    cudaStreamSynchronize(sf->comm->comm_stream);
-  }
+  DeviceGuard g(sf->comm->device);
+  // the consuming kernels run on callers' streams (and maybe inside captured graphs, where
+  // ev_take was never really recorded): wait for the whole device
+  cudaDeviceSynchronize();
   sf_free(sf);
+  cudaGetLastError();  // teardown errors (e.g. IPC unmapping) must not surface at a later launch
   return SPMAT_OK;
 }
 

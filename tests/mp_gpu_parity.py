@@ -231,20 +231,28 @@ def case_sf(c, seed):
         leafdata.append(rng.integers(-50, 50, space).astype(float))
     il, rr, ro = leaves[r]
     sf = sp.StarForest(c.comm, nroots[r], il, rr, ro)
-    for op in (sp.REPLACE, sp.SUM):
-        want = oracle.sf_bcast(nroots, leaves, rootdata, leafdata, op)[r]
-        root = torch.from_numpy(rootdata[r]).cuda()
-        leaf = torch.from_numpy(leafdata[r]).cuda()
-        sf.bcast_begin(root, leaf, op)
-        sf.bcast_end(root, leaf, op)
-        assert np.array_equal(leaf.cpu().numpy(), want), f"sf seed {seed} op {op} rank {r}"
-        # reduce leaf -> root, (source rank, leaf index) order (oracle.sf_reduce)
-        want = oracle.sf_reduce(nroots, leaves, leafdata, rootdata, op)[r]
-        root = torch.from_numpy(rootdata[r]).cuda()
-        leaf = torch.from_numpy(leafdata[r]).cuda()
-        sf.reduce_begin(leaf, root, op)
-        sf.reduce_end(leaf, root, op)
-        assert np.array_equal(root.cpu().numpy(), want), f"sf reduce seed {seed} op {op} rank {r}"
+    want_t = 1 if os.environ.get("SPMAT_HALO") == "nccl" else 2
+    assert P == 1 or sf.transport() == want_t, f"sf transport {sf.transport()}"
+    # several rounds: the NVLink transport cycles its two staging buffers and waits on the
+    # consumers' release flags from the third operation on
+    for rnd in range(3):
+        rd = [a + 100 * rnd for a in rootdata]
+        ld = [a - 7 * rnd for a in leafdata]
+        for op in (sp.REPLACE, sp.SUM):
+            want = oracle.sf_bcast(nroots, leaves, rd, ld, op)[r]
+            root = torch.from_numpy(rd[r]).cuda()
+            leaf = torch.from_numpy(ld[r]).cuda()
+            sf.bcast_begin(root, leaf, op)
+            sf.bcast_end(root, leaf, op)
+            assert np.array_equal(leaf.cpu().numpy(), want), f"sf seed {seed} round {rnd} op {op} rank {r}"
+            # reduce leaf -> root, (source rank, leaf index) order (oracle.sf_reduce)
+            want = oracle.sf_reduce(nroots, leaves, ld, rd, op)[r]
+            root = torch.from_numpy(rd[r]).cuda()
+            leaf = torch.from_numpy(ld[r]).cuda()
+            sf.reduce_begin(leaf, root, op)
+            sf.reduce_end(leaf, root, op)
+            assert np.array_equal(root.cpu().numpy(), want), f"sf reduce seed {seed} round {rnd} op {op} rank {r}"
+    sf.check()
     sf.close()
 
 

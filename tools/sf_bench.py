@@ -1,6 +1,8 @@
 """SF-pingpong / SF-unpack microbenchmark on NVLink 5 (the paper's Listing 5).
 
-    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/sf_bench.py
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/sf_bench.py [--graph]
+    (SPMAT_SF=nccl: the NCCL transport; --graph: replay the iterations from a CUDA graph, so
+    the numbers are device time rather than the Python launch rate)
 
 Two ranks; rank 0 owns n consecutive roots, rank 1 has n leaves connected one-on-one in order
 (the right SF of the paper's Fig. 1).  One iteration = SFBcastBegin/End then
@@ -8,7 +10,7 @@ SFReduceBegin/End with op REPLACE (pingpong: user buffers are the transport buff
 (unpack: an add kernel on the receiving side).  Reported: one-way latency = iteration time / 2,
 measured with CUDA events on the caller's stream (max over ranks), and the bandwidth n*8 B /
 one-way time.  Unlike GPU-aware MPI there is no device synchronisation before sending: the
-whole iteration is stream-ordered (NCCL p2p on the library's comm stream).
+whole iteration is stream-ordered.
 """
 import json
 import os
@@ -28,6 +30,8 @@ def main():
     torch.cuda.set_device(local)
     torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = sp.Comm(device=local, nranks=P, rank=r)
+    graph = "--graph" in sys.argv
+    transport = None
     stream = torch.cuda.current_stream()
     rows = []
     for logn in range(0, 24, 2):  # 8 B .. 32 MB
@@ -40,19 +44,36 @@ def main():
         rdata = torch.arange(max(nroots, 1), dtype=torch.float64, device="cuda")
         ldata = torch.zeros(max(n if r == 1 else 0, 1), dtype=torch.float64, device="cuda")
         res = {"n": n, "bytes": 8 * n}
+        transport = {2: "flagged lines over NVLink peer memory", 1: "NCCL p2p over NVLink 5"}.get(sf.transport())
         for name, op in (("replace", sp.REPLACE), ("sum", sp.SUM)):
             niter = 200 if n <= (1 << 16) else 50
-            for it in range(niter + 10):
-                if it == 10:
-                    sd.barrier()
-                    torch.cuda.synchronize()
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e0.record(stream)
-                sf.bcast_begin(rdata, ldata, op, stream)
-                sf.bcast_end(rdata, ldata, op, stream)
-                sf.reduce_begin(ldata, rdata, op, stream)
-                sf.reduce_end(ldata, rdata, op, stream)
+
+            def iteration(st):
+                sf.bcast_begin(rdata, ldata, op, st)
+                sf.bcast_end(rdata, ldata, op, st)
+                sf.reduce_begin(ldata, rdata, op, st)
+                sf.reduce_end(ldata, rdata, op, st)
+
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            for _ in range(10):
+                iteration(stream)
+            if graph:  # device time: the iterations replayed from a CUDA graph
+                g, gs = torch.cuda.CUDAGraph(), torch.cuda.Stream()
+                gs.wait_stream(stream)
+                with torch.cuda.graph(g, stream=gs):
+                    for _ in range(niter):
+                        iteration(gs)
+                torch.cuda.synchronize()
+                sd.barrier()
+                e0.record(stream)
+                g.replay()
+            else:
+                torch.cuda.synchronize()
+                sd.barrier()
+                e0.record(stream)
+                for _ in range(niter):
+                    iteration(stream)
             e1.record(stream)
             torch.cuda.synchronize()
             us = sd.max_over_ranks(e0.elapsed_time(e1) * 1e3 / niter / 2)
@@ -61,8 +82,9 @@ def main():
         rows.append(res)
         sf.close()
     if r == 0:
-        print(json.dumps({"bench": "sf_pingpong", "transport": "NCCL p2p over NVLink 5",
-                          "rows": rows}), flush=True)
+        print(json.dumps({"bench": "sf_pingpong", "transport": transport,
+                          "timing": "CUDA graph replay" if graph else "eager launches", "rows": rows}),
+              flush=True)
         print(f"{'bytes':>10s} {'REPLACE us':>11s} {'GB/s':>8s} {'SUM us':>9s} {'GB/s':>8s}")
         for x in rows:
             print(f"{x['bytes']:10d} {x['replace_us']:11.2f} {x['replace_GBps']:8.2f} "
