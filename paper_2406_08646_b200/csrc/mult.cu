@@ -103,7 +103,11 @@ static bool pipeline_ok(spmat_s *A) {
 }
 
 static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStream_t s) {
-  const int C = 8;
+  static const int C = [] {
+    const char *e = getenv("SPMAT_PIPE_CHUNKS");
+    const int c = e ? atoi(e) : 0;
+    return c >= 2 && c <= 256 ? c : 16;
+  }();
   SP_TRY(spmv_pipe_prepare(A, C));
   const int nc = A->pipe_chunks;
   const bool multi = A->comm->nranks > 1;
