@@ -306,6 +306,7 @@ struct spmat_s {
   spmat::DevBuf<int32_t> longrows;   // rows with more than kLong nonzeros
   int64_t n_long = 0;
   int tma_grid = 0;                  // persistent grid of the bulk-copy SpMV
+  int tma_grid_tail = 0;             // its grid with the fused off-diagonal add (>= tma_grid)
   spmat::DevBuf<int32_t> block_order;  // boundary row blocks first (fused off-diagonal tail)
   spmat::DevBuf<int4> blocks4;         // (r0, r1, p0, p1) per row block in claim order
   int64_t n_bblocks = 0;

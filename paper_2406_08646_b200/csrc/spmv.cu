@@ -440,8 +440,13 @@ static int tma_setup(spmat_s *A) {
   int reserve = 0;
   if (const char *e = getenv("SPMAT_RESERVE_SMS")) reserve = std::max(0, atoi(e));
   const int64_t sms = std::max<int64_t>(1, A->comm->num_sms - reserve);
-  A->tma_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * sms,
-                                                             A->n_rowblocks));
+  const int64_t full = (int64_t)std::max(per_sm, 1) * sms;
+  A->tma_grid = (int)std::max<int64_t>(1, std::min<int64_t>(full, A->n_rowblocks));
+  // with the fused off-diagonal add every CTA's comm warp takes chunks of off-diagonal rows:
+  // small matrices (fewer row blocks than chunks) get extra CTAs that only do that
+  const int64_t per = A->ro_w == 1 ? 32 * kRowsU : 32 / A->ro_w;
+  const int64_t chunks = (A->n_ro + per - 1) / per;
+  A->tma_grid_tail = (int)std::max<int64_t>(A->tma_grid, std::min<int64_t>(full, chunks));
   return SPMAT_OK;
 }
 
@@ -550,9 +555,9 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   SP_TRY(tma_setup(A));
   if (const char *tr = getenv("SPMAT_TRACE")) {  // device trace of the fused MatMult kernel
     if (atoi(tr)) {
-      SP_TRY(A->trace.alloc(kTraceCta * (size_t)A->tma_grid + 16));
+      SP_TRY(A->trace.alloc(kTraceCta * (size_t)A->tma_grid_tail + 16));
       SP_CUDA(cudaMemsetAsync(A->trace.get(), 0, A->trace.n * 8, st));
-      const unsigned long long hdr[2] = {(unsigned long long)A->tma_grid, (unsigned long long)kTraceCta};
+      const unsigned long long hdr[2] = {(unsigned long long)A->tma_grid_tail, (unsigned long long)kTraceCta};
       SP_CUDA(cudaMemcpyAsync(A->trace.get() + A->trace.n - 2, hdr, sizeof hdr, cudaMemcpyHostToDevice, st));
     }
   }
@@ -583,7 +588,8 @@ static cudaError_t launch_tma(spmat_s *A, const double *x, double *y, cudaStream
     t.nwaits = A->n_waits;
     t.ctr = A->tail_ctr.get();
   }
-  return launch_pdl(k_spmv_tma, (unsigned)A->tma_grid, kCtaThreads, kTmaSmem, s, (const int4 *)A->blocks4.get(),
+  const unsigned grid = (unsigned)(fuse_tail ? A->tma_grid_tail : A->tma_grid);
+  return launch_pdl(k_spmv_tma, grid, kCtaThreads, kTmaSmem, s, (const int4 *)A->blocks4.get(),
                     (int)A->n_rowblocks, (const int32_t *)A->rowptr_d.get(), (const int32_t *)A->col_d.get(),
                     (const double *)A->val_d.get(), x, y, A->sched.get(), h, t);
 }
