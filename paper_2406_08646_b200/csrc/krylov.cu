@@ -181,6 +181,12 @@ __device__ void finalize_cta(const FinArgs &f, int np) {
 // dot instead of two).  Called by every thread of the CTA.
 __device__ __forceinline__ void partial_done(double s, const FinArgs &f) {
   __shared__ int last;
+  if (f.count && gridDim.x == 1) {  // one CTA: no cross-CTA handshake
+    if (threadIdx.x == 0) f.partial[0] = s;
+    __syncthreads();
+    finalize_cta(f, 1);
+    return;
+  }
   if (threadIdx.x == 0) {
     f.partial[blockIdx.x] = s;
     if (f.count) {
@@ -270,12 +276,15 @@ __global__ void k_cg_pupdate(double *__restrict__ p, const double *__restrict__ 
 // ------------------------------------------------------------------ host side
 static int max_dot_blocks(spmat_s *A) { return A->comm->num_sms * 4; }
 
-// CTAs of a dot over the local rows: ~8 elements per thread, at most 4 per SM -- a function of
-// m only, so every dot of a matrix reduces in the same fixed order
+// CTAs of the update kernels (x/r update + r.r, CG init): ~8 elements per thread, at most 4
+// CTAs per SM; of a pure dot (p.q, spmat_vec_dot): one CTA up to 64 elements per thread (the
+// cross-CTA handshake costs more than the loop), else the same.  Functions of m only, so every
+// dot of a matrix reduces in the same fixed order.
 static int dot_blocks(spmat_s *A) {
   const int64_t want = (A->m + 8 * kDotThreads - 1) / (8 * kDotThreads);
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, max_dot_blocks(A)));
 }
+static int pure_dot_blocks(spmat_s *A) { return A->m <= 64 * kDotThreads ? 1 : dot_blocks(A); }
 
 static int ensure_ws(spmat_s *A) {
   if (A->cg_partial.n) return SPMAT_OK;
@@ -315,11 +324,11 @@ static FinArgs fin_args(spmat_s *A, int op, double *result, double *hist) {
 }
 
 // NCCL path: local sum of the partials, ncclAllReduce of the scalar, then the scalar step
-static int finish_nccl(spmat_s *A, int op, double *result, double *hist, cudaStream_t s) {
+static int finish_nccl(spmat_s *A, int op, double *result, double *hist, int np, cudaStream_t s) {
   if (!nccl_reduce(A)) return SPMAT_OK;
   Comm *c = A->comm;
   FinArgs f = fin_args(A, OP_DOT, nullptr, nullptr);
-  k_finalize<<<1, kDotThreads, 0, s>>>(f, dot_blocks(A));
+  k_finalize<<<1, kDotThreads, 0, s>>>(f, np);
   SP_LAUNCH();
   SP_NCCL(c->api, c->api->AllReduce(A->cg_reduced.get(), A->cg_reduced.get() + 1, 1, ncclFloat64,
                                     ncclSum, c->nccl, s));
@@ -344,12 +353,12 @@ static int cg_iteration(spmat_s *A, double *x, double *rr_hist, cudaStream_t s) 
   const int nb = dot_blocks(A);
   const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)A->comm->num_sms * 8));
   SP_TRY(spmat_mult_part(A, p, q, 7, s));                            // q = A p
-  SP_CUDA(launch_pdl(k_dot_partial, nb, kDotThreads, 0, s, (const double *)p, (const double *)q, m,
+  SP_CUDA(launch_pdl(k_dot_partial, pure_dot_blocks(A), kDotThreads, 0, s, (const double *)p, (const double *)q, m,
                      fin_args(A, OP_CG_ALPHA, nullptr, nullptr)));
-  SP_TRY(finish_nccl(A, OP_CG_ALPHA, nullptr, nullptr, s));         // alpha = rr / p.q
+  SP_TRY(finish_nccl(A, OP_CG_ALPHA, nullptr, nullptr, pure_dot_blocks(A), s));  // alpha = rr / p.q
   SP_CUDA(launch_pdl(k_cg_update, nb, kDotThreads, 0, s, x, r, (const double *)p, (const double *)q, m,
                      fin_args(A, OP_CG_BETA, nullptr, rr_hist)));
-  SP_TRY(finish_nccl(A, OP_CG_BETA, nullptr, rr_hist, s));          // beta, rr = r.r
+  SP_TRY(finish_nccl(A, OP_CG_BETA, nullptr, rr_hist, nb, s));      // beta, rr = r.r
   SP_CUDA(launch_pdl(k_cg_pupdate, gv, 256, 0, s, p, (const double *)r, m, (const CgScalars *)sc));  // p = r + beta p
   return SPMAT_OK;
 }
@@ -382,9 +391,9 @@ int spmat_vec_dot(spmat_t A, const double *a, const double *b, double *result, v
   DeviceGuard g(A->comm->device);
   cudaStream_t s = (cudaStream_t)stream;
   SP_TRY(ensure_ws(A));
-  SP_CUDA(launch_pdl(k_dot_partial, dot_blocks(A), kDotThreads, 0, s, a, b, A->m,
+  SP_CUDA(launch_pdl(k_dot_partial, pure_dot_blocks(A), kDotThreads, 0, s, a, b, A->m,
                      fin_args(A, OP_DOT, result, nullptr)));
-  return finish_nccl(A, OP_DOT, result, nullptr, s);
+  return finish_nccl(A, OP_DOT, result, nullptr, pure_dot_blocks(A), s);
 }
 
 int spmat_cg(spmat_t A, const double *b, double *x, int maxit, double *rr_hist, void *stream) {
@@ -420,7 +429,7 @@ int spmat_cg(spmat_t A, const double *b, double *x, int maxit, double *rr_hist, 
   SP_TRY(spmat_mult_part(A, x, q, 7, cs));
   SP_CUDA(launch_pdl(k_cg_init, nb, kDotThreads, 0, cs, b, (const double *)q, r, p, m,
                      fin_args(A, OP_CG_INIT, nullptr, rr_hist)));
-  SP_TRY(finish_nccl(A, OP_CG_INIT, nullptr, rr_hist, cs));
+  SP_TRY(finish_nccl(A, OP_CG_INIT, nullptr, rr_hist, nb, cs));
   if (!use_graph) {
     for (int k = 0; k < maxit; ++k) SP_TRY(cg_iteration(A, x, rr_hist, s));
     return SPMAT_OK;

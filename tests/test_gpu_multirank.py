@@ -50,3 +50,20 @@ def test_multirank_offdiag_lanes(ro_w, fuse):
     sys.stderr.write(r.stderr[-6000:])
     assert r.returncode == 0
     assert f"MULTIRANK P={P} failures=0" in r.stdout
+
+
+def test_multirank_nccl_board():
+    """CG and the device dots with the cross-rank scalar sum over ncclAllReduce instead of the
+    NVLink scalar board (SPMAT_BOARD=nccl)."""
+    P = 2
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    env = dict(os.environ)
+    env["SPMAT_BOARD"] = "nccl"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr=127.0.0.1", "--master-port=29651", os.path.join(HERE, "mp_gpu_parity.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    sys.stdout.write(r.stdout[-6000:])
+    sys.stderr.write(r.stderr[-6000:])
+    assert r.returncode == 0
+    assert f"MULTIRANK P={P} failures=0" in r.stdout
