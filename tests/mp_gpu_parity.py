@@ -365,8 +365,8 @@ def main():
              ("stencil-real", lambda: case_stencil(c, "real")),
              ("q1-int", lambda: case_q1(c, "int")), ("q1-real", lambda: case_q1(c, "real")),
              ("elasticity", lambda: case_elasticity(c))]
-    cases += [(f"random{s}", (lambda s=s: case_random(c, s))) for s in range(6)]
-    cases += [(f"sf{s}", (lambda s=s: case_sf(c, s))) for s in range(6)]
+    cases += [(f"random{s}", (lambda s=s: case_random(c, s))) for s in range(16)]
+    cases += [(f"sf{s}", (lambda s=s: case_sf(c, s))) for s in range(24)]
     cases += [("box7-int", lambda: case_box(c, 7, "int")), ("box7-real", lambda: case_box(c, 7, "real")),
               ("box27-real", lambda: case_box(c, 27, "real"))]
     cases += [("cg", lambda: case_cg(c))]

@@ -135,6 +135,29 @@ def test_nnz_closed_forms_gpu(sp, comm):
         A.close()
 
 
+def test_random_coo_acceptance_500(sp, comm):
+    """SPEC L706 on the GPU: 500 random COO instances (<= 50 % duplicates, <= 20 % negatives,
+    empty ones included) -- structure, plans and values bit-exact vs the oracle, MatMult exact
+    in integers."""
+    rng = np.random.default_rng(7060)
+    for trial in range(500):
+        M, N = int(rng.integers(1, 80)), int(rng.integers(1, 80))
+        n = int(rng.integers(0, 400))
+        i, j, v = synth.random_coo(M, N, n, dup_frac=float(rng.uniform(0, 0.5)),
+                                   neg_frac=float(rng.uniform(0, 0.2)), seed=50000 + trial)
+        O = oracle.OracleMat(M, N, [M], [N], [i], [j])
+        O.set_values([v])
+        A = sp.Mat(comm, M, N, M, N, dev(i), dev(j))
+        check_structure(A, O)
+        A.set_values(dev(v))
+        assert np.array_equal(canon(A.export("val_d")), canon(O.export(0, "val_d"))), trial
+        x = synth.x_vector(0, N, "int", seed=trial)
+        y = torch.empty(M, dtype=torch.float64, device="cuda")
+        A.mult(dev(x), y)
+        assert np.array_equal(canon(y.cpu().numpy()), canon(O.mult(x.numpy()))), trial
+        A.close()
+
+
 @pytest.mark.parametrize("seed", range(8))
 def test_random_coo_fuzz(sp, comm, seed):
     rng = np.random.default_rng(seed)

@@ -608,3 +608,74 @@ def test_q2_125pt_nnz():
         i, j, v = synth.stencil_coo((n, n, n), 125)
         A = oracle.OracleMat(n ** 3, n ** 3, [n ** 3], [n ** 3], [i], [j])
         assert A.info(0, "nnz_d") == (5 * n - 6) ** 3
+
+
+# ---------------------------------------------------------------- SPEC acceptance sizes
+def _random_sf(rng, pmax, rmax, lmax):
+    P = int(rng.integers(1, pmax + 1))
+    nroots = [int(rng.integers(0, rmax)) for _ in range(P)]
+    owners = [q for q in range(P) if nroots[q] > 0]
+    leaves, rootdata, leafdata = [], [], []
+    for p in range(P):
+        nl = int(rng.integers(0, lmax)) if owners else 0
+        space = nl + int(rng.integers(0, 4))
+        il = rng.permutation(space)[:nl] if nl else np.zeros(0, np.int64)
+        rr = rng.choice(owners, nl) if nl else np.zeros(0, np.int64)
+        ro = np.array([rng.integers(0, nroots[q]) for q in rr], dtype=np.int64)
+        leaves.append((il, rr, ro))
+        rootdata.append(rng.integers(-50, 50, nroots[p]).astype(float))
+        leafdata.append(rng.integers(-50, 50, space).astype(float))
+    return P, nroots, leaves, rootdata, leafdata
+
+
+def test_sf_acceptance_1000_random_graphs():
+    """1,000 random SFs with up to 8 ranks (holes, fan-in, empty ranks); bcast and
+    reduce, REPLACE and SUM, vs independent Python edge walks."""
+    rng = np.random.default_rng(705)
+    for trial in range(1000):
+        P, nroots, leaves, rootdata, leafdata = _random_sf(rng, 8, 9, 9)
+        for op in (oracle.REPLACE, oracle.SUM):
+            out = oracle.sf_bcast(nroots, leaves, rootdata, leafdata, op)
+            for p in range(P):
+                want = leafdata[p].copy()
+                il, rr, ro = leaves[p]
+                for l in range(len(rr)):
+                    val = rootdata[rr[l]][ro[l]]
+                    want[il[l]] = val if op == oracle.REPLACE else want[il[l]] + val
+                assert np.array_equal(out[p], want), (trial, op, p)
+            out = oracle.sf_reduce(nroots, leaves, leafdata, rootdata, op)
+            want = [r.copy() for r in rootdata]
+            for p in range(P):
+                il, rr, ro = leaves[p]
+                for l in np.argsort(il, kind="stable"):
+                    c = leafdata[p][il[l]]
+                    want[rr[l]][ro[l]] = c if op == oracle.REPLACE else want[rr[l]][ro[l]] + c
+            for q in range(P):
+                assert np.array_equal(out[q], want[q]), (trial, op, q)
+
+
+def test_random_coo_acceptance_500():
+    """500 random COO instances (<= 50 % duplicates, <= 20 % negatives, up to 8
+    ranks, uneven and empty ranks) vs a dense brute force: assembled matrix, INSERT then ADD,
+    and MatMult exact in integers."""
+    rng = np.random.default_rng(706)
+    for trial in range(500):
+        P = int(rng.integers(1, 9))
+        M, N = int(rng.integers(1, 30)), int(rng.integers(1, 30))
+        cuts = np.sort(rng.integers(0, M + 1, P - 1))
+        rs = list(np.diff(np.concatenate([[0], cuts, [M]])).astype(int))
+        cs = synth.split_sizes(N, P)
+        ii, jj, vv = [], [], []
+        for r in range(P):
+            n = int(rng.integers(0, 40))
+            i, j, v = synth.random_coo(M, N, n, dup_frac=float(rng.uniform(0, 0.5)),
+                                       neg_frac=float(rng.uniform(0, 0.2)), seed=trial * 16 + r)
+            ii.append(i); jj.append(j); vv.append(v)
+        A = oracle.OracleMat(M, N, rs, cs, ii, jj)
+        A.set_values(vv, oracle.INSERT)
+        D = numpy_dense(M, N, ii, jj, vv)
+        assert np.array_equal(A.dense(), D), trial
+        x = synth.x_vector(0, N, "int", seed=trial).numpy()
+        assert np.array_equal(A.mult(x), D @ x), trial
+        A.set_values(vv, oracle.ADD)
+        assert np.array_equal(A.dense(), 2 * D), trial
