@@ -554,3 +554,22 @@ def test_cuda_graphs(sp, comm, monkeypatch):
         outs.append((xg.cpu(), hist.cpu()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
     A.close()
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_matmult_deterministic(sp, comm, cfg):
+    """the dynamically scheduled SpMV is bitwise reproducible run to run (every row
+    is summed by one fixed lane group in a fixed order, whichever CTA claims its block)."""
+    i, j, v, sizes = synth.config_rank_coo(cfg, 1, 0, values="real", device="cuda")
+    M = sizes[0]
+    A = sp.Mat(comm, M, M, M, M, i, j)
+    A.set_values(v)
+    del i, j, v
+    x = synth.x_vector(0, M, "real", device="cuda")
+    y0 = torch.empty(M, dtype=torch.float64, device="cuda")
+    y1 = torch.empty_like(y0)
+    A.mult(x, y0)
+    for _ in range(5):
+        A.mult(x, y1)
+        assert torch.equal(y0, y1)
+    A.close()
