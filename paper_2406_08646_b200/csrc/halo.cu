@@ -210,7 +210,7 @@ int halo_peer_setup(spmat_s *A) {
   for (size_t a = 0; a < sf->snbr.size(); ++a) {
     const int q = sf->snbr[a];
     const int64_t lstart = all[(size_t)(17 + P) * q + 17 + me];
-    HaloPut p;
+    HaloPut p{};
     p.dst = A->peer_ghost[q] + lstart;
     p.dst_stride = all[(size_t)(17 + P) * q + 16];
     p.count = sf->scount[a];

@@ -98,6 +98,26 @@ __device__ __forceinline__ void halo_put_warp(const HaloPut *__restrict__ puts, 
   const int64_t per = (p.count + p.nchunk - 1) / p.nchunk;
   const int64_t lo = c * per, hi = min(p.count, lo + per);
   constexpr int U = 8;
+  if (p.cflag) {  // bulk: half the NVLink bytes of flagged lines, one release per chunk
+    double *dd = reinterpret_cast<double *>(dst);
+    for (int64_t t0 = lo + lane; t0 < hi; t0 += 32 * U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t t = t0 + 32 * u;
+        v[u] = t < hi ? __ldg(x + (p.root_idx ? p.root_idx[t] : p.root_start + t)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t t = t0 + 32 * u;
+        if (t < hi) dd[t] = v[u];
+      }
+    }
+    __threadfence_system();
+    __syncwarp();
+    if (lane == 0) st_release_sys(p.cflag + c, epoch);
+    return;
+  }
   for (int64_t t0 = lo + lane; t0 < hi; t0 += 32 * U) {
     double v[U];
 #pragma unroll
@@ -111,6 +131,19 @@ __device__ __forceinline__ void halo_put_warp(const HaloPut *__restrict__ puts, 
       if (t < hi) ll_store(dst + t, v[u], flag);
     }
   }
+}
+
+// Value t of this epoch's staging buffer gl (star forest): flagged line, or -- in a bulk
+// segment -- a plain double once its chunk's flag carries the epoch.
+__device__ __forceinline__ double sf_value(const uint4 *gl, int64_t t, const SfSeg *__restrict__ segs, int nseg,
+                                           unsigned long long epoch, int *err) {
+  int s = 0;
+  while (s + 1 < nseg && t >= segs[s + 1].start) ++s;
+  const SfSeg g = nseg ? segs[s] : SfSeg{0, 0, nullptr, 1};
+  if (!g.cflag) return ll_load(gl + t, ll_flag(epoch), err);
+  const int64_t k = t - g.start;
+  spin_until_geq(g.cflag + k / g.per, epoch, err);
+  return __ldcg(reinterpret_cast<const double *>(gl + g.start) + k);
 }
 
 // Off-diagonal SpMV-add with W lanes per row (W a power of two <= 32): thread t of a group

@@ -168,6 +168,14 @@ struct HaloPut {                       // one destination rank of my owned x ent
   const int64_t *root_idx;             // ...gather indices (device), nullptr if contiguous
   unsigned long long *my_done;         // destination -> me: "ghost buffer free" epoch (local)
   int nchunk, pad;
+  // bulk protocol (large star-forest segments): plain doubles in the first half of the
+  // destination's line region, then per chunk a fence and a release of cflag[chunk] = epoch
+  unsigned long long *cflag;           // nullptr: flagged lines (the default)
+};
+struct SfSeg {                         // consumer view of one producer's segment (star forest)
+  int64_t start, count;                // range in the staging buffer's order
+  const unsigned long long *cflag;     // bulk chunk flags (local), nullptr: flagged lines
+  int64_t per;                         // values per bulk chunk
 };
 struct HaloWait {                      // one sender of my ghost entries
   unsigned long long *peer_done;       // sender's "ghost buffer free" flag for me (IPC mapping)
@@ -219,12 +227,14 @@ struct sf_s {
   bool peer = false;
   spmat::DevBuf<uint4> bline, rline;
   int64_t bstride = 0, rstride = 0;
-  spmat::DevBuf<unsigned long long> pflags;  // [q] bcast done from receiver q, [P+q] reduce done from owner q
+  spmat::DevBuf<unsigned long long> pflags;  // [q] bcast done from receiver q, [P+q] reduce done from owner q,
+                                             // then the bulk segments' chunk flags
   spmat::DevBuf<unsigned long long> d_ep;    // [0] completed bcasts, [1] completed reduces
   std::vector<void *> peer_mem;              // opened IPC mappings
   spmat::DevBuf<HaloPut> bputs, rputs;       // bcast: my roots -> leaf owners; reduce: my leaves -> root owners
   int nbputs = 0, nrputs = 0, bchunks = 0, rchunks = 0;
   spmat::DevBuf<HaloWait> bwaits, rwaits;    // producers to release after consuming
+  spmat::DevBuf<SfSeg> bsegs, rsegs;         // consumer segment tables (bulk or flagged lines)
   int nbwaits = 0, nrwaits = 0;
   spmat::DevBuf<unsigned int> pcounter;      // last-CTA detection of the consuming kernels
   spmat::DevBuf<int> perr;                   // bounded-spin timeouts

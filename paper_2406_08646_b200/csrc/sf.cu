@@ -301,14 +301,32 @@ int sf_peer_setup(sf_s *sf) {
   sf->rstride = std::max<int64_t>(sf->nsend, 1);
   SP_TRY(sf->bline.alloc(2 * (size_t)sf->bstride));
   SP_TRY(sf->rline.alloc(2 * (size_t)sf->rstride));
-  SP_TRY(sf->pflags.alloc(2 * (size_t)P));
+  // bulk segments (>= bulk_min values): plain doubles + one release flag per put chunk, the
+  // chunk flags after the 2P done flags (bcast segments, then reduce segments).  Flagged lines
+  // move twice the bytes but need no fence: measured (SF-pingpong, 2 B200) lines are faster up
+  // to ~8 MB, bulk from ~32 MB (110 vs 121 us) -- hence the 2^21-value default.
+  int64_t bulk_min = (int64_t)1 << 21;
+  if (const char *e = getenv("SPMAT_SF_BULK_MIN")) bulk_min = std::max<int64_t>(1, atoll(e));
+  std::vector<int64_t> bflag_off(P, -1), rflag_off(P, -1);
+  int64_t nflags = 2 * (int64_t)P;
+  for (size_t a = 0; a < sf->rnbr.size(); ++a)
+    if (sf->rcount[a] >= bulk_min) {
+      bflag_off[sf->rnbr[a]] = nflags;
+      nflags += put_chunks_of(sf->rcount[a]);
+    }
+  for (size_t a = 0; a < sf->snbr.size(); ++a)
+    if (sf->scount[a] >= bulk_min) {
+      rflag_off[sf->snbr[a]] = nflags;
+      nflags += put_chunks_of(sf->scount[a]);
+    }
+  SP_TRY(sf->pflags.alloc(nflags));
   SP_TRY(sf->d_ep.alloc(2));
   SP_TRY(sf->pcounter.alloc(1));
   SP_TRY(sf->perr.alloc(1));
   SP_CUDA(cudaEventCreateWithFlags(&sf->ev_take, cudaEventDisableTiming));
   SP_CUDA(cudaMemset(sf->bline.get(), 0, sf->bline.n * sizeof(uint4)));  // flag 0: no epoch
   SP_CUDA(cudaMemset(sf->rline.get(), 0, sf->rline.n * sizeof(uint4)));
-  SP_CUDA(cudaMemset(sf->pflags.get(), 0, 2 * P * sizeof(unsigned long long)));
+  SP_CUDA(cudaMemset(sf->pflags.get(), 0, nflags * sizeof(unsigned long long)));
   SP_CUDA(cudaMemset(sf->d_ep.get(), 0, 2 * sizeof(unsigned long long)));
   SP_CUDA(cudaMemset(sf->pcounter.get(), 0, sizeof(unsigned)));
   SP_CUDA(cudaMemset(sf->perr.get(), 0, sizeof(int)));
@@ -326,13 +344,17 @@ int sf_peer_setup(sf_s *sf) {
   if (v1[0]) return SPMAT_OK;  // NCCL transport on every rank
   // per rank: 3 handles, strides, and for every peer p the offset of p's data in my bline
   // (p sends me roots) and in my rline (p sends me leaves)
-  const int W = 24 + 2 + 2 * P;
+  const int W = 24 + 2 + 4 * P;
   std::vector<int64_t> mine(W, -1), all((size_t)W * P);
   memcpy(mine.data(), h, sizeof h);
   mine[24] = sf->bstride;
   mine[25] = sf->rstride;
   for (size_t a = 0; a < sf->rnbr.size(); ++a) mine[26 + sf->rnbr[a]] = sf->roff[a];
   for (size_t a = 0; a < sf->snbr.size(); ++a) mine[26 + P + sf->snbr[a]] = sf->soff[a];
+  for (int q = 0; q < P; ++q) {
+    mine[26 + 2 * P + q] = bflag_off[q];
+    mine[26 + 3 * P + q] = rflag_off[q];
+  }
   SP_TRY(c->allgather_i64(mine.data(), W, all.data()));
   std::vector<uint4 *> pb(P, nullptr), pr(P, nullptr);
   std::vector<unsigned long long *> pf(P, nullptr);
@@ -377,6 +399,7 @@ int sf_peer_setup(sf_s *sf) {
     p.root_idx = sf->root_start[a] >= 0 ? nullptr : sf->d_root_idx.get() + sf->soff[a];
     p.my_done = sf->pflags.get() + q;
     p.nchunk = put_chunks_of(p.count);
+    p.cflag = at(q, 26 + 2 * P + me) >= 0 ? pf[q] + at(q, 26 + 2 * P + me) : nullptr;
     sf->bchunks += p.nchunk;
     bp.push_back(p);
     HaloWait w{};
@@ -393,6 +416,7 @@ int sf_peer_setup(sf_s *sf) {
     p.root_idx = sf->leaf_start[a] >= 0 ? nullptr : sf->d_leaf_idx.get() + sf->roff[a];
     p.my_done = sf->pflags.get() + P + q;
     p.nchunk = put_chunks_of(p.count);
+    p.cflag = at(q, 26 + 3 * P + me) >= 0 ? pf[q] + at(q, 26 + 3 * P + me) : nullptr;
     sf->rchunks += p.nchunk;
     rp.push_back(p);
     HaloWait w{};
@@ -404,6 +428,22 @@ int sf_peer_setup(sf_s *sf) {
     if (!src.empty()) SP_CUDA(cudaMemcpy(dst.get(), src.data(), src.size() * sizeof(src[0]), cudaMemcpyHostToDevice));
     return SPMAT_OK;
   };
+  // consumer segment tables (staging order): bcast = recv order, reduce = requester-major
+  std::vector<SfSeg> bs, rs;
+  for (size_t a = 0; a < sf->rnbr.size(); ++a) {
+    const int64_t o = bflag_off[sf->rnbr[a]];
+    const int nch = put_chunks_of(sf->rcount[a]);
+    bs.push_back({sf->roff[a], sf->rcount[a], o >= 0 ? sf->pflags.get() + o : nullptr,
+                  (sf->rcount[a] + nch - 1) / nch});
+  }
+  for (size_t a = 0; a < sf->snbr.size(); ++a) {
+    const int64_t o = rflag_off[sf->snbr[a]];
+    const int nch = put_chunks_of(sf->scount[a]);
+    rs.push_back({sf->soff[a], sf->scount[a], o >= 0 ? sf->pflags.get() + o : nullptr,
+                  (sf->scount[a] + nch - 1) / nch});
+  }
+  SP_TRY(upload(sf->bsegs, bs));
+  SP_TRY(upload(sf->rsegs, rs));
   SP_TRY(upload(sf->bputs, bp));
   SP_TRY(upload(sf->rputs, rp));
   SP_TRY(upload(sf->bwaits, bw));
@@ -434,13 +474,14 @@ static int sf_after_take(sf_s *sf, cudaStream_t stream) {
 // Bcast consumer: leaf[leaf_idx[t]] (=|+=) the value of line t of this epoch; the last CTA
 // releases the staging buffer to the senders and advances the epoch.
 __global__ void k_sf_bcast_take(const uint4 *__restrict__ lines, int64_t stride, const int64_t *__restrict__ lidx,
-                                int64_t n, double *__restrict__ leaf, int op, const HaloWait *__restrict__ waits,
-                                int nwaits, unsigned long long *ep, unsigned int *counter, int *err) {
+                                int64_t n, const SfSeg *__restrict__ segs, int nseg, double *__restrict__ leaf,
+                                int op, const HaloWait *__restrict__ waits, int nwaits, unsigned long long *ep,
+                                unsigned int *counter, int *err) {
   pdl_wait();
   const unsigned long long epoch = *ep + 1ull;
   const uint4 *gl = lines + (int64_t)(epoch & 1) * stride;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
-    const double v = ll_load(gl + t, ll_flag(epoch), err);
+    const double v = sf_value(gl, t, segs, nseg, epoch, err);
     const int64_t l = lidx[t];
     leaf[l] = op == SF_REPLACE ? v : __dadd_rn(leaf[l], v);
   }
@@ -459,7 +500,8 @@ __global__ void k_sf_bcast_take(const uint4 *__restrict__ lines, int64_t stride,
 // epoch's lines; the last CTA releases the staging buffer and advances the epoch.
 __global__ void k_sf_reduce_take(const int64_t *__restrict__ roots, const int64_t *__restrict__ ptr,
                                  const int64_t *__restrict__ code, int64_t n, const uint4 *__restrict__ lines,
-                                 int64_t stride, const double *__restrict__ leaf,
+                                 int64_t stride, const SfSeg *__restrict__ segs, int nseg,
+                                 const double *__restrict__ leaf,
                                  const int64_t *__restrict__ self_leaf, double *__restrict__ root, int op,
                                  const HaloWait *__restrict__ waits, int nwaits, unsigned long long *ep,
                                  unsigned int *counter, int *err) {
@@ -471,7 +513,7 @@ __global__ void k_sf_reduce_take(const int64_t *__restrict__ roots, const int64_
     double s = root[r];
     for (int64_t k = ptr[t]; k < ptr[t + 1]; ++k) {
       const int64_t cc = code[k];
-      const double v = cc >= 0 ? ll_load(gl + cc, ll_flag(epoch), err) : leaf[self_leaf[-cc - 1]];
+      const double v = cc >= 0 ? sf_value(gl, cc, segs, nseg, epoch, err) : leaf[self_leaf[-cc - 1]];
       s = op == SF_REPLACE ? v : __dadd_rn(s, v);
     }
     root[r] = s;
@@ -571,7 +613,8 @@ int sf_reduce_end_impl(sf_s *sf, const double *leaf, double *root, int op, cudaS
     const unsigned grid = grid_for(std::max<int64_t>(sf->n_touched, 1), 256, sf->comm->num_sms);
     SP_CUDA(launch_pdl(k_sf_reduce_take, grid, 256, 0, stream, (const int64_t *)sf->d_red_roots.get(),
                        (const int64_t *)sf->d_red_ptr.get(), (const int64_t *)sf->d_red_code.get(), sf->n_touched,
-                       (const uint4 *)sf->rline.get(), sf->rstride, (const double *)leaf,
+                       (const uint4 *)sf->rline.get(), sf->rstride, (const SfSeg *)sf->rsegs.get(),
+                       (int)sf->rsegs.n, (const double *)leaf,
                        (const int64_t *)sf->d_self_leaf.get(), root, op, (const HaloWait *)sf->rwaits.get(),
                        sf->nrwaits, sf->d_ep.get() + 1, sf->pcounter.get(), sf->perr.get()));
     SP_CUDA(cudaEventRecord(sf->ev_take, stream));
@@ -663,7 +706,8 @@ int sf_end(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stre
   if (sf->peer) {  // always launched: it also ends the epoch
     const unsigned grid = grid_for(std::max<int64_t>(sf->nrecv, 1), 256, sf->comm->num_sms);
     SP_CUDA(launch_pdl(k_sf_bcast_take, grid, 256, 0, stream, (const uint4 *)sf->bline.get(), sf->bstride,
-                       (const int64_t *)sf->d_leaf_idx.get(), sf->nrecv, leaf, op,
+                       (const int64_t *)sf->d_leaf_idx.get(), sf->nrecv, (const SfSeg *)sf->bsegs.get(),
+                       (int)sf->bsegs.n, leaf, op,
                        (const HaloWait *)sf->bwaits.get(), sf->nbwaits, sf->d_ep.get(), sf->pcounter.get(),
                        sf->perr.get()));
     SP_CUDA(cudaEventRecord(sf->ev_take, stream));

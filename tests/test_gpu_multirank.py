@@ -67,3 +67,20 @@ def test_multirank_nccl_board():
     sys.stderr.write(r.stderr[-6000:])
     assert r.returncode == 0
     assert f"MULTIRANK P={P} failures=0" in r.stdout
+
+
+def test_multirank_sf_bulk_protocol():
+    """Star-forest segments of >= 4 values take the bulk protocol (plain doubles + per-chunk
+    release flags) instead of flagged lines (SPMAT_SF_BULK_MIN=4; the default is 2^21)."""
+    P = 2
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    env = dict(os.environ)
+    env["SPMAT_SF_BULK_MIN"] = "4"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr=127.0.0.1", "--master-port=29652", os.path.join(HERE, "mp_gpu_parity.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    sys.stdout.write(r.stdout[-6000:])
+    sys.stderr.write(r.stderr[-6000:])
+    assert r.returncode == 0
+    assert f"MULTIRANK P={P} failures=0" in r.stdout
