@@ -167,6 +167,16 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream);
    written.  Collective. */
 int spmat_mult(spmat_t A, const double *x, double *y, void *stream);
 
+/* MatMultTranspose: y = A^T x (collective, enqueue-only).  x: DEVICE array of m_local doubles
+   (the row layout), y: DEVICE array of n_local doubles (the column layout).  PETSc's MPIAIJ
+   order: lvec = A_o^T x, y = A_d^T x, then the halo star forest reduces lvec into the owners' y
+   with SUM (sf_reduce): every y entry is summed from +0.0 over its column's rows in
+   ascending order, then the other ranks' sums are added in ascending rank order -- a fixed,
+   rank-count-independent order (real-valued results reproducible bit for bit).  The transposed blocks are built on
+   the first call (device radix sort, host-synchronising) and their values re-gathered after
+   every spmat_set_values_coo.  Host x or y: SPMAT_ERR_ARG. */
+int spmat_mult_transpose(spmat_t A, const double *x, double *y, void *stream);
+
 /* MatSetBlockSize analogue for the SpMV storage (block-CSR on GPU): bs = 3 checks that
    the assembled diagonal block consists of dense, aligned 3x3 blocks (node-block matrices with
    3 dofs per node) and from then on multiplies it from a 3x3 block-CSR copy (8.44 instead of

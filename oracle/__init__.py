@@ -59,6 +59,7 @@ def lib():
                                          ctypes.POINTER(i64)]
             L.orc_set_values_coo.argtypes = [p, p, p, ctypes.c_int]
             L.orc_mult.argtypes = [p, p, p]
+            L.orc_mult_transpose.argtypes = [p, p, p]
             L.orc_info.argtypes = [p, ctypes.c_int, ctypes.c_int]
             L.orc_info.restype = i64
             L.orc_export.argtypes = [p, ctypes.c_int, ctypes.c_int, p]
@@ -138,6 +139,17 @@ class OracleMat:
         st = lib().orc_mult(self._h, _ptr(x), _ptr(y))
         if st != ORC_OK:
             raise ValueError(f"oracle mult failed: {st}")
+        return y
+
+    def mult_transpose(self, x_global):
+        """y = A^T x (oracle.c orc_mult_transpose): x in the row layout (M), y in the column
+        layout (N)."""
+        x = _np(x_global, np.float64)
+        assert x.size == self.M
+        y = np.zeros(self.N, dtype=np.float64)
+        st = lib().orc_mult_transpose(self._h, _ptr(x), _ptr(y))
+        if st != ORC_OK:
+            raise ValueError(f"oracle mult_transpose failed: {st}")
         return y
 
     def cg(self, b_global, x0_global, maxit):

@@ -33,6 +33,10 @@
  *  - MatMult: y = A x with ghost x entries fetched through the halo SF (P:433-434,
  *    P:477-478), y_local = A_d x_local + A_o lvec.
  *
+ *  - MatMultTranspose (what the SF reduce enables): lvec = A_o^T x, y = A_d^T x,
+ *    then the halo SF reduces lvec into the owners' y with SUM (root value first, then the
+ *    contributions in ascending source rank).
+ *
  * Readings of points the paper leaves open:
  *  Z1  duplicate contributions are summed in ascending (src rank, k) order, one accumulator
  *      starting from +0.0;
@@ -395,6 +399,43 @@ int orc_mult(const orc_sys *S, const double *gx, double *gy) {
       }
       gy[R->rstart + q] = y;
     }
+    free(lvec);
+  }
+  return ORC_OK;
+}
+
+/*
+ * orc_mult_transpose: y = A^T x in PETSc's MPIAIJ order (MatMultTranspose; the halo star
+ * forest used in reverse, PetscSFReduce with SUM).  gx: global x (length M, the row
+ * layout), gy: global y (length N, the column layout).
+ *   per rank:  y_loc[c] = sum over the rank's rows q ascending of a_d(q,c) * x[q], from +0.0
+ *              lvec[g]  = same over the off-diagonal entries of ghost column g
+ *   then, for every rank s ascending, the owner adds lvec_s[g] to y[colmap_s[g]]
+ *   (SF reduce order: the root's value first, then ascending source rank).
+ */
+int orc_mult_transpose(const orc_sys *S, const double *gx, double *gy) {
+  if (!S) return ORC_ERR_STATE;
+  for (int r = 0; r < S->P; ++r) {
+    const orc_rank *R = &S->rk[r];
+    if (!R->values_set && R->nnz_d + R->nnz_o > 0) return ORC_ERR_STATE;
+    for (int64_t c = R->cstart; c < R->cend; ++c) gy[c] = +0.0;
+    const int64_t m = R->rend - R->rstart;
+    for (int64_t q = 0; q < m; ++q)
+      for (int64_t t = R->rowptr_d[q]; t < R->rowptr_d[q + 1]; ++t) {
+        double p = R->val_d[t] * gx[R->rstart + q];
+        gy[R->cstart + R->col_d[t]] = gy[R->cstart + R->col_d[t]] + p;
+      }
+  }
+  for (int s = 0; s < S->P; ++s) {
+    const orc_rank *R = &S->rk[s];
+    double *lvec = (double *)xcalloc(R->n_ghost, sizeof(double));
+    const int64_t m = R->rend - R->rstart;
+    for (int64_t q = 0; q < m; ++q)
+      for (int64_t t = R->rowptr_o[q]; t < R->rowptr_o[q + 1]; ++t) {
+        double p = R->val_o[t] * gx[R->rstart + q];
+        lvec[R->col_o[t]] = lvec[R->col_o[t]] + p;
+      }
+    for (int64_t g = 0; g < R->n_ghost; ++g) gy[R->colmap[g]] = gy[R->colmap[g]] + lvec[g];
     free(lvec);
   }
   return ORC_OK;

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libspmat.so")
-SOURCES = ["comm.cu", "sf.cu", "coo.cu", "spmv.cu", "mult.cu", "halo.cu", "krylov.cu", "bsr.cu"]
+SOURCES = ["comm.cu", "sf.cu", "coo.cu", "spmv.cu", "mult.cu", "halo.cu", "krylov.cu", "bsr.cu", "transpose.cu"]
 HEADERS = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "halo_dev.cuh"), os.path.join(CSRC, "ptx.cuh"),
            os.path.join(ROOT, "include", "spmat.h")]
 

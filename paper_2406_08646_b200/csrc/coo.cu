@@ -720,6 +720,7 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
   if (A->ncoo > 0 && !v) return fail(SPMAT_ERR_ARG, "spmat_set_values_coo: null v");
   if (mode == SPMAT_ADD && !A->values_set)
     return fail(SPMAT_ERR_STATE, "spmat_set_values_coo: ADD before any INSERT");
+  ++A->val_version;  // transposed values (transpose.cu) are re-gathered on next use
   spmat_comm_s *c = A->comm;
   DeviceGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;

@@ -200,7 +200,7 @@ __device__ __forceinline__ void offdiag_row_w(int64_t q, bool valid, int W,
 // Off-diagonal SpMV-add for U rows per thread, one lane per row (rows q0, q0 + stride, ...):
 // each level of the load chain (row pointers -> column/value -> ghost value, and row id -> y)
 // is issued for all U rows before any of them is used, so U rows cost one chain of
-// latencies instead of U.  Each row is summed left to right (the oracle's order).
+// latencies instead of U.  Each row is summed left to right (the serial CSR order).
 // gl != nullptr: flagged ghost lines of `flag`; else the plain ghost vector lv.
 template <int U>
 __device__ __forceinline__ void offdiag_rows_u(int64_t q0, int64_t stride, int64_t nro,

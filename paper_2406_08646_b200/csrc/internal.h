@@ -367,6 +367,11 @@ struct spmat_s {
   std::vector<cudaEvent_t> pipe_ev;                        // 2 * chunks + 2
   // CG / dot workspace (krylov.cu), allocated on first use
   spmat::DevBuf<double> cg_r, cg_p, cg_q, cg_partial, cg_scalars, cg_reduced;
+  // MatMultTranspose (transpose.cu): transposed diagonal / off-diagonal blocks, built lazily
+  bool t_built = false;
+  int64_t val_version = 0, t_val_version = -1;  // set_values count / values gathered for
+  spmat::DevBuf<int32_t> t_rowptr_d, t_col_d, t_perm_d, t_rowptr_o, t_col_o, t_perm_o;
+  spmat::DevBuf<double> t_val_d, t_val_o, t_lvec;
   spmat::DevBuf<unsigned> cg_count;  // CTA arrival counter of the dot kernels (last CTA finalizes)
 };
 

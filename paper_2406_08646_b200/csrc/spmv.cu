@@ -127,7 +127,7 @@ __global__ void k_rb_pairs(const int32_t *__restrict__ rows, const int32_t *__re
 }
 
 // W lanes per row: lane l of a row's group sums elements a+l, a+l+W, ... (8 in flight), then
-// a shuffle reduction; W = 1 is a plain left-to-right sum (the oracle's order)
+// a shuffle reduction; W = 1 is a plain left-to-right sum (the serial CSR order)
 template <int W>
 __device__ __forceinline__ void rows_w(int r0, int r1, int p0, const int *__restrict__ rp,
                                        const int *__restrict__ sc, const double *__restrict__ sv,

@@ -337,6 +337,32 @@ def case_host_pipeline(c, kind):
     A.close()
 
 
+def case_transpose(c, seed):
+    """MatMultTranspose across ranks (halo SF reduce) vs the oracle, bit-exact with real values."""
+    P, r = c.P, c.r
+    rng = np.random.default_rng(800 + seed)
+    M, N = int(rng.integers(P, 150)), int(rng.integers(P, 150))
+    rs = synth.split_sizes(M, P)
+    cs = synth.split_sizes(N, P)
+    coo = [synth.random_coo(M, N, int(rng.integers(0, 600)), dup_frac=0.4, neg_frac=0.1, values="real",
+                            seed=seed * 17 + q) for q in range(P)]
+    O = oracle.OracleMat(M, N, rs, cs, [t[0] for t in coo], [t[1] for t in coo])
+    O.set_values([t[2] for t in coo])
+    i, j, v = coo[r]
+    A = sp.Mat(c.comm, rs[r], cs[r], M, N, i.cuda(), j.cuda())
+    A.set_values(v.cuda())
+    roff, coff = synth.offsets_from_sizes(rs), synth.offsets_from_sizes(cs)
+    xg = synth.x_vector(0, M, "real", seed=seed).numpy()
+    x = torch.from_numpy(xg[roff[r]:roff[r + 1]].copy()).cuda()
+    y = torch.full((cs[r],), float("nan"), dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        A.mult_transpose(x, y)
+        want = O.mult_transpose(xg)[coff[r]:coff[r + 1]]
+        assert np.array_equal(canon(y.cpu().numpy()), canon(want)), f"transpose seed {seed} rank {r}"
+    A.check()
+    A.close()
+
+
 def case_errors(c):
     P, r = c.P, c.r
     # only the last rank has an out-of-range index: every rank must report it
@@ -372,6 +398,7 @@ def main():
     cases += [("cg", lambda: case_cg(c))]
     cases += [("host-pipeline-slab", lambda: case_host_pipeline(c, "slab")),
               ("host-pipeline-box", lambda: case_host_pipeline(c, "box"))]
+    cases += [(f"transpose{s}", (lambda s=s: case_transpose(c, s))) for s in range(6)]
     cases += [("errors", lambda: case_errors(c))]
     for name, fn in cases:
         try:

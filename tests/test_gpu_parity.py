@@ -573,3 +573,27 @@ def test_matmult_deterministic(sp, comm, cfg):
         A.mult(x, y1)
         assert torch.equal(y0, y1)
     A.close()
+
+
+def test_mult_transpose(sp, comm):
+    """MatMultTranspose vs the oracle: bit-exact, real values included (same summation order),
+    after a value refresh (ADD), on random, element (Q1) and rectangular matrices."""
+    cases = [(9 ** 3, 9 ** 3, *synth.q1_coo(9, values="real"))]
+    for seed in range(4):
+        M, N = 40 + 13 * seed, 70 - 11 * seed
+        cases.append((M, N, *synth.random_coo(M, N, 900, dup_frac=0.4, neg_frac=0.1, values="real",
+                                              seed=400 + seed)))
+    for M, N, i, j, v in cases:
+        O = oracle.OracleMat(M, N, [M], [N], [i], [j])
+        O.set_values([v])
+        A = sp.Mat(comm, M, N, M, N, dev(i), dev(j))
+        A.set_values(dev(v))
+        x = synth.x_vector(0, M, "real", seed=5, device="cuda")
+        y = torch.full((N,), float("nan"), dtype=torch.float64, device="cuda")
+        A.mult_transpose(x, y)
+        assert np.array_equal(canon(y.cpu().numpy()), canon(O.mult_transpose(x.cpu().numpy())))
+        A.set_values(dev(v), sp.ADD)  # values change: the transposed copy is re-gathered
+        O.set_values([v], oracle.ADD)
+        A.mult_transpose(x, y)
+        assert np.array_equal(canon(y.cpu().numpy()), canon(O.mult_transpose(x.cpu().numpy())))
+        A.close()

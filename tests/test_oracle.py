@@ -679,3 +679,50 @@ def test_random_coo_acceptance_500():
         assert np.array_equal(A.mult(x), D @ x), trial
         A.set_values(vv, oracle.ADD)
         assert np.array_equal(A.dense(), 2 * D), trial
+
+
+# ---------------------------------------------------------------- MatMultTranspose
+@pytest.mark.parametrize("seed", range(20))
+def test_mult_transpose_dense_and_partition(seed):
+    """orc_mult_transpose = the dense A^T x (integer values: exact in any order), on random
+    COO with uneven and empty ranks, for every partition of the same matrix."""
+    rng = np.random.default_rng(900 + seed)
+    M, N = int(rng.integers(1, 35)), int(rng.integers(1, 35))
+    n = int(rng.integers(0, 150))
+    i, j, v = synth.random_coo(M, N, n, dup_frac=0.4, neg_frac=0.15, seed=900 + seed)
+    D = numpy_dense(M, N, [i], [j], [v])
+    x = synth.x_vector(0, M, "int", seed=seed).numpy()
+    for P in (1, 2, 3, 5):
+        rs = synth.split_sizes(M, P)
+        cs = synth.split_sizes(N, P)
+        off = synth.offsets_from_sizes(rs)
+        ii = [i[(i >= off[r]) & (i < off[r + 1])] for r in range(P)]
+        jj = [j[(i >= off[r]) & (i < off[r + 1])] for r in range(P)]
+        vv = [v[(i >= off[r]) & (i < off[r + 1])] for r in range(P)]
+        A = oracle.OracleMat(M, N, rs, cs, ii, jj)
+        A.set_values(vv)
+        assert np.array_equal(A.mult_transpose(x), D.T @ x), (seed, P)
+
+
+def test_mult_transpose_symmetric_stencil():
+    """The Dirichlet 7-point Laplacian is symmetric: A^T x == A x bit for bit in integers, and
+    <A^T x, z> == <x, A z> for the nonsymmetric Q1-mass-plus-random case."""
+    n = 6
+    M = n ** 3
+    i, j, v = synth.stencil_coo((n, n, n), 7, values="int")
+    P = 3
+    rs = synth.split_sizes(M, P)
+    off = synth.offsets_from_sizes(rs)
+    ii = [i[(i >= off[r]) & (i < off[r + 1])] for r in range(P)]
+    jj = [j[(i >= off[r]) & (i < off[r + 1])] for r in range(P)]
+    vv = [v[(i >= off[r]) & (i < off[r + 1])] for r in range(P)]
+    A = oracle.OracleMat(M, M, rs, rs, ii, jj)
+    A.set_values(vv)
+    x = synth.x_vector(0, M, "int", seed=3).numpy()
+    assert np.array_equal(A.mult_transpose(x), A.mult(x))
+    # adjoint identity on a nonsymmetric matrix (integers: exact)
+    i2, j2, v2 = synth.random_coo(M, M, 3000, dup_frac=0.3, neg_frac=0.1, seed=77)
+    B = oracle.OracleMat(M, M, [M], [M], [i2], [j2])
+    B.set_values([v2])
+    z = synth.x_vector(0, M, "int", seed=4).numpy()
+    assert np.dot(B.mult_transpose(x), z) == np.dot(x, B.mult(z))
