@@ -597,3 +597,28 @@ def test_mult_transpose(sp, comm):
         A.mult_transpose(x, y)
         assert np.array_equal(canon(y.cpu().numpy()), canon(O.mult_transpose(x.cpu().numpy())))
         A.close()
+
+
+def test_mult_transpose_errors(sp, comm):
+    """spmat_mult_transpose: host arrays, aliasing and calls before set_values are refused."""
+    n = 6
+    M = n ** 3
+    i, j, v = synth.stencil_coo((n, n, n), 7, values="int")
+    A = sp.Mat(comm, M, M, M, M, dev(i), dev(j))
+    x = torch.ones(M, dtype=torch.float64, device="cuda")
+    y = torch.empty(M, dtype=torch.float64, device="cuda")
+    with pytest.raises(sp.SpmatError) as e:
+        A.mult_transpose(x, y)
+    assert e.value.status == sp.SPMAT_ERR_STATE
+    A.set_values(dev(v))
+    with pytest.raises(sp.SpmatError) as e:
+        A.mult_transpose(x.cpu(), y)
+    assert e.value.status == sp.SPMAT_ERR_ARG
+    with pytest.raises(sp.SpmatError) as e:
+        A.mult_transpose(x, x)
+    assert e.value.status == sp.SPMAT_ERR_ARG
+    A.mult_transpose(x, y)  # symmetric Laplacian: A^T 1 = A 1 = out-of-grid neighbour counts
+    y2 = torch.empty_like(y)
+    A.mult(x, y2)
+    assert torch.equal(y, y2)
+    A.close()
