@@ -1,4 +1,5 @@
-// halo_dev.cuh -- device side of the NVLink halo (shared by halo.cu and spmv.cu).
+// halo_dev.cuh -- device side of the NVLink transports: halo puts and flagged lines (halo.cu,
+// spmv.cu), the fused off-diagonal tail, star-forest segments (sf.cu), the scalar board (krylov.cu).
 #pragma once
 #include "internal.h"
 #include "ptx.cuh"
