@@ -207,6 +207,12 @@ __global__ void __launch_bounds__(kDotThreads) k_finalize(FinArgs f, int np) {
   finalize_cta(f, np);
 }
 
+constexpr int kU = 4;  // elements per thread in flight in the streaming vector kernels
+
+__device__ __forceinline__ double combine(const double (&acc)[kU]) {
+  return __dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3]));
+}
+
 // CTA c owns [c*chunk, (c+1)*chunk); partial[c] = sum of a*b there
 __global__ void __launch_bounds__(kDotThreads) k_dot_partial(const double *__restrict__ a,
                                                              const double *__restrict__ b, int64_t n,
@@ -215,9 +221,24 @@ __global__ void __launch_bounds__(kDotThreads) k_dot_partial(const double *__res
   pdl_wait();
   const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
-  double s = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kDotThreads) s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
-  partial_done(block_sum(s, red), f);
+  // kU independent accumulators (kU loads of each vector in flight per thread); the order of
+  // the sums is still a fixed function of n and the grid
+  double acc[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) acc[u] = 0.0;
+  int64_t i = lo + threadIdx.x;
+  for (; i + (kU - 1) * kDotThreads < hi; i += kU * kDotThreads) {
+    double av[kU], bv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      av[u] = a[i + u * kDotThreads];
+      bv[u] = b[i + u * kDotThreads];
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) acc[u] = __dadd_rn(acc[u], __dmul_rn(av[u], bv[u]));
+  }
+  for (; i < hi; i += kDotThreads) acc[0] = __dadd_rn(acc[0], __dmul_rn(a[i], b[i]));
+  partial_done(block_sum(combine(acc), red), f);
 }
 
 // r = b - q; p = r; partial of r.r
@@ -249,18 +270,44 @@ __global__ void __launch_bounds__(kDotThreads) k_cg_update(double *__restrict__ 
   const bool go = !f.sc->stopped;
   const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
-  double s = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kDotThreads) {
+  double acc[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) acc[u] = 0.0;
+  int64_t i = lo + threadIdx.x;
+  for (; i + (kU - 1) * kDotThreads < hi; i += kU * kDotThreads) {
+    double rv[kU], xv[kU], pv[kU], qv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t k = i + u * kDotThreads;
+      rv[u] = r[k];
+      if (go) {
+        xv[u] = x[k];
+        pv[u] = p[k];
+        qv[u] = q[k];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t k = i + u * kDotThreads;
+      if (go) {
+        x[k] = __dadd_rn(xv[u], __dmul_rn(alpha, pv[u]));
+        rv[u] = __dsub_rn(rv[u], __dmul_rn(alpha, qv[u]));
+        r[k] = rv[u];
+      }
+      acc[u] = __dadd_rn(acc[u], __dmul_rn(rv[u], rv[u]));
+    }
+  }
+  for (; i < hi; i += kDotThreads) {
     double ri = r[i];
     if (go) {
       x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
       ri = __dsub_rn(ri, __dmul_rn(alpha, q[i]));
       r[i] = ri;
     }
-    s = __dadd_rn(s, __dmul_rn(ri, ri));
+    acc[0] = __dadd_rn(acc[0], __dmul_rn(ri, ri));
   }
   // every CTA has read sc->alpha/stopped before the last one (which rewrites sc) gets here
-  partial_done(block_sum(s, red), f);
+  partial_done(block_sum(combine(acc), red), f);
 }
 
 // p = r + beta p
@@ -269,8 +316,19 @@ __global__ void k_cg_pupdate(double *__restrict__ p, const double *__restrict__ 
   pdl_wait();
   if (sc->stopped) return;
   const double beta = sc->beta;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + (kU - 1) * stride < n; i += kU * stride) {  // kU loads of each vector in flight
+    double rv[kU], pv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      rv[u] = r[i + u * stride];
+      pv[u] = p[i + u * stride];
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) p[i + u * stride] = __dadd_rn(rv[u], __dmul_rn(beta, pv[u]));
+  }
+  for (; i < n; i += stride) p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
 }
 
 // ------------------------------------------------------------------ host side
