@@ -1,5 +1,5 @@
 # 4-GPU refresh: GPU tests, C4/C4b/C5 bench lines at P=1,2,4, host-pipeline A/B, CG at P=1,2,4
-D=gpurun_out/scale3; mkdir -p $D
+D=gpurun_out/scale4; mkdir -p $D
 timeout 1300 python -m pytest tests -m gpu -q -x -p no:cacheprovider > $D/pytest.log 2>&1; tail -2 $D/pytest.log
 for cfg in c4 c4b c5; do
   python bench.py --config $cfg --no-cpu > $D/${cfg}_p1.json 2> $D/${cfg}_p1.err
