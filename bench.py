@@ -358,6 +358,9 @@ def main():
         e2e = {"value": 2 * nnz_global / te / 1e9, "unit": UNIT, "ms_per_step": te * 1e3,
                "h2d_bytes_per_step": 8 * m * P, "d2h_bytes_per_step": 8 * m * P, "steps": ke}
 
+    # ---- no NVLink wait timed out and no asynchronous CUDA/NCCL error (else the numbers are void)
+    A.check()
+
     # ---- report
     diag_bytes, off_bytes = byte_model(info, m, m, bs)
     hinfo = sp.sf_get_info(A.halo_sf())
