@@ -366,6 +366,25 @@ def main():
     hinfo = sp.sf_get_info(A.halo_sf())
     halo_bytes = 8 * (hinfo["n_recv"] + hinfo["n_send"])
     hbm_peak, peak_src, peakd = peaks()
+    # in-run pure-read reference: sum-reduce of 4 GB of doubles on this GPU
+    read_ref = None
+    try:
+        buf = torch.ones(1 << 29, dtype=torch.float64, device="cuda")
+        buf.sum()
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(5):
+            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            r0.record()
+            buf.sum()
+            r1.record()
+            torch.cuda.synchronize()
+            best = min(best, r0.elapsed_time(r1) / 1e3)
+        read_ref = buf.numel() * 8 / best / 1e9
+        del buf
+        torch.cuda.empty_cache()
+    except torch.OutOfMemoryError:
+        pass
     # with the NVLink halo the off-diagonal add runs inside the same kernel (t_off == 0):
     # that kernel then moves the diagonal and the off-diagonal bytes
     fused = info["n_offdiag_rows"] > 0 and t_off == 0.0
@@ -420,7 +439,9 @@ def main():
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
                      "algorithmic_bytes_per_launch": kernel_bytes,
-                     "avg_launch_ms": t_diag * 1e3, "peak_source": peak_src},
+                     "avg_launch_ms": t_diag * 1e3, "peak_source": peak_src,
+                     "frac_of_spec_8000": achieved / 8000.0 if achieved else None,
+                     "in_run_read_GBps": read_ref},
         "phases_ms": {"diag_spmv": t_diag * 1e3, "offdiag_spmv": t_off * 1e3,
                       "halo_comm_stream": t_halo * 1e3, "halo_bytes": halo_bytes,
                       "isolated": iso, "overlap_efficiency": overlap},
