@@ -18,6 +18,7 @@
 // whose segment contains received values are finished after the exchange, still in
 // canonical order, so the result is bit-identical to a serial sum in (src, k) order.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <climits>
@@ -516,7 +517,7 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
     DevBuf<int> dn;
     SP_TRY(dn.alloc(1));
     CUB_CALL(tmp, st, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes,
-                                                 cub::CountingInputIterator<uint32_t>(0), head.get(),
+                                                 thrust::counting_iterator<uint32_t>(0), head.get(),
                                                  segstart.get(), dn.get(), (int)nt, st));
     int hn = 0;
     SP_CUDA(cudaMemcpyAsync(&hn, dn.get(), 4, cudaMemcpyDeviceToHost, st));
@@ -601,7 +602,7 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
       k_nonempty<<<nblk(m_local), 256, 0, st>>>(cnt_o.get(), m_local, ne.get());
       SP_LAUNCH();
       CUB_CALL(tmp, st, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes,
-                                                   cub::CountingInputIterator<int32_t>(0), ne.get(),
+                                                   thrust::counting_iterator<int32_t>(0), ne.get(),
                                                    rows.get(), dn.get(), (int)m_local, st));
       SP_CUDA(cudaMemcpyAsync(&nro, dn.get(), 4, cudaMemcpyDeviceToHost, st));
       SP_CUDA(cudaStreamSynchronize(st));
@@ -661,7 +662,7 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
     DevBuf<int> dn;
     SP_TRY(dn.alloc(1));
     CUB_CALL(tmp, st, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes,
-                                                 cub::CountingInputIterator<uint32_t>(0), flag.get(),
+                                                 thrust::counting_iterator<uint32_t>(0), flag.get(),
                                                  ids.get(), dn.get(), (int)nnz, st));
     int nm = 0;
     SP_CUDA(cudaMemcpyAsync(&nm, dn.get(), 4, cudaMemcpyDeviceToHost, st));

@@ -22,6 +22,7 @@
 // CTA-per-row-block kernel that stages products in shared memory, and a plain sub-warp
 // vector CSR kernel.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <climits>
@@ -480,7 +481,7 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   k_long_rows<<<nblk(m), 256, 0, st>>>(A->rowptr_d.get(), m, flag.get(), maxlen.get());
   SP_LAUNCH();
   CUB_CALL(tmp, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes,
-                                           cub::CountingInputIterator<int32_t>(0), flag.get(),
+                                           thrust::counting_iterator<int32_t>(0), flag.get(),
                                            longrows.get(), maxlen.get() + 1, (int)m, st));
   int32_t h[2];
   SP_CUDA(cudaMemcpyAsync(h, maxlen.get(), 8, cudaMemcpyDeviceToHost, st));
@@ -535,13 +536,13 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
     k_boundary_blocks<<<nblk(nbk), 256, 0, st>>>(A->rbp.get(), nbk, A->rows_o.get(), A->n_ro, f1.get(), f0.get());
     SP_LAUNCH();
     CUB_CALL(tmp, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes,
-                                             cub::CountingInputIterator<int32_t>(0), f1.get(),
+                                             thrust::counting_iterator<int32_t>(0), f1.get(),
                                              A->block_order.get(), dn2.get(), (int)nbk, st));
     int nbb = 0;
     SP_CUDA(cudaMemcpyAsync(&nbb, dn2.get(), 4, cudaMemcpyDeviceToHost, st));
     SP_CUDA(cudaStreamSynchronize(st));
     CUB_CALL(tmp, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes,
-                                             cub::CountingInputIterator<int32_t>(0), f0.get(),
+                                             thrust::counting_iterator<int32_t>(0), f0.get(),
                                              A->block_order.get() + nbb, dn2.get() + 1, (int)nbk, st));
     A->n_bblocks = nbb;
     // (box partitions put boundary rows in most blocks: this order then sweeps the matrix
