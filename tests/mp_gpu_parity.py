@@ -363,6 +363,33 @@ def case_transpose(c, seed):
     A.close()
 
 
+def case_full_c4(c):
+    """The bench's default workload at full size (C4: 256^3 rows per rank, z-slabs, the fused
+    NVLink MatMult): sampled rows of every rank vs the oracle from the COO definition."""
+    P, r = c.P, c.r
+    i, j, v, sizes = synth.config_rank_coo("c4", P, r, values="real", device="cuda")
+    off = synth.offsets_from_sizes(sizes)
+    M = off[-1]
+    A = sp.Mat(c.comm, sizes[r], sizes[r], M, M, i, j)
+    A.set_values(v)
+    del i, j, v
+    x = synth.x_vector(off[r], off[r + 1], "real", device="cuda")
+    y = torch.empty(sizes[r], dtype=torch.float64, device="cuda")
+    for _ in range(3):  # several epochs of the NVLink halo
+        A.mult(x, y)
+    A.check()
+    g = torch.Generator().manual_seed(100 + r)
+    rows = torch.unique(torch.cat([torch.randint(off[r], off[r + 1], (800,), generator=g),
+                                   torch.tensor([off[r], off[r] + 1, off[r + 1] - 2, off[r + 1] - 1])]))
+    ih, jh, vh = synth.stencil_coo(synth.config_shape("c4", P), 7, rows=rows, values="real")
+    xg = synth.x_vector(0, M, "real").numpy()
+    ys = oracle.sample_rows(ih, jh, vh, rows.numpy(), xg)
+    got = y[(rows - off[r]).cuda()].cpu().numpy()
+    assert rel_err(got, ys) <= TOL, f"full-size C4 rank {r}"
+    A.close()
+    torch.cuda.empty_cache()
+
+
 def case_errors(c):
     P, r = c.P, c.r
     # only the last rank has an out-of-range index: every rank must report it
@@ -399,6 +426,7 @@ def main():
     cases += [("host-pipeline-slab", lambda: case_host_pipeline(c, "slab")),
               ("host-pipeline-box", lambda: case_host_pipeline(c, "box"))]
     cases += [(f"transpose{s}", (lambda s=s: case_transpose(c, s))) for s in range(6)]
+    cases += [("full-c4", lambda: case_full_c4(c))]
     cases += [("errors", lambda: case_errors(c))]
     for name, fn in cases:
         try:

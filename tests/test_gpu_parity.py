@@ -363,7 +363,7 @@ def test_determinism(sp, comm):
     A.close()
 
 
-@pytest.mark.parametrize("cfg", ["c2", "c3"])
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
 def test_full_size_sampled(sp, comm, cfg):
     """Full BASELINE sizes in the bench launch configuration: sampled rows vs the oracle
     computed one by one from the COO definition, plus A.1 over every row."""
@@ -376,8 +376,8 @@ def test_full_size_sampled(sp, comm, cfg):
     A.mult(x, y)
     rows = torch.unique(torch.cat([torch.randint(0, M, (1500,), generator=torch.Generator().manual_seed(5)),
                                    torch.tensor([0, 1, M // 2, M - 2, M - 1])]))
-    if cfg == "c2":
-        ih, jh, vh = synth.stencil_coo(synth.config_shape(cfg), 7, rows=rows, values="real")
+    if cfg in ("c2", "c4"):
+        ih, jh, vh = synth.stencil_coo(synth.config_shape(cfg, 1), 7, rows=rows, values="real")
     else:
         ih, jh, vh = i.cpu(), j.cpu(), v.cpu()
     ys = oracle.sample_rows(ih, jh, vh, rows.numpy(), x.cpu().numpy())
