@@ -144,7 +144,9 @@ int sf_destroy(sf_t sf);
    owners over NCCL; the owner sorts contributions by (i, j, src rank, k), splits the
    diagonal block (columns in [cstart, cend)) from the off-diagonal block, builds colmap
    (sorted unique ghost columns), the per-nonzero contribution plan (jmap/perm), the COO
-   send/receive plans and the halo SF.  Collective and host-synchronising.
+   send/receive plans and the halo SF.  Collective and host-synchronising: it first waits for
+   all work already queued on the device (cudaDeviceSynchronize), so device coo_i/coo_j may
+   come from kernels on any stream.
    Errors: SPMAT_ERR_RANGE if i >= M or j >= N (message names the rank and k; reported on
    every rank), SPMAT_ERR_MISMATCH if ranks disagree on M, N or the local sizes. */
 int spmat_create_coo(spmat_comm_t comm, int64_t m_local, int64_t n_local, int64_t M,

@@ -359,6 +359,10 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
   // ---- inputs on the device (memtype detection); not retained
   DevBuf<int64_t> di, dj;
   const int64_t *ci = coo_i, *cj = coo_j;
+  // device COO arrays may still be being written by the caller's kernels on any stream, and
+  // this (host-synchronising) call reads them on the library's setup stream: wait for the
+  // device first
+  SP_CUDA(cudaDeviceSynchronize());
   if (ncoo > 0) {
     if (!coo_i || !coo_j) return fail(SPMAT_ERR_ARG, "spmat_create_coo: null coo_i/coo_j");
     if (!is_device_ptr(coo_i)) {

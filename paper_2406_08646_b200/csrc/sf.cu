@@ -740,6 +740,7 @@ int sf_create(spmat_comm_t comm, int64_t nroots, int64_t nleaves, const int64_t 
   const int32_t *prr = remote_rank;
   const int64_t *pro = remote_offset;
   if (nleaves > 0) {
+    SP_CUDA(cudaDeviceSynchronize());  // device leaf arrays: the caller's kernels may still write them
     if (ilocal && is_device_ptr(ilocal)) {
       il.resize(nleaves);
       SP_CUDA(cudaMemcpy(il.data(), ilocal, nleaves * 8, cudaMemcpyDeviceToHost));
