@@ -13,8 +13,11 @@ separately and reported under "assembly".  Rank 0 prints ONE JSON line.
 Default workload: C4 -- 3D 7-point Laplacian, 256^3 rows per GPU in z-slabs (weak scaling),
 BASELINE.json configs[3], the 7-point Laplacian the north-star target is quoted on at
 1/2/4/8 B200.  Inputs: 1.74 GB per GPU of val/col/rowptr/x/y >> 126 MB L2, so no flush is
-needed between steps.  --impl reference times the serial CPU oracle (the reference arm for
-this tier) on a bounded slab of the same workload.
+needed between steps.  Timing: 5 trials of exactly K MatMults, each between a barrier and a
+device synchronisation, CUDA events on the launching stream, max over ranks per trial, the
+median trial reported.  cpu_baseline: the oracle's MatMult on the same
+matrix on 1 core and on all host cores (median of 3).  --impl reference times the oracle on
+all host cores (the reference arm for this tier) on the same matrix.
 """
 from __future__ import annotations
 
@@ -40,12 +43,14 @@ KERNEL_NAMES = {1: "k_spmv_stream (diagonal-block SpMV)", 2: "k_spmv_vector (dia
 METRIC = "MatMult GFLOP/s & HBM GB/s (% roofline), fp64, at 1/2/4/8 B200"
 UNIT = "GFLOP/s"
 FALLBACK_HBM = 6650.0
+TRIALS = 5
+NVLINK_GBPS = 900.0  # NVLink 5 per direction per GPU (B200_PROFILING.md)
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=200, help="MatMults per timed trial (5 trials)")
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="c4", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -75,8 +80,8 @@ class Clocks:
     }
 
     def __init__(self, index):
-        self.samples, self.reasons = [], set()
-        self.max_mhz = None
+        self.samples, self.mem, self.reasons = [], [], set()
+        self.max_mhz = self.mem_max_mhz = None
         self._stop = threading.Event()
         try:
             import pynvml
@@ -84,12 +89,14 @@ class Clocks:
             self.nv = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.mem_max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_MEM)
         except Exception:
             self.nv = None
 
     def _sample(self):
         nv = self.nv
         self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        self.mem.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_MEM))
         try:
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
         except Exception:
@@ -104,7 +111,7 @@ class Clocks:
                 self._sample()
             except Exception:
                 return
-            self._stop.wait(0.02)
+            self._stop.wait(0.002)
 
     def __enter__(self):
         if self.nv:
@@ -123,7 +130,9 @@ class Clocks:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "mem_mhz": statistics.median(self.mem), "mem_max_mhz": self.mem_max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "sample_period_ms": 2}
 
 
 # ------------------------------------------------------------------ byte / flop model
@@ -141,52 +150,150 @@ def byte_model(info, m, n, bs=1):
 
 
 # ------------------------------------------------------------------ CPU oracle legs
-def cpu_sample_workload(cfg):
-    """A bounded slab of the same workload for the serial oracle (~seconds of CPU work)."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+MAX_ORACLE_ROWS = 1 << 25  # rows of the benchmarked matrix the oracle holds in host memory
+
+
+def oracle_workload(cfg, P=1):
+    """The matrix the oracle multiplies: the benchmarked matrix itself when the oracle can hold
+    it -- row-sorted, duplicate-free COO (the stencil configs) goes through the direct CSR
+    builder, SURVEY.md §8(d) -- else a bounded sample (element / node-block COO: the general
+    tuple-sort assembly on a smaller grid).  Returns (csr, x, description, same_config)."""
+    import oracle
     c = synth.CONFIGS[cfg]
-    if c["kind"] == "stencil":
-        shape = list(c["shape"])
-        if len(shape) == 3:
-            shape[-1] = min(shape[-1], 16)
-        shape = tuple(shape)
-        i, j, v = synth.stencil_coo(shape, c["npts"], values="real")
-        M = int(np.prod(shape))
-        desc = f"{'x'.join(map(str, shape))} {c['npts']}-pt slab of {cfg}"
-    elif c["kind"] == "q1":
+    if c["kind"] in ("stencil", "box"):
+        if c["kind"] == "stencil":
+            shape = synth.config_shape(cfg, P)
+            M = int(np.prod(shape))
+            R = min(M, MAX_ORACLE_ROWS)
+            i, j, v = synth.stencil_coo(shape, c["npts"], rows=(0, R), values="real")
+        else:  # the one-box (P=1) matrix: natural lexicographic order
+            i, j, v, sizes = synth.config_rank_coo(cfg, 1, 0, values="real")
+            M = R = sizes[0]
+        C = oracle.OracleCsr(R, M, i, j, v)
+        del i, j, v
+        x = synth.x_vector(0, M, "real").numpy()
+        same = R == M and (c["kind"] == "stencil" or P == 1)
+        desc = (f"the benchmarked matrix ({synth.CONFIG_TEXT[cfg]}, {M} rows)" if same else
+                f"rows [0, {R}) of the {M}-row matrix of {cfg} at {P} GPUs")
+        return C, x, desc + " via oracle.OracleCsr (direct CSR, oracle.c orc_csr_direct)", same
+    if c["kind"] == "q1":
         n = 40
         i, j, v = synth.q1_coo(n, values="real")
         M = n ** 3
-        desc = f"Q1 {n}^3 nodes (element COO) sample of {cfg}"
+        desc = f"Q1 {n}^3 nodes (element COO, general oracle assembly) sample of {cfg}"
     else:
         n = 24
         i, j, v = synth.elasticity_coo(n, values="real")
         M = 3 * n ** 3
-        desc = f"3-dof 27-pt {n}^3 sample of {cfg}"
-    return M, i, j, v, desc
-
-
-def run_oracle(cfg, steps, warmup, budget_s=None):
-    import oracle
-    M, i, j, v, desc = cpu_sample_workload(cfg)
+        desc = f"3-dof 27-pt {n}^3 nodes (general oracle assembly) sample of {cfg}"
     O = oracle.OracleMat(M, M, [M], [M], [i], [j])
     O.set_values([v])
-    nnz = O.info(0, "nnz_d")
+    C = oracle.OracleCsr.from_oracle(O)
     x = synth.x_vector(0, M, "real").numpy()
-    for _ in range(warmup):
-        O.mult(x)
-    times = []
-    t_end = time.perf_counter() + (budget_s or 1e9)
-    for _ in range(steps):
+    return C, x, desc, False
+
+
+def time_oracle(C, x, nthreads, reps):
+    """Median over reps of one oracle MatMult (orc_csr_mult: orc_mult's per-row loop, serial or
+    over nthreads row slices; bit-identical either way, tests/test_oracle.py)."""
+    y = np.zeros(C.M)
+    C.mult(x, nthreads=nthreads, out=y)  # first touch
+    ts = []
+    for _ in range(reps):
         t0 = time.perf_counter()
-        O.mult(x)
-        times.append(time.perf_counter() - t0)
-        if budget_s and time.perf_counter() > t_end:
+        C.mult(x, nthreads=nthreads, out=y)
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts)
+
+
+def run_oracle(cfg, P=1, reps=3):
+    """cpu_baseline: the oracle on 1 core and on all host cores, median of
+    `reps`, same byte/flop model as the GPU line."""
+    C, x, desc, same = oracle_workload(cfg, P)
+    nt = host_threads()
+    t1 = time_oracle(C, x, 1, reps)
+    tn = time_oracle(C, x, nt, reps) if nt > 1 else t1
+    flops = 2 * C.nnz
+    byts = 12 * C.nnz + 4 * (C.M + 1) + 8 * C.N + 8 * C.M
+    return {"value": flops / tn / 1e9, "unit": UNIT, "cores": nt, "kind": "oracle",
+            "value_1core": flops / t1 / 1e9, "value_all_cores": flops / tn / 1e9,
+            "GBps_1core": byts / t1 / 1e9, "GBps_all_cores": byts / tn / 1e9,
+            "ms_per_matmult_1core": t1 * 1e3, "ms_per_matmult_all_cores": tn * 1e3,
+            "cpu_model": cpu_model(), "sched_getaffinity": nt, "reps": reps, "stat": "median",
+            "same_config": same, "rows": C.M, "nnz": C.nnz,
+            "sample": f"{desc}: {C.M} rows, {C.nnz} nnz; oracle/oracle.c orc_csr_mult "
+                      f"(gcc -O2 -ffp-contract=off), 1 thread and {nt} threads (row slices)"}
+
+
+# ------------------------------------------------------------------ shared line parts
+def config_dict(cfg, P, values):
+    """The workload as both arms name it (computed from the config alone, so the reference
+    arm's line carries the identical dict)."""
+    c = synth.CONFIGS[cfg]
+    M = synth.config_rows(cfg, P)
+    part = {"box": "box (cube) decomposition", "stencil": "z-slabs", "q1": "z-slabs",
+            "elasticity": "z-slabs"}[c["kind"]]
+    l2 = ("no flush: per-GPU inputs exceed the L2 (see roofline.l2_bytes)" if cfg != "c1" else
+          "no flush: 0.3 MB latency case, L2-resident by design")
+    return {"workload": synth.CONFIG_TEXT[cfg], "config_id": cfg, "rows_global": M,
+            "rows_per_gpu": M // P, "partition": part, "values": values,
+            "parallelism": f"row-partitioned MPIAIJ x{P}", "l2": l2}
+
+
+def reference_line(a, cfg):
+    """--impl reference: the oracle (the reference arm of this tier) on the host's cores, on
+    the benchmarked matrix (or, past MAX_ORACLE_ROWS, its leading rows), K timed steps after W
+    warm-up steps, each step one all-core oracle MatMult (bounded to ~2 minutes)."""
+    C, x, desc, same = oracle_workload(cfg, a.gpus)
+    nt = host_threads()
+    y = np.zeros(C.M)
+    for _ in range(max(a.warmup, 1)):
+        C.mult(x, nthreads=nt, out=y)
+    ts = []
+    t_end = time.perf_counter() + 120
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        C.mult(x, nthreads=nt, out=y)
+        ts.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end:
             break
-    t = sum(times) / len(times)
-    return {"value": 2 * nnz / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{desc}: {M} rows, {nnz} nnz, {len(times)} serial MatMults "
-                      f"(oracle/oracle.c, gcc -O2, 1 thread)",
-            "ms_per_matmult": t * 1e3}
+    t = sum(ts) / len(ts)
+    t1 = time_oracle(C, x, 1, 3)
+    val = 2 * C.nnz / t / 1e9
+    return {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+            "n_gpus": a.gpus, "steps": len(ts), "warmup": a.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True,
+            "scaling": "weak" if synth.CONFIGS[cfg]["per_gpu"] else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(cfg, a.gpus, "real"),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": nt, "kind": "oracle",
+                             "value_1core": 2 * C.nnz / t1 / 1e9, "value_all_cores": val,
+                             "cpu_model": cpu_model(), "sched_getaffinity": nt,
+                             "same_config": same, "rows": C.M, "nnz": C.nnz,
+                             "sample": f"{desc}: {C.M} rows, {C.nnz} nnz; each step one oracle "
+                                       f"MatMult on {nt} threads (oracle.c orc_csr_mult, row "
+                                       f"slices); value_1core = median of 3 serial MatMults"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
 
 
 # ------------------------------------------------------------------ main
@@ -215,19 +322,7 @@ def main():
     if a.impl == "reference":
         if rank != 0:
             return 0
-        ref = run_oracle(cfg, a.steps, a.warmup, budget_s=120)
-        line = {"impl": "reference", "metric": METRIC, "value": ref["value"], "unit": UNIT,
-                "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-                "ms_per_step": ref["ms_per_matmult"], "higher_is_better": True,
-                "scaling": "weak" if synth.CONFIGS[cfg]["per_gpu"] else "strong",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": synth.CONFIG_TEXT[cfg], "config_id": cfg,
-                           "sample": ref["sample"]},
-                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": ref["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0},
-                "gpu_launches": 0}
-        emit(line)
+        emit(reference_line(a, cfg))
         return 0
 
     if a.kernel:
@@ -285,21 +380,24 @@ def main():
         A.mult(x, y, stream)
     torch.cuda.synchronize()
 
-    # ---- timed region: exactly K MatMults, barrier + sync on both sides, max over ranks
+    # ---- timed region: TRIALS trials of exactly K MatMults each, barrier + sync on both sides
+    # of every trial, max over ranks per trial, median over trials
     A.profile(True)
     A.profile_read()  # clear
     clk = Clocks(local)
-    barrier()
-    torch.cuda.synchronize()
+    trials = []
     with clk:
-        ev0.record(stream)
-        for _ in range(a.steps):
-            A.mult(x, y, stream)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    t_local = ev0.elapsed_time(ev1) / 1e3 / a.steps
-    t_step = max_over_ranks(t_local)
+        for _ in range(TRIALS):
+            barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for _ in range(a.steps):
+                A.mult(x, y, stream)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            trials.append(max_over_ranks(ev0.elapsed_time(ev1) / 1e3 / a.steps))
+    t_step = statistics.median(trials)
     prof_ms, prof_n = A.profile_read()
     A.profile(False)
     t_diag = prof_ms[0] / max(prof_n[0], 1) / 1e3
@@ -404,7 +502,7 @@ def main():
             per_step_kernels += 1 if info["spmv_kernel_id"] != 3 else 0
     if info["spmv_kernel_id"] == 3 and info["max_row_nnz"] > 2560:
         per_step_kernels += 1  # k_spmv_long
-    traffic = None
+    traffic = None  # from the committed ncu --set full capture (profiles/traffic.json), not this run
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
@@ -412,6 +510,21 @@ def main():
             traffic = tr.get("traffic_bytes_per_launch") if tr else None
         except Exception:
             traffic = None
+    l2_bytes = torch.cuda.get_device_properties(local).L2_cache_size
+    # halo against NVLink: bytes on the wire per direction (16-byte flagged lines
+    # with the device-initiated transport, 8-byte values with NCCL) over the isolated halo time
+    halo = None
+    if P > 1:
+        line_b = 16 if halo_mode == 2 else 8
+        out_b = max_over_ranks(line_b * hinfo["n_send"])
+        in_b = max_over_ranks(line_b * hinfo["n_recv"])
+        th = iso.get("halo", 0.0) / 1e3
+        halo = {"transport": {1: "nccl", 2: "nvlink-peer-stores"}.get(halo_mode, str(halo_mode)),
+                "wire_bytes_out": out_b, "wire_bytes_in": in_b, "payload_bytes_out": out_b * 8 // line_b,
+                "isolated_ms": th * 1e3, "nvlink_GBps_per_dir": NVLINK_GBPS,
+                "halo_nvlink_frac": (max(out_b, in_b) / th / 1e9 / NVLINK_GBPS) if th > 0 else None,
+                "note": "isolated halo = put kernel + wait for every ghost line + buffer release, "
+                        "latency-bound at these sizes (0.5-2 MB)"}
     gflops = 2 * nnz_global / t_step / 1e9
     gbs_gpu = (diag_bytes + off_bytes) / t_step / 1e9
     line = {
@@ -421,42 +534,44 @@ def main():
         "n_gpus": P,
         "steps": a.steps,
         "warmup": a.warmup,
+        "trials": TRIALS,
         "ms_per_step": t_step * 1e3,
+        "trials_ms_per_step": [t * 1e3 for t in trials],
         "higher_is_better": True,
         "scaling": "weak" if synth.CONFIGS[cfg]["per_gpu"] else "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {
-            "workload": synth.CONFIG_TEXT[cfg], "config_id": cfg, "rows_global": M,
-            "nnz_global": nnz_global, "rows_per_gpu": m, "partition": "z-slabs",
-            "values": a.values, "parallelism": f"row-partitioned MPIAIJ x{P}",
-            "l2": f"no flush: per-GPU inputs {(diag_bytes + off_bytes) / 1e9:.2f} GB > 126 MB L2",
-        },
+        "config": config_dict(cfg, P, a.values),
+        "nnz_global": nnz_global,
         "hbm_gbs_per_gpu": gbs_gpu,
         "pct_hbm_roofline": gbs_gpu / hbm_peak,
         "roofline": {"bound": "hbm", "kernel": KERNEL_NAMES.get(info["spmv_kernel_id"], "?"),
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak if achieved else None, "traffic": traffic,
+                     "traffic_source": "profiles/traffic.json (committed ncu --set full capture)"
+                                       if traffic else None,
                      "algorithmic_bytes_per_launch": kernel_bytes,
                      "avg_launch_ms": t_diag * 1e3, "peak_source": peak_src,
                      "frac_of_spec_8000": achieved / 8000.0 if achieved else None,
-                     "in_run_read_GBps": read_ref},
+                     "in_run_read_GBps": read_ref, "l2_bytes": l2_bytes,
+                     "inputs_bytes_per_gpu": diag_bytes + off_bytes,
+                     "inputs_exceed_l2": diag_bytes + off_bytes > l2_bytes},
         "phases_ms": {"diag_spmv": t_diag * 1e3, "offdiag_spmv": t_off * 1e3,
                       "halo_comm_stream": t_halo * 1e3, "halo_bytes": halo_bytes,
                       "isolated": iso, "overlap_efficiency": overlap},
+        "halo": halo,
         "assembly": {"create_coo_s": t_create, "set_values_coo_ms": t_setvals * 1e3,
                      "coo_entries_per_rank": ncoo,
                      "set_values_GBps": (12 * ncoo + 12 * nnz_local) / t_setvals / 1e9},
         "e2e": e2e,
-        "gpu_launches": per_step_kernels * a.steps,
+        "gpu_launches": per_step_kernels * a.steps * TRIALS,
         "clocks": clk.summary(),
         "spmv_kernel_id": info["spmv_kernel_id"],
     }
     if rank == 0 and P == 1 and not a.no_cpu:
         try:
-            cb = run_oracle(cfg, 1000, 1, budget_s=20)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"] = run_oracle(cfg, 1)
         except Exception as ex:  # the CPU leg never decides the GPU number
             line["cpu_baseline"] = {"error": str(ex)}
     if rank == 0:

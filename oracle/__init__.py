@@ -40,7 +40,7 @@ def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so (plain gcc, no FMA contraction)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".{os.getpid()}.tmp"
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-pthread",
                                "-shared", "-fPIC", "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
     return _LIB
@@ -69,7 +69,8 @@ def lib():
             L.orc_sf_reduce.argtypes = [ctypes.c_int, p, p, p, p, p, p, p, p, ctypes.c_int]
             L.orc_sample_rows.argtypes = [i64, p, p, p, i64, p, p, p]
             L.orc_cg.argtypes = [p, p, p, ctypes.c_int, p]
-            L.orc_dense_coo.argtypes = [i64, i64, i64, p, p, p, p]
+            L.orc_csr_direct.argtypes = [i64, i64, i64, p, p, p, p, p, p, ctypes.POINTER(i64)]
+            L.orc_csr_mult.argtypes = [i64, p, p, p, p, p, ctypes.c_int]
             _lib = L
     return _lib
 
@@ -269,10 +270,46 @@ def sample_rows(coo_i, coo_j, coo_v, rows, x_global):
     return y
 
 
-def dense_coo(M, N, coo_i, coo_j, coo_v):
-    gi, gj, gv = _np(coo_i, np.int64), _np(coo_j, np.int64), _np(coo_v, np.float64)
-    A = np.zeros((M, N))
-    st = lib().orc_dense_coo(M, N, gi.size, _ptr(gi), _ptr(gj), _ptr(gv), _ptr(A))
-    if st != ORC_OK:
-        raise ValueError(f"oracle dense_coo failed: {st}")
-    return A
+class OracleCsr:
+    """One rank's CSR built directly from a row-sorted, duplicate-free COO (oracle.c
+    orc_csr_direct) -- full-size matrices for timing the oracle beside the GPU."""
+
+    def __init__(self, M, N, coo_i, coo_j, coo_v):
+        gi, gj, gv = _np(coo_i, np.int64), _np(coo_j, np.int64), _np(coo_v, np.float64)
+        self.M, self.N = int(M), int(N)
+        nvalid = int(np.count_nonzero((gi >= 0) & (gj >= 0)))
+        self.rowptr = np.zeros(self.M + 1, dtype=np.int64)
+        self.col = np.zeros(max(nvalid, 1), dtype=np.int64)
+        self.val = np.zeros(max(nvalid, 1), dtype=np.float64)
+        nnz = ctypes.c_int64(0)
+        st = lib().orc_csr_direct(self.M, self.N, gi.size, _ptr(gi), _ptr(gj), _ptr(gv),
+                                  _ptr(self.rowptr), _ptr(self.col), _ptr(self.val),
+                                  ctypes.byref(nnz))
+        if st == ORC_ERR_RANGE:
+            raise ValueError("orc_csr_direct: index out of range")
+        if st != ORC_OK:
+            raise ValueError("orc_csr_direct: COO not in CSR order without duplicates")
+        self.nnz = nnz.value
+
+    @classmethod
+    def from_oracle(cls, O, r=0):
+        """Rank r's diagonal-block CSR of an OracleMat with no off-diagonal block (P=1)."""
+        assert O.info(r, "nnz_o") == 0
+        C = cls.__new__(cls)
+        C.M = O.info(r, "rend") - O.info(r, "rstart")
+        C.N = O.info(r, "cend") - O.info(r, "cstart")
+        C.rowptr = O.export(r, "rowptr_d")
+        C.col = O.export(r, "col_d")
+        C.val = O.export(r, "val_d")
+        C.nnz = int(C.col.size)
+        return C
+
+    def mult(self, x, nthreads=1, out=None):
+        x = _np(x, np.float64)
+        assert x.size == self.N
+        y = out if out is not None else np.zeros(self.M, dtype=np.float64)
+        st = lib().orc_csr_mult(self.M, _ptr(self.rowptr), _ptr(self.col), _ptr(self.val),
+                                _ptr(x), _ptr(y), int(nthreads))
+        if st != ORC_OK:
+            raise ValueError(f"orc_csr_mult failed: {st}")
+        return y

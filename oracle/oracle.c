@@ -52,6 +52,7 @@
  * Multi-rank runs are simulated in-process: the oracle loops over ranks and moves data
  * between them by direct indexing (SURVEY.md §4 "Multi-rank without a cluster").
  */
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -622,18 +623,86 @@ int orc_sample_rows(int64_t ncoo, const int64_t *gi, const int64_t *gj, const do
 }
 
 /*
- * orc_dense_coo: the dense matrix of a COO (tiny grids only, brute force P6):
- * A[i*N + j] = +0.0 + sum over k ascending of v[k] for valid (i, j).
+ * orc_csr_direct: the COO definition A_ij = +0.0 + sum of v[k] (negatives ignored
+ * P:675-676, INSERT reading Z2) for the special case of a COO whose valid entries are already
+ * in CSR order with no duplicate positions: rows ascending, columns strictly ascending within
+ * a row -- the Listing-3 stencil COO is of this form.  Every nonzero then has
+ * exactly one contribution, so a_ij = +0.0 + v[k] and the CSR is the valid entries in input
+ * order.  This is the "direct CSR generation" of SURVEY.md §8(d) for matrices too large for
+ * the tuple sort of orc_create_coo (full-size oracle timing); any input not of that form is
+ * refused with ORC_ERR_ARG (never silently assembled), an index >= M or >= N with ORC_ERR_RANGE.
+ * rowptr: int64[M+1]; col: int64[>= valid entries]; val: f64[same]; *nnz_out = valid entries.
  */
-int orc_dense_coo(int64_t M, int64_t N, int64_t ncoo, const int64_t *gi, const int64_t *gj,
-                  const double *gv, double *A) {
-  for (int64_t t = 0; t < M * N; ++t) A[t] = +0.0;
+int orc_csr_direct(int64_t M, int64_t N, int64_t ncoo, const int64_t *gi, const int64_t *gj,
+                   const double *gv, int64_t *rowptr, int64_t *col, double *val, int64_t *nnz_out) {
+  int64_t nnz = 0, row = 0, last_i = -1, last_j = -1;
+  rowptr[0] = 0;
   for (int64_t k = 0; k < ncoo; ++k) {
     if (gi[k] < 0 || gj[k] < 0) continue;
     if (gi[k] >= M || gj[k] >= N) return ORC_ERR_RANGE;
-    A[gi[k] * N + gj[k]] = A[gi[k] * N + gj[k]] + gv[k];
+    if (gi[k] < last_i || (gi[k] == last_i && gj[k] <= last_j)) return ORC_ERR_ARG;
+    while (row < gi[k]) rowptr[++row] = nnz;  /* close rows up to gi[k] - 1 */
+    col[nnz] = gj[k];
+    val[nnz] = +0.0 + gv[k];
+    ++nnz;
+    last_i = gi[k];
+    last_j = gj[k];
   }
+  while (row < M) rowptr[++row] = nnz;
+  *nnz_out = nnz;
   return ORC_OK;
+}
+
+/*
+ * orc_csr_mult: y = A x for one rank's CSR with no off-diagonal block -- per row the same
+ * left-to-right sum from +0.0 of separately rounded products as orc_mult's S_d (O5), so the
+ * result is bit-identical to orc_mult.  nthreads > 1 splits the rows into nthreads contiguous
+ * slices, one POSIX thread each, every row still computed by that same serial loop (the
+ * "all host cores" leg of the oracle timed beside the GPU); the slicing
+ * cannot change any value.  Timing aid only: the checks use orc_mult.
+ */
+typedef struct {
+  int64_t r0, r1;
+  const int64_t *rowptr, *col;
+  const double *val, *x;
+  double *y;
+} orc_slice;
+
+static void *orc_csr_rows(void *arg) {
+  const orc_slice *s = (const orc_slice *)arg;
+  for (int64_t q = s->r0; q < s->r1; ++q) {
+    double sd = +0.0;
+    for (int64_t t = s->rowptr[q]; t < s->rowptr[q + 1]; ++t) {
+      double p = s->val[t] * s->x[s->col[t]];
+      sd = sd + p;
+    }
+    s->y[q] = sd;
+  }
+  return NULL;
+}
+
+int orc_csr_mult(int64_t m, const int64_t *rowptr, const int64_t *col, const double *val,
+                 const double *x, double *y, int nthreads) {
+  if (nthreads < 1 || nthreads > 4096) return ORC_ERR_ARG;
+  orc_slice *S = (orc_slice *)xcalloc((size_t)nthreads, sizeof(orc_slice));
+  pthread_t *T = (pthread_t *)xcalloc((size_t)nthreads, sizeof(pthread_t));
+  int st = ORC_OK, started = 0;
+  for (int t = 0; t < nthreads; ++t) {
+    S[t].r0 = m * t / nthreads;
+    S[t].r1 = m * (t + 1) / nthreads;
+    S[t].rowptr = rowptr; S[t].col = col; S[t].val = val; S[t].x = x; S[t].y = y;
+  }
+  if (nthreads == 1) {
+    orc_csr_rows(&S[0]);
+  } else {
+    for (int t = 0; t < nthreads; ++t) {
+      if (pthread_create(&T[t], NULL, orc_csr_rows, &S[t]) != 0) { st = ORC_ERR_OOM; break; }
+      ++started;
+    }
+    for (int t = 0; t < started; ++t) pthread_join(T[t], NULL);
+  }
+  free(T); free(S);
+  return st;
 }
 
 /* dot product, left to right from +0.0 (VecDot) */

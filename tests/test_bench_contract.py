@@ -22,6 +22,10 @@ def _check_line(out, n_gpus):
     assert "workload" in d["config"]
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
+    # 1 core and all cores, CPU model, affinity count, on the benchmarked matrix
+    assert cb["value_1core"] > 0 and cb["value_all_cores"] == cb["value"] and cb["cpu_model"]
+    assert cb["sched_getaffinity"] == cb["cores"] == len(os.sched_getaffinity(0))
+    assert cb["same_config"] is True and cb["rows"] == d["config"]["rows_global"]
     e = d["e2e"]
     assert e["value"] == d["value"] and e["unit"] == d["unit"]
     assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
@@ -37,7 +41,7 @@ def test_reference_arm_single_process():
 def test_reference_arm_torchrun_two_ranks():
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
                         "--master-addr=127.0.0.1", "--master-port=29702", os.path.join(ROOT, "bench.py"),
-                        "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1"],
+                        "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1", "--config", "c2"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     _check_line(r.stdout, 2)

@@ -463,6 +463,87 @@ def test_sample_rows_matches_full_p1():
     assert np.array_equal(oracle.sample_rows(i, j, v, rows, x), A.mult(x)[rows])
 
 
+@pytest.mark.parametrize("shape,npts", [((64, 64), 5), ((9, 7, 6), 7), ((7, 7, 7), 125), ((11, 3, 5), 27)])
+def test_csr_direct_equals_coo_assembly(shape, npts):
+    """orc_csr_direct (the full-size timing path) is the COO definition specialised to
+    duplicate-free, row-sorted COO: its CSR equals orc_create_coo + INSERT bit for bit, the
+    numpy scatter-add brute force, and the stencil A.1 closed form (out-of-grid counts)."""
+    M = int(np.prod(shape))
+    for values in ("int", "real"):
+        A, ii, jj, vv = build_stencil(shape, npts, values=values)
+        C = oracle.OracleCsr(M, M, ii[0], jj[0], vv[0])
+        assert C.nnz == A.info(0, "nnz_d")
+        assert np.array_equal(C.rowptr, A.export(0, "rowptr_d"))
+        assert np.array_equal(C.col[:C.nnz], A.export(0, "col_d"))
+        assert np.array_equal(C.val[:C.nnz].view(np.int64), A.export(0, "val_d").view(np.int64))
+        x = synth.x_vector(0, M, values).numpy()
+        assert np.array_equal(C.mult(x).view(np.int64), A.mult(x).view(np.int64))
+        if M <= 500:
+            D = numpy_dense(M, M, ii, jj, vv)
+            dense = np.zeros((M, M))
+            for q in range(M):
+                dense[q, C.col[C.rowptr[q]:C.rowptr[q + 1]]] = C.val[C.rowptr[q]:C.rowptr[q + 1]]
+            assert np.array_equal(dense, D)
+    # A.1 closed form on the integer stencil: number of out-of-grid neighbours (P3)
+    A, ii, jj, vv = build_stencil(shape, npts, values="int")
+    C = oracle.OracleCsr(M, M, ii[0], jj[0], vv[0])
+    offs = synth.stencil_offsets(len(shape), npts)
+    g = np.arange(M)
+    coords, rem = [], g
+    for n in shape:
+        coords.append(rem % n)
+        rem = rem // n
+    out = np.zeros(M)
+    for o in offs:
+        inside = np.ones(M, dtype=bool)
+        for d, n in enumerate(shape):
+            c = coords[d] + o[d]
+            inside &= (c >= 0) & (c < n)
+        out += ~inside
+    assert np.array_equal(C.mult(np.ones(M)), out)
+
+
+def test_csr_direct_refuses_other_coo():
+    """Duplicates or unsorted entries are refused (ValueError), never assembled silently;
+    negatives are skipped; out-of-range indices raise."""
+    i, j, v = synth.q1_coo(4, values="real")  # element COO: duplicate positions
+    with pytest.raises(ValueError):
+        oracle.OracleCsr(64, 64, i, j, v)
+    with pytest.raises(ValueError):
+        oracle.OracleCsr(3, 3, np.array([0, 1, 0]), np.array([0, 0, 1]), np.ones(3))
+    with pytest.raises(ValueError):
+        oracle.OracleCsr(3, 3, np.array([0, 0]), np.array([2, 1]), np.ones(2))
+    with pytest.raises(ValueError):
+        oracle.OracleCsr(3, 3, np.array([0, 3]), np.array([0, 0]), np.ones(2))
+    C = oracle.OracleCsr(4, 4, np.array([-1, 0, 2, 2, 3]), np.array([0, 1, -5, 3, 0]),
+                         np.array([9.0, -0.0, 7.0, 2.0, 3.0]))
+    assert C.nnz == 3 and list(C.rowptr) == [0, 1, 1, 2, 3]
+    assert list(C.col[:3]) == [1, 3, 0]
+    assert C.val[0] == 0.0 and not np.signbit(C.val[0])  # INSERT: +0.0 + (-0.0) = +0.0 (Z2)
+
+
+@pytest.mark.parametrize("nthreads", [1, 2, 3, 8, 64])
+def test_csr_mult_threads_bit_identical(nthreads):
+    """The all-cores oracle leg (row slices over POSIX threads) gives orc_mult's y bit for bit,
+    also with more threads than rows."""
+    for shape, npts in (((20, 17, 9), 7), ((5, 3), 5), ((6, 6, 6), 27)):
+        M = int(np.prod(shape))
+        A, ii, jj, vv = build_stencil(shape, npts, values="real")
+        C = oracle.OracleCsr(M, M, ii[0], jj[0], vv[0])
+        x = synth.x_vector(0, M, "real").numpy()
+        want = A.mult(x)
+        assert np.array_equal(C.mult(x, nthreads=nthreads).view(np.int64), want.view(np.int64))
+    # element COO (duplicates) through the general assembly, then the threaded row loop
+    i, j, v = synth.q1_coo(6, values="real")
+    A = oracle.OracleMat(216, 216, [216], [216], [i], [j])
+    A.set_values([v])
+    C = oracle.OracleCsr.from_oracle(A)
+    x = synth.x_vector(0, 216, "real").numpy()
+    assert np.array_equal(C.mult(x, nthreads=nthreads).view(np.int64), A.mult(x).view(np.int64))
+    with pytest.raises(ValueError):
+        C.mult(x, nthreads=0)
+
+
 def test_spec_sf_reduce_examples():
     g = _parse_golden("spec_sf_examples.txt")
     t = g["reduce_pingpong_sum"].split()
