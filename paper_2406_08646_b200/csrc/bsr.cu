@@ -273,6 +273,9 @@ int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s) {
 
 static int bsr_setup(spmat_s *A) {
   cudaStream_t st = A->comm->setup_stream;
+  // the caller's spmat_set_values_coo may still be writing val_d on its own stream, and this
+  // (host-synchronising) call reads the CSR on the setup stream: wait for the device first
+  SP_CUDA(cudaDeviceSynchronize());
   const int64_t mb = A->m / 3;
   DevBuf<int> bad;
   SP_TRY(bad.alloc(1));
@@ -324,11 +327,7 @@ static int bsr_setup(spmat_s *A) {
   }
   SP_TRY(A->bsched.alloc(2));
   SP_CUDA(cudaMemsetAsync(A->bsched.get(), 0, 8, st));
-  static bool attr = false;
-  if (!attr) {
-    SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
-    attr = true;
-  }
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
   int per_sm = 0;
   SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_bsr3, kCtaT, kBsrSmem));
   A->bsr_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * A->comm->num_sms,

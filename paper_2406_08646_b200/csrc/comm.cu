@@ -119,6 +119,14 @@ int Comm::allreduce_max_i64(int64_t *v, int64_t count) {
   return SPMAT_OK;
 }
 
+int Comm::agree(int local_status, const char *what) {
+  int64_t v = local_status;
+  SP_TRY(allreduce_max_i64(&v, 1));
+  if (v == SPMAT_OK) return SPMAT_OK;
+  if (local_status != SPMAT_OK) return local_status;
+  return fail((int)v, "%s: failed on another rank (status %lld)", what, (long long)v);
+}
+
 int Comm::exchange_dev(const void *d_send, const int64_t *soff, const int64_t *scount,
                        void *d_recv, const int64_t *roff, const int64_t *rcount,
                        size_t elem_bytes, cudaStream_t stream) {

@@ -353,51 +353,63 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
                 "spmat_create_coo: ranks disagree on M,N or local sizes do not sum (M=%lld N=%lld)",
                 (long long)M, (long long)N);
   const int64_t rstart = roff[me], cstart = coff[me], cend = coff[me + 1];
-  if (m_local > INT32_MAX - 1) return fail(SPMAT_ERR_ARG, "m_local must be < 2^31");
+  // Errors found on one rank only are agreed on (Comm::agree) before the next collective, so
+  // every rank returns an error instead of the others blocking in NCCL.
+  const char *who = "spmat_create_coo";
 
   Tmp tmp;
   // ---- inputs on the device (memtype detection); not retained
   DevBuf<int64_t> di, dj;
   const int64_t *ci = coo_i, *cj = coo_j;
-  // device COO arrays may still be being written by the caller's kernels on any stream, and
-  // this (host-synchronising) call reads them on the library's setup stream: wait for the
-  // device first
-  SP_CUDA(cudaDeviceSynchronize());
-  if (ncoo > 0) {
-    if (!coo_i || !coo_j) return fail(SPMAT_ERR_ARG, "spmat_create_coo: null coo_i/coo_j");
-    if (!is_device_ptr(coo_i)) {
-      SP_TRY(di.alloc(ncoo));
-      SP_CUDA(cudaMemcpyAsync(di.get(), coo_i, ncoo * 8, cudaMemcpyHostToDevice, st));
-      ci = di.get();
+  SP_TRY(c->agree([&]() -> int {
+    if (m_local > INT32_MAX - 1) return fail(SPMAT_ERR_ARG, "m_local must be < 2^31");
+    if ((uint64_t)ncoo >= (1ull << 32)) return fail(SPMAT_ERR_ARG, "ncoo must be < 2^32");
+    // device COO arrays may still be being written by the caller's kernels on any stream, and
+    // this (host-synchronising) call reads them on the library's setup stream: wait for the
+    // device first
+    SP_CUDA(cudaDeviceSynchronize());
+    if (ncoo > 0) {
+      if (!coo_i || !coo_j) return fail(SPMAT_ERR_ARG, "spmat_create_coo: null coo_i/coo_j");
+      if (!is_device_ptr(coo_i)) {
+        SP_TRY(di.alloc(ncoo));
+        SP_CUDA(cudaMemcpyAsync(di.get(), coo_i, ncoo * 8, cudaMemcpyHostToDevice, st));
+        ci = di.get();
+      }
+      if (!is_device_ptr(coo_j)) {
+        SP_TRY(dj.alloc(ncoo));
+        SP_CUDA(cudaMemcpyAsync(dj.get(), coo_j, ncoo * 8, cudaMemcpyHostToDevice, st));
+        cj = dj.get();
+      }
     }
-    if (!is_device_ptr(coo_j)) {
-      SP_TRY(dj.alloc(ncoo));
-      SP_CUDA(cudaMemcpyAsync(dj.get(), coo_j, ncoo * 8, cudaMemcpyHostToDevice, st));
-      cj = dj.get();
-    }
-  }
-  if ((uint64_t)ncoo >= (1ull << 32)) return fail(SPMAT_ERR_ARG, "ncoo must be < 2^32");
+    return SPMAT_OK;
+  }(), who));
 
   // ---- 1. classify
   DevBuf<int64_t> droff;
-  SP_TRY(droff.alloc(P + 1));
-  SP_CUDA(cudaMemcpyAsync(droff.get(), roff.data(), (P + 1) * 8, cudaMemcpyHostToDevice, st));
   DevBuf<unsigned long long> dbad;
-  SP_TRY(dbad.alloc(1));
-  SP_CUDA(cudaMemsetAsync(dbad.get(), 0xff, 8, st));
   DevBuf<uint32_t> dest, dest2, kk, kk2;
-  SP_TRY(dest.alloc(ncoo));
-  if (ncoo > 0) {
-    k_classify<<<nblk(ncoo), 256, 0, st>>>(ci, cj, ncoo, M, N, droff.get(), P, dest.get(), dbad.get());
-    SP_LAUNCH();
-  }
   unsigned long long bad = ~0ull;
-  SP_CUDA(cudaMemcpyAsync(&bad, dbad.get(), 8, cudaMemcpyDeviceToHost, st));
-  SP_CUDA(cudaStreamSynchronize(st));
-  {
-    int64_t b = bad == ~0ull ? -1 : (int64_t)bad;
+  const int sB = [&]() -> int {
+    SP_TRY(droff.alloc(P + 1));
+    SP_CUDA(cudaMemcpyAsync(droff.get(), roff.data(), (P + 1) * 8, cudaMemcpyHostToDevice, st));
+    SP_TRY(dbad.alloc(1));
+    SP_CUDA(cudaMemsetAsync(dbad.get(), 0xff, 8, st));
+    SP_TRY(dest.alloc(ncoo));
+    if (ncoo > 0) {
+      k_classify<<<nblk(ncoo), 256, 0, st>>>(ci, cj, ncoo, M, N, droff.get(), P, dest.get(), dbad.get());
+      SP_LAUNCH();
+    }
+    SP_CUDA(cudaMemcpyAsync(&bad, dbad.get(), 8, cudaMemcpyDeviceToHost, st));
+    SP_CUDA(cudaStreamSynchronize(st));
+    return SPMAT_OK;
+  }();
+  {  // the range-error exchange also carries the local status (-2 - status)
+    int64_t b = sB != SPMAT_OK ? -2 - (int64_t)sB : (bad == ~0ull ? -1 : (int64_t)bad);
     std::vector<int64_t> allbad(P);
     SP_TRY(c->allgather_i64(&b, 1, allbad.data()));
+    for (int r = 0; r < P; ++r)
+      if (allbad[r] <= -2)
+        return sB != SPMAT_OK ? sB : fail((int)(-2 - allbad[r]), "%s: failed on rank %d", who, r);
     for (int r = 0; r < P; ++r)
       if (allbad[r] >= 0)
         return fail(SPMAT_ERR_RANGE, "spmat_create_coo: COO index out of range on rank %d at k=%lld",
@@ -405,10 +417,15 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
   }
 
   // ---- 2. stable sort (dest, k) -> per-destination k lists
+  std::vector<int64_t> dofs(P + 2, 0);
+  int64_t nlocal = 0;
+  spmat_s *A = new spmat_s();
+  std::unique_ptr<spmat_s, int (*)(spmat_s *)> guard(A, [](spmat_s *a) { return spmat_destroy(a); });
+  A->comm = c;
+  const int sC = [&]() -> int {
   SP_TRY(kk.alloc(ncoo));
   SP_TRY(kk2.alloc(ncoo));
   SP_TRY(dest2.alloc(ncoo));
-  std::vector<int64_t> dofs(P + 2, 0);
   if (ncoo > 0) {
     k_iota<<<nblk(ncoo), 256, 0, st>>>(kk.get(), ncoo);
     SP_LAUNCH();
@@ -427,14 +444,11 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
   kk2.release();
   dest.release();
   dest2.release();
-  spmat_s *A = new spmat_s();
-  std::unique_ptr<spmat_s, int (*)(spmat_s *)> guard(A, [](spmat_s *a) { return spmat_destroy(a); });
-  A->comm = c;
   A->M = M; A->N = N; A->m = m_local; A->n = n_local;
   A->rstart = rstart; A->rend = roff[me + 1]; A->cstart = cstart; A->cend = cend;
   A->roff = roff; A->coff = coff;
   A->ncoo = ncoo;
-  const int64_t nlocal = dofs[me + 1] - dofs[me];
+  nlocal = dofs[me + 1] - dofs[me];
   A->send_count.assign(P, 0);
   A->send_off.assign(P + 1, 0);
   for (int d = 0; d < P; ++d) A->send_count[d] = d == me ? 0 : dofs[d + 1] - dofs[d];
@@ -446,32 +460,46 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
   if (dofs[P] - dofs[me + 1] > 0)
     SP_CUDA(cudaMemcpyAsync(A->sendperm.get() + dofs[me], kk.get() + dofs[me + 1],
                             (dofs[P] - dofs[me + 1]) * 4, cudaMemcpyDeviceToDevice, st));
+  return SPMAT_OK;
+  }();
 
   // ---- 3. exchange (i, j) of off-rank entries
-  {
-    std::vector<int64_t> allc((size_t)P * P);
-    SP_TRY(c->allgather_i64(A->send_count.data(), P, allc.data()));
+  {  // the count exchange also carries the local status (last element)
+    std::vector<int64_t> mine(P + 1, 0), allc((size_t)P * (P + 1));
+    if (sC == SPMAT_OK)
+      for (int d = 0; d < P; ++d) mine[d] = A->send_count[d];
+    mine[P] = sC;
+    SP_TRY(c->allgather_i64(mine.data(), P + 1, allc.data()));
+    for (int r = 0; r < P; ++r)
+      if (allc[(size_t)r * (P + 1) + P] != SPMAT_OK)
+        return sC != SPMAT_OK ? sC : fail((int)allc[(size_t)r * (P + 1) + P], "%s: failed on rank %d", who, r);
     A->recv_count.assign(P, 0);
     A->recv_off.assign(P + 1, 0);
-    for (int s = 0; s < P; ++s) A->recv_count[s] = s == me ? 0 : allc[(size_t)s * P + me];
+    for (int s = 0; s < P; ++s) A->recv_count[s] = s == me ? 0 : allc[(size_t)s * (P + 1) + me];
     for (int s = 0; s < P; ++s) A->recv_off[s + 1] = A->recv_off[s] + A->recv_count[s];
     A->nrecv = A->recv_off[P];
   }
-  if ((uint64_t)ncoo + (uint64_t)A->nrecv >= (1ull << 32))
-    return fail(SPMAT_ERR_ARG, "ncoo + received entries must be < 2^32");
   DevBuf<longlong2> sij, rij;
-  SP_TRY(sij.alloc(A->nsend));
-  SP_TRY(rij.alloc(A->nrecv));
-  if (A->nsend > 0) {
-    k_gather_ij<<<nblk(A->nsend), 256, 0, st>>>(ci, cj, A->sendperm.get(), A->nsend, sij.get());
-    SP_LAUNCH();
-  }
+  SP_TRY(c->agree([&]() -> int {
+    if ((uint64_t)ncoo + (uint64_t)A->nrecv >= (1ull << 32))
+      return fail(SPMAT_ERR_ARG, "ncoo + received entries must be < 2^32");
+    SP_TRY(sij.alloc(A->nsend));
+    SP_TRY(rij.alloc(A->nrecv));
+    if (A->nsend > 0) {
+      k_gather_ij<<<nblk(A->nsend), 256, 0, st>>>(ci, cj, A->sendperm.get(), A->nsend, sij.get());
+      SP_LAUNCH();
+    }
+    return SPMAT_OK;
+  }(), who));
   SP_TRY(c->exchange_dev(sij.get(), A->send_off.data(), A->send_count.data(), rij.get(),
                          A->recv_off.data(), A->recv_count.data(), sizeof(longlong2), st));
   sij.release();
 
   // ---- 4. canonical contributions, keyed (row, col), stable radix sort
   const int64_t nt = nlocal + A->nrecv;
+  std::vector<int64_t> cm, off;
+  std::vector<int32_t> own;
+  SP_TRY(c->agree([&]() -> int {
   if (nt >= INT32_MAX) return fail(SPMAT_ERR_ARG, "more than 2^31 contributions on one rank");
   A->ncontrib = nt;
   DevBuf<uint64_t> key, key2;
@@ -683,8 +711,9 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
 
   // ---- 6. halo SF from colmap: leaf g -> (owner(colmap[g]), colmap[g] - cstart_owner)
   {
-    std::vector<int64_t> cm(A->n_ghost), off(A->n_ghost);
-    std::vector<int32_t> own(A->n_ghost);
+    cm.resize(A->n_ghost);
+    off.resize(A->n_ghost);
+    own.resize(A->n_ghost);
     if (A->n_ghost)
       SP_CUDA(cudaMemcpyAsync(cm.data(), A->colmap.get(), A->n_ghost * 8, cudaMemcpyDeviceToHost, st));
     SP_CUDA(cudaStreamSynchronize(st));
@@ -693,9 +722,11 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
       own[g] = q;
       off[g] = cm[g] - coff[q];
     }
-    SP_TRY(sf_build(c, n_local, A->n_ghost, nullptr, own.data(), off.data(), &A->halo));
   }
-  SP_TRY(spmv_prepare(A, st));
+  return SPMAT_OK;
+  }(), who));
+  SP_TRY(sf_build(c, n_local, A->n_ghost, nullptr, own.data(), off.data(), &A->halo));
+  SP_TRY(c->agree(spmv_prepare(A, st), who));
   SP_TRY(halo_peer_setup(A));
   SP_CUDA(cudaStreamSynchronize(st));
   A->plan_builds = 1;

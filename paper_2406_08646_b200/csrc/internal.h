@@ -121,6 +121,23 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   cfg.numAttrs = pdl_on() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
+// Cooperative launch: every CTA of the grid is resident at once, or the launch fails (instead of
+// CTAs that spin on peer data waiting for CTAs that other work keeps off the SMs).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                               cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
 
 // is `p` a device (or managed) pointer?
 bool is_device_ptr(const void *p);
@@ -137,6 +154,10 @@ struct Comm {
   // Collectives used by setup (host-synchronising).  All operate on host arrays.
   int allgather_i64(const int64_t *send, int64_t count, int64_t *recv_host);  // recv: count*P
   int allreduce_max_i64(int64_t *v, int64_t count);
+  // Agree on a status found locally before the next collective: every rank returns an error
+  // (its own, or "failed on another rank") if any rank failed, instead of the others
+  // blocking in NCCL.  Collective, host-synchronising.
+  int agree(int local_status, const char *what);
   // Exchange variable-size int64 payloads (host-side counts known on both sides):
   // send[d] of scount[d] elements to d, recv from s of rcount[s] elements; device buffers.
   int exchange_dev(const void *d_send, const int64_t *soff, const int64_t *scount,
@@ -330,6 +351,10 @@ struct spmat_s {
   std::vector<cudaEvent_t> prof_ev[3];  // pairs per kind
   size_t prof_n[3] = {0, 0, 0};
   int64_t plan_builds = 0;
+  // environment switches, read when the matrix is created (not process-wide statics)
+  bool env_no_fuse = false;     // SPMAT_FUSE=0: standalone put kernel instead of the fused puts
+  bool env_no_tail = false;     // SPMAT_FUSE_TAIL=0: off-diagonal add as its own kernel
+  int env_pipe_chunks = 16;     // SPMAT_PIPE_CHUNKS: row chunks of the host-buffer pipeline
   // device-initiated halo over NVLink peer memory (halo.cu)
   bool peer = false;
   spmat::DevBuf<unsigned long long> halo_flags;  // [q]: done flag from receiver q

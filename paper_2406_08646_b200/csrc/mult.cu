@@ -37,8 +37,7 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
       // (only k_spmv_tma has comm warps: a comm-warp variant of the 3x3 block kernel capped it
       // at 64 registers and lost more on the stream than the overlap gained -- C5 P=2 1.43 ms
       // either way, P=1 -2 %)
-      static const bool no_fuse = getenv("SPMAT_FUSE") && !strcmp(getenv("SPMAT_FUSE"), "0");
-      fused = !no_fuse && (part & 1) && A->kernel_id == 3 && A->m > 0 && A->n_rowblocks > 0;
+      fused = !A->env_no_fuse && (part & 1) && A->kernel_id == 3 && A->m > 0 && A->n_rowblocks > 0;
       if (!fused) {
         pe = A->profile ? prof_pair(A, 2) : nullptr;
         if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
@@ -47,8 +46,7 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
       }
     }
     // full MatMult, no long rows: the off-diagonal SpMV-add runs in the same kernel's tail
-    static const bool no_tail = getenv("SPMAT_FUSE_TAIL") && !strcmp(getenv("SPMAT_FUSE_TAIL"), "0");
-    const bool tail = fused && (part & 4) && A->n_ro > 0 && A->n_long == 0 && !no_tail;
+    const bool tail = fused && (part & 4) && A->n_ro > 0 && A->n_long == 0 && !A->env_no_tail;
     if (part & 1) {
       pe = A->profile ? prof_pair(A, 0) : nullptr;
       if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
@@ -103,12 +101,7 @@ static bool pipeline_ok(spmat_s *A) {
 }
 
 static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStream_t s) {
-  static const int C = [] {
-    const char *e = getenv("SPMAT_PIPE_CHUNKS");
-    const int c = e ? atoi(e) : 0;
-    return c >= 2 && c <= 256 ? c : 16;
-  }();
-  SP_TRY(spmv_pipe_prepare(A, C));
+  SP_TRY(spmv_pipe_prepare(A, A->env_pipe_chunks));
   const int nc = A->pipe_chunks;
   const bool multi = A->comm->nranks > 1;
   if (!A->pipe_in) {

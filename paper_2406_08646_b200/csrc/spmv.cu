@@ -430,11 +430,8 @@ static int lanes_for(double mean) {  // W lanes per row from the mean row length
 }
 
 static int tma_setup(spmat_s *A) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    SP_CUDA(cudaFuncSetAttribute(k_spmv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-    attr_set = true;
-  }
+  // per device (the attribute belongs to the current device's context): set at every setup
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
   int per_sm = 0;
   SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_tma, kCtaThreads, kTmaSmem));
   // SPMAT_RESERVE_SMS leaves SMs free for concurrently running kernels (e.g. NCCL's)
@@ -453,6 +450,15 @@ static int tma_setup(spmat_s *A) {
 
 int spmv_prepare(spmat_s *A, cudaStream_t st) {
   const int64_t m = A->m, nnz = A->nnz_d;
+  {
+    const char *e = getenv("SPMAT_FUSE");
+    A->env_no_fuse = e && !strcmp(e, "0");
+    e = getenv("SPMAT_FUSE_TAIL");
+    A->env_no_tail = e && !strcmp(e, "0");
+    e = getenv("SPMAT_PIPE_CHUNKS");
+    const int c = e ? atoi(e) : 0;
+    A->env_pipe_chunks = c >= 2 && c <= 256 ? c : 16;
+  }
   A->kernel_id = KERNEL_TMA;
   const char *env = getenv("SPMAT_SPMV_KERNEL");
   if (env && !strcmp(env, "vector")) A->kernel_id = KERNEL_VECTOR;
@@ -590,6 +596,10 @@ static cudaError_t launch_tma(spmat_s *A, const double *x, double *y, cudaStream
     t.ctr = A->tail_ctr.get();
   }
   const unsigned grid = (unsigned)(fuse_tail ? A->tma_grid_tail : A->tma_grid);
+  if (fuse_tail)  // comm warps spin on lines written by the peers' CTAs: all CTAs co-resident
+    return launch_coop(k_spmv_tma, grid, kCtaThreads, kTmaSmem, s, (const int4 *)A->blocks4.get(),
+                       (int)A->n_rowblocks, (const int32_t *)A->rowptr_d.get(), (const int32_t *)A->col_d.get(),
+                       (const double *)A->val_d.get(), x, y, A->sched.get(), h, t);
   return launch_pdl(k_spmv_tma, grid, kCtaThreads, kTmaSmem, s, (const int4 *)A->blocks4.get(),
                     (int)A->n_rowblocks, (const int32_t *)A->rowptr_d.get(), (const int32_t *)A->col_d.get(),
                     (const double *)A->val_d.get(), x, y, A->sched.get(), h, t);

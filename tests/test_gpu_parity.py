@@ -363,26 +363,133 @@ def test_determinism(sp, comm):
     A.close()
 
 
-@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
-def test_full_size_sampled(sp, comm, cfg):
-    """Full BASELINE sizes in the bench launch configuration: sampled rows vs the oracle
-    computed one by one from the COO definition, plus A.1 over every row."""
-    i, j, v, sizes = synth.config_rank_coo(cfg, 1, 0, values="real", device="cuda")
+def _grid_coords(M, shape, dof=1):
+    """Node coordinates (fastest axis first) of every row, on the device."""
+    g = torch.arange(M, device="cuda") // dof
+    out = []
+    for n in shape:
+        out.append(g % n)
+        g = g // n
+    return out
+
+
+def closed_form_a1(cfg, M):
+    """A.1 of the integer-valued config matrix over EVERY row:
+    7-point stencil: number of out-of-grid neighbours; Q1 mass x216 element assembly:
+    27 * prod_d (interior_d ? 2 : 1); 3-dof Kronecker K27 (x) B3: 6 * prod_d (4 + n_d), n_d the
+    node's in-grid neighbours along d."""
+    c = synth.CONFIGS[cfg]
+    if c["kind"] == "stencil":
+        shape = synth.config_shape(cfg, 1)
+        return sum(((x == 0).double() + (x == n - 1).double())
+                   for x, n in zip(_grid_coords(M, shape), shape))
+    n = c["n"]
+    if c["kind"] == "q1":
+        w = torch.ones(M, dtype=torch.float64, device="cuda") * 27
+        for x in _grid_coords(M, (n, n, n)):
+            w = w * torch.where((x > 0) & (x < n - 1), 2.0, 1.0).double()
+        return w
+    w = torch.ones(M, dtype=torch.float64, device="cuda") * 6
+    for x in _grid_coords(M, (n, n, n), dof=3):
+        w = w * (4 + (x > 0).double() + (x < n - 1).double())
+    return w
+
+
+FULL = [("c2", 1), ("c3", 1), ("c4", 1), ("c5", 1), ("c5", 3)]
+
+
+@pytest.mark.parametrize("cfg,bs", FULL)
+def test_full_size(sp, comm, cfg, bs):
+    """BASELINE configs at full size in the bench's launch configuration (persistent grid,
+    every CTA wrapping its stage ring many times; C5 at 1.94 G COO entries, 1.92 G nonzeros,
+    close to the int32 / 2^32 limits of the plan):
+    * integer values: nnz closed form, and A.1 over EVERY row equal to the closed form
+      (exact arithmetic, so bit-exact);
+    * real values: sampled rows against the oracle computed one by one from the COO
+      definition (oracle.sample_rows), relative max-norm <= 1e-12."""
+    i, j, v, sizes = synth.config_rank_coo(cfg, 1, 0, values="int", device="cuda")
     M = sizes[0]
     A = sp.Mat(comm, M, M, M, M, i, j)
+    del i, j
+    if bs == 3:
+        A.set_block_size(3)
     A.set_values(v)
-    x = synth.x_vector(0, M, "real", device="cuda")
+    del v
+    torch.cuda.empty_cache()
+    nnz_want = {"c2": 7 * 128 ** 3 - 6 * 128 ** 2, "c3": (3 * 160 - 2) ** 3,
+                "c4": 7 * 256 ** 3 - 6 * 256 ** 2, "c5": 9 * (3 * 200 - 2) ** 3}[cfg]
+    info = A.info()
+    assert info["nnz_d"] == nnz_want and info["nnz_o"] == 0
+    assert info["spmv_kernel_id"] == (4 if bs == 3 else 3)
     y = torch.empty(M, dtype=torch.float64, device="cuda")
+    A.mult(torch.ones(M, dtype=torch.float64, device="cuda"), y)
+    want = closed_form_a1(cfg, M)
+    bad = torch.nonzero(y != want)
+    assert bad.numel() == 0, f"{bad.numel()} rows differ, first {bad[:5].flatten().tolist()}"
+    del want
+    # real values: refresh the values (same plan) and compare sampled rows with the oracle
+    _, _, v, _ = synth.config_rank_coo(cfg, 1, 0, values="real", device="cuda")
+    A.set_values(v)
+    del v
+    torch.cuda.empty_cache()
+    x = synth.x_vector(0, M, "real", device="cuda")
     A.mult(x, y)
-    rows = torch.unique(torch.cat([torch.randint(0, M, (1500,), generator=torch.Generator().manual_seed(5)),
-                                   torch.tensor([0, 1, M // 2, M - 2, M - 1])]))
-    if cfg in ("c2", "c4"):
+    xh = x.cpu().numpy()
+    c = synth.CONFIGS[cfg]
+    if c["kind"] == "stencil":
+        rows = torch.unique(torch.cat([torch.randint(0, M, (1500,), generator=torch.Generator().manual_seed(5)),
+                                       torch.tensor([0, 1, M // 2, M - 2, M - 1])]))
         ih, jh, vh = synth.stencil_coo(synth.config_shape(cfg, 1), 7, rows=rows, values="real")
-    else:
-        ih, jh, vh = i.cpu(), j.cpu(), v.cpu()
-    ys = oracle.sample_rows(ih, jh, vh, rows.numpy(), x.cpu().numpy())
+        ys = oracle.sample_rows(ih, jh, vh, rows.numpy(), xh)
+    elif c["kind"] == "q1":  # the elements touching the sampled rows' nodes
+        n = c["n"]
+        nodes = torch.unique(torch.cat([torch.randint(0, M, (300,), generator=torch.Generator().manual_seed(5)),
+                                        torch.tensor([0, M // 2, M - 1])]))
+        ix, iy, iz = nodes % n, (nodes // n) % n, nodes // (n * n)
+        el = []
+        for dz in (0, 1):
+            for dy in (0, 1):
+                for dx in (0, 1):
+                    ex, ey, ez = ix - dx, iy - dy, iz - dz
+                    ok = (ex >= 0) & (ex < n - 1) & (ey >= 0) & (ey < n - 1) & (ez >= 0) & (ez < n - 1)
+                    el.append((ex + (n - 1) * (ey + (n - 1) * ez))[ok])
+        elems = torch.unique(torch.cat(el))
+        ih, jh, vh = synth.q1_coo(n, elems=elems, variant="mass", values="real")
+        rows = nodes
+        ys = oracle.sample_rows(ih, jh, vh, rows.numpy(), xh)
+    else:  # node windows at the start, middle and end of the matrix
+        n = c["n"]
+        N = n ** 3
+        parts_i, parts_j, parts_v, rws = [], [], [], []
+        for a0 in (0, 40_000, N // 2 - 17, N - 64 * n - 5, N - 64):
+            ih, jh, vh = synth.elasticity_coo(n, nodes=(a0, a0 + 64), values="real")
+            parts_i.append(ih); parts_j.append(jh); parts_v.append(vh)
+            rws.append(torch.arange(3 * a0, 3 * (a0 + 64)))
+        rows = torch.unique(torch.cat(rws))
+        ys = oracle.sample_rows(torch.cat(parts_i), torch.cat(parts_j), torch.cat(parts_v), rows.numpy(), xh)
     assert rel_err(y[rows.cuda()].cpu().numpy(), ys) <= TOL
-    del i, j, v
+    A.close()
+    del x, y
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("values", ["int", "real"])
+def test_every_row_many_blocks_per_cta(sp, comm, values):
+    """~900 k rows (~3.4 k row blocks: several per persistent CTA, so every CTA wraps its
+    2-stage ring and flips the mbarrier parities) compared with the full oracle on EVERY row."""
+    shape = (96, 96, 96)
+    M = 96 ** 3
+    i, j, v = synth.stencil_coo(shape, 7, values=values)
+    O = oracle.OracleMat(M, M, [M], [M], [i], [j])
+    O.set_values([v])
+    x = synth.x_vector(0, M, values)
+    A, y = run_single(sp, comm, M, M, i, j, v, x)
+    assert A.info()["spmv_kernel_id"] == 3
+    yo = O.mult(x.numpy())
+    if values == "int":
+        assert np.array_equal(canon(y), canon(yo))
+    else:
+        assert rel_err(y, yo) <= TOL
     A.close()
 
 
