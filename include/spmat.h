@@ -194,8 +194,14 @@ int spmat_mult_part(spmat_t A, const double *x, double *y, int part, void *strea
 
 /* info[0..15] = rstart, rend, cstart, cend, nnz_d, nnz_o, n_ghost, n_offdiag_rows,
    n_contrib, n_send (COO entries sent), n_recv (COO entries received), n_mixed (nonzeros
-   with received contributions), spmv_kernel_id, n_rowblocks, max_row_nnz, plan_builds */
-int spmat_get_info(spmat_t A, int64_t info[16]);
+   with received contributions), spmv_kernel_id, n_rowblocks, max_row_nnz, plan_builds;
+   info[16..31] = block_size, offdiag_3x3 (1: the off-diagonal block is kept in 3x3 blocks
+   too), offdiag_lanes, halo_mode (0 one rank, 1 NCCL, 2 NVLink stores), and cumulative
+   counters since create (host-side, counted when work is enqueued): nccl_bytes_sent,
+   nccl_bytes_recv (COO value exchange + NCCL-mode halo), nvlink_bytes_put (halo lines stored
+   into peers: 16 B per value), n_mult, n_set_values, then spmv_grid, offdiag_grid, 0...
+   The caller provides 32 entries. */
+int spmat_get_info(spmat_t A, int64_t info[32]);
 
 /* Test hook: copy a device array to host.  All integer arrays are returned as int64.
      0 rowptr_d[m+1]   1 col_d (local)   2 val_d (f64)   3 rowptr_o[m+1] (full rows)

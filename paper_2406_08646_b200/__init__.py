@@ -42,7 +42,9 @@ EXPORT = dict(rowptr_d=0, col_d=1, val_d=2, rowptr_o=3, col_o=4, val_o=5, colmap
               csrc=8, cpos=9, send_count=10, send_k=11, recv_count=12, rows_o=13)
 INFO_KEYS = ("rstart", "rend", "cstart", "cend", "nnz_d", "nnz_o", "n_ghost", "n_offdiag_rows",
              "n_contrib", "n_send", "n_recv", "n_mixed", "spmv_kernel_id", "n_rowblocks",
-             "max_row_nnz", "plan_builds")
+             "max_row_nnz", "plan_builds", "block_size", "offdiag_3x3", "offdiag_lanes", "halo_mode",
+             "nccl_bytes_sent", "nccl_bytes_recv", "nvlink_bytes_put", "n_mult", "n_set_values",
+             "spmv_grid", "offdiag_grid")
 SF_INFO_KEYS = ("nroots", "nleaves", "n_send_nbr", "n_recv_nbr", "n_send", "n_recv", "n_self",
                 "packed")
 SF_EXPORT = dict(recv_ranks=0, recv_counts=1, leaf_idx=2, send_ranks=3, send_counts=4,
@@ -253,7 +255,7 @@ def spmat_mult_part(A_h, x, y, part, stream=None):
 
 
 def spmat_get_info(A_h) -> dict:
-    a = np.zeros(16, dtype=np.int64)
+    a = np.zeros(32, dtype=np.int64)
     _check(load().spmat_get_info(A_h, _ptr(a)), "spmat_get_info")
     return dict(zip(INFO_KEYS, (int(v) for v in a)))
 

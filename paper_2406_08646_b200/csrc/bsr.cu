@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cstring>
 
+#include "halo_dev.cuh"
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -172,9 +173,11 @@ __device__ __forceinline__ void brows_w(int br0, int br1, int bp0, const int *__
 __global__ void __launch_bounds__(kCtaT, 3)
     k_spmv_bsr3(const int4 *__restrict__ blocks, int n_blocks, const int32_t *__restrict__ browptr,
                 const int32_t *__restrict__ bcol, const double *__restrict__ bval,
-                const double *__restrict__ x, double *__restrict__ y, unsigned int *__restrict__ sched) {
+                const double *__restrict__ x, double *__restrict__ y, unsigned int *__restrict__ sched,
+                int trigger) {
   extern __shared__ __align__(128) unsigned char smem[];
   BsrStage *st = reinterpret_cast<BsrStage *>(smem);
+  if (trigger) pdl_trigger();  // let k_offdiag_bsr3 start beside this grid (see there)
   unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + kStagesB * sizeof(BsrStage));
   unsigned long long *empty = full + kStagesB;
   const int tid = threadIdx.x, warp = tid >> 5, lane32 = tid & 31;
@@ -243,6 +246,163 @@ __global__ void __launch_bounds__(kCtaT, 3)
   }
 }
 
+// ------------------------------------------------------------------ off-diagonal 3x3 blocks
+// warp per row triple t of the compressed off-diagonal rows: rows 3br..3br+2, equal column
+// lists made of aligned ghost triples (3 dofs of one ghost node)
+__global__ void k_bsr_o_check(const int32_t *__restrict__ rows, const int32_t *__restrict__ rowptr,
+                              const int32_t *__restrict__ col, int64_t nobr, int *__restrict__ bad) {
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= nobr) return;
+  const int r0 = rows[3 * t];
+  const int a0 = rowptr[3 * t], a1 = rowptr[3 * t + 1], a2 = rowptr[3 * t + 2], a3 = rowptr[3 * t + 3];
+  const int len = a1 - a0;
+  if (r0 % 3 || rows[3 * t + 1] != r0 + 1 || rows[3 * t + 2] != r0 + 2 || a2 - a1 != len || a3 - a2 != len ||
+      len % 3) {
+    if (lane == 0) atomicOr(bad, 1);
+    return;
+  }
+  for (int p = lane; p < len; p += 32) {
+    const int c0 = col[a0 + p];
+    bool ok = c0 == col[a1 + p] && c0 == col[a2 + p];
+    ok = ok && ((p % 3 == 0) ? (c0 % 3 == 0) : (c0 == col[a0 + p - 1] + 1));
+    if (!ok) atomicOr(bad, 1);
+  }
+}
+
+__global__ void k_bsr_o_build(const int32_t *__restrict__ rows, const int32_t *__restrict__ rowptr,
+                              const int32_t *__restrict__ col, int64_t nobr, int32_t *__restrict__ ob_rows,
+                              int32_t *__restrict__ ob_rowptr, int32_t *__restrict__ ob_col) {
+  GSTRIDE(t, nobr + 1) {
+    const int a = rowptr[3 * t];
+    ob_rowptr[t] = a / 9;
+    if (t < nobr) {
+      ob_rows[t] = rows[3 * t] / 3;
+      const int nb_row = (rowptr[3 * t + 1] - a) / 3;
+      for (int q = 0; q < nb_row; ++q) ob_col[a / 9 + q] = col[a + 3 * q] / 3;
+    }
+  }
+}
+
+// warp per block row: ob_val[9*(b0+q) + 3i + j] = val_o[rowptr_o[3t+i] + 3q + j]
+__global__ void k_bsr_o_refresh(const int32_t *__restrict__ rowptr, const double *__restrict__ val,
+                                const int32_t *__restrict__ ob_rowptr, int64_t nobr, double *__restrict__ ob_val) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = warp; t < nobr; t += nwarps) {
+    const int b0 = ob_rowptr[t], n = ob_rowptr[t + 1] - b0;
+    const int r0 = rowptr[3 * t], r1 = rowptr[3 * t + 1], r2 = rowptr[3 * t + 2];
+    for (int v = lane; v < 9 * n; v += 32) {
+      const int q = v / 9, i = (v % 9) / 3, j = v % 3;
+      const int base = i == 0 ? r0 : (i == 1 ? r1 : r2);
+      ob_val[9 * (int64_t)b0 + v] = val[base + 3 * q + j];
+    }
+  }
+}
+
+// Off-diagonal SpMV-add y += A_o lvec on 3x3 blocks (block CSR L1163).
+// W lanes per block row; a lane takes blocks a+lane, a+lane+W, ... (ascending columns), loads
+// each block's 3 ghost values (flagged lines of this epoch, or the NCCL ghost vector) once for
+// the block's 3 rows, and adds v_i0*g_0, v_i1*g_1, v_i2*g_2 per row i (W = 1: the CSR row's
+// left-to-right order); then a shuffle tree over the W lanes.
+// Two phases.  Phase 1 -- every read of A_o and of the ghost lines, the latency-bound part --
+// runs BEFORE pdl_wait: the block SpMV triggers dependents at entry, and this kernel's CTAs
+// (kObT threads, <= 48 registers) fit in the registers the block SpMV's 3 CTAs per SM leave
+// free, so the whole phase overlaps the bandwidth-bound diagonal sweep.  Sums go to obuf.
+// Phase 2 after pdl_wait (the diagonal y is final): the SAME thread adds its sums into y.
+// The last CTA releases the ghost buffer to the senders and advances the epoch (NVLink mode).
+constexpr int kObT = 64;
+template <int W, bool PEER>
+__global__ void __launch_bounds__(kObT, 20)
+    k_offdiag_bsr3(const int32_t *__restrict__ ob_rows, const int32_t *__restrict__ ob_rowptr,
+                   const int32_t *__restrict__ ob_col, const double *__restrict__ ob_val,
+                   const uint4 *ghost_base, int64_t ghost_stride, const double *lvec, double *y,
+                   double *obuf, int64_t nobr, const HaloWait *__restrict__ waits, int nwaits,
+                   unsigned long long *epoch_ctr, unsigned int *counter, int *err) {
+  // the epoch counter is written only by the MatMult's last kernel, never by the block SpMV
+  // this grid overlaps, so it may be read before pdl_wait
+  const unsigned long long epoch = PEER ? *epoch_ctr + 1ull : 0ull;
+  const uint32_t flag = ll_flag(epoch);
+  const uint4 *gl = PEER ? ghost_base + (int64_t)(epoch & 1) * ghost_stride : nullptr;
+  const int sub = threadIdx.x & (W - 1);
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  constexpr int U = 2;  // blocks per lane in flight
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nobr * W; base += step) {
+    const int64_t q = (base + threadIdx.x) / W;
+    const bool valid = q < nobr;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (valid) {
+      const int a = ob_rowptr[q], z = ob_rowptr[q + 1];
+      for (int e0 = a + sub; e0 < z; e0 += U * W) {
+        int c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) c[u] = e0 + u * W < z ? ob_col[e0 + u * W] : -1;
+        double g[U][3];
+        if (PEER) {
+          uint4 raw[U][3];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+              if (c[u] >= 0) raw[u][j] = ll_load_raw(gl + 3 * (int64_t)c[u] + j);
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+              g[u][j] = c[u] >= 0 ? ll_value(gl + 3 * (int64_t)c[u] + j, raw[u][j], flag, err) : 0.0;
+        } else {
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) g[u][j] = c[u] >= 0 ? __ldcg(lvec + 3 * (int64_t)c[u] + j) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (c[u] < 0) continue;
+          const double *v = ob_val + 9 * (int64_t)(e0 + u * W);
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            s0 = __dadd_rn(s0, __dmul_rn(__ldg(v + j), g[u][j]));
+            s1 = __dadd_rn(s1, __dmul_rn(__ldg(v + 3 + j), g[u][j]));
+            s2 = __dadd_rn(s2, __dmul_rn(__ldg(v + 6 + j), g[u][j]));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = W >> 1; o > 0; o >>= 1) {
+      s0 = __dadd_rn(s0, __shfl_down_sync(0xffffffffu, s0, o, W));
+      s1 = __dadd_rn(s1, __shfl_down_sync(0xffffffffu, s1, o, W));
+      s2 = __dadd_rn(s2, __shfl_down_sync(0xffffffffu, s2, o, W));
+    }
+    if (valid && sub == 0) {
+      obuf[3 * q] = s0;
+      obuf[3 * q + 1] = s1;
+      obuf[3 * q + 2] = s2;
+    }
+  }
+  pdl_wait();  // the diagonal SpMV's y is complete and visible
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nobr * W; base += step) {
+    const int64_t q = (base + threadIdx.x) / W;
+    if (q < nobr && sub == 0) {
+      const int64_t r = 3 * (int64_t)ob_rows[q];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) y[r + i] = __dadd_rn(__ldcg(y + r + i), obuf[3 * q + i]);
+    }
+  }
+  if (!PEER) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(counter, 1u) == gridDim.x - 1) {
+      atomicExch(counter, 0u);
+      for (int w = 0; w < nwaits; ++w) st_release_sys(waits[w].peer_done, epoch);
+      *epoch_ctr = epoch;  // this MatMult is done
+    }
+  }
+}
+
 #define CUB_CALL2(tmp, call_with_tmp)                                          \
   do {                                                                         \
     size_t temp_storage_bytes = 0;                                             \
@@ -256,18 +416,93 @@ __global__ void __launch_bounds__(kCtaT, 3)
 }  // namespace
 
 int bsr_refresh(spmat_s *A, cudaStream_t s) {
-  if (A->bs != 3 || A->mb == 0) return SPMAT_OK;
-  k_bsr_refresh<<<nb(A->mb * 32), 256, 0, s>>>(A->rowptr_d.get(), A->val_d.get(), A->browptr.get(),
-                                                A->mb, A->bval.get());
+  if (A->bs != 3) return SPMAT_OK;
+  if (A->mb > 0) {
+    k_bsr_refresh<<<nb(A->mb * 32), 256, 0, s>>>(A->rowptr_d.get(), A->val_d.get(), A->browptr.get(),
+                                                  A->mb, A->bval.get());
+    SP_LAUNCH();
+  }
+  if (A->ob_ok && A->obr > 0) {
+    k_bsr_o_refresh<<<nb(A->obr * 32), 256, 0, s>>>(A->rowptr_o.get(), A->val_o.get(), A->ob_rowptr.get(),
+                                                     A->obr, A->ob_val.get());
+    SP_LAUNCH();
+  }
+  return SPMAT_OK;
+}
+
+int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool trigger) {
+  k_spmv_bsr3<<<(unsigned)A->bsr_grid, kCtaT, kBsrSmem, s>>>(A->bblocks4.get(), (int)A->n_brblocks,
+                                                           A->browptr.get(), A->bcol.get(), A->bval.get(),
+                                                           x, y, A->bsched.get(), trigger ? 1 : 0);
   SP_LAUNCH();
   return SPMAT_OK;
 }
 
-int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s) {
-  k_spmv_bsr3<<<(unsigned)A->bsr_grid, kCtaT, kBsrSmem, s>>>(A->bblocks4.get(), (int)A->n_brblocks,
-                                                           A->browptr.get(), A->bcol.get(), A->bval.get(),
-                                                           x, y, A->bsched.get());
+// y += A_o lvec on the 3x3 block copy.  overlapped: launched right after the block SpMV (which
+// then triggers dependents): a grid that fits beside it (A->ob_grid); else a full grid.
+template <int W>
+static cudaError_t launch_ob(spmat_s *A, double *y, const double *lvec, cudaStream_t s, unsigned grid) {
+  const bool peer = lvec == nullptr;
+  return launch_pdl(peer ? k_offdiag_bsr3<W, true> : k_offdiag_bsr3<W, false>, grid, kObT, 0, s, (const int32_t *)A->ob_rows.get(),
+                    (const int32_t *)A->ob_rowptr.get(), (const int32_t *)A->ob_col.get(),
+                    (const double *)A->ob_val.get(), peer ? (const uint4 *)A->ghost.get() : nullptr,
+                    A->ghost_stride, lvec, y, A->ob_buf.get(), A->obr,
+                    peer ? (const HaloWait *)A->halo_waits.get() : nullptr, peer ? A->n_waits : 0,
+                    peer ? A->d_epoch.get() : nullptr, peer ? A->halo_counter.get() : nullptr,
+                    peer ? A->halo_err.get() : nullptr);
+}
+
+int bsr_offdiag(spmat_s *A, double *y, const double *lvec, bool overlapped, cudaStream_t s) {
+  const int64_t work = A->obr * A->ob_w;
+  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + kObT - 1) / kObT, 16L * A->comm->num_sms));
+  if (overlapped) grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid, A->ob_grid));
+  cudaError_t e;
+  switch (A->ob_w) {
+    case 1: e = launch_ob<1>(A, y, lvec, s, grid); break;
+    case 2: e = launch_ob<2>(A, y, lvec, s, grid); break;
+    case 8: e = launch_ob<8>(A, y, lvec, s, grid); break;
+    default: e = launch_ob<4>(A, y, lvec, s, grid); break;
+  }
+  SP_CUDA(e);
+  return SPMAT_OK;
+}
+
+// 3x3 block copy of the off-diagonal block, when it is made of aligned blocks (else the CSR
+// off-diagonal kernels stay in use)
+static int bsr_o_setup(spmat_s *A, cudaStream_t st) {
+  A->ob_ok = false;
+  if (A->n_ro == 0 || A->n_ro % 3) return SPMAT_OK;
+  const int64_t nobr = A->n_ro / 3;
+  DevBuf<int> bad;
+  SP_TRY(bad.alloc(1));
+  SP_CUDA(cudaMemsetAsync(bad.get(), 0, 4, st));
+  k_bsr_o_check<<<nb(nobr * 32), 256, 0, st>>>(A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(), nobr, bad.get());
   SP_LAUNCH();
+  int hbad = 0;
+  SP_CUDA(cudaMemcpyAsync(&hbad, bad.get(), 4, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  if (hbad) return SPMAT_OK;
+  A->obr = nobr;
+  A->onnzb = A->nnz_o / 9;
+  SP_TRY(A->ob_rows.alloc(nobr));
+  SP_TRY(A->ob_rowptr.alloc(nobr + 1));
+  SP_TRY(A->ob_col.alloc(A->onnzb));
+  SP_TRY(A->ob_val.alloc(9 * A->onnzb));
+  SP_TRY(A->ob_buf.alloc(3 * nobr));
+  k_bsr_o_build<<<nb(nobr + 1), 256, 0, st>>>(A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(), nobr,
+                                              A->ob_rows.get(), A->ob_rowptr.get(), A->ob_col.get());
+  SP_LAUNCH();
+  // lanes per block row: the largest power of two <= 8 with >= 2 blocks per lane on average
+  A->ob_w = 1;
+  while (A->ob_w < 8 && 4 * A->ob_w * nobr <= A->onnzb) A->ob_w *= 2;
+  if (const char *w = getenv("SPMAT_OB_W")) {
+    const int v = atoi(w);
+    if (v == 1 || v == 2 || v == 4 || v == 8) A->ob_w = v;
+  }
+  // CTAs that fit beside the block SpMV's CTAs: one per SM (kObT threads, <= 48 registers)
+  A->ob_grid = A->comm->num_sms;
+  A->ob_ok = true;
+  if (const char *e = getenv("SPMAT_BSR_OFFDIAG")) A->ob_ok = atoi(e) != 0;
   return SPMAT_OK;
 }
 
@@ -332,6 +567,7 @@ static int bsr_setup(spmat_s *A) {
   SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_bsr3, kCtaT, kBsrSmem));
   A->bsr_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * A->comm->num_sms,
                                                            std::max<int64_t>(A->n_brblocks, 1)));
+  SP_TRY(bsr_o_setup(A, st));
   A->bs = 3;
   A->kernel_id = 4;
   if (A->values_set) SP_TRY(bsr_refresh(A, st));

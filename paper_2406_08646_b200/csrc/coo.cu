@@ -773,7 +773,10 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
                            A->recvbuf.get(), A->recv_off.data(), A->recv_count.data(),
                            sizeof(double), c->comm_stream));
     SP_CUDA(cudaEventRecord(A->ev_recv_done, c->comm_stream));
+    A->stat_nccl_sent += 8 * A->nsend;
+    A->stat_nccl_recv += 8 * A->nrecv;
   }
+  ++A->stat_setvals;
   if (nnz > 0) {
     // ILP kernel when nonzeros have ~1 contribution (stencil COO); with many duplicates of
     // varying count (element COO) one nonzero per thread keeps more threads busy
@@ -806,11 +809,15 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
   return SPMAT_OK;
 }
 
-int spmat_get_info(spmat_t A, int64_t info[16]) {
+int spmat_get_info(spmat_t A, int64_t info[32]) {
   if (!A || !info) return fail(SPMAT_ERR_ARG, "spmat_get_info: null argument");
-  int64_t v[16] = {A->rstart, A->rend, A->cstart, A->cend, A->nnz_d, A->nnz_o, A->n_ghost,
+  const int64_t mode = A->comm->nranks == 1 ? 0 : (A->peer ? 2 : 1);
+  int64_t v[32] = {A->rstart, A->rend, A->cstart, A->cend, A->nnz_d, A->nnz_o, A->n_ghost,
                    A->n_ro, A->ncontrib, A->nsend, A->nrecv, A->n_mixed, A->kernel_id,
-                   A->n_rowblocks, A->max_row_nnz, A->plan_builds};
+                   A->n_rowblocks, A->max_row_nnz, A->plan_builds,
+                   A->bs, A->ob_ok ? 1 : 0, A->ob_ok ? A->ob_w : A->ro_w, mode,
+                   A->stat_nccl_sent, A->stat_nccl_recv, A->stat_nvlink_put, A->stat_mults,
+                   A->stat_setvals, A->bs == 3 ? A->bsr_grid : A->tma_grid, A->ob_ok ? A->ob_grid : 0};
   memcpy(info, v, sizeof v);
   return SPMAT_OK;
 }

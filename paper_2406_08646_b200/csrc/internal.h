@@ -351,6 +351,8 @@ struct spmat_s {
   std::vector<cudaEvent_t> prof_ev[3];  // pairs per kind
   size_t prof_n[3] = {0, 0, 0};
   int64_t plan_builds = 0;
+  // counters (spmat_get_info): bytes enqueued on NCCL / stored into peers, calls
+  int64_t stat_nccl_sent = 0, stat_nccl_recv = 0, stat_nvlink_put = 0, stat_mults = 0, stat_setvals = 0;
   // environment switches, read when the matrix is created (not process-wide statics)
   bool env_no_fuse = false;     // SPMAT_FUSE=0: standalone put kernel instead of the fused puts
   bool env_no_tail = false;     // SPMAT_FUSE_TAIL=0: off-diagonal add as its own kernel
@@ -381,6 +383,15 @@ struct spmat_s {
   spmat::DevBuf<double> bval;
   spmat::DevBuf<int4> bblocks4;
   spmat::DevBuf<unsigned int> bsched;
+  // 3x3 block copy of the off-diagonal block (when it is made of aligned 3x3 blocks too):
+  // block rows ob_rows (block-row ids), ob_rowptr, ob_col (ghost block = 3 consecutive ghost
+  // lines), ob_val (9 per block); ob_buf holds the per-row sums between the two phases of
+  // k_offdiag_bsr3 (bsr.cu)
+  bool ob_ok = false;
+  int64_t obr = 0, onnzb = 0;
+  int ob_w = 4, ob_grid = 0;
+  spmat::DevBuf<int32_t> ob_rows, ob_rowptr, ob_col;
+  spmat::DevBuf<double> ob_val, ob_buf;
   // host-buffer MatMult pipeline (mult.cu / spmv.cu), built on first use
   int pipe_chunks = 0;
   std::vector<int64_t> pipe_block, pipe_row, pipe_xmin, pipe_xneed;  // row-order block range, row range, x rows read
@@ -409,7 +420,10 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream, bool 
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
 void cg_graph_release(spmat_s *A);            // drop the captured CG iteration
 int bsr_refresh(spmat_s *A, cudaStream_t s);  // bval from the CSR values
-int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s);
+int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool trigger = false);
+// off-diagonal SpMV-add on the 3x3 block copy: NVLink ghost lines of this epoch (ends the
+// epoch, like k_spmv_offdiag_peer) or, with lvec != nullptr, the NCCL ghost vector
+int bsr_offdiag(spmat_s *A, double *y, const double *lvec, bool overlapped, cudaStream_t s);
 // host-buffer pipeline (single rank): row chunks of the diagonal SpMV
 int spmv_pipe_prepare(spmat_s *A, int chunks);  // chunk rows + the x columns each chunk reads
 int spmv_diag_chunk(spmat_s *A, const double *x, double *y, int k, cudaStream_t s);

@@ -28,6 +28,15 @@ static cudaEvent_t *prof_pair(spmat_s *A, int kind) {
 static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStream_t s) {
   const bool multi = A->comm->nranks > 1;
   cudaEvent_t *pe;
+  if (part == 7) ++A->stat_mults;
+  if (multi && (part & 2) && A->halo) {  // bytes this MatMult's halo moves (one direction each)
+    if (A->peer) {
+      A->stat_nvlink_put += 16 * A->halo->nsend;
+    } else {
+      A->stat_nccl_sent += 8 * A->halo->nsend;
+      A->stat_nccl_recv += 8 * A->halo->nrecv;
+    }
+  }
   if (multi && A->peer) {  // device-initiated halo over NVLink (halo.cu)
     bool fused = false;
     if (part & 2) {
@@ -47,17 +56,27 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
     }
     // full MatMult, no long rows: the off-diagonal SpMV-add runs in the same kernel's tail
     const bool tail = fused && (part & 4) && A->n_ro > 0 && A->n_long == 0 && !A->env_no_tail;
+    // 3x3 blocks: the block off-diagonal kernel starts beside the block SpMV (PDL trigger) and
+    // does its A_o / ghost-line reads while the diagonal sweep runs (bsr.cu k_offdiag_bsr3)
+    const bool ob = A->bs == 3 && A->ob_ok && (part & 6) == 6 && A->n_ro > 0;
+    const bool ob_overlap = ob && (part & 1) && !A->profile;
     if (part & 1) {
       pe = A->profile ? prof_pair(A, 0) : nullptr;
       if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
-      SP_TRY(spmv_diag(A, x, y, s, fused, tail));
+      if (A->bs == 3 && A->m > 0)
+        SP_TRY(bsr_spmv(A, x, y, s, ob_overlap));
+      else
+        SP_TRY(spmv_diag(A, x, y, s, fused, tail));
       if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
     }
     if (tail) return SPMAT_OK;
     if (part & 2) {
       pe = (A->profile && (part & 4) && A->n_ro > 0) ? prof_pair(A, 1) : nullptr;
       if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
-      SP_TRY(halo_peer_offdiag(A, y, s, (part & 4) != 0));
+      if (ob)
+        SP_TRY(bsr_offdiag(A, y, nullptr, ob_overlap, s));
+      else
+        SP_TRY(halo_peer_offdiag(A, y, s, (part & 4) != 0));
       if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
     } else if ((part & 4) && A->n_ro > 0) {
       SP_TRY(spmv_offdiag(A, y, s));
@@ -104,6 +123,8 @@ static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStrea
   SP_TRY(spmv_pipe_prepare(A, A->env_pipe_chunks));
   const int nc = A->pipe_chunks;
   const bool multi = A->comm->nranks > 1;
+  ++A->stat_mults;
+  if (multi) A->stat_nvlink_put += 16 * A->halo->nsend;
   if (!A->pipe_in) {
     int lo = 0, hi = 0;
     SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));

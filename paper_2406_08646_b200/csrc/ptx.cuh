@@ -13,6 +13,10 @@ namespace spmat {
 // 115 us per iteration) than the launch overlap saved; the implicit trigger at exit still
 // takes ~2.5 us off each iteration.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// The one exception (bsr.cu): the 3x3 block SpMV triggers at entry when the next kernel is the
+// block off-diagonal SpMV-add, which is sized to fit beside it on every SM and does all its
+// latency-bound reads before its pdl_wait.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);

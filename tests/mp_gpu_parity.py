@@ -81,6 +81,8 @@ def check_matrix(c, name, M, N, row_sizes, col_sizes, coo, values, x_global, exa
         A.set_block_size(bs)
     c.halo_mode = A.halo_mode()
     info = A.info()
+    if bs == 3 and info["n_offdiag_rows"] > 0 and os.environ.get("SPMAT_BSR_OFFDIAG", "1") != "0":
+        assert info["offdiag_3x3"] == 1, f"{name}: off-diagonal block not kept in 3x3 blocks"
     assert info["rstart"] == O.info(r, "rstart") and info["cstart"] == O.info(r, "cstart")
     for key in ("rowptr_d", "col_d", "rowptr_o", "col_o", "colmap", "jmap", "send_count",
                 "recv_count", "send_k"):
@@ -196,6 +198,14 @@ def case_elasticity(c):
     x = synth.x_vector(0, M, "real").numpy()
     check_matrix(c, "elasticity", M, M, sizes, sizes, coo, "real", x, exact_y=False)
     check_matrix(c, "elasticity-bsr", M, M, sizes, sizes, coo, "real", x, exact_y=False, bs=3)
+    # larger slabs, integer values: the 3x3 off-diagonal kernel must be bit-exact
+    n = 4 * P
+    M = 3 * n ** 3
+    sizes = synth.slab_sizes((n, n, n), P, dof=3)
+    nodes = sizes[0] // 3
+    coo = [synth.elasticity_coo(n, nodes=(q * nodes, (q + 1) * nodes), values="int") for q in range(P)]
+    x = synth.x_vector(0, M, "int").numpy()
+    check_matrix(c, "elasticity-bsr-int", M, M, sizes, sizes, coo, "int", x, exact_y=True, bs=3)
 
 
 def case_random(c, seed):
@@ -371,10 +381,24 @@ def case_full_c4(c):
     off = synth.offsets_from_sizes(sizes)
     M = off[-1]
     A = sp.Mat(c.comm, sizes[r], sizes[r], M, M, i, j)
-    A.set_values(v)
-    del i, j, v
-    x = synth.x_vector(off[r], off[r + 1], "real", device="cuda")
+    del i, j
     y = torch.empty(sizes[r], dtype=torch.float64, device="cuda")
+    # integer values: A.1 over EVERY row of every rank = out-of-grid neighbour count (P3)
+    _, _, vi, _ = synth.config_rank_coo("c4", P, r, values="int", device="cuda")
+    A.set_values(vi)
+    del vi
+    A.mult(torch.ones(sizes[r], dtype=torch.float64, device="cuda"), y)
+    shape = synth.config_shape("c4", P)
+    g = torch.arange(off[r], off[r + 1], device="cuda")
+    want = torch.zeros_like(y)
+    for n in shape:
+        cc = g % n
+        want += (cc == 0).double() + (cc == n - 1).double()
+        g = g // n
+    assert torch.equal(y, want), f"full-size C4 A.1 rank {r}: {int((y != want).sum())} rows differ"
+    A.set_values(v)
+    del v
+    x = synth.x_vector(off[r], off[r + 1], "real", device="cuda")
     for _ in range(3):  # several epochs of the NVLink halo
         A.mult(x, y)
     A.check()
@@ -390,8 +414,73 @@ def case_full_c4(c):
     torch.cuda.empty_cache()
 
 
+def case_full_c5(c):
+    """C5 at full size (24 M rows, 1.92 G nonzeros, z-slabs of 200/P planes) with 3x3 blocks
+    (diagonal and off-diagonal) and with CSR: A.1 over EVERY row of every rank against the
+    Kronecker closed form 6 * prod_d (4 + n_d) (integer values, exact), then real values on
+    node windows at the slab boundaries vs the oracle from the COO definition."""
+    P, r = c.P, c.r
+    n = 200
+    i, j, vi, sizes = synth.config_rank_coo("c5", P, r, values="int", device="cuda")
+    off = synth.offsets_from_sizes(sizes)
+    M = off[-1]
+    A = sp.Mat(c.comm, sizes[r], sizes[r], M, M, i, j)
+    del i, j
+    A.set_values(vi)
+    del vi
+    torch.cuda.empty_cache()
+    node = torch.arange(off[r], off[r + 1], device="cuda") // 3
+    want = torch.full((sizes[r],), 6.0, dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        cc = node % n
+        want *= 4 + (cc > 0).double() + (cc < n - 1).double()
+        node = node // n
+    y = torch.empty(sizes[r], dtype=torch.float64, device="cuda")
+    ones = torch.ones(sizes[r], dtype=torch.float64, device="cuda")
+    for bs in (3, 1):
+        A.set_block_size(bs)
+        for _ in range(3):
+            A.mult(ones, y)
+        A.check()
+        assert torch.equal(y, want), f"C5 bs={bs} A.1 rank {r}: {int((y != want).sum())} rows differ"
+    del want, ones
+    _, _, v, _ = synth.config_rank_coo("c5", P, r, values="real", device="cuda")
+    A.set_values(v)
+    del v
+    torch.cuda.empty_cache()
+    x = synth.x_vector(off[r], off[r + 1], "real", device="cuda")
+    xg = synth.x_vector(0, M, "real").numpy()
+    n0, n1 = off[r] // 3, off[r + 1] // 3
+    pi, pj, pv, rws = [], [], [], []
+    for a0 in sorted({n0, max(n0, n1 - 64 * n - 5), (n0 + n1) // 2, n1 - 64}):
+        ih, jh, vh = synth.elasticity_coo(n, nodes=(a0, a0 + 64), values="real")
+        pi.append(ih); pj.append(jh); pv.append(vh)
+        rws.append(torch.arange(3 * a0, 3 * (a0 + 64)))
+    rows = torch.unique(torch.cat(rws))
+    ys = oracle.sample_rows(torch.cat(pi), torch.cat(pj), torch.cat(pv), rows.numpy(), xg)
+    for bs in (3, 1):
+        A.set_block_size(bs)
+        A.mult(x, y)
+        A.check()
+        got = y[(rows - off[r]).cuda()].cpu().numpy()
+        assert rel_err(got, ys) <= TOL, f"full-size C5 bs={bs} rank {r}: {rel_err(got, ys)}"
+    A.close()
+    torch.cuda.empty_cache()
+
+
 def case_errors(c):
     P, r = c.P, c.r
+    # an error only one rank can see (its m_local >= 2^31): every rank returns an error, none
+    # blocks in the next collective (Comm::agree)
+    big = 1 << 31
+    mloc = big if r == P - 1 else 2
+    Mg = 2 * (P - 1) + big
+    try:
+        sp.Mat(c.comm, mloc, mloc, Mg, Mg, torch.zeros(0, dtype=torch.int64, device="cuda"),
+               torch.zeros(0, dtype=torch.int64, device="cuda"))
+        raise AssertionError("rank-local error not raised")
+    except sp.SpmatError as e:
+        assert e.status == sp.SPMAT_ERR_ARG, e
     # only the last rank has an out-of-range index: every rank must report it
     i = torch.tensor([0, 1] if r < P - 1 else [0, 99], device="cuda") + c.r * 2
     j = torch.tensor([0, 1], device="cuda")
@@ -426,8 +515,11 @@ def main():
     cases += [("host-pipeline-slab", lambda: case_host_pipeline(c, "slab")),
               ("host-pipeline-box", lambda: case_host_pipeline(c, "box"))]
     cases += [(f"transpose{s}", (lambda s=s: case_transpose(c, s))) for s in range(6)]
-    cases += [("full-c4", lambda: case_full_c4(c))]
+    cases += [("full-c4", lambda: case_full_c4(c)), ("full-c5", lambda: case_full_c5(c))]
     cases += [("errors", lambda: case_errors(c))]
+    only = [s for s in os.environ.get("MP_CASES", "").split(",") if s]
+    if only:
+        cases = [(nm, fn) for nm, fn in cases if any(nm.startswith(s) for s in only)]
     for name, fn in cases:
         try:
             fn()
