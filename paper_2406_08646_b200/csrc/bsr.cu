@@ -81,6 +81,23 @@ __global__ void k_bsr_build(const int32_t *__restrict__ rowptr, const int32_t *_
   }
 }
 
+// the inverse: val[rowptr[3br+i] + 3q + j] = bval[9*(bp0+q) + 3i + j]
+__global__ void k_bsr_unrefresh(const int32_t *__restrict__ rowptr, const double *__restrict__ bval,
+                                const int32_t *__restrict__ browptr, int64_t mb, double *__restrict__ val) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t br = warp; br < mb; br += nwarps) {
+    const int bp0 = browptr[br], nbr = browptr[br + 1] - bp0;
+    const int r0 = rowptr[3 * br], r1 = rowptr[3 * br + 1], r2 = rowptr[3 * br + 2];
+    for (int v = lane; v < 9 * nbr; v += 32) {
+      const int q = v / 9, i = (v % 9) / 3, j = v % 3;
+      const int base = i == 0 ? r0 : (i == 1 ? r1 : r2);
+      val[base + 3 * q + j] = bval[9 * (int64_t)bp0 + v];
+    }
+  }
+}
+
 // warp per block row: bval[9*(bp0+q) + 3i + j] = val[rowptr[3br+i] + 3q + j]
 __global__ void k_bsr_refresh(const int32_t *__restrict__ rowptr, const double *__restrict__ val,
                               const int32_t *__restrict__ browptr, int64_t mb, double *__restrict__ bval) {
@@ -415,9 +432,9 @@ __global__ void __launch_bounds__(kObT, 20)
 
 }  // namespace
 
-int bsr_refresh(spmat_s *A, cudaStream_t s) {
+int bsr_refresh(spmat_s *A, cudaStream_t s, bool diag) {
   if (A->bs != 3) return SPMAT_OK;
-  if (A->mb > 0) {
+  if (diag && A->mb > 0) {
     k_bsr_refresh<<<nb(A->mb * 32), 256, 0, s>>>(A->rowptr_d.get(), A->val_d.get(), A->browptr.get(),
                                                   A->mb, A->bval.get());
     SP_LAUNCH();
@@ -427,6 +444,17 @@ int bsr_refresh(spmat_s *A, cudaStream_t s) {
                                                      A->obr, A->ob_val.get());
     SP_LAUNCH();
   }
+  return SPMAT_OK;
+}
+
+int csr_sync(spmat_s *A, cudaStream_t s) {
+  if (!A->val_d_stale) return SPMAT_OK;
+  if (A->mb > 0) {
+    k_bsr_unrefresh<<<nb(A->mb * 32), 256, 0, s>>>(A->rowptr_d.get(), A->bval.get(), A->browptr.get(), A->mb,
+                                                    A->val_d.get());
+    SP_LAUNCH();
+  }
+  A->val_d_stale = false;
   return SPMAT_OK;
 }
 
@@ -506,6 +534,12 @@ static int bsr_o_setup(spmat_s *A, cudaStream_t st) {
   return SPMAT_OK;
 }
 
+static int bsr_o_env(spmat_s *A) {
+  const char *e = getenv("SPMAT_NUMERIC_BSR");
+  A->env_numeric_csr = e && atoi(e) == 0;
+  return SPMAT_OK;
+}
+
 static int bsr_setup(spmat_s *A) {
   cudaStream_t st = A->comm->setup_stream;
   // the caller's spmat_set_values_coo may still be writing val_d on its own stream, and this
@@ -568,6 +602,7 @@ static int bsr_setup(spmat_s *A) {
   A->bsr_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * A->comm->num_sms,
                                                            std::max<int64_t>(A->n_brblocks, 1)));
   SP_TRY(bsr_o_setup(A, st));
+  SP_TRY(bsr_o_env(A));
   A->bs = 3;
   A->kernel_id = 4;
   if (A->values_set) SP_TRY(bsr_refresh(A, st));
@@ -586,6 +621,11 @@ int spmat_set_block_size(spmat_t A, int bs) {
   DeviceGuard g(A->comm->device);
   cg_graph_release(A);  // a captured CG iteration would still launch the old kernel
   if (bs == 1) {
+    if (A->val_d_stale) {  // the values live in bval: bring the CSR copy up to date first
+      SP_CUDA(cudaDeviceSynchronize());
+      SP_TRY(csr_sync(A, A->comm->setup_stream));
+      SP_CUDA(cudaStreamSynchronize(A->comm->setup_stream));
+    }
     A->bs = 1;
     A->kernel_id = 3;
     return SPMAT_OK;

@@ -254,6 +254,101 @@ __global__ void k_numeric_local(const uint32_t *__restrict__ jmap, const uint32_
   }
 }
 
+// Element COO (several contributions per nonzero, C3: 1..8): one nonzero per thread, its
+// contribution segment read kSeg at a time -- the kSeg perm loads, then the kSeg v gathers, are
+// each issued together before any is used, so a segment costs one jmap -> perm -> v chain of
+// latencies instead of one per contribution -- then summed in canonical order.
+constexpr int kSeg = 8;
+__global__ void __launch_bounds__(256) k_numeric_seg(
+    const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm, const double *__restrict__ v,
+    uint64_t ncoo, int64_t nnz_d, int64_t nnz, double *__restrict__ val_d, double *__restrict__ val_o,
+    int mode) {
+  GRID_STRIDE(z, nnz) {
+    const uint32_t t0 = __ldg(jmap + z), t1 = __ldg(jmap + z + 1);
+    double s = 0.0;
+    bool local = true;
+    for (uint32_t a = t0; a < t1; a += kSeg) {
+      uint32_t q[kSeg];
+#pragma unroll
+      for (int k = 0; k < kSeg; ++k) q[k] = a + k < t1 ? __ldg(perm + a + k) : 0u;
+      double w[kSeg];
+#pragma unroll
+      for (int k = 0; k < kSeg; ++k) w[k] = (a + k < t1 && q[k] < ncoo) ? __ldg(v + q[k]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < kSeg; ++k) {
+        if (a + k < t1) {
+          if (q[k] >= ncoo) local = false;  // received contribution: k_numeric_mixed finishes it
+          s = __dadd_rn(s, w[k]);
+        }
+      }
+    }
+    if (local) {
+      double *dst = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
+      *dst = mode == SPMAT_INSERT ? __dadd_rn(0.0, s) : __dadd_rn(*dst, s);
+    }
+  }
+}
+
+// 3x3 blocks (spmat_set_block_size(A, 3)), no received contributions: the numeric step writes
+// the block copy bval directly (the CSR val_d is then stale until spmat_sync_csr_values) -- one
+// pass over the compulsory bytes instead of val_d plus a val_d -> bval copy.  A warp walks a
+// block row's 9*nb values in bval order (v = 9q + 3i + j is nonzero rowptr[3br+i] + 3q + j),
+// kNumU values per lane in flight, each summed in canonical order.
+__global__ void __launch_bounds__(256) k_numeric_bsr3(
+    const int32_t *__restrict__ rowptr, const int32_t *__restrict__ browptr, const uint32_t *__restrict__ jmap,
+    const uint32_t *__restrict__ perm, const double *__restrict__ v, int64_t mb, double *__restrict__ bval,
+    int mode) {
+  constexpr int U = 4;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t br = warp; br < mb; br += nwarps) {
+    const int bp0 = browptr[br], n9 = 9 * (browptr[br + 1] - bp0);
+    const int r0 = rowptr[3 * br], r1 = rowptr[3 * br + 1], r2 = rowptr[3 * br + 2];
+    for (int v0 = lane; v0 < n9; v0 += 32 * U) {
+      uint32_t a[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int vv = v0 + 32 * u;
+        const int q = vv / 9, i = (vv % 9) / 3, j = vv % 3;
+        const int z = (i == 0 ? r0 : (i == 1 ? r1 : r2)) + 3 * q + j;
+        a[u] = vv < n9 ? __ldg(jmap + z) : 0u;
+        b[u] = vv < n9 ? __ldg(jmap + z + 1) : 0u;
+      }
+      double s[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) s[u] = 0.0;
+      for (;;) {  // one contribution of every unfinished value per round (canonical order)
+        bool any = false;
+        uint32_t q[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          q[u] = a[u] < b[u] ? __ldg(perm + a[u]) : 0u;
+          any |= a[u] < b[u];
+        }
+        if (!any) break;
+        double w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) w[u] = a[u] < b[u] ? __ldg(v + q[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (a[u] < b[u]) {
+            s[u] = __dadd_rn(s[u], w[u]);
+            ++a[u];
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int vv = v0 + 32 * u;
+        if (vv < n9) {
+          double *dst = bval + 9 * (int64_t)bp0 + vv;
+          *dst = mode == SPMAT_INSERT ? __dadd_rn(0.0, s[u]) : __dadd_rn(*dst, s[u]);
+        }
+      }
+    }
+  }
+}
+
 // Default numeric kernel: each thread finishes kNumU nonzeros z = base + u*blockDim + tid
 // (coalesced across the warp), advancing all of them one contribution per round so every
 // level of the jmap -> perm -> v chain has kNumU loads in flight.  Each nonzero is still
@@ -263,9 +358,9 @@ constexpr int kNumU = 4;
 __global__ void __launch_bounds__(256) k_numeric_ilp(
     const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm, const double *__restrict__ v,
     uint64_t ncoo, int64_t nnz_d, int64_t nnz, double *__restrict__ val_d, double *__restrict__ val_o,
-    int mode) {
+    int mode, int64_t z0) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * kNumU;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kNumU + threadIdx.x; base < nnz; base += stride) {
+  for (int64_t base = z0 + (int64_t)blockIdx.x * blockDim.x * kNumU + threadIdx.x; base < nnz; base += stride) {
     uint32_t a[kNumU], b[kNumU];
     double s[kNumU];
     bool ok[kNumU];
@@ -777,23 +872,39 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
     A->stat_nccl_recv += 8 * A->nrecv;
   }
   ++A->stat_setvals;
+  // 3x3 blocks and no received contributions: the diagonal values go straight into bval
+  const bool direct_bsr = A->bs == 3 && A->n_mixed == 0 && A->mb > 0 && !A->env_numeric_csr;
   if (nnz > 0) {
     // ILP kernel when nonzeros have ~1 contribution (stencil COO); with many duplicates of
-    // varying count (element COO) one nonzero per thread keeps more threads busy
+    // varying count (element COO) one nonzero per thread with its segment read kSeg at a time
     const char *nk = getenv("SPMAT_NUMERIC_KERNEL");
-    bool plain = (double)A->ncontrib > 1.5 * (double)nnz;
-    if (nk) plain = !strcmp(nk, "plain");
-    if (plain) {
-      k_numeric_local<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
-                                                A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
-    } else {
-      const int64_t blocks = std::min<int64_t>((nnz + 256 * kNumU - 1) / (256 * kNumU),
-                                               (int64_t)A->comm->num_sms * 32);
-      k_numeric_ilp<<<(unsigned)blocks, 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
-                                                     A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
+    int kind = (double)A->ncontrib > 1.5 * (double)nnz ? 2 : 0;  // 0 ilp, 1 plain, 2 seg
+    if (nk) kind = !strcmp(nk, "plain") ? 1 : (!strcmp(nk, "seg") ? 2 : 0);
+    const int64_t z0 = direct_bsr ? A->nnz_d : 0;  // direct_bsr: off-diagonal nonzeros only
+    if (direct_bsr) {
+      const int64_t blocks = std::min<int64_t>((A->mb + 7) / 8, (int64_t)A->comm->num_sms * 64);
+      k_numeric_bsr3<<<(unsigned)blocks, 256, 0, s>>>(A->rowptr_d.get(), A->browptr.get(), A->jmap.get(),
+                                                      A->perm.get(), v, A->mb, A->bval.get(), mode);
+      SP_LAUNCH();
     }
-    SP_LAUNCH();
+    if (nnz > z0) {
+      if (kind == 1) {
+        k_numeric_local<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
+                                                  A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
+      } else if (kind == 2 && z0 == 0) {
+        k_numeric_seg<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
+                                                A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
+      } else {
+        const int64_t blocks = std::min<int64_t>((nnz - z0 + 256 * kNumU - 1) / (256 * kNumU),
+                                                 (int64_t)A->comm->num_sms * 32);
+        k_numeric_ilp<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
+            A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo, A->nnz_d, nnz, A->val_d.get(), A->val_o.get(),
+            mode, z0);
+      }
+      SP_LAUNCH();
+    }
   }
+  A->val_d_stale = direct_bsr;
   if (exchange) {
     SP_CUDA(cudaStreamWaitEvent(s, A->ev_recv_done, 0));
     if (A->n_mixed > 0) {
@@ -804,7 +915,7 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
       SP_LAUNCH();
     }
   }
-  SP_TRY(bsr_refresh(A, s));  // block copy of the diagonal values, if any
+  SP_TRY(bsr_refresh(A, s, !direct_bsr));  // block copies of the values, if any
   A->values_set = true;
   return SPMAT_OK;
 }
@@ -859,6 +970,10 @@ int spmat_export(spmat_t A, int what, void *host_buf, int64_t cap, int64_t *len)
   if (!A || !len) return fail(SPMAT_ERR_ARG, "spmat_export: null argument");
   DeviceGuard g(A->comm->device);
   SP_CUDA(cudaDeviceSynchronize());
+  if (what == 2 && A->val_d_stale) {  // values written straight into the 3x3 block copy
+    SP_TRY(csr_sync(A, A->comm->setup_stream));
+    SP_CUDA(cudaStreamSynchronize(A->comm->setup_stream));
+  }
   const int P = A->comm->nranks;
   std::vector<int64_t> out;
   std::vector<double> outd;

@@ -388,6 +388,10 @@ struct spmat_s {
   // lines), ob_val (9 per block); ob_buf holds the per-row sums between the two phases of
   // k_offdiag_bsr3 (bsr.cu)
   bool ob_ok = false;
+  // set_values wrote the diagonal values straight into bval (k_numeric_bsr3): val_d is stale
+  // until csr_sync (export, MatMultTranspose, set_block_size(A, 1))
+  bool val_d_stale = false;
+  bool env_numeric_csr = false;  // SPMAT_NUMERIC_BSR=0: always val_d, then the bval copy
   int64_t obr = 0, onnzb = 0;
   int ob_w = 4, ob_grid = 0;
   spmat::DevBuf<int32_t> ob_rows, ob_rowptr, ob_col;
@@ -419,7 +423,8 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream, bool 
               bool fuse_tail = false);
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
 void cg_graph_release(spmat_s *A);            // drop the captured CG iteration
-int bsr_refresh(spmat_s *A, cudaStream_t s);  // bval from the CSR values
+int bsr_refresh(spmat_s *A, cudaStream_t s, bool diag = true);  // bval (diag) and ob_val from the CSR values
+int csr_sync(spmat_s *A, cudaStream_t s);  // val_d from bval when set_values wrote bval directly
 int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool trigger = false);
 // off-diagonal SpMV-add on the 3x3 block copy: NVLink ghost lines of this epoch (ends the
 // epoch, like k_spmv_offdiag_peer) or, with lvec != nullptr, the NCCL ghost vector

@@ -141,6 +141,7 @@ static int transpose_prepare(spmat_s *A, cudaStream_t s) {
     A->t_val_version = -1;
   }
   if (A->t_val_version != A->val_version) {  // values changed since the last gather
+    SP_TRY(csr_sync(A, s));  // (stream order: after the set_values that wrote bval)
     if (A->nnz_d > 0) {
       k_gather_val<<<tblocks(A->nnz_d), 256, 0, s>>>(A->val_d.get(), A->t_perm_d.get(), A->nnz_d, A->t_val_d.get());
       SP_LAUNCH();

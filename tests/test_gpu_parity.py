@@ -516,7 +516,7 @@ def test_kernel_variants(sp, comm, kernel, case, monkeypatch):
     A.close()
 
 
-@pytest.mark.parametrize("numeric", ["ilp", "plain"])
+@pytest.mark.parametrize("numeric", ["ilp", "plain", "seg"])
 def test_numeric_kernels(sp, comm, numeric, monkeypatch):
     """Both COO numeric kernels give the oracle's values bit for bit (Z1 order), also with
     ~20 contributions per nonzero."""
@@ -617,6 +617,36 @@ def test_block_csr_3x3(sp, comm, values):
     A.mult(dev(x), y)
     assert rel_err(y.cpu().numpy(), O.mult(x.numpy())) <= TOL
     A.set_block_size(1)
+    A.close()
+    # set_values AFTER set_block_size(3): the numeric step writes the block copy directly
+    # (k_numeric_bsr3); the CSR values are brought up to date on demand (export, transpose,
+    # back to CSR) -- all bit-exact against the oracle's assembly (canonical order, Z1)
+    O = oracle.OracleMat(M, M, [M], [M], [i], [j])
+    O.set_values([v])
+    A = sp.Mat(comm, M, M, M, M, dev(i), dev(j))
+    A.set_block_size(3)
+    for mode in (sp.INSERT, sp.ADD, sp.ADD):
+        A.set_values(dev(v), mode)
+        if mode == sp.ADD:
+            O.set_values([v], oracle.ADD)
+        A.mult(dev(x), y)
+        yo = O.mult(x.numpy())
+        if values == "int":
+            assert np.array_equal(canon(y.cpu().numpy()), canon(yo))
+        else:
+            assert rel_err(y.cpu().numpy(), yo) <= TOL
+    assert np.array_equal(canon(A.export("val_d")), canon(O.export(0, "val_d")))
+    yt = torch.empty(M, dtype=torch.float64, device="cuda")
+    A.set_values(dev(v), sp.ADD)
+    O.set_values([v], oracle.ADD)
+    A.mult_transpose(dev(x), yt)  # gathers the transposed values from the synced CSR copy
+    assert rel_err(yt.cpu().numpy(), O.mult_transpose(x.numpy())) <= TOL
+    A.set_values(dev(v), sp.ADD)
+    O.set_values([v], oracle.ADD)
+    A.set_block_size(1)  # back to CSR: val_d synced from the block copy
+    A.mult(dev(x), y)
+    assert rel_err(y.cpu().numpy(), O.mult(x.numpy())) <= TOL
+    assert np.array_equal(canon(A.export("val_d")), canon(O.export(0, "val_d")))
     A.close()
     i, j, v = synth.stencil_coo((9, 9, 9), 7)
     B = sp.Mat(comm, 729, 729, 729, 729, dev(i), dev(j))
