@@ -627,7 +627,7 @@ int spmat_set_block_size(spmat_t A, int bs) {
       SP_CUDA(cudaStreamSynchronize(A->comm->setup_stream));
     }
     A->bs = 1;
-    A->kernel_id = 3;
+    A->kernel_id = A->kernel_id_csr;
     return SPMAT_OK;
   }
   if (bs != 3) return fail(SPMAT_ERR_ARG, "spmat_set_block_size: only 1 and 3 are supported");

@@ -331,6 +331,7 @@ struct spmat_s {
   bool values_set = false;
   // SpMV schedule
   int kernel_id = 0;
+  int kernel_id_csr = 0;             // the CSR kernel chosen at create (restored by set_block_size(A, 1))
   int64_t n_rowblocks = 0, max_row_nnz = 0;
   int lanes = 1;                     // lanes per row of the diagonal SpMV (row statistics)
   spmat::DevBuf<int2> rbp;           // n_rowblocks + 1 (first row, first nonzero) pairs

@@ -43,7 +43,8 @@ constexpr int kLong = 512;                    // rows longer than this get their
 constexpr int kCap = kBudget + kLong;         // max nonzeros of a staged row block
 constexpr int kStages = 2;                    // row blocks in flight per CTA
 
-enum { KERNEL_STREAM = 1, KERNEL_VECTOR = 2, KERNEL_TMA = 3 };
+enum { KERNEL_STREAM = 1, KERNEL_VECTOR = 2, KERNEL_TMA = 3, KERNEL_DIRECT = 5 };
+constexpr int64_t kSmallBytes = 16ll << 20;  // below this the direct kernel (latency-bound sizes)
 
 // one shared-memory stage; every array starts 16-byte aligned (bulk-copy requirement)
 struct __align__(16) TmaStage {
@@ -361,6 +362,44 @@ __global__ void __launch_bounds__(kThreads) k_spmv_stream(
   }
 }
 
+// ------------------------------------------------------------------ small matrices: direct
+// Latency-bound sizes (a few MB, L2-resident: C1, Kuu-sized): no persistent grid, no
+// mbarrier ring, no claim counter -- W lanes per row straight from global memory, each lane
+// issuing 8 (col, val) loads, then their 8 x gathers, before it sums; one launch-to-store
+// chain of rowptr -> col/val -> x -> y.  W = 1 sums each row left to right (serial order).
+template <int W>
+__global__ void __launch_bounds__(128) k_spmv_direct(const int32_t *__restrict__ rowptr,
+                                                     const int32_t *__restrict__ col,
+                                                     const double *__restrict__ val,
+                                                     const double *__restrict__ x,
+                                                     double *__restrict__ y, int64_t m) {
+  pdl_wait();
+  constexpr int U = 8;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / W;
+  const int lane = threadIdx.x & (W - 1);
+  const bool valid = row < m;
+  const int a = valid ? __ldg(rowptr + row) : 0, z = valid ? __ldg(rowptr + row + 1) : 0;
+  double s = 0.0;
+  for (int e0 = a + lane; e0 < z; e0 += U * W) {
+    int c[U];
+    double v[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * W;
+      c[u] = e < z ? __ldg(col + e) : 0;
+      v[u] = e < z ? __ldg(val + e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * W < z) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+  }
+#pragma unroll
+  for (int o = W >> 1; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o, W));
+  if (valid && lane == 0) y[row] = s;
+}
+
 // ------------------------------------------------------------------ alternative: vector
 template <int W>
 __global__ void __launch_bounds__(256) k_spmv_vector(const int32_t *__restrict__ rowptr,
@@ -460,9 +499,16 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
     A->env_pipe_chunks = c >= 2 && c <= 256 ? c : 16;
   }
   A->kernel_id = KERNEL_TMA;
+  // small matrices on one rank (or with the NCCL halo): the direct kernel; the NVLink halo
+  // needs the comm warps of the bulk-copy kernel
+  const bool small = 12 * nnz + 20 * m < kSmallBytes && (A->comm->nranks == 1 || (getenv("SPMAT_HALO") && !strcmp(getenv("SPMAT_HALO"), "nccl")));
+  if (small) A->kernel_id = KERNEL_DIRECT;
   const char *env = getenv("SPMAT_SPMV_KERNEL");
+  if (env && !strcmp(env, "tma")) A->kernel_id = KERNEL_TMA;
+  if (env && !strcmp(env, "direct")) A->kernel_id = KERNEL_DIRECT;
   if (env && !strcmp(env, "vector")) A->kernel_id = KERNEL_VECTOR;
   if (env && !strcmp(env, "stream")) A->kernel_id = KERNEL_STREAM;
+  A->kernel_id_csr = A->kernel_id;
   A->max_row_nnz = 0;
   A->n_rowblocks = 0;
   A->lanes = lanes_for(m ? (double)nnz / (double)m : 0.0);
@@ -606,6 +652,14 @@ static cudaError_t launch_tma(spmat_s *A, const double *x, double *y, cudaStream
 }
 
 template <int W>
+static cudaError_t launch_direct(spmat_s *A, const double *x, double *y, cudaStream_t s) {
+  const int64_t threads = A->m * W;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, (threads + 127) / 128);
+  return launch_pdl(k_spmv_direct<W>, grid, 128, 0, s, (const int32_t *)A->rowptr_d.get(),
+                    (const int32_t *)A->col_d.get(), (const double *)A->val_d.get(), x, y, A->m);
+}
+
+template <int W>
 static void launch_vector(spmat_s *A, const double *x, double *y, cudaStream_t s) {
   k_spmv_vector<W><<<nblk(A->m * W), 256, 0, s>>>(A->rowptr_d.get(), A->col_d.get(), A->val_d.get(),
                                                   x, y, A->m);
@@ -614,6 +668,19 @@ static void launch_vector(spmat_s *A, const double *x, double *y, cudaStream_t s
 int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_put, bool fuse_tail) {
   if (A->m == 0) return SPMAT_OK;
   if (A->bs == 3) return bsr_spmv(A, x, y, s);
+  if (A->kernel_id == KERNEL_DIRECT) {
+    cudaError_t e;
+    switch (A->lanes) {
+      case 1: e = launch_direct<1>(A, x, y, s); break;
+      case 2: e = launch_direct<2>(A, x, y, s); break;
+      case 4: e = launch_direct<4>(A, x, y, s); break;
+      case 8: e = launch_direct<8>(A, x, y, s); break;
+      case 16: e = launch_direct<16>(A, x, y, s); break;
+      default: e = launch_direct<32>(A, x, y, s); break;
+    }
+    SP_CUDA(e);
+    return SPMAT_OK;
+  }
   if (A->kernel_id == KERNEL_VECTOR) {
     switch (std::max(A->lanes, 4)) {
       case 4: launch_vector<4>(A, x, y, s); break;

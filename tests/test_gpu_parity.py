@@ -104,6 +104,14 @@ def test_single_rank_parity(sp, comm, case, values):
     A.close()
 
 
+def test_small_matrices_take_the_direct_kernel(sp, comm):
+    """Latency-bound sizes (C1: 0.3 MB) run the direct kernel, large ones the bulk-copy one."""
+    M, N, i, j, v = CASES["c1_5pt64"]("int")
+    A = sp.Mat(comm, M, N, M, N, dev(i), dev(j))
+    assert A.info()["spmv_kernel_id"] == 5
+    A.close()
+
+
 def test_p1_pins_on_gpu(sp, comm):
     """Closed forms evaluated by the GPU path: A.1 and polynomial x (P3, P4)."""
     n = 33
@@ -181,8 +189,11 @@ def test_random_coo_fuzz(sp, comm, seed):
     A.close()
 
 
-def test_long_rows(sp, comm):
-    """Rows longer than the row-block cap take the CTA-reduction path."""
+@pytest.mark.parametrize("kernel", ["tma", "direct"])
+def test_long_rows(sp, comm, kernel, monkeypatch):
+    """Rows longer than the row-block cap take the CTA-reduction path (bulk-copy kernel) or
+    the lane loop (direct kernel)."""
+    monkeypatch.setenv("SPMAT_SPMV_KERNEL", kernel)
     M, N = 50, 6000
     rows, cols = [], []
     for r in range(M):
@@ -197,6 +208,7 @@ def test_long_rows(sp, comm):
     A = sp.Mat(comm, M, N, M, N, dev(i), dev(j))
     A.set_values(dev(v))
     assert A.info()["max_row_nnz"] == 5000
+    assert A.info()["spmv_kernel_id"] == {"tma": 3, "direct": 5}[kernel]
     for values in ("int", "real"):
         x = synth.x_vector(0, N, values)
         y = torch.empty(M, dtype=torch.float64, device="cuda")
@@ -493,7 +505,7 @@ def test_every_row_many_blocks_per_cta(sp, comm, values):
     A.close()
 
 
-@pytest.mark.parametrize("kernel", ["tma", "stream", "vector"])
+@pytest.mark.parametrize("kernel", ["tma", "stream", "vector", "direct"])
 @pytest.mark.parametrize("case", ["7pt_ragged", "q1_9", "el_6", "c1_5pt64"])
 def test_kernel_variants(sp, comm, kernel, case, monkeypatch):
     """Every diagonal SpMV variant (chosen at create time) against the oracle."""
@@ -503,7 +515,7 @@ def test_kernel_variants(sp, comm, kernel, case, monkeypatch):
     O.set_values([v])
     x = synth.x_vector(0, N, "real")
     A, y = run_single(sp, comm, M, N, i, j, v, x)
-    assert A.info()["spmv_kernel_id"] == {"stream": 1, "vector": 2, "tma": 3}[kernel]
+    assert A.info()["spmv_kernel_id"] == {"stream": 1, "vector": 2, "tma": 3, "direct": 5}[kernel]
     assert rel_err(y, O.mult(x.numpy())) <= TOL
     # integer mode is exact in any summation order
     vi = CASES[case]("int")[4]
