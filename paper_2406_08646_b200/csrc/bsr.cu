@@ -336,10 +336,11 @@ __global__ void __launch_bounds__(kObT, 20)
                    const int32_t *__restrict__ ob_col, const double *__restrict__ ob_val,
                    const uint4 *ghost_base, int64_t ghost_stride, const double *lvec, double *y,
                    double *obuf, int64_t nobr, const HaloWait *__restrict__ waits, int nwaits,
-                   unsigned long long *epoch_ctr, unsigned int *counter, int *err) {
+                   unsigned long long *epoch_ctr, unsigned int *counter, int *err, int cur) {
   // the epoch counter is written only by the MatMult's last kernel, never by the block SpMV
-  // this grid overlaps, so it may be read before pdl_wait
-  const unsigned long long epoch = PEER ? *epoch_ctr + 1ull : 0ull;
+  // this grid overlaps, so it may be read before pdl_wait.  cur = 0: the lines of the last
+  // completed epoch (an isolated off-diagonal part, nothing to end)
+  const unsigned long long epoch = PEER ? *epoch_ctr + (cur ? 1ull : 0ull) : 0ull;
   const uint32_t flag = ll_flag(epoch);
   const uint4 *gl = PEER ? ghost_base + (int64_t)(epoch & 1) * ghost_stride : nullptr;
   const int sub = threadIdx.x & (W - 1);
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(kObT, 20)
       for (int i = 0; i < 3; ++i) y[r + i] = __dadd_rn(__ldcg(y + r + i), obuf[3 * q + i]);
     }
   }
-  if (!PEER) return;
+  if (!PEER || !cur) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -469,7 +470,8 @@ int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool trigge
 // y += A_o lvec on the 3x3 block copy.  overlapped: launched right after the block SpMV (which
 // then triggers dependents): a grid that fits beside it (A->ob_grid); else a full grid.
 template <int W>
-static cudaError_t launch_ob(spmat_s *A, double *y, const double *lvec, cudaStream_t s, unsigned grid) {
+static cudaError_t launch_ob(spmat_s *A, double *y, const double *lvec, cudaStream_t s, unsigned grid,
+                             int cur) {
   const bool peer = lvec == nullptr;
   return launch_pdl(peer ? k_offdiag_bsr3<W, true> : k_offdiag_bsr3<W, false>, grid, kObT, 0, s, (const int32_t *)A->ob_rows.get(),
                     (const int32_t *)A->ob_rowptr.get(), (const int32_t *)A->ob_col.get(),
@@ -477,19 +479,19 @@ static cudaError_t launch_ob(spmat_s *A, double *y, const double *lvec, cudaStre
                     A->ghost_stride, lvec, y, A->ob_buf.get(), A->obr,
                     peer ? (const HaloWait *)A->halo_waits.get() : nullptr, peer ? A->n_waits : 0,
                     peer ? A->d_epoch.get() : nullptr, peer ? A->halo_counter.get() : nullptr,
-                    peer ? A->halo_err.get() : nullptr);
+                    peer ? A->halo_err.get() : nullptr, cur);
 }
 
-int bsr_offdiag(spmat_s *A, double *y, const double *lvec, bool overlapped, cudaStream_t s) {
+int bsr_offdiag(spmat_s *A, double *y, const double *lvec, bool overlapped, cudaStream_t s, bool cur) {
   const int64_t work = A->obr * A->ob_w;
   unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + kObT - 1) / kObT, 16L * A->comm->num_sms));
   if (overlapped) grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid, A->ob_grid));
   cudaError_t e;
   switch (A->ob_w) {
-    case 1: e = launch_ob<1>(A, y, lvec, s, grid); break;
-    case 2: e = launch_ob<2>(A, y, lvec, s, grid); break;
-    case 8: e = launch_ob<8>(A, y, lvec, s, grid); break;
-    default: e = launch_ob<4>(A, y, lvec, s, grid); break;
+    case 1: e = launch_ob<1>(A, y, lvec, s, grid, cur ? 1 : 0); break;
+    case 2: e = launch_ob<2>(A, y, lvec, s, grid, cur ? 1 : 0); break;
+    case 8: e = launch_ob<8>(A, y, lvec, s, grid, cur ? 1 : 0); break;
+    default: e = launch_ob<4>(A, y, lvec, s, grid, cur ? 1 : 0); break;
   }
   SP_CUDA(e);
   return SPMAT_OK;

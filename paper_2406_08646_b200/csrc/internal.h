@@ -429,7 +429,8 @@ int csr_sync(spmat_s *A, cudaStream_t s);  // val_d from bval when set_values wr
 int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool trigger = false);
 // off-diagonal SpMV-add on the 3x3 block copy: NVLink ghost lines of this epoch (ends the
 // epoch, like k_spmv_offdiag_peer) or, with lvec != nullptr, the NCCL ghost vector
-int bsr_offdiag(spmat_s *A, double *y, const double *lvec, bool overlapped, cudaStream_t s);
+// cur: this MatMult's epoch (waits for its lines, ends the epoch); else the last completed one
+int bsr_offdiag(spmat_s *A, double *y, const double *lvec, bool overlapped, cudaStream_t s, bool cur = true);
 // host-buffer pipeline (single rank): row chunks of the diagonal SpMV
 int spmv_pipe_prepare(spmat_s *A, int chunks);  // chunk rows + the x columns each chunk reads
 int spmv_diag_chunk(spmat_s *A, const double *x, double *y, int k, cudaStream_t s);

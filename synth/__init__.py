@@ -127,6 +127,9 @@ def stencil_offsets(ndim: int, npts: int):
     if npts == 3 ** ndim:
         import itertools
         return [tuple(t) for t in itertools.product((-1, 0, 1), repeat=ndim)]
+    if ndim == 3 and npts == 45:  # Bump_2911-density box: 3 x 3 planes x 5 along the fastest axis
+        import itertools
+        return [tuple(t) for t in itertools.product((-1, 0, 1), (-1, 0, 1), (-2, -1, 0, 1, 2))]
     if npts == 5 ** ndim:  # Q2-like: every node within distance 2 per axis
         import itertools
         return [tuple(t) for t in itertools.product((-2, -1, 0, 1, 2), repeat=ndim)]
@@ -361,6 +364,9 @@ CONFIGS = {
     # variants: C4 per-GPU cubes in a box decomposition; Q2-like 125-point
     "c4b": dict(kind="box", local=(256, 256, 256), npts=7, per_gpu=True),
     "q2": dict(kind="stencil", shape=(96, 96, 96), npts=125, per_gpu=False),
+    # the density of the paper's Bump_2911 (~3 M rows, ~128 M nonzeros):
+    # a 45-point (5 x 3 x 3 box) stencil on 144^3 nodes -- 2.99 M rows, 132 M nonzeros
+    "bump": dict(kind="stencil", shape=(144, 144, 144), npts=45, per_gpu=False),
 }
 
 CONFIG_TEXT = {
@@ -371,6 +377,7 @@ CONFIG_TEXT = {
     "c5": "3D 3-dof 27-point elasticity-like 200^3, strong scaling",
     "c4b": "3D 7-point Laplacian 256^3 per GPU, box (cube) decomposition with renumbering",
     "q2": "3D 125-point (Q2-like) stencil 96^3",
+    "bump": "3D 45-point (5x3x3 box) stencil 144^3: Bump_2911 density (2.99 M rows, 132 M nnz)",
 }
 
 

@@ -80,6 +80,7 @@ CASES = {
     "el_6": lambda values: (3 * 6 ** 3,) * 2 + synth.elasticity_coo(6, values=values),
     "27pt_2d9": lambda values: (81, 81) + synth.stencil_coo((9, 9), 9, values=values),
     "q2_125pt": lambda values: (9 ** 3,) * 2 + synth.stencil_coo((9, 9, 9), 125, values=values),
+    "bump_45pt": lambda values: (13 * 11 * 9,) * 2 + synth.stencil_coo((13, 11, 9), 45, values=values),
 }
 
 

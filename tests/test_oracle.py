@@ -463,7 +463,8 @@ def test_sample_rows_matches_full_p1():
     assert np.array_equal(oracle.sample_rows(i, j, v, rows, x), A.mult(x)[rows])
 
 
-@pytest.mark.parametrize("shape,npts", [((64, 64), 5), ((9, 7, 6), 7), ((7, 7, 7), 125), ((11, 3, 5), 27)])
+@pytest.mark.parametrize("shape,npts", [((64, 64), 5), ((9, 7, 6), 7), ((7, 7, 7), 125), ((11, 3, 5), 27),
+                                        ((9, 7, 6), 45)])
 def test_csr_direct_equals_coo_assembly(shape, npts):
     """orc_csr_direct (the full-size timing path) is the COO definition specialised to
     duplicate-free, row-sorted COO: its CSR equals orc_create_coo + INSERT bit for bit, the
@@ -473,6 +474,8 @@ def test_csr_direct_equals_coo_assembly(shape, npts):
         A, ii, jj, vv = build_stencil(shape, npts, values=values)
         C = oracle.OracleCsr(M, M, ii[0], jj[0], vv[0])
         assert C.nnz == A.info(0, "nnz_d")
+        if npts == 45:  # box 5 x 3 x 3: per axis 5n-6 or 3n-2 in-grid (node, offset) pairs
+            assert C.nnz == (5 * shape[0] - 6) * (3 * shape[1] - 2) * (3 * shape[2] - 2)
         assert np.array_equal(C.rowptr, A.export(0, "rowptr_d"))
         assert np.array_equal(C.col[:C.nnz], A.export(0, "col_d"))
         assert np.array_equal(C.val[:C.nnz].view(np.int64), A.export(0, "val_d").view(np.int64))

@@ -7,7 +7,9 @@ vector updates, all scalars on the device, no host synchronisation), max over ra
 Context: 690 us (CG) vs 676 us (CGAsync) per iteration on Bump_2911
 (~3 M rows, 128 M nnz, 6 x V100); 300 vs 250 us on Kuu (~7 K rows, 340 K nnz).  The
 "kuu" config here is a synthetic of that size (3-dof 27-point on 13^3 nodes: 6.6 K rows,
-~0.5 M nnz); "bump" is a 7-point 144^3 grid (3 M rows) for scale.
+~0.5 M nnz); "bump" has Bump_2911's size AND density (synth config "bump": a 45-point 5x3x3
+box stencil on 144^3 nodes, 2.99 M rows, 132 M nonzeros, 44 per row); "bump7" is round 1's
+7-point 144^3 stand-in (same rows, 1/6 of the nonzeros).
 """
 import argparse
 import json
@@ -30,7 +32,7 @@ def problem(name, P, r):
         i, j, v = synth.elasticity_coo(n, values="int", device="cuda")
         keep = (i >= off[r]) & (i < off[r + 1])
         return i[keep], j[keep], v[keep], sizes
-    if name == "bump":
+    if name == "bump7":  # round-1 stand-in: the row count of Bump_2911, not its density
         shape = (144, 144, 144)
         sizes = synth.split_sizes(144 ** 3, P)
         off = synth.offsets_from_sizes(sizes)
