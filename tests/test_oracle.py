@@ -497,10 +497,10 @@ def test_csr_direct_equals_coo_assembly(shape, npts):
         coords.append(rem % n)
         rem = rem // n
     out = np.zeros(M)
-    for o in offs:
+    for o in offs:  # offsets are (d_slowest, ..., d_fastest), coords fastest first
         inside = np.ones(M, dtype=bool)
         for d, n in enumerate(shape):
-            c = coords[d] + o[d]
+            c = coords[d] + o[len(shape) - 1 - d]
             inside &= (c >= 0) & (c < n)
         out += ~inside
     assert np.array_equal(C.mult(np.ones(M)), out)
