@@ -136,6 +136,45 @@ class Clocks:
                 "sample_period_ms": 2}
 
 
+# ------------------------------------------------------------------ NVLink counters (NVML)
+class NvLink:
+    """Hardware NVLink byte counters of this GPU (NVML field values, summed over links): the
+    bytes the halo actually put on the wire, read around the timed trials.  Tries the byte
+    counters (NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES), then the throughput counters (KiB)."""
+    FIELDS = (("count_bytes", 202, 204, 1), ("throughput_kib", 138, 139, 1024))
+
+    def __init__(self, index):
+        self.h, self.field = None, None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            for f in self.FIELDS:
+                if self._read(f) is not None:
+                    self.field = f
+                    break
+        except Exception:
+            self.h = None
+
+    def _read(self, f):
+        tx = rx = 0
+        ok = 0
+        for link in range(18):
+            try:
+                a, b = self.nv.nvmlDeviceGetFieldValues(self.h, [(f[1], link), (f[2], link)])
+                if a.nvmlReturn == 0 and b.nvmlReturn == 0:
+                    tx += int(a.value.ullVal) * f[3]
+                    rx += int(b.value.ullVal) * f[3]
+                    ok += 1
+            except Exception:
+                return None
+        return (tx, rx) if ok else None
+
+    def read(self):
+        return self._read(self.field) if self.field else None
+
+
 # ------------------------------------------------------------------ byte / flop model
 def byte_model(info, m, n, bs=1):
     """Algorithmic bytes per MatMult (int32 indices, fp64 values); with 3x3
@@ -387,6 +426,8 @@ def main():
     # spmat_profile) for the roofline's kernel duration -- kept out of the headline trials,
     # where the extra event records would lengthen latency-bound steps (C1)
     clk = Clocks(local)
+    nvl = NvLink(local) if P > 1 else None
+    nvl0 = nvl.read() if nvl else None
     trials = []
     with clk:
         for _ in range(TRIALS):
@@ -400,6 +441,7 @@ def main():
             barrier()
             trials.append(max_over_ranks(ev0.elapsed_time(ev1) / 1e3 / a.steps))
         t_step = statistics.median(trials)
+        nvl1 = nvl.read() if nvl else None
         A.profile(True)
         A.profile_read()  # clear
         barrier()
@@ -535,6 +577,11 @@ def main():
                 "halo_nvlink_frac": (max(out_b, in_b) / th / 1e9 / NVLINK_GBPS) if th > 0 else None,
                 "note": "isolated halo = put kernel + wait for every ghost line + buffer release, "
                         "latency-bound at these sizes (0.5-2 MB)"}
+        if nvl0 and nvl1:  # hardware counters over the TRIALS x K timed MatMults (this rank)
+            ns = TRIALS * a.steps
+            halo["nvml_counter"] = nvl.field[0]
+            halo["nvml_tx_bytes_per_step"] = (nvl1[0] - nvl0[0]) / ns
+            halo["nvml_rx_bytes_per_step"] = (nvl1[1] - nvl0[1]) / ns
     gflops = 2 * nnz_global / t_step / 1e9
     gbs_gpu = (diag_bytes + off_bytes) / t_step / 1e9
     line = {

@@ -14,6 +14,7 @@
 // blocks in ascending column order and adds v_i0*x_0, v_i1*x_1, v_i2*x_2 for each block row i,
 // which with W = 1 is exactly the CSR row's left-to-right order.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <cstring>
@@ -38,6 +39,7 @@ struct __align__(16) BsrStage {
   int col[(kCapD / 9 + 11) & ~3];  // multiples of 4 ints keep every array 16-byte aligned
   int rp[(kMaxBR + 11) & ~3];
   int4 hdr;  // br0, br1, bp0, bp1
+  int4 ext;  // .x, .y: off-diagonal block rows [t0, t1) of this row block (fused MatMult)
 };
 constexpr size_t kBsrSmem = kStagesB * sizeof(BsrStage) + 2 * kStagesB * sizeof(unsigned long long);
 
@@ -187,14 +189,89 @@ __device__ __forceinline__ void brows_w(int br0, int br1, int bp0, const int *__
   }
 }
 
+// Fused off-diagonal blocks (NVLink halo): row blocks holding block rows with off-diagonal
+// blocks are claimed LAST (by then the neighbours' ghost lines, stored at the start of their
+// MatMult, have long landed); once the consumer warps have written such a block's diagonal
+// y (named barrier), they add its off-diagonal block rows y[3br+i] += sum_b A_o(br,b) g(b):
+// the off-diagonal product streams with the diagonal one instead of running as a separate
+// latency-bound kernel.  The last CTA to finish releases the ghost buffer and ends the epoch.
+struct BsrOff {
+  const int2 *range;                    // per claim index: [t0, t1); nullptr: not fused
+  const int32_t *rows, *rowptr, *col;   // ob_rows, ob_rowptr, ob_col
+  const double *val;                    // ob_val
+  const uint4 *ghost;                   // flagged ghost lines, buffer (epoch & 1) at ghost_stride
+  int64_t ghost_stride;
+  unsigned long long *epoch_ctr;
+  const HaloWait *waits;
+  int nwaits;
+  unsigned int *done;                   // CTAs whose consumers finished (epoch end)
+  int *err;
+};
+
+// W = 4 lanes per off-diagonal block row, every consumer thread of the CTA takes part
+// (uniform loop bound: all lanes reach the shuffles).  Not inlined: the hot diagonal loop keeps
+// its register budget.
+static __device__ __noinline__ void bsr_off_rows(const BsrOff off, int t0, int t1, double *y, int tid,
+                                                 unsigned long long epoch) {
+  constexpr int W = 4, U = 2;
+  const uint32_t flag = ll_flag(epoch);
+  const uint4 *gl = off.ghost + (int64_t)(epoch & 1) * off.ghost_stride;
+  const int sub = tid & (W - 1);
+  for (int base = t0; base < t1; base += kT / W) {
+    const int t = base + tid / W;
+    const bool valid = t < t1;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (valid) {
+      const int a = off.rowptr[t], z = off.rowptr[t + 1];
+      for (int e0 = a + sub; e0 < z; e0 += U * W) {
+        int c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) c[u] = e0 + u * W < z ? off.col[e0 + u * W] : -1;
+        uint4 raw[U][3];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (c[u] >= 0) raw[u][j] = ll_load_raw(gl + 3 * (int64_t)c[u] + j);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (c[u] < 0) continue;
+          const double *v = off.val + 9 * (int64_t)(e0 + u * W);
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const double g = ll_value(gl + 3 * (int64_t)c[u] + j, raw[u][j], flag, off.err);
+            s0 = __dadd_rn(s0, __dmul_rn(__ldg(v + j), g));
+            s1 = __dadd_rn(s1, __dmul_rn(__ldg(v + 3 + j), g));
+            s2 = __dadd_rn(s2, __dmul_rn(__ldg(v + 6 + j), g));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = W >> 1; o > 0; o >>= 1) {
+      s0 = __dadd_rn(s0, __shfl_down_sync(0xffffffffu, s0, o, W));
+      s1 = __dadd_rn(s1, __shfl_down_sync(0xffffffffu, s1, o, W));
+      s2 = __dadd_rn(s2, __shfl_down_sync(0xffffffffu, s2, o, W));
+    }
+    if (valid && sub == 0) {
+      const int64_t r = 3 * (int64_t)off.rows[t];
+      y[r] = __dadd_rn(y[r], s0);
+      y[r + 1] = __dadd_rn(y[r + 1], s1);
+      y[r + 2] = __dadd_rn(y[r + 2], s2);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kCtaT, 3)
     k_spmv_bsr3(const int4 *__restrict__ blocks, int n_blocks, const int32_t *__restrict__ browptr,
                 const int32_t *__restrict__ bcol, const double *__restrict__ bval,
                 const double *__restrict__ x, double *__restrict__ y, unsigned int *__restrict__ sched,
-                int trigger) {
+                const BsrOff off) {
   extern __shared__ __align__(128) unsigned char smem[];
   BsrStage *st = reinterpret_cast<BsrStage *>(smem);
-  if (trigger) pdl_trigger();  // let k_offdiag_bsr3 start beside this grid (see there)
+  // this MatMult's halo epoch (fused off-diagonal blocks): read by every CTA before its
+  // consumers finish, so before the last CTA stores it back
+  const unsigned long long epoch = off.range ? *off.epoch_ctr + 1ull : 0ull;
   unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + kStagesB * sizeof(BsrStage));
   unsigned long long *empty = full + kStagesB;
   const int tid = threadIdx.x, warp = tid >> 5, lane32 = tid & 31;
@@ -227,6 +304,12 @@ __global__ void __launch_bounds__(kCtaT, 3)
         return;
       }
       st[s].hdr = H;
+      if (off.range) {
+        const int2 rg = off.range[b];
+        st[s].ext = make_int4(rg.x, rg.y, 0, 0);
+      } else {
+        st[s].ext = make_int4(0, 0, 0, 0);
+      }
       const int64_t v0 = 9 * (int64_t)H.z, v1 = 9 * (int64_t)H.w;
       const int64_t va = v0 & ~1ll, ve = (v1 + 1) & ~1ll;
       const int ca = H.z & ~3, ce = (H.w + 3) & ~3;
@@ -248,6 +331,7 @@ __global__ void __launch_bounds__(kCtaT, 3)
     const int4 h = st[s].hdr;
     if (h.x < 0) break;
     const int br0 = h.x, br1 = h.y, bp0 = h.z;
+    const int t0 = st[s].ext.x, t1 = st[s].ext.y;
     const double *sv = st[s].val + ((9 * (int64_t)bp0) & 1);
     const int *sc = st[s].col + (bp0 & 3);
     const int *rp = st[s].rp - (br0 & ~3);
@@ -260,6 +344,22 @@ __global__ void __launch_bounds__(kCtaT, 3)
     else brows_w<32>(br0, br1, bp0, rp, sc, sv, x, y, tid);
     __syncwarp();
     if (lane32 == 0) mbar_arrive(&empty[s]);
+    if (t1 > t0) {  // this block's diagonal y is written by all consumer warps: add A_o g
+      asm volatile("bar.sync 1, %0;" ::"r"(kT) : "memory");
+      bsr_off_rows(off, t0, t1, y, tid, epoch);
+    }
+  }
+  if (off.range) {  // the last CTA whose consumers are done ends the MatMult's halo epoch
+    asm volatile("bar.sync 2, %0;" ::"r"(kT) : "memory");
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(off.done, 1u) == gridDim.x - 1) {
+        atomicExch(off.done, 0u);
+        __threadfence();
+        for (int w = 0; w < off.nwaits; ++w) st_release_sys(off.waits[w].peer_done, epoch);
+        *off.epoch_ctr = epoch;
+      }
+    }
   }
 }
 
@@ -323,23 +423,24 @@ __global__ void k_bsr_o_refresh(const int32_t *__restrict__ rowptr, const double
 // each block's 3 ghost values (flagged lines of this epoch, or the NCCL ghost vector) once for
 // the block's 3 rows, and adds v_i0*g_0, v_i1*g_1, v_i2*g_2 per row i (W = 1: the CSR row's
 // left-to-right order); then a shuffle tree over the W lanes.
-// Two phases.  Phase 1 -- every read of A_o and of the ghost lines, the latency-bound part --
-// runs BEFORE pdl_wait: the block SpMV triggers dependents at entry, and this kernel's CTAs
-// (kObT threads, <= 48 registers) fit in the registers the block SpMV's 3 CTAs per SM leave
-// free, so the whole phase overlaps the bandwidth-bound diagonal sweep.  Sums go to obuf.
-// Phase 2 after pdl_wait (the diagonal y is final): the SAME thread adds its sums into y.
-// The last CTA releases the ghost buffer to the senders and advances the epoch (NVLink mode).
-constexpr int kObT = 64;
+// Standalone kernel (NCCL ghost vector, isolated parts, SPMAT_BSR_FUSE=0); the full MatMult
+// with the NVLink halo adds the off-diagonal blocks inside k_spmv_bsr3 (bsr_off_rows).  The
+// last CTA releases the ghost buffer to the senders and advances the epoch (NVLink mode, cur).
+// (Measured and dropped: this kernel as a PDL dependent sized to fit beside the block SpMV,
+// doing its reads before pdl_wait -- 2 warps per SM starved by the saturated HBM: C5 P=4
+// 0.93 ms per MatMult against 0.74 ms sequential.)
+constexpr int kObT = 256;
 template <int W, bool PEER>
-__global__ void __launch_bounds__(kObT, 20)
+__global__ void __launch_bounds__(kObT)
     k_offdiag_bsr3(const int32_t *__restrict__ ob_rows, const int32_t *__restrict__ ob_rowptr,
                    const int32_t *__restrict__ ob_col, const double *__restrict__ ob_val,
                    const uint4 *ghost_base, int64_t ghost_stride, const double *lvec, double *y,
-                   double *obuf, int64_t nobr, const HaloWait *__restrict__ waits, int nwaits,
+                   int64_t nobr, const HaloWait *__restrict__ waits, int nwaits,
                    unsigned long long *epoch_ctr, unsigned int *counter, int *err, int cur) {
   // the epoch counter is written only by the MatMult's last kernel, never by the block SpMV
   // this grid overlaps, so it may be read before pdl_wait.  cur = 0: the lines of the last
   // completed epoch (an isolated off-diagonal part, nothing to end)
+  pdl_wait();
   const unsigned long long epoch = PEER ? *epoch_ctr + (cur ? 1ull : 0ull) : 0ull;
   const uint32_t flag = ll_flag(epoch);
   const uint4 *gl = PEER ? ghost_base + (int64_t)(epoch & 1) * ghost_stride : nullptr;
@@ -395,18 +496,10 @@ __global__ void __launch_bounds__(kObT, 20)
       s2 = __dadd_rn(s2, __shfl_down_sync(0xffffffffu, s2, o, W));
     }
     if (valid && sub == 0) {
-      obuf[3 * q] = s0;
-      obuf[3 * q + 1] = s1;
-      obuf[3 * q + 2] = s2;
-    }
-  }
-  pdl_wait();  // the diagonal SpMV's y is complete and visible
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nobr * W; base += step) {
-    const int64_t q = (base + threadIdx.x) / W;
-    if (q < nobr && sub == 0) {
       const int64_t r = 3 * (int64_t)ob_rows[q];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) y[r + i] = __dadd_rn(__ldcg(y + r + i), obuf[3 * q + i]);
+      y[r] = __dadd_rn(__ldcg(y + r), s0);
+      y[r + 1] = __dadd_rn(__ldcg(y + r + 1), s1);
+      y[r + 2] = __dadd_rn(__ldcg(y + r + 2), s2);
     }
   }
   if (!PEER || !cur) return;
@@ -418,6 +511,37 @@ __global__ void __launch_bounds__(kObT, 20)
       for (int w = 0; w < nwaits; ++w) st_release_sys(waits[w].peer_done, epoch);
       *epoch_ctr = epoch;  // this MatMult is done
     }
+  }
+}
+
+// per row block (br0, br1): off-diagonal block rows [t0, t1) with br0 <= ob_rows[t] < br1
+__global__ void k_bsr_obrange(const int4 *__restrict__ blk, int64_t nbk, const int32_t *__restrict__ ob_rows,
+                              int64_t nobr, int2 *__restrict__ rng, uint32_t *__restrict__ f_in,
+                              uint32_t *__restrict__ f_out) {
+  GSTRIDE(b, nbk) {
+    int64_t lo = 0, hi = nobr;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (ob_rows[mid] < blk[b].x) lo = mid + 1; else hi = mid;
+    }
+    const int64_t t0 = lo;
+    hi = nobr;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (ob_rows[mid] < blk[b].y) lo = mid + 1; else hi = mid;
+    }
+    rng[b] = make_int2((int)t0, (int)lo);
+    f_in[b] = lo > t0 ? 1u : 0u;
+    f_out[b] = lo > t0 ? 0u : 1u;
+  }
+}
+
+__global__ void k_bsr_permute(const int4 *__restrict__ nat, const int2 *__restrict__ rng,
+                              const int32_t *__restrict__ order, int64_t nbk, int4 *__restrict__ blk,
+                              int2 *__restrict__ out_rng) {
+  GSTRIDE(c, nbk) {
+    blk[c] = nat[order[c]];
+    out_rng[c] = rng[order[c]];
   }
 }
 
@@ -459,16 +583,30 @@ int csr_sync(spmat_s *A, cudaStream_t s) {
   return SPMAT_OK;
 }
 
-int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool trigger) {
+int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_off) {
+  BsrOff off{};
+  if (fuse_off) {  // NVLink halo: off-diagonal blocks inside the kernel, which ends the epoch
+    off.range = A->ob_range.get();
+    off.rows = A->ob_rows.get();
+    off.rowptr = A->ob_rowptr.get();
+    off.col = A->ob_col.get();
+    off.val = A->ob_val.get();
+    off.ghost = A->ghost.get();
+    off.ghost_stride = A->ghost_stride;
+    off.epoch_ctr = A->d_epoch.get();
+    off.waits = A->halo_waits.get();
+    off.nwaits = A->n_waits;
+    off.done = A->ob_done.get();
+    off.err = A->halo_err.get();
+  }
   k_spmv_bsr3<<<(unsigned)A->bsr_grid, kCtaT, kBsrSmem, s>>>(A->bblocks4.get(), (int)A->n_brblocks,
                                                            A->browptr.get(), A->bcol.get(), A->bval.get(),
-                                                           x, y, A->bsched.get(), trigger ? 1 : 0);
+                                                           x, y, A->bsched.get(), off);
   SP_LAUNCH();
   return SPMAT_OK;
 }
 
-// y += A_o lvec on the 3x3 block copy.  overlapped: launched right after the block SpMV (which
-// then triggers dependents): a grid that fits beside it (A->ob_grid); else a full grid.
+// y += A_o lvec on the 3x3 block copy (standalone kernel)
 template <int W>
 static cudaError_t launch_ob(spmat_s *A, double *y, const double *lvec, cudaStream_t s, unsigned grid,
                              int cur) {
@@ -476,16 +614,15 @@ static cudaError_t launch_ob(spmat_s *A, double *y, const double *lvec, cudaStre
   return launch_pdl(peer ? k_offdiag_bsr3<W, true> : k_offdiag_bsr3<W, false>, grid, kObT, 0, s, (const int32_t *)A->ob_rows.get(),
                     (const int32_t *)A->ob_rowptr.get(), (const int32_t *)A->ob_col.get(),
                     (const double *)A->ob_val.get(), peer ? (const uint4 *)A->ghost.get() : nullptr,
-                    A->ghost_stride, lvec, y, A->ob_buf.get(), A->obr,
+                    A->ghost_stride, lvec, y, A->obr,
                     peer ? (const HaloWait *)A->halo_waits.get() : nullptr, peer ? A->n_waits : 0,
                     peer ? A->d_epoch.get() : nullptr, peer ? A->halo_counter.get() : nullptr,
                     peer ? A->halo_err.get() : nullptr, cur);
 }
 
-int bsr_offdiag(spmat_s *A, double *y, const double *lvec, bool overlapped, cudaStream_t s, bool cur) {
+int bsr_offdiag(spmat_s *A, double *y, const double *lvec, cudaStream_t s, bool cur) {
   const int64_t work = A->obr * A->ob_w;
   unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + kObT - 1) / kObT, 16L * A->comm->num_sms));
-  if (overlapped) grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid, A->ob_grid));
   cudaError_t e;
   switch (A->ob_w) {
     case 1: e = launch_ob<1>(A, y, lvec, s, grid, cur ? 1 : 0); break;
@@ -518,7 +655,6 @@ static int bsr_o_setup(spmat_s *A, cudaStream_t st) {
   SP_TRY(A->ob_rowptr.alloc(nobr + 1));
   SP_TRY(A->ob_col.alloc(A->onnzb));
   SP_TRY(A->ob_val.alloc(9 * A->onnzb));
-  SP_TRY(A->ob_buf.alloc(3 * nobr));
   k_bsr_o_build<<<nb(nobr + 1), 256, 0, st>>>(A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(), nobr,
                                               A->ob_rows.get(), A->ob_rowptr.get(), A->ob_col.get());
   SP_LAUNCH();
@@ -529,8 +665,6 @@ static int bsr_o_setup(spmat_s *A, cudaStream_t st) {
     const int v = atoi(w);
     if (v == 1 || v == 2 || v == 4 || v == 8) A->ob_w = v;
   }
-  // CTAs that fit beside the block SpMV's CTAs: one per SM (kObT threads, <= 48 registers)
-  A->ob_grid = A->comm->num_sms;
   A->ob_ok = true;
   if (const char *e = getenv("SPMAT_BSR_OFFDIAG")) A->ob_ok = atoi(e) != 0;
   return SPMAT_OK;
@@ -539,6 +673,44 @@ static int bsr_o_setup(spmat_s *A, cudaStream_t st) {
 static int bsr_o_env(spmat_s *A) {
   const char *e = getenv("SPMAT_NUMERIC_BSR");
   A->env_numeric_csr = e && atoi(e) == 0;
+  e = getenv("SPMAT_BSR_FUSE");
+  A->env_no_bsr_fuse = e && atoi(e) == 0;
+  return SPMAT_OK;
+}
+
+// Claim order of the block SpMV with off-diagonal blocks: row blocks without off-diagonal
+// block rows first, the others last (by then every neighbour's ghost lines have landed), and
+// per claim index the range [t0, t1) of off-diagonal block rows inside the row block.
+static int bsr_claim_order(spmat_s *A, cudaStream_t st) {
+  const int64_t nbk = A->n_brblocks;
+  DevBuf<int4> nat;
+  DevBuf<int2> rng;
+  DevBuf<uint32_t> f_in, f_out;
+  DevBuf<int32_t> order;
+  DevBuf<int> dn;
+  DevBuf<char> tmp;
+  SP_TRY(nat.alloc(nbk));
+  SP_TRY(rng.alloc(nbk));
+  SP_TRY(f_in.alloc(nbk));
+  SP_TRY(f_out.alloc(nbk));
+  SP_TRY(order.alloc(nbk));
+  SP_TRY(dn.alloc(2));
+  SP_CUDA(cudaMemcpyAsync(nat.get(), A->bblocks4.get(), nbk * sizeof(int4), cudaMemcpyDeviceToDevice, st));
+  k_bsr_obrange<<<nb(nbk), 256, 0, st>>>(nat.get(), nbk, A->ob_rows.get(), A->obr, rng.get(), f_in.get(), f_out.get());
+  SP_LAUNCH();
+  CUB_CALL2(tmp, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes, thrust::counting_iterator<int32_t>(0),
+                                            f_out.get(), order.get(), dn.get(), (int)nbk, st));
+  int nfirst = 0;
+  SP_CUDA(cudaMemcpyAsync(&nfirst, dn.get(), 4, cudaMemcpyDeviceToHost, st));
+  SP_CUDA(cudaStreamSynchronize(st));
+  CUB_CALL2(tmp, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes, thrust::counting_iterator<int32_t>(0),
+                                            f_in.get(), order.get() + nfirst, dn.get() + 1, (int)nbk, st));
+  SP_TRY(A->ob_range.alloc(nbk));
+  k_bsr_permute<<<nb(nbk), 256, 0, st>>>(nat.get(), rng.get(), order.get(), nbk, A->bblocks4.get(), A->ob_range.get());
+  SP_LAUNCH();
+  SP_TRY(A->ob_done.alloc(1));
+  SP_CUDA(cudaMemsetAsync(A->ob_done.get(), 0, 4, st));
+  SP_CUDA(cudaStreamSynchronize(st));
   return SPMAT_OK;
 }
 
@@ -605,6 +777,7 @@ static int bsr_setup(spmat_s *A) {
                                                            std::max<int64_t>(A->n_brblocks, 1)));
   SP_TRY(bsr_o_setup(A, st));
   SP_TRY(bsr_o_env(A));
+  if (A->ob_ok && A->n_brblocks > 0) SP_TRY(bsr_claim_order(A, st));
   A->bs = 3;
   A->kernel_id = 4;
   if (A->values_set) SP_TRY(bsr_refresh(A, st));

@@ -928,7 +928,7 @@ int spmat_get_info(spmat_t A, int64_t info[32]) {
                    A->n_rowblocks, A->max_row_nnz, A->plan_builds,
                    A->bs, A->ob_ok ? 1 : 0, A->ob_ok ? A->ob_w : A->ro_w, mode,
                    A->stat_nccl_sent, A->stat_nccl_recv, A->stat_nvlink_put, A->stat_mults,
-                   A->stat_setvals, A->bs == 3 ? A->bsr_grid : A->tma_grid, A->ob_ok ? A->ob_grid : 0};
+                   A->stat_setvals, A->bs == 3 ? A->bsr_grid : A->tma_grid, 0};
   memcpy(info, v, sizeof v);
   return SPMAT_OK;
 }

@@ -386,17 +386,21 @@ struct spmat_s {
   spmat::DevBuf<unsigned int> bsched;
   // 3x3 block copy of the off-diagonal block (when it is made of aligned 3x3 blocks too):
   // block rows ob_rows (block-row ids), ob_rowptr, ob_col (ghost block = 3 consecutive ghost
-  // lines), ob_val (9 per block); ob_buf holds the per-row sums between the two phases of
-  // k_offdiag_bsr3 (bsr.cu)
+  // lines), ob_val (9 per block); ob_range: per claim index of the block SpMV, the block rows
+  // [t0, t1) of A_o in that row block (row blocks with off-diagonal block rows are claimed
+  // last, so the fused kernel adds them after the ghost lines have landed)
   bool ob_ok = false;
   // set_values wrote the diagonal values straight into bval (k_numeric_bsr3): val_d is stale
   // until csr_sync (export, MatMultTranspose, set_block_size(A, 1))
   bool val_d_stale = false;
   bool env_numeric_csr = false;  // SPMAT_NUMERIC_BSR=0: always val_d, then the bval copy
   int64_t obr = 0, onnzb = 0;
-  int ob_w = 4, ob_grid = 0;
+  int ob_w = 4;
+  bool env_no_bsr_fuse = false;  // SPMAT_BSR_FUSE=0: the standalone off-diagonal kernel
   spmat::DevBuf<int32_t> ob_rows, ob_rowptr, ob_col;
-  spmat::DevBuf<double> ob_val, ob_buf;
+  spmat::DevBuf<double> ob_val;
+  spmat::DevBuf<int2> ob_range;
+  spmat::DevBuf<unsigned int> ob_done;
   // host-buffer MatMult pipeline (mult.cu / spmv.cu), built on first use
   int pipe_chunks = 0;
   std::vector<int64_t> pipe_block, pipe_row, pipe_xmin, pipe_xneed;  // row-order block range, row range, x rows read
@@ -426,11 +430,13 @@ int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
 void cg_graph_release(spmat_s *A);            // drop the captured CG iteration
 int bsr_refresh(spmat_s *A, cudaStream_t s, bool diag = true);  // bval (diag) and ob_val from the CSR values
 int csr_sync(spmat_s *A, cudaStream_t s);  // val_d from bval when set_values wrote bval directly
-int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool trigger = false);
+// fuse_off: also add the 3x3 off-diagonal blocks from this epoch's ghost lines and end the
+// epoch (full MatMult, NVLink halo)
+int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_off = false);
 // off-diagonal SpMV-add on the 3x3 block copy: NVLink ghost lines of this epoch (ends the
 // epoch, like k_spmv_offdiag_peer) or, with lvec != nullptr, the NCCL ghost vector
 // cur: this MatMult's epoch (waits for its lines, ends the epoch); else the last completed one
-int bsr_offdiag(spmat_s *A, double *y, const double *lvec, bool overlapped, cudaStream_t s, bool cur = true);
+int bsr_offdiag(spmat_s *A, double *y, const double *lvec, cudaStream_t s, bool cur = true);
 // host-buffer pipeline (single rank): row chunks of the diagonal SpMV
 int spmv_pipe_prepare(spmat_s *A, int chunks);  // chunk rows + the x columns each chunk reads
 int spmv_diag_chunk(spmat_s *A, const double *x, double *y, int k, cudaStream_t s);

@@ -56,25 +56,25 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
     }
     // full MatMult, no long rows: the off-diagonal SpMV-add runs in the same kernel's tail
     const bool tail = fused && (part & 4) && A->n_ro > 0 && A->n_long == 0 && !A->env_no_tail;
-    // 3x3 blocks: the block off-diagonal kernel starts beside the block SpMV (PDL trigger) and
-    // does its A_o / ghost-line reads while the diagonal sweep runs (bsr.cu k_offdiag_bsr3)
+    // 3x3 blocks: the block SpMV adds the off-diagonal blocks of its boundary row blocks
+    // (claimed last) from this epoch's ghost lines and ends the epoch (bsr.cu bsr_off_rows)
     const bool ob = A->bs == 3 && A->ob_ok && (part & 6) == 6 && A->n_ro > 0;
-    const bool ob_overlap = ob && (part & 1) && !A->profile;
+    const bool ob_fused = ob && (part & 1) && A->m > 0 && !A->env_no_bsr_fuse;
     if (part & 1) {
       pe = A->profile ? prof_pair(A, 0) : nullptr;
       if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
       if (A->bs == 3 && A->m > 0)
-        SP_TRY(bsr_spmv(A, x, y, s, ob_overlap));
+        SP_TRY(bsr_spmv(A, x, y, s, ob_fused));
       else
         SP_TRY(spmv_diag(A, x, y, s, fused, tail));
       if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
     }
-    if (tail) return SPMAT_OK;
+    if (tail || ob_fused) return SPMAT_OK;
     if (part & 2) {
       pe = (A->profile && (part & 4) && A->n_ro > 0) ? prof_pair(A, 1) : nullptr;
       if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
       if (ob)
-        SP_TRY(bsr_offdiag(A, y, nullptr, ob_overlap, s));
+        SP_TRY(bsr_offdiag(A, y, nullptr, s));
       else
         SP_TRY(halo_peer_offdiag(A, y, s, (part & 4) != 0));
       if (pe) SP_CUDA(cudaEventRecord(pe[1], s));

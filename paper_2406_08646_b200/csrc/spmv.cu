@@ -709,7 +709,7 @@ int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t s) {
   if (A->n_ro == 0) return SPMAT_OK;
   if (A->bs == 3 && A->ob_ok)  // NCCL ghost vector, or (isolated part) the landed lines
-    return A->peer ? bsr_offdiag(A, y, nullptr, false, s, false) : bsr_offdiag(A, y, A->lvec.get(), false, s);
+    return A->peer ? bsr_offdiag(A, y, nullptr, s, false) : bsr_offdiag(A, y, A->lvec.get(), s);
   k_spmv_offdiag<<<nblk(A->ro_w == 1 ? (A->n_ro + kRowsU - 1) / kRowsU : A->n_ro * A->ro_w), 256, 0, s>>>(
       A->rows_o.get(), A->rowptr_o.get(), A->col_o.get(), A->val_o.get(), A->lvec.get(),
       A->peer ? A->ghost.get() : nullptr, A->ghost_stride, A->peer ? A->d_epoch.get() : nullptr, y,

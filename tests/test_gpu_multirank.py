@@ -52,20 +52,23 @@ def test_multirank_offdiag_lanes(ro_w, fuse):
     assert f"MULTIRANK P={P} failures=0" in r.stdout
 
 
-@pytest.mark.parametrize("env", [{"SPMAT_OB_W": "1"}, {"SPMAT_OB_W": "8"}, {"SPMAT_BSR_OFFDIAG": "0"},
-                                 {"SPMAT_PDL": "0"}, {"SPMAT_HALO": "nccl"}])
-def test_multirank_offdiag_3x3(env):
-    """The 3x3 block off-diagonal SpMV-add (k_offdiag_bsr3) with forced lanes per block row,
-    switched off (CSR off-diagonal kernels), without PDL (no overlap with the block SpMV), and
-    on the NCCL ghost vector -- elasticity cases (real and integer) and full-size C5."""
+ENV3 = [{"SPMAT_BSR_FUSE": "1"}, {"SPMAT_BSR_FUSE": "0", "SPMAT_OB_W": "1"},
+        {"SPMAT_BSR_FUSE": "0", "SPMAT_OB_W": "8"}, {"SPMAT_BSR_OFFDIAG": "0"}, {"SPMAT_HALO": "nccl"}]
+
+
+@pytest.mark.parametrize("k", range(len(ENV3)))
+def test_multirank_offdiag_3x3(k):
+    """3x3 off-diagonal blocks: added inside the block SpMV (default), by the standalone kernel
+    with forced lanes per block row, switched off (CSR off-diagonal kernels), and on the NCCL
+    ghost vector -- elasticity cases (real and integer) and full-size C5."""
+    env = ENV3[k]
     P = 2
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
     e = dict(os.environ)
     e.update(env)
     e["MP_CASES"] = "elasticity,full-c5"
-    port = 29721 + sorted(["SPMAT_OB_W1", "SPMAT_OB_W8", "SPMAT_BSR_OFFDIAG0", "SPMAT_PDL0", "SPMAT_HALOnccl"]).index(
-        "".join(k + v for k, v in env.items()))
+    port = 29721 + k
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(HERE, "mp_gpu_parity.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=e)
