@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--values", default="real", choices=["real", "int"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="launch every MatMult from Python (no CUDA graph)")
     ap.add_argument("--kernel", default=None, help="SPMAT_SPMV_KERNEL override")
     ap.add_argument("--block-size", type=int, default=None,
                     help="spmat_set_block_size (default: 3 for the 3-dof config c5, else 1)")
@@ -284,6 +285,12 @@ def run_oracle(cfg, P=1, reps=3):
                       f"(gcc -O2 -ffp-contract=off), 1 thread and {nt} threads (row slices)"}
 
 
+def sdist_agree_launch(launch, max_over_ranks):
+    """Every rank times the same way: graphs only if every rank captured one."""
+    ok = 0.0 if launch == "cuda_graph" else 1.0
+    return launch if max_over_ranks(ok) == 0.0 else ("eager" if launch == "cuda_graph" else launch)
+
+
 # ------------------------------------------------------------------ shared line parts
 def config_dict(cfg, P, values):
     """The workload as both arms name it (computed from the config alone, so the reference
@@ -420,6 +427,32 @@ def main():
         A.mult(x, y, stream)
     torch.cuda.synchronize()
 
+    # ---- the K MatMults of a trial captured once as a CUDA graph (the launch-bound small
+    # configs would otherwise measure Python's launch rate); NCCL-mode halos stay eager
+    launch, graph = "eager", None
+    if not a.eager and (P == 1 or A.halo_mode() == 2):
+        try:
+            gs = torch.cuda.Stream()
+            gs.wait_stream(stream)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=gs):
+                for _ in range(a.steps):
+                    A.mult(x, y, gs)
+            stream.wait_stream(gs)
+            for _ in range(2):
+                graph.replay()
+            y2 = torch.empty_like(y)
+            A.mult(x, y2, stream)  # the replayed MatMult equals an eager one bit for bit
+            torch.cuda.synchronize()
+            launch = "cuda_graph" if torch.equal(y, y2) else "eager (graph result differs)"
+            del y2
+        except Exception as ex:  # capture refused: time eager launches instead
+            graph, launch = None, f"eager (graph capture failed: {type(ex).__name__})"
+            torch.cuda.synchronize()
+    launch = sdist_agree_launch(launch, max_over_ranks)
+    if not launch.startswith("cuda_graph"):
+        graph = None
+
     # ---- timed region: TRIALS trials of exactly K MatMults each, barrier + sync on both sides
     # of every trial, max over ranks per trial, median over trials; then one
     # more trial of K MatMults with per-kernel CUDA events on the launching stream (in-library,
@@ -434,8 +467,11 @@ def main():
             barrier()
             torch.cuda.synchronize()
             ev0.record(stream)
-            for _ in range(a.steps):
-                A.mult(x, y, stream)
+            if graph is not None:
+                graph.replay()
+            else:
+                for _ in range(a.steps):
+                    A.mult(x, y, stream)
             ev1.record(stream)
             torch.cuda.synchronize()
             barrier()
@@ -592,6 +628,7 @@ def main():
         "steps": a.steps,
         "warmup": a.warmup,
         "trials": TRIALS,
+        "launch": launch,
         "ms_per_step": t_step * 1e3,
         "trials_ms_per_step": [t * 1e3 for t in trials],
         "higher_is_better": True,

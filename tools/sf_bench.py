@@ -79,6 +79,32 @@ def main():
             us = sd.max_over_ranks(e0.elapsed_time(e1) * 1e3 / niter / 2)
             res[f"{name}_us"] = us
             res[f"{name}_GBps"] = 8 * n / us / 1e3
+            if "--breakdown" in sys.argv and n >= (1 << 18) and name == "replace":
+                # per-call device time of each half on each rank (eager, events between calls):
+                # rank 0's bcast_begin = the put kernel (stores over NVLink), rank 1's
+                # bcast_end = the consuming kernel (waits for the lines, copies them out)
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+                acc = [0.0] * 4
+                for _ in range(niter):
+                    sd.barrier()
+                    torch.cuda.synchronize()
+                    ev[0].record(stream)
+                    sf.bcast_begin(rdata, ldata, op, stream)
+                    ev[1].record(stream)
+                    sf.bcast_end(rdata, ldata, op, stream)
+                    ev[2].record(stream)
+                    sf.reduce_begin(ldata, rdata, op, stream)
+                    ev[3].record(stream)
+                    sf.reduce_end(ldata, rdata, op, stream)
+                    ev[4].record(stream)
+                    torch.cuda.synchronize()
+                    for k in range(4):
+                        acc[k] += ev[k].elapsed_time(ev[k + 1]) * 1e3 / niter
+                allp = [None, None]
+                torch.distributed.all_gather_object(allp, acc)
+                res["breakdown_us"] = {"rank0_bcast_begin(put)": allp[0][0], "rank1_bcast_end(take)": allp[1][1],
+                                       "rank1_reduce_begin(put)": allp[1][2], "rank0_reduce_end(take)": allp[0][3]}
+                res["put_GBps"] = 8 * n / allp[0][0] / 1e3 if allp[0][0] > 0 else None
         rows.append(res)
         sf.close()
     if r == 0:
