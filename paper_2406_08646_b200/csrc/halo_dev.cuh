@@ -272,7 +272,7 @@ constexpr int kRowsU = 4;  // rows per thread of the one-lane-per-row off-diagon
 static __device__ __noinline__ void tail_warp(const SpmvTail tail, unsigned long long epoch, int *err,
                                               double *y, unsigned long long *trc, int consumer_warps) {
   const int lane = threadIdx.x & 31;
-  if (lane == 0) {
+  if (lane == 0 && !tail.blk_done) {
     // short backoff: with box partitions 444 warps may wait the whole sweep here
     const unsigned target = (unsigned)(consumer_warps * tail.n_bblocks);
     const long long t0 = clock64();
@@ -298,6 +298,23 @@ static __device__ __noinline__ void tail_warp(const SpmvTail tail, unsigned long
     if (lane == 0) c = atomicAdd(tail.ctr + 1, 1u);
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c >= n_chunks) break;
+    if (tail.blk_done) {  // progressive: wait until the row blocks holding this chunk's rows are done
+      if (lane == 0) {
+        const int2 bb = tail.chunk_blk[c];
+        const long long t0 = clock64();
+        unsigned ns = 32;
+        for (int b = bb.x; b <= bb.y; ++b)
+          while (ld_acquire_gpu(tail.blk_done + b) != flag) {
+            if (clock64() - t0 > kSpinLimit) {
+              atomicExch(err, 2);
+              break;
+            }
+            __nanosleep(ns);
+            ns = ns < 256 ? 2 * ns : ns;
+          }
+      }
+      __syncwarp();
+    }
     if (w == 1) {
       offdiag_rows_u<kRowsU>(c * per + lane, 32, tail.n_ro, tail.rows, tail.rowptr, tail.col, tail.val, gl,
                              nullptr, flag, err, y);
