@@ -148,7 +148,11 @@ int sf_destroy(sf_t sf);
    all work already queued on the device (cudaDeviceSynchronize), so device coo_i/coo_j may
    come from kernels on any stream.
    Errors: SPMAT_ERR_RANGE if i >= M or j >= N (message names the rank and k; reported on
-   every rank), SPMAT_ERR_MISMATCH if ranks disagree on M, N or the local sizes. */
+   every rank), SPMAT_ERR_MISMATCH if ranks disagree on M, N or the local sizes,
+   SPMAT_ERR_ARG for m_local >= 2^31, ncoo >= 2^32, null coo_i/coo_j with ncoo > 0, or more
+   than 2^31 contributions on a rank.  An error found on one rank only (an argument, an
+   allocation) is agreed on before the next collective step: every rank returns an error
+   (the others "failed on another rank") instead of blocking in NCCL. */
 int spmat_create_coo(spmat_comm_t comm, int64_t m_local, int64_t n_local, int64_t M,
                      int64_t N, int64_t ncoo, const int64_t *coo_i, const int64_t *coo_j,
                      spmat_t *out);
@@ -158,7 +162,10 @@ int spmat_create_coo(spmat_comm_t comm, int64_t m_local, int64_t n_local, int64_
    the comm stream, overlapped with the kernel that finishes every nonzero whose
    contributions are all local; nonzeros with received contributions are finished after the
    exchange.  Each nonzero is summed by one thread in ascending (src rank, k) order: no
-   atomics, deterministic.  Collective. */
+   atomics, deterministic.  After spmat_set_block_size(A, 3) (and when no
+   contribution is received from another rank) the diagonal values are summed straight into
+   the 3x3 block copy; the CSR copy is brought up to date when it is needed (export,
+   MatMultTranspose, set_block_size(A, 1)).  Collective. */
 int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream);
 
 /* MatMult y = A x.  x: n_local doubles, y: m_local doubles, x != y.
@@ -166,7 +173,12 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream);
    diagonal-block SpMV on `stream`, bcast_end, off-diagonal SpMV-add on `stream`.
    Host pointers (pinned or pageable; memtype detected as in P:252-260): x is copied to the
    device and y back inside the call's stream order; the call then returns after y is
-   written.  Collective. */
+   written.  Collective.
+   NVLink halo: a peer that never delivers (bounded device spins, ~20 s) makes the affected
+   ghost values 0.0 and sets an error word that the call itself cannot report without a
+   host synchronisation -- spmat_check() reports it (SPMAT_ERR_NCCL).  The fused kernel
+   (comm warps spinning on peer data) is launched cooperatively, so every CTA is resident
+   or the launch fails. */
 int spmat_mult(spmat_t A, const double *x, double *y, void *stream);
 
 /* MatMultTranspose: y = A^T x (collective, enqueue-only).  x: DEVICE array of m_local doubles
@@ -184,7 +196,10 @@ int spmat_mult_transpose(spmat_t A, const double *x, double *y, void *stream);
    3 dofs per node) and from then on multiplies it from a 3x3 block-CSR copy (8.44 instead of
    12 bytes per nonzero), refreshed after every spmat_set_values_coo; bs = 1 returns to CSR.
    SPMAT_ERR_ARG if the structure is not blocked (the matrix keeps CSR).  Local, host-
-   synchronising. */
+   synchronising.  With several ranks, an off-diagonal block made of aligned 3x3 blocks too
+   (node-block COO) is also kept as 3x3 blocks and multiplied by its own kernel
+   (SPMAT_BSR_OFFDIAG=0: the CSR off-diagonal kernels; SPMAT_BSR_FUSE=1: added inside the
+   block SpMV instead of after it). */
 int spmat_set_block_size(spmat_t A, int bs);
 
 /* Parts of MatMult for isolated timing: part bit 1 = diagonal SpMV (y = A_d x), bit 2 =

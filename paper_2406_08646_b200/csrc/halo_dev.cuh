@@ -158,7 +158,8 @@ __device__ __forceinline__ void offdiag_row_w(int64_t q, bool valid, int W,
                                               const int32_t *__restrict__ rowptr,
                                               const int32_t *__restrict__ col,
                                               const double *__restrict__ val, const uint4 *gl,
-                                              const double *lv, uint32_t flag, int *err, double *y) {
+                                              const double *lv, uint32_t flag, int *err, double *y,
+                                              double *obuf = nullptr) {
   constexpr int KB = 4;
   const int sub = threadIdx.x & (W - 1);
   double s = 0.0;
@@ -193,8 +194,12 @@ __device__ __forceinline__ void offdiag_row_w(int64_t q, bool valid, int W,
   }
   for (int o = W >> 1; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o, W));
   if (valid && sub == 0) {
-    const int r = rows[q];
-    y[r] = __dadd_rn(__ldcg(y + r), s);
+    if (obuf) {  // split tail: the sum alone, added into y after the sweep
+      obuf[q] = s;
+    } else {
+      const int r = rows[q];
+      y[r] = __dadd_rn(__ldcg(y + r), s);
+    }
   }
 }
 
@@ -209,7 +214,8 @@ __device__ __forceinline__ void offdiag_rows_u(int64_t q0, int64_t stride, int64
                                                const int32_t *__restrict__ rowptr,
                                                const int32_t *__restrict__ col,
                                                const double *__restrict__ val, const uint4 *gl,
-                                               const double *lv, uint32_t flag, int *err, double *y) {
+                                               const double *lv, uint32_t flag, int *err, double *y,
+                                               double *obuf = nullptr) {
   int a[U], b[U];
   double s[U];
 #pragma unroll
@@ -248,6 +254,12 @@ __device__ __forceinline__ void offdiag_rows_u(int64_t q0, int64_t stride, int64
         if (c[u] >= 0) s[u] = __dadd_rn(s[u], __dmul_rn(v[u], g[u]));
     }
   }
+  if (obuf) {  // split tail: the sums alone, added into y after the sweep
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (q0 + u * stride < nro) obuf[q0 + u * stride] = s[u];
+    return;
+  }
   int r[U];
   double yo[U];
 #pragma unroll
@@ -269,10 +281,101 @@ constexpr int kRowsU = 4;  // rows per thread of the one-lane-per-row off-diagon
 // 251.6 us).  The last comm warp to finish releases the ghost buffer to the senders and
 // resets the counters for the next launch.  Not inlined, and not called from the consumer
 // path: either raised the streaming loop's register demand (C4 P=1 262 -> 302 us measured).
+// Split tail (boundary rows in most row blocks, e.g. box partitions; natural claim order):
+// while the consumers sweep, the comm warps compute every off-diagonal row's sum from the ghost
+// lines into obuf -- no dependence on y; once all row blocks are written (every consumer warp
+// adds its block count to ctr[0] when it finishes), they add obuf into y, a short
+// bandwidth-bound pass instead of the whole latency-bound tail after the sweep.
+static __device__ __forceinline__ bool wait_ctr(const unsigned *c, unsigned target, int *err) {
+  const long long t0 = clock64();
+  unsigned ns = 64;
+  while (ld_acquire_gpu(c) < target) {
+    if (clock64() - t0 > kSpinLimit) {
+      atomicExch(err, 2);
+      return false;
+    }
+    __nanosleep(ns);
+    ns = ns < 256 ? 2 * ns : ns;
+  }
+  return true;
+}
+
+static __device__ __noinline__ void split_tail(const SpmvTail tail, unsigned long long epoch, int *err,
+                                               double *y, unsigned long long *trc, int consumer_warps) {
+  const int lane = threadIdx.x & 31;
+  const uint4 *gl = tail.ghost + (int64_t)(epoch & 1) * tail.ghost_stride;
+  const uint32_t flag = ll_flag(epoch);
+  const int w = tail.w;
+  const int64_t per = w == 1 ? 32 * kRowsU : 32 / w;
+  const int64_t n_chunks = (tail.n_ro + per - 1) / per;
+  for (;;) {  // 1. sums
+    int64_t c = 0;
+    if (lane == 0) c = atomicAdd(tail.ctr + 1, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= n_chunks) break;
+    if (w == 1) {
+      offdiag_rows_u<kRowsU>(c * per + lane, 32, tail.n_ro, tail.rows, tail.rowptr, tail.col, tail.val, gl,
+                             nullptr, flag, err, y, tail.obuf);
+    } else {
+      const int64_t q = c * per + lane / w;
+      offdiag_row_w(q, q < tail.n_ro, w, tail.rows, tail.rowptr, tail.col, tail.val, gl, nullptr, flag, err, y,
+                    tail.obuf);
+    }
+  }
+  // 2. every row block written (and this warp's sums visible: the fence below orders them
+  //    before the adds of any warp that reads them after the same counter)
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    atomicAdd(tail.ctr + 3, 1u);  // comm warps whose sums are out
+    wait_ctr(tail.ctr, (unsigned)(consumer_warps * tail.n_bblocks), err);
+    wait_ctr(tail.ctr + 3, gridDim.x, err);
+    if (trc) trc[4] = gtimer();
+  }
+  __syncwarp();
+  const int64_t per2 = 32 * 8;  // 3. y[rows[q]] += obuf[q], 8 rows per lane in flight
+  const int64_t n2 = (tail.n_ro + per2 - 1) / per2;
+  for (;;) {
+    int64_t c = 0;
+    if (lane == 0) c = atomicAdd(tail.ctr + 4, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= n2) break;
+    int r[8];
+    double o[8], yv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t q = c * per2 + u * 32 + lane;
+      r[u] = q < tail.n_ro ? tail.rows[q] : -1;
+      o[u] = q < tail.n_ro ? __ldcg(tail.obuf + q) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) yv[u] = r[u] >= 0 ? __ldcg(y + r[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (r[u] >= 0) y[r[u]] = __dadd_rn(yv[u], o[u]);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    if (trc) trc[5] = gtimer();
+    __threadfence();
+    if (atomicAdd(tail.ctr + 2, 1u) == gridDim.x - 1) {
+      for (int k = 0; k < 5; ++k)
+        if (k != 2) atomicExch(tail.ctr + k, 0u);
+      atomicExch(tail.ctr + 2, 0u);
+      __threadfence();
+      for (int q = 0; q < tail.nwaits; ++q) st_release_sys(tail.waits[q].peer_done, epoch);
+    }
+  }
+}
+
 static __device__ __noinline__ void tail_warp(const SpmvTail tail, unsigned long long epoch, int *err,
                                               double *y, unsigned long long *trc, int consumer_warps) {
   const int lane = threadIdx.x & 31;
-  if (lane == 0 && !tail.blk_done) {
+  if (tail.obuf) {  // split tail: sums first (ghost lines only), the y adds after the sweep
+    split_tail(tail, epoch, err, y, trc, consumer_warps);
+    return;
+  }
+  if (lane == 0) {
     // short backoff: with box partitions 444 warps may wait the whole sweep here
     const unsigned target = (unsigned)(consumer_warps * tail.n_bblocks);
     const long long t0 = clock64();
@@ -298,23 +401,6 @@ static __device__ __noinline__ void tail_warp(const SpmvTail tail, unsigned long
     if (lane == 0) c = atomicAdd(tail.ctr + 1, 1u);
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c >= n_chunks) break;
-    if (tail.blk_done) {  // progressive: wait until the row blocks holding this chunk's rows are done
-      if (lane == 0) {
-        const int2 bb = tail.chunk_blk[c];
-        const long long t0 = clock64();
-        unsigned ns = 32;
-        for (int b = bb.x; b <= bb.y; ++b)
-          while (ld_acquire_gpu(tail.blk_done + b) != flag) {
-            if (clock64() - t0 > kSpinLimit) {
-              atomicExch(err, 2);
-              break;
-            }
-            __nanosleep(ns);
-            ns = ns < 256 ? 2 * ns : ns;
-          }
-      }
-      __syncwarp();
-    }
     if (w == 1) {
       offdiag_rows_u<kRowsU>(c * per + lane, 32, tail.n_ro, tail.rows, tail.rowptr, tail.col, tail.val, gl,
                              nullptr, flag, err, y);

@@ -293,13 +293,13 @@ struct SpmvTail {                      // fused off-diagonal SpMV-add (comm warp
   int64_t n_ro;
   const HaloWait *waits;
   int nwaits, w;                       // w: lanes per off-diagonal row (power of two <= 32)
-  unsigned int *ctr;                   // [0] boundary-block warps done, [1] chunk claims, [2] comm warps done
+  unsigned int *ctr;                   // [0] boundary-block warps done, [1] chunk claims, [2] comm warps done,
+                                       // [3] split tail: comm warps with sums out, [4] add-pass claims
   unsigned long long *trace;           // SPMAT_TRACE=1: globaltimer stamps (nullptr = off)
-  // progressive tail (boundary rows in most row blocks, e.g. box partitions): natural claim
-  // order; the producer publishes each consumed row block (blk_done[claim] = epoch) and a
-  // comm warp starts off-diagonal chunk c once the row blocks [chunk_blk[c].x, .y] are done
-  unsigned int *blk_done;              // nullptr: boundary-blocks-first mode
-  const int2 *chunk_blk;
+  // split tail (boundary rows in most row blocks, e.g. box partitions): natural claim order,
+  // every block counts as a boundary block; the off-diagonal sums go to obuf during the sweep
+  // and are added into y after it (halo_dev.cuh split_tail)
+  double *obuf;                        // nullptr: boundary-blocks-first tail
 };
 
 // ------------------------------------------------------------------ matrix
@@ -347,9 +347,8 @@ struct spmat_s {
   spmat::DevBuf<int32_t> block_order;  // boundary row blocks first (fused off-diagonal tail)
   spmat::DevBuf<int4> blocks4;         // (r0, r1, p0, p1) per row block in claim order
   int64_t n_bblocks = 0;
-  bool tail_progressive = false;       // SpmvTail.blk_done mode (boundary rows in most row blocks)
-  spmat::DevBuf<unsigned int> blk_done;
-  spmat::DevBuf<int2> chunk_blk;
+  bool tail_split = false;             // SpmvTail.obuf mode (boundary rows in most row blocks)
+  spmat::DevBuf<double> tail_obuf;
   spmat::DevBuf<unsigned int> tail_ctr;
   spmat::DevBuf<unsigned long long> trace;  // SPMAT_TRACE: [cta][kTraceCta] globaltimer stamps + header
   spmat::DevBuf<unsigned int> sched; // its block counter + finished-CTA counter

@@ -113,26 +113,6 @@ __global__ void k_boundary_blocks(const int2 *__restrict__ rb, int64_t nb, const
   }
 }
 
-// chunk c of the off-diagonal rows [c*per, min(nro, (c+1)*per)): the row blocks holding its
-// first and last row (natural order: claim index = row block index)
-__global__ void k_chunk_blocks(const int32_t *__restrict__ rows_o, int64_t nro, int64_t per,
-                               const int2 *__restrict__ rb, int64_t nb, int2 *__restrict__ out, int64_t nch) {
-  GRID_STRIDE(c, nch) {
-    const int64_t q0 = c * per, q1 = min(nro, q0 + per) - 1;
-    int bb[2];
-    for (int k = 0; k < 2; ++k) {
-      const int r = rows_o[k ? q1 : q0];
-      int64_t lo = 0, hi = nb - 1;  // last b with rb[b].x <= r
-      while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (rb[mid].x <= r) lo = mid; else hi = mid - 1;
-      }
-      bb[k] = (int)lo;
-    }
-    out[c] = make_int2(bb[0], bb[1]);
-  }
-}
-
 // blocks4[c] = (r0, r1, p0, p1) of the row block claimed c-th (order == nullptr: identity)
 __global__ void k_blocks4(const int2 *__restrict__ rb, const int32_t *__restrict__ order, int64_t nb,
                           int4 *__restrict__ out) {
@@ -233,31 +213,12 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
     int b_next = (int)atomicAdd(sched, 1u);
     int4 H = make_int4(0, 0, 0, 0);
     if (b < n_total) bounds(b, H);
-    // progressive tail: the claim index staged in each stage; once a stage's empty barrier
-    // completes, its row block is fully consumed (the consumers' y stores precede their
-    // arrivals), and the producer publishes it for the comm warps (fence + flag = epoch)
-    int bq[kStages];
-    const uint32_t eflag = (uint32_t)epoch;
-    auto publish_block = [&](int c) {
-      __threadfence();
-      atomicExch(tail.blk_done + c, eflag);
-    };
     for (int it = 0;; ++it) {
       const int s = it % kStages;
       if (it >= kStages) mbar_wait(&empty[s], (uint32_t)(((it / kStages) - 1) & 1));
-      const int done_b = (tail.blk_done && it >= kStages) ? bq[s] : -1;
       if (b >= n_total) {  // out of work: terminal header, then hand the counter back
         st[s].hdr = make_int4(-1, 0, 0, 0);
         mbar_arrive_tx(&full[s], 0);
-        if (tail.blk_done) {  // publish the blocks still in flight once they are consumed
-          if (done_b >= 0) publish_block(done_b);
-          for (int j = it - kStages + 1; j < it; ++j) {
-            if (j < 0) continue;
-            const int s2 = j % kStages;
-            mbar_wait(&empty[s2], (uint32_t)((j / kStages) & 1));
-            publish_block(bq[s2]);
-          }
-        }
         __threadfence();
         if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
           atomicExch(sched, 0u);
@@ -282,8 +243,6 @@ __global__ void __launch_bounds__(kCtaThreads, 3)
           bulk_g2s(st[s].rp, rowptr + ra, (re - ra) * 4, &full[s], policy);
         }
       }
-      bq[s] = b;
-      if (done_b >= 0) publish_block(done_b);  // after the next copy is on its way
       b = b_next;
       if (b < n_total) {
         b_next = (int)atomicAdd(sched, 1u);
@@ -614,11 +573,11 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
     SP_CUDA(cudaMemcpyAsync(A->longrows.get(), longrows.get(), (size_t)nlong * 4, cudaMemcpyDeviceToDevice, st));
   SP_TRY(A->sched.alloc(2));
   SP_CUDA(cudaMemsetAsync(A->sched.get(), 0, 8, st));
-  SP_TRY(A->tail_ctr.alloc(3));
-  SP_CUDA(cudaMemsetAsync(A->tail_ctr.get(), 0, 12, st));
+  SP_TRY(A->tail_ctr.alloc(5));
+  SP_CUDA(cudaMemsetAsync(A->tail_ctr.get(), 0, 20, st));
 
   A->n_bblocks = 0;
-  A->tail_progressive = false;
+  A->tail_split = false;
   if (A->n_ro > 0) {  // claim order for the fused off-diagonal tail: boundary blocks first
     const int64_t nbk = A->n_rowblocks;
     DevBuf<uint32_t> f1, f0;
@@ -640,22 +599,15 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
                                              A->block_order.get() + nbb, dn2.get() + 1, (int)nbk, st));
     A->n_bblocks = nbb;
     // Boundary rows in most row blocks (box partitions): boundary-first would sweep the matrix
-    // twice and, in natural order, a tail after the whole sweep idles; instead the natural
-    // order with per-block completion flags -- the comm warps add each chunk of off-diagonal
-    // rows as soon as the row blocks holding them are consumed (SpmvTail.blk_done)
-    const char *pe = getenv("SPMAT_PROGRESSIVE_TAIL");
-    A->tail_progressive = pe ? atoi(pe) != 0 : 2 * nbb > nbk;
-    if (A->tail_progressive) {
+    // twice (the diagonal SpMV alone loses ~6 %), and in natural order the latency-bound tail
+    // waits for the whole sweep; instead natural order with the split tail -- sums during the
+    // sweep, one short add pass after it (halo_dev.cuh split_tail)
+    const char *pe = getenv("SPMAT_SPLIT_TAIL");
+    A->tail_split = pe ? atoi(pe) != 0 : 2 * nbb > nbk;
+    if (A->tail_split) {
       A->block_order.release();
-      A->n_bblocks = 0;
-      const int64_t per = A->ro_w == 1 ? 32 * kRowsU : 32 / A->ro_w;
-      const int64_t nch = (A->n_ro + per - 1) / per;
-      SP_TRY(A->chunk_blk.alloc(nch));
-      SP_TRY(A->blk_done.alloc(nbk));
-      SP_CUDA(cudaMemsetAsync(A->blk_done.get(), 0, nbk * 4, st));
-      k_chunk_blocks<<<nblk(nch), 256, 0, st>>>(A->rows_o.get(), A->n_ro, per, A->rbp.get(), nbk,
-                                                A->chunk_blk.get(), nch);
-      SP_LAUNCH();
+      A->n_bblocks = nbk;  // every block counts: the add pass waits for the whole sweep
+      SP_TRY(A->tail_obuf.alloc(A->n_ro));
     }
   }
   SP_TRY(A->blocks4.alloc(A->n_rowblocks));
@@ -697,10 +649,7 @@ static cudaError_t launch_tma(spmat_s *A, const double *x, double *y, cudaStream
     t.waits = A->halo_waits.get();
     t.nwaits = A->n_waits;
     t.ctr = A->tail_ctr.get();
-    if (A->tail_progressive) {
-      t.blk_done = A->blk_done.get();
-      t.chunk_blk = A->chunk_blk.get();
-    }
+    if (A->tail_split) t.obuf = A->tail_obuf.get();
   }
   const unsigned grid = (unsigned)(fuse_tail ? A->tma_grid_tail : A->tma_grid);
   if (fuse_tail)  // comm warps spin on lines written by the peers' CTAs: all CTAs co-resident
