@@ -270,6 +270,10 @@ int peer_put_launch(const HaloPut *puts, int nputs, int chunks, const double *sr
 }
 
 int put_chunks_of(int64_t count) { return put_chunks(count); }
+// bulk segments: 8 x the values of a flagged-line chunk per warp (16 KB per system fence)
+int bulk_chunks_of(int64_t count) {
+  return (int)std::max<int64_t>(1, (count + 8 * kPutChunk - 1) / (8 * kPutChunk));
+}
 
 // standalone put of the current epoch on stream s
 int halo_peer_put(spmat_s *A, const double *x, cudaStream_t s) {

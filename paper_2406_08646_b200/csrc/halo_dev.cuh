@@ -101,7 +101,28 @@ __device__ __forceinline__ void halo_put_warp(const HaloPut *__restrict__ puts, 
   constexpr int U = 8;
   if (p.cflag) {  // bulk: half the NVLink bytes of flagged lines, one release per chunk
     double *dd = reinterpret_cast<double *>(dst);
-    for (int64_t t0 = lo + lane; t0 < hi; t0 += 32 * U) {
+    const double *src = x + p.root_start;
+    int64_t t0 = lo + lane;
+    if (!p.root_idx && !(lo & 1) && !(((uintptr_t)src) & 15)) {  // 16-byte loads and stores
+      const double2 *s2 = reinterpret_cast<const double2 *>(src + lo);
+      double2 *d2 = reinterpret_cast<double2 *>(dd + lo);
+      const int64_t n2 = (hi - lo) / 2;
+      for (int64_t k0 = lane; k0 < n2; k0 += 32 * U) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t k = k0 + 32 * u;
+          v[u] = k < n2 ? __ldg(s2 + k) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t k = k0 + 32 * u;
+          if (k < n2) d2[k] = v[u];
+        }
+      }
+      t0 = lo + 2 * n2 + lane;  // odd tail
+    }
+    for (; t0 < hi; t0 += 32 * U) {
       double v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {

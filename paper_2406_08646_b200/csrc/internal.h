@@ -449,7 +449,8 @@ int spmv_pipe_prepare(spmat_s *A, int chunks);  // chunk rows + the x columns ea
 int spmv_diag_chunk(spmat_s *A, const double *x, double *y, int k, cudaStream_t s);
 int peer_put_launch(const HaloPut *puts, int nputs, int chunks, const double *src,
                     const unsigned long long *epoch_ctr, int *err, cudaStream_t s);
-int put_chunks_of(int64_t count);  // put warps (chunks) for `count` values
+int put_chunks_of(int64_t count);   // put warps (chunks) for `count` values (flagged lines)
+int bulk_chunks_of(int64_t count);  // put warps of a bulk segment (one fence + flag per chunk)
 int sf_peer_setup(sf_s *sf);       // collective; leaves sf->peer false (NCCL) when unavailable
 int halo_peer_setup(spmat_s *A);                  // collective; leaves A->peer false on NCCL
 void halo_peer_release(spmat_s *A);

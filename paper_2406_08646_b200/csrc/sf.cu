@@ -312,12 +312,12 @@ int sf_peer_setup(sf_s *sf) {
   for (size_t a = 0; a < sf->rnbr.size(); ++a)
     if (sf->rcount[a] >= bulk_min) {
       bflag_off[sf->rnbr[a]] = nflags;
-      nflags += put_chunks_of(sf->rcount[a]);
+      nflags += bulk_chunks_of(sf->rcount[a]);
     }
   for (size_t a = 0; a < sf->snbr.size(); ++a)
     if (sf->scount[a] >= bulk_min) {
       rflag_off[sf->snbr[a]] = nflags;
-      nflags += put_chunks_of(sf->scount[a]);
+      nflags += bulk_chunks_of(sf->scount[a]);
     }
   SP_TRY(sf->pflags.alloc(nflags));
   SP_TRY(sf->d_ep.alloc(2));
@@ -398,8 +398,8 @@ int sf_peer_setup(sf_s *sf) {
     p.root_start = sf->root_start[a] >= 0 ? sf->root_start[a] : 0;
     p.root_idx = sf->root_start[a] >= 0 ? nullptr : sf->d_root_idx.get() + sf->soff[a];
     p.my_done = sf->pflags.get() + q;
-    p.nchunk = put_chunks_of(p.count);
     p.cflag = at(q, 26 + 2 * P + me) >= 0 ? pf[q] + at(q, 26 + 2 * P + me) : nullptr;
+    p.nchunk = p.cflag ? bulk_chunks_of(p.count) : put_chunks_of(p.count);
     sf->bchunks += p.nchunk;
     bp.push_back(p);
     HaloWait w{};
@@ -415,8 +415,8 @@ int sf_peer_setup(sf_s *sf) {
     p.root_start = sf->leaf_start[a] >= 0 ? sf->leaf_start[a] : 0;
     p.root_idx = sf->leaf_start[a] >= 0 ? nullptr : sf->d_leaf_idx.get() + sf->roff[a];
     p.my_done = sf->pflags.get() + P + q;
-    p.nchunk = put_chunks_of(p.count);
     p.cflag = at(q, 26 + 3 * P + me) >= 0 ? pf[q] + at(q, 26 + 3 * P + me) : nullptr;
+    p.nchunk = p.cflag ? bulk_chunks_of(p.count) : put_chunks_of(p.count);
     sf->rchunks += p.nchunk;
     rp.push_back(p);
     HaloWait w{};
@@ -432,13 +432,13 @@ int sf_peer_setup(sf_s *sf) {
   std::vector<SfSeg> bs, rs;
   for (size_t a = 0; a < sf->rnbr.size(); ++a) {
     const int64_t o = bflag_off[sf->rnbr[a]];
-    const int nch = put_chunks_of(sf->rcount[a]);
+    const int nch = o >= 0 ? bulk_chunks_of(sf->rcount[a]) : put_chunks_of(sf->rcount[a]);
     bs.push_back({sf->roff[a], sf->rcount[a], o >= 0 ? sf->pflags.get() + o : nullptr,
                   (sf->rcount[a] + nch - 1) / nch});
   }
   for (size_t a = 0; a < sf->snbr.size(); ++a) {
     const int64_t o = rflag_off[sf->snbr[a]];
-    const int nch = put_chunks_of(sf->scount[a]);
+    const int nch = o >= 0 ? bulk_chunks_of(sf->scount[a]) : put_chunks_of(sf->scount[a]);
     rs.push_back({sf->soff[a], sf->scount[a], o >= 0 ? sf->pflags.get() + o : nullptr,
                   (sf->scount[a] + nch - 1) / nch});
   }
