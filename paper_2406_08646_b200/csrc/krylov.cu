@@ -272,6 +272,49 @@ __global__ void __launch_bounds__(kDotThreads) k_dot_partial(const double *__res
   partial_done(block_sum(combine(acc), red), f);
 }
 
+// Small matrices on one rank (the direct SpMV kernel's regime, e.g. Kuu-sized): q = A p and
+// the p.q partial in ONE kernel -- W lanes per row as in k_spmv_direct (8 (col, val) loads,
+// then 8 x gathers per lane in flight), q[r] stored, q[r]*p[r] summed per CTA by the fixed
+// tree, the last CTA finalizes alpha.  One launch and one pass over p and q fewer per iteration.
+template <int W>
+__global__ void __launch_bounds__(kDotThreads) k_cg_spmv_dot(const int32_t *__restrict__ rowptr,
+                                                             const int32_t *__restrict__ col,
+                                                             const double *__restrict__ val,
+                                                             const double *__restrict__ p, double *__restrict__ q,
+                                                             int64_t m, FinArgs f) {
+  __shared__ double red[kDotThreads / 32];
+  pdl_wait();
+  constexpr int U = 8;
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / W;
+  const int lane = threadIdx.x & (W - 1);
+  const bool valid = row < m;
+  const int a = valid ? __ldg(rowptr + row) : 0, z = valid ? __ldg(rowptr + row + 1) : 0;
+  double s = 0.0;
+  for (int e0 = a + lane; e0 < z; e0 += U * W) {
+    int c[U];
+    double v[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * W;
+      c[u] = e < z ? __ldg(col + e) : 0;
+      v[u] = e < z ? __ldg(val + e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = p[c[u]];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * W < z) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+  }
+#pragma unroll
+  for (int o = W >> 1; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o, W));
+  double pq = 0.0;
+  if (valid && lane == 0) {
+    q[row] = s;
+    pq = __dmul_rn(p[row], s);
+  }
+  partial_done(block_sum(pq, red), f);
+}
+
 static inline bool aligned16(const void *p, const void *q) {
   return (((uintptr_t)p | (uintptr_t)q) & 15) == 0;
 }
@@ -445,11 +488,30 @@ static int cg_iteration(spmat_s *A, double *x, double *rr_hist, cudaStream_t s) 
   CgScalars *sc = (CgScalars *)A->cg_scalars.get();
   const int nb = dot_blocks(A);
   const unsigned gv = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, (int64_t)A->comm->num_sms * 8));
-  SP_TRY(spmat_mult_part(A, p, q, 7, s));                            // q = A p
-  SP_CUDA(launch_pdl(aligned16(p, q) ? k_dot_partial<true> : k_dot_partial<false>, pure_dot_blocks(A),
-                     kDotThreads, 0, s, (const double *)p, (const double *)q, m,
-                     fin_args(A, OP_CG_ALPHA, nullptr, nullptr)));
-  SP_TRY(finish_nccl(A, OP_CG_ALPHA, nullptr, nullptr, pure_dot_blocks(A), s));  // alpha = rr / p.q
+  const int64_t fused_grid = (m * A->lanes + kDotThreads - 1) / kDotThreads;
+  if (A->comm->nranks == 1 && A->kernel_id == 5 && A->bs == 1 && m > 0 && fused_grid <= max_dot_blocks(A)) {
+    // q = A p and p.q in one kernel (small matrices, one rank)
+    const FinArgs f = fin_args(A, OP_CG_ALPHA, nullptr, nullptr);
+    const int32_t *rp = A->rowptr_d.get(), *cl = A->col_d.get();
+    const double *vl = A->val_d.get();
+    const unsigned g = (unsigned)fused_grid;
+    cudaError_t e;
+    switch (A->lanes) {
+      case 1: e = launch_pdl(k_cg_spmv_dot<1>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
+      case 2: e = launch_pdl(k_cg_spmv_dot<2>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
+      case 4: e = launch_pdl(k_cg_spmv_dot<4>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
+      case 8: e = launch_pdl(k_cg_spmv_dot<8>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
+      case 16: e = launch_pdl(k_cg_spmv_dot<16>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
+      default: e = launch_pdl(k_cg_spmv_dot<32>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
+    }
+    SP_CUDA(e);
+  } else {
+    SP_TRY(spmat_mult_part(A, p, q, 7, s));                            // q = A p
+    SP_CUDA(launch_pdl(aligned16(p, q) ? k_dot_partial<true> : k_dot_partial<false>, pure_dot_blocks(A),
+                       kDotThreads, 0, s, (const double *)p, (const double *)q, m,
+                       fin_args(A, OP_CG_ALPHA, nullptr, nullptr)));
+    SP_TRY(finish_nccl(A, OP_CG_ALPHA, nullptr, nullptr, pure_dot_blocks(A), s));  // alpha = rr / p.q
+  }
   SP_CUDA(launch_pdl(k_cg_update, nb, kDotThreads, 0, s, x, r, (const double *)p, (const double *)q, m,
                      fin_args(A, OP_CG_BETA, nullptr, rr_hist)));
   SP_TRY(finish_nccl(A, OP_CG_BETA, nullptr, rr_hist, nb, s));      // beta, rr = r.r
