@@ -293,12 +293,15 @@ __global__ void __launch_bounds__(256) k_numeric_seg(
 // the block copy bval directly (the CSR val_d is then stale until spmat_sync_csr_values) -- one
 // pass over the compulsory bytes instead of val_d plus a val_d -> bval copy.  A warp walks a
 // block row's 9*nb values in bval order (v = 9q + 3i + j is nonzero rowptr[3br+i] + 3q + j),
-// kNumU values per lane in flight, each summed in canonical order.
+// kNumU values per lane in flight, each summed in canonical order.  ONE: every nonzero has
+// exactly one contribution (ncontrib == nnz, e.g. node-block COO without duplicates), so
+// jmap[z] == z -- the jmap reads and one level of the load chain disappear.
+template <bool ONE>
 __global__ void __launch_bounds__(256) k_numeric_bsr3(
     const int32_t *__restrict__ rowptr, const int32_t *__restrict__ browptr, const uint32_t *__restrict__ jmap,
     const uint32_t *__restrict__ perm, const double *__restrict__ v, int64_t mb, double *__restrict__ bval,
     int mode) {
-  constexpr int U = 4;
+  constexpr int U = ONE ? 8 : 4;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -312,8 +315,8 @@ __global__ void __launch_bounds__(256) k_numeric_bsr3(
         const int vv = v0 + 32 * u;
         const int q = vv / 9, i = (vv % 9) / 3, j = vv % 3;
         const int z = (i == 0 ? r0 : (i == 1 ? r1 : r2)) + 3 * q + j;
-        a[u] = vv < n9 ? __ldg(jmap + z) : 0u;
-        b[u] = vv < n9 ? __ldg(jmap + z + 1) : 0u;
+        a[u] = vv < n9 ? (ONE ? (uint32_t)z : __ldg(jmap + z)) : 0u;
+        b[u] = vv < n9 ? (ONE ? (uint32_t)z + 1u : __ldg(jmap + z + 1)) : 0u;
       }
       double s[U];
 #pragma unroll
@@ -349,12 +352,13 @@ __global__ void __launch_bounds__(256) k_numeric_bsr3(
   }
 }
 
-// Default numeric kernel: each thread finishes kNumU nonzeros z = base + u*blockDim + tid
+// Default numeric kernel (ONE: jmap[z] == z, as in k_numeric_bsr3): each thread finishes kNumU nonzeros z = base + u*blockDim + tid
 // (coalesced across the warp), advancing all of them one contribution per round so every
 // level of the jmap -> perm -> v chain has kNumU loads in flight.  Each nonzero is still
 // summed in canonical order by one thread; a nonzero meeting a received contribution is left
 // for k_numeric_mixed.
 constexpr int kNumU = 4;
+template <bool ONE>
 __global__ void __launch_bounds__(256) k_numeric_ilp(
     const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm, const double *__restrict__ v,
     uint64_t ncoo, int64_t nnz_d, int64_t nnz, double *__restrict__ val_d, double *__restrict__ val_o,
@@ -367,8 +371,8 @@ __global__ void __launch_bounds__(256) k_numeric_ilp(
 #pragma unroll
     for (int u = 0; u < kNumU; ++u) {
       const int64_t z = base + (int64_t)u * blockDim.x;
-      a[u] = z < nnz ? __ldg(jmap + z) : 0u;
-      b[u] = z < nnz ? __ldg(jmap + z + 1) : 0u;
+      a[u] = z < nnz ? (ONE ? (uint32_t)z : __ldg(jmap + z)) : 0u;
+      b[u] = z < nnz ? (ONE ? (uint32_t)z + 1u : __ldg(jmap + z + 1)) : 0u;
       s[u] = 0.0;
       ok[u] = z < nnz;
     }
@@ -881,10 +885,16 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
     int kind = (double)A->ncontrib > 1.5 * (double)nnz ? 2 : 0;  // 0 ilp, 1 plain, 2 seg
     if (nk) kind = !strcmp(nk, "plain") ? 1 : (!strcmp(nk, "seg") ? 2 : 0);
     const int64_t z0 = direct_bsr ? A->nnz_d : 0;  // direct_bsr: off-diagonal nonzeros only
+    // one contribution per nonzero (every nonzero has at least one): jmap is the identity
+    const bool one = A->ncontrib == nnz && !A->env_numeric_jmap;
     if (direct_bsr) {
       const int64_t blocks = std::min<int64_t>((A->mb + 7) / 8, (int64_t)A->comm->num_sms * 64);
-      k_numeric_bsr3<<<(unsigned)blocks, 256, 0, s>>>(A->rowptr_d.get(), A->browptr.get(), A->jmap.get(),
-                                                      A->perm.get(), v, A->mb, A->bval.get(), mode);
+      if (one)
+        k_numeric_bsr3<true><<<(unsigned)blocks, 256, 0, s>>>(A->rowptr_d.get(), A->browptr.get(), A->jmap.get(),
+                                                              A->perm.get(), v, A->mb, A->bval.get(), mode);
+      else
+        k_numeric_bsr3<false><<<(unsigned)blocks, 256, 0, s>>>(A->rowptr_d.get(), A->browptr.get(), A->jmap.get(),
+                                                               A->perm.get(), v, A->mb, A->bval.get(), mode);
       SP_LAUNCH();
     }
     if (nnz > z0) {
@@ -897,9 +907,14 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
       } else {
         const int64_t blocks = std::min<int64_t>((nnz - z0 + 256 * kNumU - 1) / (256 * kNumU),
                                                  (int64_t)A->comm->num_sms * 32);
-        k_numeric_ilp<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
-            A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo, A->nnz_d, nnz, A->val_d.get(), A->val_o.get(),
-            mode, z0);
+        if (one)
+          k_numeric_ilp<true><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
+              A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo, A->nnz_d, nnz, A->val_d.get(), A->val_o.get(),
+              mode, z0);
+        else
+          k_numeric_ilp<false><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
+              A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo, A->nnz_d, nnz, A->val_d.get(), A->val_o.get(),
+              mode, z0);
       }
       SP_LAUNCH();
     }
