@@ -352,6 +352,64 @@ __global__ void __launch_bounds__(256) k_numeric_bsr3(
   }
 }
 
+// k_numeric_bsr3 for one contribution per nonzero (node-block COO, C5): straight-line
+// perm -> v -> store per value, 8 values per lane in flight, and the next block row's
+// (browptr, rowptr) prefetched while the current one is gathered -- per block row one chain of
+// two dependent loads instead of three (the index loads were the first link).
+__global__ void __launch_bounds__(256) k_numeric_bsr3_one(
+    const int32_t *__restrict__ rowptr, const int32_t *__restrict__ browptr, const uint32_t *__restrict__ perm,
+    const double *__restrict__ v, int64_t mb, double *__restrict__ bval, int mode) {
+  constexpr int U = 8;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t br = warp;
+  if (br >= mb) return;
+  int bp0 = browptr[br], bp1 = browptr[br + 1];
+  int r0 = rowptr[3 * br], r1 = rowptr[3 * br + 1], r2 = rowptr[3 * br + 2];
+  for (;;) {
+    const int64_t nb = br + nwarps;
+    int nbp0 = 0, nbp1 = 0, nr0 = 0, nr1 = 0, nr2 = 0;
+    if (nb < mb) {  // prefetch: independent of the gathers below
+      nbp0 = browptr[nb];
+      nbp1 = browptr[nb + 1];
+      nr0 = rowptr[3 * nb];
+      nr1 = rowptr[3 * nb + 1];
+      nr2 = rowptr[3 * nb + 2];
+    }
+    const int n9 = 9 * (bp1 - bp0);
+    for (int v0 = lane; v0 < n9; v0 += 32 * U) {
+      uint32_t q[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int vv = v0 + 32 * u;
+        const int qq = vv / 9, i = (vv % 9) / 3, j = vv % 3;
+        const int z = (i == 0 ? r0 : (i == 1 ? r1 : r2)) + 3 * qq + j;
+        q[u] = vv < n9 ? __ldg(perm + z) : 0u;
+      }
+      double w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] = v0 + 32 * u < n9 ? __ldg(v + q[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int vv = v0 + 32 * u;
+        if (vv < n9) {
+          const double s = __dadd_rn(0.0, w[u]);  // the one-term canonical sum
+          double *dst = bval + 9 * (int64_t)bp0 + vv;
+          *dst = mode == SPMAT_INSERT ? __dadd_rn(0.0, s) : __dadd_rn(*dst, s);
+        }
+      }
+    }
+    if (nb >= mb) break;
+    br = nb;
+    bp0 = nbp0;
+    bp1 = nbp1;
+    r0 = nr0;
+    r1 = nr1;
+    r2 = nr2;
+  }
+}
+
 // Default numeric kernel (ONE: jmap[z] == z, as in k_numeric_bsr3): each thread finishes kNumU nonzeros z = base + u*blockDim + tid
 // (coalesced across the warp), advancing all of them one contribution per round so every
 // level of the jmap -> perm -> v chain has kNumU loads in flight.  Each nonzero is still
@@ -890,8 +948,8 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
     if (direct_bsr) {
       const int64_t blocks = std::min<int64_t>((A->mb + 7) / 8, (int64_t)A->comm->num_sms * 64);
       if (one)
-        k_numeric_bsr3<true><<<(unsigned)blocks, 256, 0, s>>>(A->rowptr_d.get(), A->browptr.get(), A->jmap.get(),
-                                                              A->perm.get(), v, A->mb, A->bval.get(), mode);
+        k_numeric_bsr3_one<<<(unsigned)blocks, 256, 0, s>>>(A->rowptr_d.get(), A->browptr.get(), A->perm.get(), v,
+                                                            A->mb, A->bval.get(), mode);
       else
         k_numeric_bsr3<false><<<(unsigned)blocks, 256, 0, s>>>(A->rowptr_d.get(), A->browptr.get(), A->jmap.get(),
                                                                A->perm.get(), v, A->mb, A->bval.get(), mode);
