@@ -181,6 +181,14 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream);
    or the launch fails. */
 int spmat_mult(spmat_t A, const double *x, double *y, void *stream);
 
+/* spmat_mult that never blocks the host, also for host x / y (which must then be pinned to
+   overlap): the copies and the MatMult are only enqueued, y is valid and x may be rewritten
+   once the work enqueued on `stream` has completed (synchronise the stream or an event).
+   Consecutive calls alternate between two device staging slots, so call k+1's upload of x
+   overlaps call k's download of y (PCIe is full duplex).  Device pointers: as spmat_mult.
+   Collective. */
+int spmat_mult_async(spmat_t A, const double *x, double *y, void *stream);
+
 /* MatMultTranspose: y = A^T x (collective, enqueue-only).  x: DEVICE array of m_local doubles
    (the row layout), y: DEVICE array of n_local doubles (the column layout).  PETSc's MPIAIJ
    order: lvec = A_o^T x, y = A_d^T x, then the halo star forest reduces lvec into the owners' y

@@ -411,6 +411,7 @@ struct spmat_s {
   spmat::DevBuf<unsigned int> ob_done;
   // host-buffer MatMult pipeline (mult.cu / spmv.cu), built on first use
   int pipe_chunks = 0;
+  int pipe_slot = 0;                       // staging slot of the next host-buffer call (double-buffered)
   std::vector<int64_t> pipe_block, pipe_row, pipe_xmin, pipe_xneed;  // row-order block range, row range, x rows read
   std::vector<int64_t> pipe_q;             // [chunks+1] first compressed off-diagonal row of each chunk
   std::vector<char> pipe_put_chunk;        // chunk holds x rows the NVLink puts read

@@ -119,7 +119,13 @@ static bool pipeline_ok(spmat_s *A) {
   return A->comm->nranks == 1 || A->peer;
 }
 
-static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStream_t s) {
+// Calls alternate between two staging slots (x and y copies on the device), so with
+// asynchronous calls (spmat_mult_async) call k+1's upload overlaps call k's download -- PCIe is
+// full duplex.  Slot reuse is ordered by events: the upload into a slot waits for the SpMV
+// that read it two calls ago, the SpMV writing a slot's y for that slot's last download; the
+// put of the next call (several ranks) for this call's epoch end.  The caller's stream waits
+// for this call's last download, so its completion means y is on the host.
+static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStream_t s, bool async) {
   SP_TRY(spmv_pipe_prepare(A, A->env_pipe_chunks));
   const int nc = A->pipe_chunks;
   const bool multi = A->comm->nranks > 1;
@@ -132,19 +138,27 @@ static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStrea
     SP_CUDA(cudaStreamCreateWithFlags(&A->pipe_out, cudaStreamNonBlocking));
     SP_CUDA(cudaStreamCreateWithPriority(&A->pipe_comm, cudaStreamNonBlocking, hi));
   }
-  while (A->pipe_ev.size() < (size_t)(2 * nc + 3)) {
+  // [0,nc) x chunk in, [nc,2nc) y chunk done, 2nc start, 2nc+1 end, 2nc+2 puts done,
+  // 2nc+3+slot: slot's x free (its SpMV done), 2nc+5+slot: slot's y downloaded, 2nc+7 epoch end
+  while (A->pipe_ev.size() < (size_t)(2 * nc + 8)) {
     cudaEvent_t e;
     SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     A->pipe_ev.push_back(e);
   }
-  if (A->xstage.n < (size_t)A->n) SP_TRY(A->xstage.alloc(A->n));
-  if (A->ystage.n < (size_t)A->m) SP_TRY(A->ystage.alloc(A->m));
-  double *dx = A->xstage.get(), *dy = A->ystage.get();
-  // [0,nc) x chunk in, [nc,2nc) y chunk done, 2nc start, 2nc+1 end, 2nc+2 puts done
+  if (A->xstage.n < 2 * (size_t)A->n) SP_TRY(A->xstage.alloc(2 * (size_t)A->n));
+  if (A->ystage.n < 2 * (size_t)A->m) SP_TRY(A->ystage.alloc(2 * (size_t)A->m));
+  const int slot = A->pipe_slot;
+  A->pipe_slot ^= 1;
+  double *dx = A->xstage.get() + (size_t)slot * A->n, *dy = A->ystage.get() + (size_t)slot * A->m;
   cudaEvent_t *ev = A->pipe_ev.data();
-  SP_CUDA(cudaEventRecord(ev[2 * nc], s));  // earlier work on s (users of the staging buffers)
-  SP_CUDA(cudaStreamWaitEvent(A->pipe_in, ev[2 * nc], 0));
-  SP_CUDA(cudaStreamWaitEvent(A->pipe_out, ev[2 * nc], 0));
+  cudaEvent_t ev_xfree = ev[2 * nc + 3 + slot], ev_yfree = ev[2 * nc + 5 + slot], ev_epoch = ev[2 * nc + 7];
+  if (!async) {  // earlier work on s (e.g. a device-pointer MatMult using the same buffers)
+    SP_CUDA(cudaEventRecord(ev[2 * nc], s));
+    SP_CUDA(cudaStreamWaitEvent(A->pipe_in, ev[2 * nc], 0));
+    SP_CUDA(cudaStreamWaitEvent(A->pipe_out, ev[2 * nc], 0));
+  }
+  SP_CUDA(cudaStreamWaitEvent(A->pipe_in, ev_xfree, 0));  // the SpMV of two calls ago read this slot
+  SP_CUDA(cudaStreamWaitEvent(s, ev_yfree, 0));           // this slot's y of two calls ago is downloaded
   std::vector<int> order;
   for (int pass = 0; pass < 2; ++pass)  // chunks the puts read first
     for (int k = 0; k < nc; ++k)
@@ -155,7 +169,8 @@ static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStrea
     SP_CUDA(cudaEventRecord(ev[k], A->pipe_in));
   }
   if (multi) {
-    SP_CUDA(cudaStreamWaitEvent(A->pipe_comm, ev[2 * nc], 0));
+    if (!async) SP_CUDA(cudaStreamWaitEvent(A->pipe_comm, ev[2 * nc], 0));
+    SP_CUDA(cudaStreamWaitEvent(A->pipe_comm, ev_epoch, 0));  // the previous call's epoch is over
     for (int k = 0; k < nc; ++k)
       if (A->pipe_put_chunk[k]) SP_CUDA(cudaStreamWaitEvent(A->pipe_comm, ev[k], 0));
     SP_TRY(halo_peer_put(A, dx, A->pipe_comm));
@@ -182,31 +197,29 @@ static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStrea
   if (multi) {  // the put read this epoch's number: it must be done before the epoch advances
     if (!put_waited) SP_CUDA(cudaStreamWaitEvent(s, ev[2 * nc + 2], 0));
     SP_TRY(halo_peer_epoch_end(A, s));
+    SP_CUDA(cudaEventRecord(ev_epoch, s));
   }
-  SP_CUDA(cudaEventRecord(ev[2 * nc + 1], A->pipe_out));
-  SP_CUDA(cudaStreamWaitEvent(s, ev[2 * nc + 1], 0));
-  SP_CUDA(cudaStreamSynchronize(s));
+  SP_CUDA(cudaEventRecord(ev_xfree, s));
+  SP_CUDA(cudaEventRecord(ev_yfree, A->pipe_out));
+  SP_CUDA(cudaStreamWaitEvent(s, ev_yfree, 0));
+  if (!async) SP_CUDA(cudaStreamSynchronize(s));
   return SPMAT_OK;
 }
 
-}  // namespace spmat
-
-using namespace spmat;
-
-extern "C" {
-
-int spmat_mult(spmat_t A, const double *x, double *y, void *stream) {
-  if (!A) return fail(SPMAT_ERR_ARG, "spmat_mult: null matrix");
-  if ((A->n > 0 && !x) || (A->m > 0 && !y)) return fail(SPMAT_ERR_ARG, "spmat_mult: null x or y");
-  if (x && (const void *)x == (const void *)y) return fail(SPMAT_ERR_ARG, "spmat_mult: x and y alias");
+// spmat_mult / spmat_mult_async body: device pointers enqueue only; host pointers are staged
+// (pipelined when large enough), and with async == false the call returns after y is written
+static int mult_entry(spmat_t A, const double *x, double *y, void *stream, bool async, const char *who) {
+  if (!A) return fail(SPMAT_ERR_ARG, "%s: null matrix", who);
+  if ((A->n > 0 && !x) || (A->m > 0 && !y)) return fail(SPMAT_ERR_ARG, "%s: null x or y", who);
+  if (x && (const void *)x == (const void *)y) return fail(SPMAT_ERR_ARG, "%s: x and y alias", who);
   if (!A->values_set && A->nnz_d + A->nnz_o > 0)
-    return fail(SPMAT_ERR_STATE, "spmat_mult before spmat_set_values_coo");
+    return fail(SPMAT_ERR_STATE, "%s before spmat_set_values_coo", who);
   DeviceGuard g(A->comm->device);
   cudaStream_t s = (cudaStream_t)stream;
   const bool hx = A->n > 0 && !is_device_ptr(x);
   const bool hy = A->m > 0 && !is_device_ptr(y);
   if (!hx && !hy) return mult_impl(A, x, y, 7, s);
-  if (hx && hy && pipeline_ok(A)) return mult_host_pipelined(A, x, y, s);
+  if (hx && hy && pipeline_ok(A)) return mult_host_pipelined(A, x, y, s, async);
   // host buffers: stage through device copies inside the stream order
   const double *dx = x;
   double *dy = y;
@@ -221,8 +234,22 @@ int spmat_mult(spmat_t A, const double *x, double *y, void *stream) {
   }
   SP_TRY(mult_impl(A, dx, dy, 7, s));
   if (hy) SP_CUDA(cudaMemcpyAsync(y, dy, A->m * 8, cudaMemcpyDeviceToHost, s));
-  SP_CUDA(cudaStreamSynchronize(s));
+  if (!async) SP_CUDA(cudaStreamSynchronize(s));
   return SPMAT_OK;
+}
+
+}  // namespace spmat
+
+using namespace spmat;
+
+extern "C" {
+
+int spmat_mult(spmat_t A, const double *x, double *y, void *stream) {
+  return mult_entry(A, x, y, stream, false, "spmat_mult");
+}
+
+int spmat_mult_async(spmat_t A, const double *x, double *y, void *stream) {
+  return mult_entry(A, x, y, stream, true, "spmat_mult_async");
 }
 
 int spmat_mult_part(spmat_t A, const double *x, double *y, int part, void *stream) {

@@ -343,6 +343,20 @@ def case_host_pipeline(c, kind):
         A.mult(xh, yh)
         assert torch.equal(yh, yd.cpu()), f"host pipeline {kind} rank {r}"
         A.mult(x, yd)
+    # asynchronous calls through the two staging slots (epochs chained by events), one sync
+    xs = [synth.x_vector(off[r], off[r + 1], "real", seed=30 + k, device="cuda") for k in range(4)]
+    want = []
+    for xk in xs:
+        A.mult(xk, yd)
+        want.append(yd.cpu())
+    xhs = [xk.cpu().pin_memory() for xk in xs]
+    yhs = [torch.full((sizes[r],), float("nan"), dtype=torch.float64).pin_memory() for _ in xs]
+    s = torch.cuda.current_stream()
+    for xk, yk in zip(xhs, yhs):
+        A.mult_async(xk, yk, s)
+    s.synchronize()
+    for k, (yk, w) in enumerate(zip(yhs, want)):
+        assert torch.equal(yk, w), f"async host pipeline {kind} rank {r} call {k}"
     A.check()
     A.close()
 

@@ -603,6 +603,20 @@ def test_host_pipeline_matches_device(sp, comm):
     for _ in range(2):
         A.mult(xh, yh)
         assert torch.equal(yh, yd.cpu())
+    # asynchronous calls: 5 different x in flight through the two staging slots, one sync
+    xs = [synth.x_vector(0, M, "real", seed=20 + k, device="cuda") for k in range(5)]
+    want = []
+    for xk in xs:
+        A.mult(xk, yd)
+        want.append(yd.cpu())
+    xhs = [xk.cpu().pin_memory() for xk in xs]
+    yhs = [torch.full((M,), float("nan"), dtype=torch.float64).pin_memory() for _ in xs]
+    s = torch.cuda.current_stream()
+    for xk, yk in zip(xhs, yhs):
+        A.mult_async(xk, yk, s)
+    s.synchronize()
+    for yk, w in zip(yhs, want):
+        assert torch.equal(yk, w)
     A.close()
 
 
