@@ -795,6 +795,7 @@ using namespace spmat;
 extern "C" {
 
 int spmat_set_block_size(spmat_t A, int bs) {
+  SP_NVTX("spmat_set_block_size");
   if (!A) return fail(SPMAT_ERR_ARG, "spmat_set_block_size: null matrix");
   DeviceGuard g(A->comm->device);
   cg_graph_release(A);  // a captured CG iteration would still launch the old kernel

@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -83,6 +84,7 @@ int nccl_api(NcclApi **out) {
     LOADSYM(AllReduce, "ncclAllReduce");
     LOADSYM(AllGather, "ncclAllGather");
 #undef LOADSYM
+    *(void **)(&g_nccl.CommInitRankConfig) = dlsym(h, "ncclCommInitRankConfig");  // optional
     g_nccl.loaded = true;
   }
   *out = &g_nccl;
@@ -199,7 +201,21 @@ int spmat_comm_create(const unsigned char *id, int nranks, int rank, int device,
     }
     ncclUniqueId uid;
     memcpy(&uid, id, 128);
-    ncclResult_t r = c->api->CommInitRank(&c->nccl, nranks, uid, rank);
+    // NCCL's kernels share the SMs with the persistent SpMV (NCCL-mode halo, COO value
+    // exchange): cap them -- ncclConfig_t.maxCTAs, default 4, SPMAT_NCCL_MAX_CTAS=0
+    // for NCCL's own choice
+    int max_ctas = 4;
+    if (const char *e = getenv("SPMAT_NCCL_MAX_CTAS")) max_ctas = atoi(e);
+    ncclResult_t r;
+    if (c->api->CommInitRankConfig && max_ctas > 0) {
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      cfg.maxCTAs = max_ctas;
+      cfg.minCTAs = 1;
+      r = c->api->CommInitRankConfig(&c->nccl, nranks, uid, rank, &cfg);
+      c->nccl_max_ctas = max_ctas;
+    } else {
+      r = c->api->CommInitRank(&c->nccl, nranks, uid, rank);
+    }
     if (r != ncclSuccess) {
       const char *msg = c->api->GetErrorString(r);
       delete c;

@@ -899,6 +899,7 @@ extern "C" {
 
 int spmat_create_coo(spmat_comm_t comm, int64_t m_local, int64_t n_local, int64_t M, int64_t N,
                      int64_t ncoo, const int64_t *coo_i, const int64_t *coo_j, spmat_t *out) {
+  SP_NVTX("spmat_create_coo");
   if (!comm || !out) return fail(SPMAT_ERR_ARG, "spmat_create_coo: null argument");
   *out = nullptr;
   if (ncoo < 0) return fail(SPMAT_ERR_ARG, "spmat_create_coo: negative ncoo");
@@ -907,6 +908,7 @@ int spmat_create_coo(spmat_comm_t comm, int64_t m_local, int64_t n_local, int64_
 }
 
 int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
+  SP_NVTX("spmat_set_values_coo");
   if (!A) return fail(SPMAT_ERR_ARG, "spmat_set_values_coo: null matrix");
   if (mode != SPMAT_INSERT && mode != SPMAT_ADD)
     return fail(SPMAT_ERR_ARG, "spmat_set_values_coo: bad mode %d", mode);

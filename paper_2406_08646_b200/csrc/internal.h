@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "nccl.h"
 #include "spmat.h"
 
@@ -38,6 +40,7 @@ struct NcclApi {
   bool loaded = false;
   ncclResult_t (*GetUniqueId)(ncclUniqueId *);
   ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+  ncclResult_t (*CommInitRankConfig)(ncclComm_t *, int, ncclUniqueId, int, ncclConfig_t *);  // may be null
   ncclResult_t (*CommDestroy)(ncclComm_t);
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *);
   const char *(*GetErrorString)(ncclResult_t);
@@ -59,6 +62,17 @@ int nccl_api(NcclApi **out);
       return ::spmat::fail(SPMAT_ERR_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #expr,    \
                            (api)->GetErrorString(_r));                                   \
   } while (0)
+
+// ------------------------------------------------------------------ NVTX
+// Host-side ranges around every ABI entry point (header-only NVTX v3: a no-op unless a tool
+// such as Nsight Systems is attached), so a trace shows create / set_values / mult / SF calls.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
+#define SP_NVTX(name) ::spmat::NvtxRange _nvtx_range_(name)
 
 // ------------------------------------------------------------------ device guard
 struct DeviceGuard {
@@ -150,6 +164,7 @@ struct Comm {
   cudaStream_t comm_stream = nullptr;   // high priority, non-blocking
   cudaStream_t setup_stream = nullptr;  // used by collective setup calls
   int num_sms = 148;
+  int nccl_max_ctas = 0;                // ncclConfig_t.maxCTAs used at init (0: NCCL's default)
 
   // Collectives used by setup (host-synchronising).  All operate on host arrays.
   int allgather_i64(const int64_t *send, int64_t count, int64_t *recv_host);  // recv: count*P

@@ -543,6 +543,7 @@ using namespace spmat;
 extern "C" {
 
 int spmat_vec_dot(spmat_t A, const double *a, const double *b, double *result, void *stream) {
+  SP_NVTX("spmat_vec_dot");
   if (!A || !result || (A->m > 0 && (!a || !b))) return fail(SPMAT_ERR_ARG, "spmat_vec_dot: null argument");
   DeviceGuard g(A->comm->device);
   cudaStream_t s = (cudaStream_t)stream;
@@ -553,6 +554,7 @@ int spmat_vec_dot(spmat_t A, const double *a, const double *b, double *result, v
 }
 
 int spmat_cg(spmat_t A, const double *b, double *x, int maxit, double *rr_hist, void *stream) {
+  SP_NVTX("spmat_cg");
   if (!A || maxit < 0 || (A->m > 0 && (!b || !x)))
     return fail(SPMAT_ERR_ARG, "spmat_cg: bad argument");
   if (A->M != A->N || A->m != A->n) return fail(SPMAT_ERR_ARG, "spmat_cg: matrix must be square");

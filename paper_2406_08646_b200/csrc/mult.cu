@@ -245,14 +245,17 @@ using namespace spmat;
 extern "C" {
 
 int spmat_mult(spmat_t A, const double *x, double *y, void *stream) {
+  SP_NVTX("spmat_mult");
   return mult_entry(A, x, y, stream, false, "spmat_mult");
 }
 
 int spmat_mult_async(spmat_t A, const double *x, double *y, void *stream) {
+  SP_NVTX("spmat_mult_async");
   return mult_entry(A, x, y, stream, true, "spmat_mult_async");
 }
 
 int spmat_mult_part(spmat_t A, const double *x, double *y, int part, void *stream) {
+  SP_NVTX("spmat_mult_part");
   if (!A) return fail(SPMAT_ERR_ARG, "spmat_mult_part: null matrix");
   if (part < 1 || part > 7) return fail(SPMAT_ERR_ARG, "spmat_mult_part: bad part %d", part);
   if (x && (const void *)x == (const void *)y) return fail(SPMAT_ERR_ARG, "spmat_mult_part: x and y alias");

@@ -728,6 +728,7 @@ extern "C" {
 
 int sf_create(spmat_comm_t comm, int64_t nroots, int64_t nleaves, const int64_t *ilocal,
               const int32_t *remote_rank, const int64_t *remote_offset, sf_t *out) {
+  SP_NVTX("sf_create");
   if (!comm || !out) return fail(SPMAT_ERR_ARG, "sf_create: null argument");
   *out = nullptr;
   if (nleaves > 0 && (!remote_rank || !remote_offset))
@@ -761,6 +762,7 @@ int sf_create(spmat_comm_t comm, int64_t nroots, int64_t nleaves, const int64_t 
 }
 
 int sf_bcast_begin(sf_t sf, const double *rootdata, double *leafdata, int op, void *stream) {
+  SP_NVTX("sf_bcast_begin");
   if (!sf) return fail(SPMAT_ERR_ARG, "sf_bcast_begin: null sf");
   if ((sf->nsend > 0 || sf->nself > 0) && !rootdata)
     return fail(SPMAT_ERR_ARG, "sf_bcast_begin: null rootdata");
@@ -771,12 +773,14 @@ int sf_bcast_begin(sf_t sf, const double *rootdata, double *leafdata, int op, vo
 }
 
 int sf_bcast_end(sf_t sf, const double *rootdata, double *leafdata, int op, void *stream) {
+  SP_NVTX("sf_bcast_end");
   if (!sf) return fail(SPMAT_ERR_ARG, "sf_bcast_end: null sf");
   DeviceGuard g(sf->comm->device);
   return sf_end(sf, rootdata, leafdata, op, (cudaStream_t)stream);
 }
 
 int sf_reduce_begin(sf_t sf, const double *leafdata, double *rootdata, int op, void *stream) {
+  SP_NVTX("sf_reduce_begin");
   if (!sf) return fail(SPMAT_ERR_ARG, "sf_reduce_begin: null sf");
   if ((sf->nrecv > 0 || sf->nself > 0) && !leafdata)
     return fail(SPMAT_ERR_ARG, "sf_reduce_begin: null leafdata");
@@ -786,6 +790,7 @@ int sf_reduce_begin(sf_t sf, const double *leafdata, double *rootdata, int op, v
 }
 
 int sf_reduce_end(sf_t sf, const double *leafdata, double *rootdata, int op, void *stream) {
+  SP_NVTX("sf_reduce_end");
   if (!sf) return fail(SPMAT_ERR_ARG, "sf_reduce_end: null sf");
   DeviceGuard g(sf->comm->device);
   return sf_reduce_end_impl(sf, leafdata, rootdata, op, (cudaStream_t)stream);

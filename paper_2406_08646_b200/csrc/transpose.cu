@@ -162,6 +162,7 @@ using namespace spmat;
 extern "C" {
 
 int spmat_mult_transpose(spmat_t A, const double *x, double *y, void *stream) {
+  SP_NVTX("spmat_mult_transpose");
   if (!A) return fail(SPMAT_ERR_ARG, "spmat_mult_transpose: null matrix");
   if ((A->m > 0 && !x) || (A->n > 0 && !y)) return fail(SPMAT_ERR_ARG, "spmat_mult_transpose: null x or y");
   if (x && (const void *)x == (const void *)y) return fail(SPMAT_ERR_ARG, "spmat_mult_transpose: x and y alias");
