@@ -258,7 +258,7 @@ __global__ void k_numeric_local(const uint32_t *__restrict__ jmap, const uint32_
 // contribution segment read kSeg at a time -- the kSeg perm loads, then the kSeg v gathers, are
 // each issued together before any is used, so a segment costs one jmap -> perm -> v chain of
 // latencies instead of one per contribution -- then summed in canonical order.
-constexpr int kSeg = 8;
+template <int kSeg>
 __global__ void __launch_bounds__(256) k_numeric_seg(
     const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm, const double *__restrict__ v,
     uint64_t ncoo, int64_t nnz_d, int64_t nnz, double *__restrict__ val_d, double *__restrict__ val_o,
@@ -962,8 +962,14 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
         k_numeric_local<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
                                                   A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
       } else if (kind == 2 && z0 == 0) {
-        k_numeric_seg<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
-                                                A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
+        // contributions read 4 at a time by default (element COO averages ~2.4 per nonzero;
+        // 8-wide predication issued more instructions than it hid latency)
+        if (A->env_numeric_seg == 8)
+          k_numeric_seg<8><<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
+                                                     A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
+        else
+          k_numeric_seg<4><<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
+                                                     A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
       } else {
         const int64_t blocks = std::min<int64_t>((nnz - z0 + 256 * kNumU - 1) / (256 * kNumU),
                                                  (int64_t)A->comm->num_sms * 32);
