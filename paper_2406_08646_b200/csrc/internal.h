@@ -417,7 +417,7 @@ struct spmat_s {
   bool val_d_stale = false;
   bool env_numeric_csr = false;  // SPMAT_NUMERIC_BSR=0: always val_d, then the bval copy
   bool env_numeric_jmap = false; // SPMAT_NUMERIC_JMAP=1: read jmap even when it is the identity
-  int env_numeric_seg = 4;       // SPMAT_NUMERIC_SEG=4|8: contributions per step of k_numeric_seg
+  int env_numeric_seg = 8;       // SPMAT_NUMERIC_SEG=4|8: contributions per step of k_numeric_seg
   int64_t obr = 0, onnzb = 0;
   int ob_w = 4;
   bool env_no_bsr_fuse = false;  // SPMAT_BSR_FUSE=0: the standalone off-diagonal kernel

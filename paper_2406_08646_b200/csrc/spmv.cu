@@ -495,7 +495,7 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
     e = getenv("SPMAT_FUSE_TAIL");
     A->env_no_tail = e && !strcmp(e, "0");
     e = getenv("SPMAT_NUMERIC_SEG");
-    A->env_numeric_seg = (e && atoi(e) == 8) ? 8 : 4;
+    A->env_numeric_seg = (e && atoi(e) == 4) ? 4 : 8;
     e = getenv("SPMAT_NUMERIC_JMAP");
     A->env_numeric_jmap = e && atoi(e) != 0;
     e = getenv("SPMAT_PIPE_CHUNKS");

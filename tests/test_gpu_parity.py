@@ -529,7 +529,7 @@ def test_kernel_variants(sp, comm, kernel, case, monkeypatch):
     A.close()
 
 
-@pytest.mark.parametrize("numeric", ["ilp", "plain", "seg", "seg-8", "ilp-jmap"])
+@pytest.mark.parametrize("numeric", ["ilp", "plain", "seg", "seg-4", "ilp-jmap"])
 def test_numeric_kernels(sp, comm, numeric, monkeypatch):
     """Every COO numeric kernel gives the oracle's values bit for bit (Z1 order), also with
     ~20 contributions per nonzero, and with one contribution per nonzero (stencil COO: jmap is
@@ -537,8 +537,8 @@ def test_numeric_kernels(sp, comm, numeric, monkeypatch):
     monkeypatch.setenv("SPMAT_NUMERIC_KERNEL", numeric.split("-")[0])
     if numeric.endswith("jmap"):
         monkeypatch.setenv("SPMAT_NUMERIC_JMAP", "1")
-    if numeric.endswith("8"):
-        monkeypatch.setenv("SPMAT_NUMERIC_SEG", "8")
+    if numeric.endswith("4"):
+        monkeypatch.setenv("SPMAT_NUMERIC_SEG", "4")
     for M, i, j, v in [(9 ** 3, *synth.q1_coo(9, values="real")),
                        (20 * 17 * 9, *synth.stencil_coo((20, 17, 9), 7, values="real")),
                        (50, *synth.random_coo(50, 50, 3000, dup_frac=0.9, neg_frac=0.1, values="real")),
