@@ -44,6 +44,14 @@ bool pdl_on() {
   return on;
 }
 
+int coop_mode() {
+  static const int mode = [] {
+    const char *e = getenv("SPMAT_COOP");
+    return e ? atoi(e) : 1;
+  }();
+  return mode;
+}
+
 bool is_device_ptr(const void *p) {
   if (!p) return false;
   cudaPointerAttributes attr;

@@ -120,6 +120,7 @@ struct DevBuf {
 // Launch with programmatic stream serialization (PDL, ptx.cuh) unless SPMAT_PDL=0: the
 // kernel's CTAs may start while the previous kernel of the stream drains.
 bool pdl_on();
+int coop_mode();  // SPMAT_COOP: 0 plain launch, 1 cooperative (default), 2 cooperative + PDL
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t s, Args... args) {
@@ -145,11 +146,17 @@ inline cudaError_t launch_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, 
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeCooperative;
   at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = coop_mode() == 2 && pdl_on() ? 2 : 1;
+  if (coop_mode() == 0) {  // SPMAT_COOP=0: plain (PDL) launch, no co-residency guarantee
+    cfg.attrs = at + 1;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+  }
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 

@@ -21,17 +21,22 @@ def counters(h):
     if nv is None:
         return out
     for name, fid in FIELDS.items():
-        tot, ok = 0, 0
-        for link in range(18):
+        tot, ok, rets = 0, 0, set()
+        for link in list(range(18)) + [0xFFFFFFFF]:
             try:
                 v = nv.nvmlDeviceGetFieldValues(h, [(fid, link)])[0]
+                rets.add(int(v.nvmlReturn))
                 if v.nvmlReturn == 0:
                     tot += int(v.value.ullVal)
                     ok += 1
-            except Exception:  # noqa: BLE001
-                pass
+            except Exception as ex:  # noqa: BLE001
+                rets.add(type(ex).__name__)
         out[name] = (tot, ok)
+        RETS[name] = sorted(map(str, rets))
     return out
+
+
+RETS = {}
 
 
 def main():
@@ -63,6 +68,7 @@ def main():
         rows.append({"MB": mb, "us": ms * 1e3, "GBps": mb * (1 << 20) / ms / 1e6,
                      "counter_delta_per_copy": {k: v[0] / it for k, v in d.items()},
                      "links_answering": {k: v[1] for k, v in d.items()}})
+        rows[-1]["nvml_returns"] = dict(RETS)
         print(json.dumps(rows[-1]), flush=True)
     print(json.dumps({"bench": "nvlink_ce_copy", "rows": rows}))
 
