@@ -44,6 +44,10 @@ bool pdl_on() {
   return on;
 }
 
+void note_fallback(const Comm *c, const char *what, const char *why) {
+  if (c->rank == 0) fprintf(stderr, "libspmat: %s uses NCCL instead of NVLink peer memory: %s\n", what, why);
+}
+
 int coop_mode() {
   static const int mode = [] {
     const char *e = getenv("SPMAT_COOP");

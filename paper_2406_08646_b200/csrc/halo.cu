@@ -146,6 +146,8 @@ int halo_peer_setup(spmat_s *A) {
   {  // agree on feasibility before allocating anything rank-specific
     int64_t vote0[2] = {want ? 0 : 1, fail};
     SP_TRY(c->allreduce_max_i64(vote0, 2));
+    if (!vote0[0] && vote0[1])
+      note_fallback(c, "the MatMult halo", "ghost leaves not contiguous per owner (or self edges) on some rank");
     if (vote0[0] || vote0[1]) return SPMAT_OK;  // NCCL halo on every rank
   }
   SP_TRY(A->halo_flags.alloc(P));  // [q]: done flag from receiver q
@@ -168,6 +170,7 @@ int halo_peer_setup(spmat_s *A) {
   // agree on the mode before anything else collective
   int64_t vote[2] = {want ? 0 : 1, fail};
   SP_TRY(c->allreduce_max_i64(vote, 2));
+  if (!vote[0] && vote[1]) note_fallback(c, "the MatMult halo", "cudaIpcGetMemHandle failed on some rank");
   if (vote[0] || vote[1]) return SPMAT_OK;  // NCCL halo on every rank
   // exchange handles and, per (receiver, sender), the receiver's leaf start for that sender
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
@@ -201,6 +204,7 @@ int halo_peer_setup(spmat_s *A) {
   int64_t v2[1] = {open_fail};
   SP_TRY(c->allreduce_max_i64(v2, 1));
   if (v2[0]) {
+    note_fallback(c, "the MatMult halo", "cudaIpcOpenMemHandle failed on some rank (peers not on one node?)");
     halo_peer_release(A);
     return SPMAT_OK;
   }

@@ -197,6 +197,8 @@ struct Comm {
   DevBuf<unsigned long long> d_board_epoch;  // completed board reductions (device, graph-safe)
 };
 int board_setup(Comm *c);      // collective; leaves board_ok false when IPC is unavailable
+// say plainly (stderr, rank 0) that a transport fell back from NVLink peer memory to NCCL
+void note_fallback(const Comm *c, const char *what, const char *why);
 void board_release(Comm *c);
 
 }  // namespace spmat

@@ -69,6 +69,8 @@ int board_setup(Comm *c) {
   int64_t vote[1] = {fail};
   SP_TRY(c->allreduce_max_i64(vote, 1));
   if (vote[0]) {
+    if (!(getenv("SPMAT_BOARD") && !strcmp(getenv("SPMAT_BOARD"), "nccl")))
+      note_fallback(c, "the cross-rank dot sums", "CUDA IPC of the scalar board failed on some rank");
     board_release(c);
     return SPMAT_OK;  // reductions fall back to ncclAllReduce
   }

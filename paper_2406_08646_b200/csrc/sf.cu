@@ -341,7 +341,10 @@ int sf_peer_setup(sf_s *sf) {
   }
   int64_t v1[1] = {fail_};
   SP_TRY(c->allreduce_max_i64(v1, 1));
-  if (v1[0]) return SPMAT_OK;  // NCCL transport on every rank
+  if (v1[0]) {
+    note_fallback(c, "a star forest", "cudaIpcGetMemHandle failed on some rank");
+    return SPMAT_OK;  // NCCL transport on every rank
+  }
   // per rank: 3 handles, strides, and for every peer p the offset of p's data in my bline
   // (p sends me roots) and in my rline (p sends me leaves)
   const int W = 24 + 2 + 4 * P;
@@ -381,6 +384,7 @@ int sf_peer_setup(sf_s *sf) {
   int64_t v2[1] = {open_fail};
   SP_TRY(c->allreduce_max_i64(v2, 1));
   if (v2[0]) {
+    note_fallback(c, "a star forest", "cudaIpcOpenMemHandle failed on some rank (peers not on one node?)");
     for (void *m : sf->peer_mem) cudaIpcCloseMemHandle(m);
     sf->peer_mem.clear();
     return SPMAT_OK;
