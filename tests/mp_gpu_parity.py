@@ -127,9 +127,17 @@ def check_matrix(c, name, M, N, row_sizes, col_sizes, coo, values, x_global, exa
     assert rel_err(y.cpu().numpy(), yo2) <= TOL
     assert A.info()["plan_builds"] == 1
     # many back-to-back MatMults (exercises the halo epoch protocol), then check y again
+    i0 = A.info()
     for _ in range(20):
         A.mult(xl, y)
     A.check()
+    i1 = A.info()  # byte counters: 20 MatMults' halo (16 B lines over NVLink, 8 B over NCCL)
+    assert i1["n_mult"] - i0["n_mult"] == 20
+    nsend = sp.sf_get_info(A.halo_sf())["n_send"]
+    if i1["halo_mode"] == 2:
+        assert i1["nvlink_bytes_put"] - i0["nvlink_bytes_put"] == 20 * 16 * nsend, f"{name}: NVLink counter"
+    elif i1["halo_mode"] == 1:
+        assert i1["nccl_bytes_sent"] - i0["nccl_bytes_sent"] == 20 * 8 * nsend, f"{name}: NCCL counter"
     assert rel_err(y.cpu().numpy(), yo2) <= TOL
     A.close()
     return info, yg

@@ -359,6 +359,15 @@ def test_repeated_set_values_no_replan(sp, comm):
     O = oracle.OracleMat(M, M, [M], [M], [i], [j])
     O.set_values([v * 3])
     assert np.array_equal(canon(A.export("val_d")), canon(O.export(0, "val_d")))
+    # counters of spmat_get_info: calls, and no NCCL / NVLink bytes on one rank
+    x = torch.ones(M, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(x)
+    for _ in range(4):
+        A.mult(x, y)
+    info = A.info()
+    assert info["n_set_values"] == 3 and info["n_mult"] == 4 and info["halo_mode"] == 0
+    assert info["nccl_bytes_sent"] == info["nccl_bytes_recv"] == info["nvlink_bytes_put"] == 0
+    assert info["block_size"] == 1 and info["spmv_grid"] >= 0
     A.close()
 
 
