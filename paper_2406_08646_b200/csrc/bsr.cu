@@ -140,7 +140,9 @@ __global__ void k_bsr_blocks4(const int32_t *__restrict__ bounds, const int32_t 
   }
 }
 
-template <int W>
+// FMA: each block row's 9 products accumulated with fused multiply-adds (half the fp64 pipe
+// instructions; a different rounding, still within the 1e-12 bar and exact for integer data)
+template <int W, bool FMA>
 __device__ __forceinline__ void brows_w(int br0, int br1, int bp0, const int *__restrict__ rp,
                                         const int *__restrict__ sc, const double *__restrict__ sv,
                                         const double *__restrict__ x, double *__restrict__ y, int tid) {
@@ -165,9 +167,15 @@ __device__ __forceinline__ void brows_w(int br0, int br1, int bp0, const int *__
           const double *v = sv + 9 * e;
 #pragma unroll
           for (int jj = 0; jj < 3; ++jj) {
-            y0 = __dadd_rn(y0, __dmul_rn(v[jj], xv[u][jj]));
-            y1 = __dadd_rn(y1, __dmul_rn(v[3 + jj], xv[u][jj]));
-            y2 = __dadd_rn(y2, __dmul_rn(v[6 + jj], xv[u][jj]));
+            if (FMA) {
+              y0 = __fma_rn(v[jj], xv[u][jj], y0);
+              y1 = __fma_rn(v[3 + jj], xv[u][jj], y1);
+              y2 = __fma_rn(v[6 + jj], xv[u][jj], y2);
+            } else {
+              y0 = __dadd_rn(y0, __dmul_rn(v[jj], xv[u][jj]));
+              y1 = __dadd_rn(y1, __dmul_rn(v[3 + jj], xv[u][jj]));
+              y2 = __dadd_rn(y2, __dmul_rn(v[6 + jj], xv[u][jj]));
+            }
           }
         }
       }
@@ -262,6 +270,7 @@ static __device__ __noinline__ void bsr_off_rows(const BsrOff off, int t0, int t
   }
 }
 
+template <bool FMA, bool FUSE>
 __global__ void __launch_bounds__(kCtaT, 3)
     k_spmv_bsr3(const int4 *__restrict__ blocks, int n_blocks, const int32_t *__restrict__ browptr,
                 const int32_t *__restrict__ bcol, const double *__restrict__ bval,
@@ -271,7 +280,7 @@ __global__ void __launch_bounds__(kCtaT, 3)
   BsrStage *st = reinterpret_cast<BsrStage *>(smem);
   // this MatMult's halo epoch (fused off-diagonal blocks): read by every CTA before its
   // consumers finish, so before the last CTA stores it back
-  const unsigned long long epoch = off.range ? *off.epoch_ctr + 1ull : 0ull;
+  const unsigned long long epoch = FUSE ? *off.epoch_ctr + 1ull : 0ull;
   unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + kStagesB * sizeof(BsrStage));
   unsigned long long *empty = full + kStagesB;
   const int tid = threadIdx.x, warp = tid >> 5, lane32 = tid & 31;
@@ -304,11 +313,9 @@ __global__ void __launch_bounds__(kCtaT, 3)
         return;
       }
       st[s].hdr = H;
-      if (off.range) {
+      if (FUSE) {
         const int2 rg = off.range[b];
         st[s].ext = make_int4(rg.x, rg.y, 0, 0);
-      } else {
-        st[s].ext = make_int4(0, 0, 0, 0);
       }
       const int64_t v0 = 9 * (int64_t)H.z, v1 = 9 * (int64_t)H.w;
       const int64_t va = v0 & ~1ll, ve = (v1 + 1) & ~1ll;
@@ -331,25 +338,25 @@ __global__ void __launch_bounds__(kCtaT, 3)
     const int4 h = st[s].hdr;
     if (h.x < 0) break;
     const int br0 = h.x, br1 = h.y, bp0 = h.z;
-    const int t0 = st[s].ext.x, t1 = st[s].ext.y;
+    const int t0 = FUSE ? st[s].ext.x : 0, t1 = FUSE ? st[s].ext.y : 0;
     const double *sv = st[s].val + ((9 * (int64_t)bp0) & 1);
     const int *sc = st[s].col + (bp0 & 3);
     const int *rp = st[s].rp - (br0 & ~3);
     const int nbr = br1 - br0;
-    if (nbr * 2 > kT) brows_w<1>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 4 > kT) brows_w<2>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 8 > kT) brows_w<4>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 16 > kT) brows_w<8>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 32 > kT) brows_w<16>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else brows_w<32>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    if (nbr * 2 > kT) brows_w<1, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 4 > kT) brows_w<2, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 8 > kT) brows_w<4, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 16 > kT) brows_w<8, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 32 > kT) brows_w<16, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else brows_w<32, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
     __syncwarp();
     if (lane32 == 0) mbar_arrive(&empty[s]);
-    if (t1 > t0) {  // this block's diagonal y is written by all consumer warps: add A_o g
+    if (FUSE && t1 > t0) {  // this block's diagonal y is written by all consumer warps: add A_o g
       asm volatile("bar.sync 1, %0;" ::"r"(kT) : "memory");
       bsr_off_rows(off, t0, t1, y, tid, epoch);
     }
   }
-  if (off.range) {  // the last CTA whose consumers are done ends the MatMult's halo epoch
+  if (FUSE) {  // the last CTA whose consumers are done ends the MatMult's halo epoch
     asm volatile("bar.sync 2, %0;" ::"r"(kT) : "memory");
     if (tid == 0) {
       __threadfence();
@@ -599,9 +606,10 @@ int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_o
     off.done = A->ob_done.get();
     off.err = A->halo_err.get();
   }
-  k_spmv_bsr3<<<(unsigned)A->bsr_grid, kCtaT, kBsrSmem, s>>>(A->bblocks4.get(), (int)A->n_brblocks,
-                                                           A->browptr.get(), A->bcol.get(), A->bval.get(),
-                                                           x, y, A->bsched.get(), off);
+  auto kern = fuse_off ? (A->env_bsr_fma ? k_spmv_bsr3<true, true> : k_spmv_bsr3<false, true>)
+                      : (A->env_bsr_fma ? k_spmv_bsr3<true, false> : k_spmv_bsr3<false, false>);
+  kern<<<(unsigned)A->bsr_grid, kCtaT, kBsrSmem, s>>>(A->bblocks4.get(), (int)A->n_brblocks, A->browptr.get(),
+                                                    A->bcol.get(), A->bval.get(), x, y, A->bsched.get(), off);
   SP_LAUNCH();
   return SPMAT_OK;
 }
@@ -676,6 +684,8 @@ static int bsr_o_env(spmat_s *A) {
   // off-diagonal blocks inside the block SpMV only on request: measured on B200 (C5, same box)
   // the in-kernel add stalls each boundary row block's stage ring for a ghost-read latency
   // chain (0.859 vs 0.836 ms at P=4, 1.660 vs 1.625 ms at P=2); the standalone kernel wins
+  e = getenv("SPMAT_BSR_FMA");
+  A->env_bsr_fma = e && atoi(e) != 0;
   e = getenv("SPMAT_BSR_FUSE");
   A->env_no_bsr_fuse = !(e && atoi(e) != 0);
   return SPMAT_OK;
@@ -773,9 +783,12 @@ static int bsr_setup(spmat_s *A) {
   }
   SP_TRY(A->bsched.alloc(2));
   SP_CUDA(cudaMemsetAsync(A->bsched.get(), 0, 8, st));
-  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
   int per_sm = 0;
-  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_bsr3, kCtaT, kBsrSmem));
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_bsr3<false, false>, kCtaT, kBsrSmem));
   A->bsr_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * A->comm->num_sms,
                                                            std::max<int64_t>(A->n_brblocks, 1)));
   SP_TRY(bsr_o_setup(A, st));

@@ -430,6 +430,7 @@ struct spmat_s {
   int64_t obr = 0, onnzb = 0;
   int ob_w = 4;
   bool env_no_bsr_fuse = false;  // SPMAT_BSR_FUSE=0: the standalone off-diagonal kernel
+  bool env_bsr_fma = false;      // SPMAT_BSR_FMA=1: fused multiply-adds in the block SpMV
   spmat::DevBuf<int32_t> ob_rows, ob_rowptr, ob_col;
   spmat::DevBuf<double> ob_val;
   spmat::DevBuf<int2> ob_range;
