@@ -126,7 +126,9 @@ static bool pipeline_ok(spmat_s *A) {
 // put of the next call (several ranks) for this call's epoch end.  The caller's stream waits
 // for this call's last download, so its completion means y is on the host.
 static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStream_t s, bool async) {
-  SP_TRY(spmv_pipe_prepare(A, A->env_pipe_chunks));
+  // asynchronous calls overlap across calls, so few chunks (less per-copy and per-kernel
+  // overhead); synchronous calls need the chunks to overlap within the call
+  SP_TRY(spmv_pipe_prepare(A, async ? A->env_pipe_chunks_async : A->env_pipe_chunks));
   const int nc = A->pipe_chunks;
   const bool multi = A->comm->nranks > 1;
   ++A->stat_mults;
