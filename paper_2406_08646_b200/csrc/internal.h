@@ -389,7 +389,7 @@ struct spmat_s {
   bool env_no_fuse = false;     // SPMAT_FUSE=0: standalone put kernel instead of the fused puts
   bool env_no_tail = false;     // SPMAT_FUSE_TAIL=0: off-diagonal add as its own kernel
   int env_pipe_chunks = 16;     // SPMAT_PIPE_CHUNKS: row chunks of the host-buffer pipeline
-  int env_pipe_chunks_async = 2;  // SPMAT_PIPE_CHUNKS_ASYNC: the same for spmat_mult_async
+  int env_pipe_chunks_async = 1;  // SPMAT_PIPE_CHUNKS_ASYNC: the same for spmat_mult_async (measured 1: 3.06 ms, 2: 3.24, 8: 3.33 on C4)
   // device-initiated halo over NVLink peer memory (halo.cu)
   bool peer = false;
   spmat::DevBuf<unsigned long long> halo_flags;  // [q]: done flag from receiver q

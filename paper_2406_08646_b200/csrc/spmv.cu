@@ -503,7 +503,7 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
     A->env_pipe_chunks = c >= 2 && c <= 256 ? c : 16;
     e = getenv("SPMAT_PIPE_CHUNKS_ASYNC");
     const int ca = e ? atoi(e) : 0;
-    A->env_pipe_chunks_async = ca >= 1 && ca <= 256 ? ca : 2;
+    A->env_pipe_chunks_async = ca >= 1 && ca <= 256 ? ca : 1;
   }
   A->kernel_id = KERNEL_TMA;
   // small matrices on one rank (or with the NCCL halo): the direct kernel; the NVLink halo
