@@ -142,13 +142,13 @@ __global__ void k_bsr_blocks4(const int32_t *__restrict__ bounds, const int32_t 
 
 // FMA: each block row's 9 products accumulated with fused multiply-adds (half the fp64 pipe
 // instructions; a different rounding, still within the 1e-12 bar and exact for integer data)
-template <int W, bool FMA>
+template <int W, bool FMA, int NT>
 __device__ __forceinline__ void brows_w(int br0, int br1, int bp0, const int *__restrict__ rp,
                                         const int *__restrict__ sc, const double *__restrict__ sv,
                                         const double *__restrict__ x, double *__restrict__ y, int tid) {
   constexpr int U = 4;  // blocks per lane in flight
   const int lane = tid & (W - 1);
-  for (int br = br0 + tid / W; br < br1; br += kT / W) {
+  for (int br = br0 + tid / W; br < br1; br += NT / W) {
     const int a = rp[br] - bp0, z = rp[br + 1] - bp0;
     double y0 = 0.0, y1 = 0.0, y2 = 0.0;
     for (int e0 = a + lane; e0 < z; e0 += U * W) {
@@ -214,6 +214,12 @@ struct BsrOff {
   int nwaits;
   unsigned int *done;                   // CTAs whose consumers finished (epoch end)
   int *err;
+  // comm-warp mode: this epoch's puts, boundary row blocks claimed first, tail counters
+  const HaloPut *puts;
+  int nputs, put_chunks;
+  int n_bblocks;                        // row blocks with off-diagonal block rows (claimed first)
+  int64_t nobr;
+  unsigned int *ctr;                    // [0] boundary-block warps done, [1] chunk claims, [2] comm warps done
 };
 
 // W = 4 lanes per off-diagonal block row, every consumer thread of the CTA takes part
@@ -270,7 +276,99 @@ static __device__ __noinline__ void bsr_off_rows(const BsrOff off, int t0, int t
   }
 }
 
-template <bool FMA, bool FUSE>
+// Comm-warp mode (NVLink halo, the default with 3x3 off-diagonal blocks): one warp of every
+// CTA stores this rank's boundary x into the neighbours' ghost lines at kernel start, waits
+// until the boundary row blocks (claimed first) are written, then adds the 3x3 off-diagonal
+// block rows in chunks of 8 (4 lanes each) beside the consumers' streaming -- the k_spmv_tma
+// design on 3x3 blocks.  The consumers lose one warp (7 instead of 8): a C5 row block holds
+// ~11 block rows, which 7 warps still cover in one pass.  The last comm warp releases the
+// ghost buffer and ends the epoch.
+static __device__ __noinline__ void bsr_comm_tail(const BsrOff off, unsigned long long epoch, double *y,
+                                                  int consumer_warps) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) {
+    const unsigned target = (unsigned)(consumer_warps * off.n_bblocks);
+    const long long t0 = clock64();
+    unsigned ns = 64;
+    while (ld_acquire_gpu(off.ctr) < target) {
+      if (clock64() - t0 > kSpinLimit) {
+        atomicExch(off.err, 2);
+        break;
+      }
+      __nanosleep(ns);
+      ns = ns < 256 ? 2 * ns : ns;
+    }
+  }
+  __syncwarp();
+  constexpr int W = 4, U = 2;
+  const uint32_t flag = ll_flag(epoch);
+  const uint4 *gl = off.ghost + (int64_t)(epoch & 1) * off.ghost_stride;
+  const int sub = lane & (W - 1);
+  const int64_t n_chunks = (off.nobr + 32 / W - 1) / (32 / W);
+  for (;;) {
+    int64_t c = 0;
+    if (lane == 0) c = atomicAdd(off.ctr + 1, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= n_chunks) break;
+    const int64_t t = c * (32 / W) + lane / W;
+    const bool valid = t < off.nobr;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (valid) {
+      const int a = off.rowptr[t], z = off.rowptr[t + 1];
+      for (int e0 = a + sub; e0 < z; e0 += U * W) {
+        int cc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) cc[u] = e0 + u * W < z ? off.col[e0 + u * W] : -1;
+        uint4 raw[U][3];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (cc[u] >= 0) raw[u][j] = ll_load_raw(gl + 3 * (int64_t)cc[u] + j);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (cc[u] < 0) continue;
+          const double *v = off.val + 9 * (int64_t)(e0 + u * W);
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const double g = ll_value(gl + 3 * (int64_t)cc[u] + j, raw[u][j], flag, off.err);
+            s0 = __dadd_rn(s0, __dmul_rn(__ldg(v + j), g));
+            s1 = __dadd_rn(s1, __dmul_rn(__ldg(v + 3 + j), g));
+            s2 = __dadd_rn(s2, __dmul_rn(__ldg(v + 6 + j), g));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = W >> 1; o > 0; o >>= 1) {
+      s0 = __dadd_rn(s0, __shfl_down_sync(0xffffffffu, s0, o, W));
+      s1 = __dadd_rn(s1, __shfl_down_sync(0xffffffffu, s1, o, W));
+      s2 = __dadd_rn(s2, __shfl_down_sync(0xffffffffu, s2, o, W));
+    }
+    if (valid && sub == 0) {
+      const int64_t r = 3 * (int64_t)off.rows[t];
+      y[r] = __dadd_rn(__ldcg(y + r), s0);
+      y[r + 1] = __dadd_rn(__ldcg(y + r + 1), s1);
+      y[r + 2] = __dadd_rn(__ldcg(y + r + 2), s2);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence();
+    if (atomicAdd(off.ctr + 2, 1u) == gridDim.x - 1) {
+      atomicExch(off.ctr, 0u);
+      atomicExch(off.ctr + 1, 0u);
+      atomicExch(off.ctr + 2, 0u);
+      __threadfence();
+      for (int q = 0; q < off.nwaits; ++q) st_release_sys(off.waits[q].peer_done, epoch);
+      *off.epoch_ctr = epoch;  // this MatMult is done
+    }
+  }
+}
+
+// MODE 0: diagonal only; 1: off-diagonal blocks added by the consumers (claimed last);
+// 2: comm warp (puts + off-diagonal tail, boundary row blocks claimed first)
+template <bool FMA, int MODE>
 __global__ void __launch_bounds__(kCtaT, 3)
     k_spmv_bsr3(const int4 *__restrict__ blocks, int n_blocks, const int32_t *__restrict__ browptr,
                 const int32_t *__restrict__ bcol, const double *__restrict__ bval,
@@ -280,19 +378,27 @@ __global__ void __launch_bounds__(kCtaT, 3)
   BsrStage *st = reinterpret_cast<BsrStage *>(smem);
   // this MatMult's halo epoch (fused off-diagonal blocks): read by every CTA before its
   // consumers finish, so before the last CTA stores it back
-  const unsigned long long epoch = FUSE ? *off.epoch_ctr + 1ull : 0ull;
+  constexpr bool FUSE = MODE == 1;
+  constexpr int NT = MODE == 2 ? kT - 32 : kT;  // consumer threads
+  const unsigned long long epoch = MODE ? *off.epoch_ctr + 1ull : 0ull;
   unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + kStagesB * sizeof(BsrStage));
   unsigned long long *empty = full + kStagesB;
   const int tid = threadIdx.x, warp = tid >> 5, lane32 = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < kStagesB; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kT / 32);
+      mbar_init(&empty[s], NT / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (warp == kT / 32) {  // producer
+  if (MODE == 2 && warp == NT / 32 + 1) {  // comm warp: puts, then the off-diagonal tail
+    for (int c = blockIdx.x; c < off.put_chunks; c += gridDim.x)
+      halo_put_warp(off.puts, off.nputs, c, x, epoch, off.err);
+    bsr_comm_tail(off, epoch, y, NT / 32);
+    return;
+  }
+  if (warp == NT / 32) {  // producer
     if (lane32 != 0) return;
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
@@ -316,6 +422,8 @@ __global__ void __launch_bounds__(kCtaT, 3)
       if (FUSE) {
         const int2 rg = off.range[b];
         st[s].ext = make_int4(rg.x, rg.y, 0, 0);
+      } else if (MODE == 2) {
+        st[s].ext = make_int4(0, 0, b < off.n_bblocks ? 1 : 0, 0);
       }
       const int64_t v0 = 9 * (int64_t)H.z, v1 = 9 * (int64_t)H.w;
       const int64_t va = v0 & ~1ll, ve = (v1 + 1) & ~1ll;
@@ -332,10 +440,23 @@ __global__ void __launch_bounds__(kCtaT, 3)
       }
     }
   }
+  // comm-warp mode: boundary row blocks are claimed first, so a warp publishes how many it wrote
+  // (one fence + one atomic per warp) when it meets its first other claim
+  unsigned bdone = 0;
+  bool published = MODE != 2;
   for (int it = 0;; ++it) {  // consumers
     const int s = it % kStagesB;
     mbar_wait(&full[s], (uint32_t)((it / kStagesB) & 1));
     const int4 h = st[s].hdr;
+    const int bnd = MODE == 2 ? st[s].ext.z : 0;
+    if (!published && (h.x < 0 || !bnd)) {
+      published = true;
+      __syncwarp();
+      if (lane32 == 0 && bdone) {
+        __threadfence();
+        atomicAdd(off.ctr, bdone);
+      }
+    }
     if (h.x < 0) break;
     const int br0 = h.x, br1 = h.y, bp0 = h.z;
     const int t0 = FUSE ? st[s].ext.x : 0, t1 = FUSE ? st[s].ext.y : 0;
@@ -343,14 +464,15 @@ __global__ void __launch_bounds__(kCtaT, 3)
     const int *sc = st[s].col + (bp0 & 3);
     const int *rp = st[s].rp - (br0 & ~3);
     const int nbr = br1 - br0;
-    if (nbr * 2 > kT) brows_w<1, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 4 > kT) brows_w<2, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 8 > kT) brows_w<4, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 16 > kT) brows_w<8, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 32 > kT) brows_w<16, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else brows_w<32, FMA>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    if (nbr * 2 > NT) brows_w<1, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 4 > NT) brows_w<2, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 8 > NT) brows_w<4, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 16 > NT) brows_w<8, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 32 > NT) brows_w<16, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else brows_w<32, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
     __syncwarp();
     if (lane32 == 0) mbar_arrive(&empty[s]);
+    bdone += bnd;
     if (FUSE && t1 > t0) {  // this block's diagonal y is written by all consumer warps: add A_o g
       asm volatile("bar.sync 1, %0;" ::"r"(kT) : "memory");
       bsr_off_rows(off, t0, t1, y, tid, epoch);
@@ -590,9 +712,9 @@ int csr_sync(spmat_s *A, cudaStream_t s) {
   return SPMAT_OK;
 }
 
-int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_off) {
+int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, int mode) {
   BsrOff off{};
-  if (fuse_off) {  // NVLink halo: off-diagonal blocks inside the kernel, which ends the epoch
+  if (mode) {  // NVLink halo: off-diagonal blocks inside the kernel, which ends the epoch
     off.range = A->ob_range.get();
     off.rows = A->ob_rows.get();
     off.rowptr = A->ob_rowptr.get();
@@ -606,8 +728,23 @@ int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_o
     off.done = A->ob_done.get();
     off.err = A->halo_err.get();
   }
-  auto kern = fuse_off ? (A->env_bsr_fma ? k_spmv_bsr3<true, true> : k_spmv_bsr3<false, true>)
-                      : (A->env_bsr_fma ? k_spmv_bsr3<true, false> : k_spmv_bsr3<false, false>);
+  if (mode == 2) {  // comm warps: this epoch's puts and the off-diagonal tail
+    off.puts = A->halo_puts.get();
+    off.nputs = A->n_puts;
+    off.put_chunks = A->put_chunks_total;
+    off.n_bblocks = (int)A->ob_nbblocks;
+    off.nobr = A->obr;
+    off.ctr = A->ob_ctr.get();
+  }
+  auto kern = mode == 1 ? (A->env_bsr_fma ? k_spmv_bsr3<true, 1> : k_spmv_bsr3<false, 1>)
+            : mode == 2 ? (A->env_bsr_fma ? k_spmv_bsr3<true, 2> : k_spmv_bsr3<false, 2>)
+                        : (A->env_bsr_fma ? k_spmv_bsr3<true, 0> : k_spmv_bsr3<false, 0>);
+  if (mode == 2) {  // comm warps spin on the peers' lines: every CTA co-resident
+    SP_CUDA(launch_coop(kern, (unsigned)A->bsr_grid, kCtaT, kBsrSmem, s, (const int4 *)A->bblocks4.get(),
+                        (int)A->n_brblocks, (const int32_t *)A->browptr.get(), (const int32_t *)A->bcol.get(),
+                        (const double *)A->bval.get(), x, y, A->bsched.get(), off));
+    return SPMAT_OK;
+  }
   kern<<<(unsigned)A->bsr_grid, kCtaT, kBsrSmem, s>>>(A->bblocks4.get(), (int)A->n_brblocks, A->browptr.get(),
                                                     A->bcol.get(), A->bval.get(), x, y, A->bsched.get(), off);
   SP_LAUNCH();
@@ -681,20 +818,24 @@ static int bsr_o_setup(spmat_s *A, cudaStream_t st) {
 static int bsr_o_env(spmat_s *A) {
   const char *e = getenv("SPMAT_NUMERIC_BSR");
   A->env_numeric_csr = e && atoi(e) == 0;
-  // off-diagonal blocks inside the block SpMV only on request: measured on B200 (C5, same box)
-  // the in-kernel add stalls each boundary row block's stage ring for a ghost-read latency
-  // chain (0.859 vs 0.836 ms at P=4, 1.660 vs 1.625 ms at P=2); the standalone kernel wins
   e = getenv("SPMAT_BSR_FMA");
   A->env_bsr_fma = e && atoi(e) != 0;
+  // off-diagonal blocks with the NVLink halo: 2 = comm warps of the block SpMV (puts + tail,
+  // default), 1 = added by the consumers themselves (measured slower: each boundary row block
+  // stalls its CTA's stage ring for a ghost-read latency chain, 0.859 vs 0.836 ms at P=4),
+  // 0 = standalone put kernel + block SpMV + standalone off-diagonal kernel
   e = getenv("SPMAT_BSR_FUSE");
-  A->env_no_bsr_fuse = !(e && atoi(e) != 0);
+  A->bsr_fuse_mode = e ? atoi(e) : 2;
+  if (A->bsr_fuse_mode < 0 || A->bsr_fuse_mode > 2) A->bsr_fuse_mode = 2;
   return SPMAT_OK;
 }
 
-// Claim order of the block SpMV with off-diagonal blocks: row blocks without off-diagonal
-// block rows first, the others last (by then every neighbour's ghost lines have landed), and
-// per claim index the range [t0, t1) of off-diagonal block rows inside the row block.
+// Claim order of the block SpMV with off-diagonal blocks, and per claim index the range
+// [t0, t1) of off-diagonal block rows inside the row block.  Comm-warp mode: row blocks with
+// off-diagonal block rows FIRST (the comm warps add them while the rest streams); in-kernel
+// mode: LAST (by then every neighbour's ghost lines have landed).
 static int bsr_claim_order(spmat_s *A, cudaStream_t st) {
+  const bool boundary_first = A->bsr_fuse_mode != 1;
   const int64_t nbk = A->n_brblocks;
   DevBuf<int4> nat;
   DevBuf<int2> rng;
@@ -711,18 +852,22 @@ static int bsr_claim_order(spmat_s *A, cudaStream_t st) {
   SP_CUDA(cudaMemcpyAsync(nat.get(), A->bblocks4.get(), nbk * sizeof(int4), cudaMemcpyDeviceToDevice, st));
   k_bsr_obrange<<<nb(nbk), 256, 0, st>>>(nat.get(), nbk, A->ob_rows.get(), A->obr, rng.get(), f_in.get(), f_out.get());
   SP_LAUNCH();
+  uint32_t *fa = boundary_first ? f_in.get() : f_out.get(), *fb = boundary_first ? f_out.get() : f_in.get();
   CUB_CALL2(tmp, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes, thrust::counting_iterator<int32_t>(0),
-                                            f_out.get(), order.get(), dn.get(), (int)nbk, st));
+                                            fa, order.get(), dn.get(), (int)nbk, st));
   int nfirst = 0;
   SP_CUDA(cudaMemcpyAsync(&nfirst, dn.get(), 4, cudaMemcpyDeviceToHost, st));
   SP_CUDA(cudaStreamSynchronize(st));
   CUB_CALL2(tmp, cub::DeviceSelect::Flagged(d_temp_storage, temp_storage_bytes, thrust::counting_iterator<int32_t>(0),
-                                            f_in.get(), order.get() + nfirst, dn.get() + 1, (int)nbk, st));
+                                            fb, order.get() + nfirst, dn.get() + 1, (int)nbk, st));
+  A->ob_nbblocks = boundary_first ? nfirst : (int64_t)nbk - nfirst;
   SP_TRY(A->ob_range.alloc(nbk));
   k_bsr_permute<<<nb(nbk), 256, 0, st>>>(nat.get(), rng.get(), order.get(), nbk, A->bblocks4.get(), A->ob_range.get());
   SP_LAUNCH();
   SP_TRY(A->ob_done.alloc(1));
   SP_CUDA(cudaMemsetAsync(A->ob_done.get(), 0, 4, st));
+  SP_TRY(A->ob_ctr.alloc(3));
+  SP_CUDA(cudaMemsetAsync(A->ob_ctr.get(), 0, 12, st));
   SP_CUDA(cudaStreamSynchronize(st));
   return SPMAT_OK;
 }
@@ -783,12 +928,14 @@ static int bsr_setup(spmat_s *A) {
   }
   SP_TRY(A->bsched.alloc(2));
   SP_CUDA(cudaMemsetAsync(A->bsched.get(), 0, 8, st));
-  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
-  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
-  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
-  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
+  SP_CUDA(cudaFuncSetAttribute(k_spmv_bsr3<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsrSmem));
   int per_sm = 0;
-  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_bsr3<false, false>, kCtaT, kBsrSmem));
+  SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_bsr3<false, 0>, kCtaT, kBsrSmem));
   A->bsr_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * A->comm->num_sms,
                                                            std::max<int64_t>(A->n_brblocks, 1)));
   SP_TRY(bsr_o_setup(A, st));

@@ -430,7 +430,9 @@ struct spmat_s {
   int env_numeric_seg = 8;       // SPMAT_NUMERIC_SEG=4|8: contributions per step of k_numeric_seg
   int64_t obr = 0, onnzb = 0;
   int ob_w = 4;
-  bool env_no_bsr_fuse = false;  // SPMAT_BSR_FUSE=0: the standalone off-diagonal kernel
+  int bsr_fuse_mode = 2;         // SPMAT_BSR_FUSE: 2 comm warps (default), 1 in-kernel add, 0 standalone kernels
+  int64_t ob_nbblocks = 0;       // row blocks with off-diagonal block rows
+  spmat::DevBuf<unsigned int> ob_ctr;  // comm-warp tail counters
   bool env_bsr_fma = false;      // SPMAT_BSR_FMA=1: fused multiply-adds in the block SpMV
   spmat::DevBuf<int32_t> ob_rows, ob_rowptr, ob_col;
   spmat::DevBuf<double> ob_val;
@@ -466,9 +468,10 @@ int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
 void cg_graph_release(spmat_s *A);            // drop the captured CG iteration
 int bsr_refresh(spmat_s *A, cudaStream_t s, bool diag = true);  // bval (diag) and ob_val from the CSR values
 int csr_sync(spmat_s *A, cudaStream_t s);  // val_d from bval when set_values wrote bval directly
-// fuse_off: also add the 3x3 off-diagonal blocks from this epoch's ghost lines and end the
-// epoch (full MatMult, NVLink halo)
-int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, bool fuse_off = false);
+// mode 1 / 2: also add the 3x3 off-diagonal blocks from this epoch's ghost lines and end the
+// epoch (full MatMult, NVLink halo) -- by the consumers (1) or by comm warps that also do the
+// puts (2); 0: diagonal only
+int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, int mode = 0);
 // off-diagonal SpMV-add on the 3x3 block copy: NVLink ghost lines of this epoch (ends the
 // epoch, like k_spmv_offdiag_peer) or, with lvec != nullptr, the NCCL ghost vector
 // cur: this MatMult's epoch (waits for its lines, ends the epoch); else the last completed one

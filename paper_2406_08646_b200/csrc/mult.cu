@@ -47,7 +47,9 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
       // at 64 registers and lost more on the stream than the overlap gained -- C5 P=2 1.43 ms
       // either way, P=1 -2 %)
       fused = !A->env_no_fuse && (part & 1) && A->kernel_id == 3 && A->m > 0 && A->n_rowblocks > 0;
-      if (!fused) {
+      // 3x3 blocks, comm-warp mode: the block SpMV's comm warps do the puts
+      const bool bsr_comm = A->bs == 3 && A->ob_ok && A->bsr_fuse_mode == 2 && part == 7 && A->m > 0 && A->n_ro > 0;
+      if (!fused && !bsr_comm) {
         pe = A->profile ? prof_pair(A, 2) : nullptr;
         if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
         SP_TRY(halo_peer_put(A, x, s));
@@ -59,12 +61,14 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
     // 3x3 blocks: the block SpMV adds the off-diagonal blocks of its boundary row blocks
     // (claimed last) from this epoch's ghost lines and ends the epoch (bsr.cu bsr_off_rows)
     const bool ob = A->bs == 3 && A->ob_ok && (part & 6) == 6 && A->n_ro > 0;
-    const bool ob_fused = ob && (part & 1) && A->m > 0 && !A->env_no_bsr_fuse;
+    const int ob_mode =
+        (ob && (part & 1) && A->m > 0) ? (A->bsr_fuse_mode == 2 && part == 7 ? 2 : (A->bsr_fuse_mode == 1 ? 1 : 0)) : 0;
+    const bool ob_fused = ob_mode != 0;
     if (part & 1) {
       pe = A->profile ? prof_pair(A, 0) : nullptr;
       if (pe) SP_CUDA(cudaEventRecord(pe[0], s));
       if (A->bs == 3 && A->m > 0)
-        SP_TRY(bsr_spmv(A, x, y, s, ob_fused));
+        SP_TRY(bsr_spmv(A, x, y, s, ob_mode));
       else
         SP_TRY(spmv_diag(A, x, y, s, fused, tail));
       if (pe) SP_CUDA(cudaEventRecord(pe[1], s));
