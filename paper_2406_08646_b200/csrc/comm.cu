@@ -214,9 +214,10 @@ int spmat_comm_create(const unsigned char *id, int nranks, int rank, int device,
     ncclUniqueId uid;
     memcpy(&uid, id, 128);
     // NCCL's kernels share the SMs with the persistent SpMV (NCCL-mode halo, COO value
-    // exchange): cap them -- ncclConfig_t.maxCTAs, default 4, SPMAT_NCCL_MAX_CTAS=0
-    // for NCCL's own choice
-    int max_ctas = 4;
+    // exchange); SURVEY §2.6 proposed capping them (ncclConfig_t.maxCTAs).  Measured on B200
+    // (C4, P=2, NCCL halo): cap 4 -> 0.290 ms per MatMult vs 0.276 ms uncapped, and the 32 MB
+    // SF-pingpong 481 vs 107 us -- so no cap by default; SPMAT_NCCL_MAX_CTAS=n sets one
+    int max_ctas = 0;
     if (const char *e = getenv("SPMAT_NCCL_MAX_CTAS")) max_ctas = atoi(e);
     ncclResult_t r;
     if (c->api->CommInitRankConfig && max_ctas > 0) {
