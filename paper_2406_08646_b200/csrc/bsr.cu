@@ -824,9 +824,13 @@ static int bsr_o_env(spmat_s *A) {
   // default), 1 = added by the consumers themselves (measured slower: each boundary row block
   // stalls its CTA's stage ring for a ghost-read latency chain, 0.859 vs 0.836 ms at P=4),
   // 0 = standalone put kernel + block SpMV + standalone off-diagonal kernel
+  // Default per rank: comm warps when the off-diagonal block rows are >= 2.5 % of the rank's
+  // block rows (C5 interior ranks at P=4: 0.635 vs 0.650 ms), else the standalone kernels (one
+  // neighbour, C5 P=2: 1.280 vs 1.295 ms -- the 8th consumer warp is worth more there).  Ranks
+  // may differ: both modes store the same flagged lines into the same peer buffers.
   e = getenv("SPMAT_BSR_FUSE");
-  A->bsr_fuse_mode = e ? atoi(e) : 2;
-  if (A->bsr_fuse_mode < 0 || A->bsr_fuse_mode > 2) A->bsr_fuse_mode = 2;
+  A->bsr_fuse_mode = e ? atoi(e) : (A->obr * 40 >= A->mb ? 2 : 0);
+  if (A->bsr_fuse_mode < 0 || A->bsr_fuse_mode > 2) A->bsr_fuse_mode = 0;
   return SPMAT_OK;
 }
 
