@@ -289,6 +289,71 @@ __global__ void __launch_bounds__(256) k_numeric_seg(
   }
 }
 
+// Element COO, warp-cooperative: a warp takes 32 consecutive nonzeros, whose contribution
+// segments are one contiguous range of perm (<= kWSpan entries): the lanes load that range
+// coalesced (8 perm loads, then their 8 v gathers, per lane in flight) into shared memory, then
+// each lane sums its own nonzero's segment from shared memory in canonical order.  No per-lane
+// predication over a fixed segment width.  A range longer than kWSpan falls back to each lane
+// summing its segment from global memory.
+constexpr int kWSpan = 256;
+__global__ void __launch_bounds__(256) k_numeric_warp(
+    const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm, const double *__restrict__ v,
+    uint64_t ncoo, int64_t nnz_d, int64_t nnz, double *__restrict__ val_d, double *__restrict__ val_o,
+    int mode) {
+  __shared__ double sw[8][kWSpan];
+  __shared__ uint32_t sq[8][kWSpan];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t z0 = ((int64_t)blockIdx.x * 8 + wib) * 32; z0 < nnz; z0 += nwarps * 32) {
+    const int64_t z = z0 + lane;
+    const bool valid = z < nnz;
+    const uint32_t a = valid ? __ldg(jmap + z) : 0u, b = valid ? __ldg(jmap + z + 1) : 0u;
+    const int last = (int)(nnz - 1 - z0 < 31 ? nnz - 1 - z0 : 31);
+    const uint32_t base = __shfl_sync(0xffffffffu, a, 0), end = __shfl_sync(0xffffffffu, b, last);
+    const uint32_t span = end - base;
+    double s = 0.0;
+    bool local = true;
+    if (span <= (uint32_t)kWSpan) {
+      uint32_t q[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t t = lane + 32 * k;
+        q[k] = t < span ? __ldg(perm + base + t) : 0u;
+      }
+      double w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] = (lane + 32 * k < span && q[k] < ncoo) ? __ldg(v + q[k]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t t = lane + 32 * k;
+        if (t < span) {
+          sq[wib][t] = q[k];
+          sw[wib][t] = w[k];
+        }
+      }
+      __syncwarp();
+      for (uint32_t t = a - base; t < b - base; ++t) {
+        if (sq[wib][t] >= ncoo) local = false;  // received contribution: k_numeric_mixed finishes it
+        s = __dadd_rn(s, sw[wib][t]);
+      }
+      __syncwarp();
+    } else {
+      for (uint32_t t = a; t < b; ++t) {
+        const uint32_t p = __ldg(perm + t);
+        if (p >= ncoo) {
+          local = false;
+          break;
+        }
+        s = __dadd_rn(s, __ldg(v + p));
+      }
+    }
+    if (valid && local) {
+      double *dst = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
+      *dst = mode == SPMAT_INSERT ? __dadd_rn(0.0, s) : __dadd_rn(*dst, s);
+    }
+  }
+}
+
 // 3x3 blocks (spmat_set_block_size(A, 3)), no received contributions: the numeric step writes
 // the block copy bval directly (the CSR val_d is then stale until spmat_sync_csr_values) -- one
 // pass over the compulsory bytes instead of val_d plus a val_d -> bval copy.  A warp walks a
@@ -943,7 +1008,7 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
     // varying count (element COO) one nonzero per thread with its segment read kSeg at a time
     const char *nk = getenv("SPMAT_NUMERIC_KERNEL");
     int kind = (double)A->ncontrib > 1.5 * (double)nnz ? 2 : 0;  // 0 ilp, 1 plain, 2 seg
-    if (nk) kind = !strcmp(nk, "plain") ? 1 : (!strcmp(nk, "seg") ? 2 : 0);
+    if (nk) kind = !strcmp(nk, "plain") ? 1 : (!strcmp(nk, "seg") ? 2 : (!strcmp(nk, "warp") ? 3 : 0));
     const int64_t z0 = direct_bsr ? A->nnz_d : 0;  // direct_bsr: off-diagonal nonzeros only
     // one contribution per nonzero (every nonzero has at least one): jmap is the identity
     const bool one = A->ncontrib == nnz && !A->env_numeric_jmap;
@@ -958,7 +1023,11 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
       SP_LAUNCH();
     }
     if (nnz > z0) {
-      if (kind == 1) {
+      if (kind == 3 && z0 == 0) {
+        const int64_t blocks = std::min<int64_t>((nnz + 255) / 256, (int64_t)A->comm->num_sms * 64);
+        k_numeric_warp<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(
+            A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo, A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
+      } else if (kind == 1) {
         k_numeric_local<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
                                                   A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
       } else if (kind == 2 && z0 == 0) {
