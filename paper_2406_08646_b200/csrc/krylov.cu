@@ -162,6 +162,7 @@ __device__ void finalize_cta(const FinArgs &f, int np) {
     *f.result = g;
   } else if (f.op == OP_CG_INIT) {
     sc->rr = g;
+    sc->beta = 0.0;  // the small-matrix path forms p_0 = r_0 + 0 * p (p = r after init)
     sc->stopped = g == 0.0 ? 1 : 0;
     sc->iter = 0;
     if (f.hist) f.hist[0] = g;
@@ -278,14 +279,19 @@ __global__ void __launch_bounds__(kDotThreads) k_dot_partial(const double *__res
 // the p.q partial in ONE kernel -- W lanes per row as in k_spmv_direct (8 (col, val) loads,
 // then 8 x gathers per lane in flight), q[r] stored, q[r]*p[r] summed per CTA by the fixed
 // tree, the last CTA finalizes alpha.  One launch and one pass over p and q fewer per iteration.
+// With the p update folded in (the small path's 2-kernel iteration): p holds p_{i-1}, and every
+// use forms p_i = r + beta p_{i-1} on the fly (the same rounded operations as k_cg_pupdate, so
+// the same bits); k_cg_update_p then stores p_i.
 template <int W>
 __global__ void __launch_bounds__(kDotThreads) k_cg_spmv_dot(const int32_t *__restrict__ rowptr,
                                                              const int32_t *__restrict__ col,
                                                              const double *__restrict__ val,
                                                              const double *__restrict__ p, double *__restrict__ q,
-                                                             int64_t m, FinArgs f) {
+                                                             int64_t m, FinArgs f, const double *__restrict__ r) {
   __shared__ double red[kDotThreads / 32];
   pdl_wait();
+  const double beta = f.sc->beta;  // read before this kernel's last CTA rewrites the scalars
+  auto pv = [&](int64_t c) { return r ? __dadd_rn(r[c], __dmul_rn(beta, p[c])) : p[c]; };
   constexpr int U = 8;
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / W;
   const int lane = threadIdx.x & (W - 1);
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(kDotThreads) k_cg_spmv_dot(const int32_t *__re
       v[u] = e < z ? __ldg(val + e) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) xv[u] = p[c[u]];
+    for (int u = 0; u < U; ++u) xv[u] = pv(c[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u)
       if (e0 + u * W < z) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
@@ -312,7 +318,7 @@ __global__ void __launch_bounds__(kDotThreads) k_cg_spmv_dot(const int32_t *__re
   double pq = 0.0;
   if (valid && lane == 0) {
     q[row] = s;
-    pq = __dmul_rn(p[row], s);
+    pq = __dmul_rn(pv(row), s);
   }
   partial_done(block_sum(pq, red), f);
 }
@@ -388,6 +394,33 @@ __global__ void __launch_bounds__(kDotThreads) k_cg_update(double *__restrict__ 
   }
   // every CTA has read sc->alpha/stopped before the last one (which rewrites sc) gets here
   partial_done(block_sum(combine(acc), red), f);
+}
+
+// The small path's update: p_i = r + beta p_{i-1} formed and stored here (the p update folded
+// in, one kernel fewer per iteration), then x += alpha p_i, r -= alpha q, r.r partials.
+__global__ void __launch_bounds__(kDotThreads) k_cg_update_p(double *__restrict__ x, double *__restrict__ r,
+                                                             double *__restrict__ p, const double *__restrict__ q,
+                                                             int64_t n, FinArgs f) {
+  __shared__ double red[kDotThreads / 32];
+  pdl_wait();
+  const double alpha = f.sc->alpha, beta = f.sc->beta;
+  const bool go = !f.sc->stopped;
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kDotThreads) {
+    double ri = r[i];
+    if (go) {
+      const double pi = __dadd_rn(ri, __dmul_rn(beta, p[i]));
+      p[i] = pi;
+      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pi));
+      ri = __dsub_rn(ri, __dmul_rn(alpha, q[i]));
+      r[i] = ri;
+    }
+    acc = __dadd_rn(acc, __dmul_rn(ri, ri));
+  }
+  // every CTA has read sc->alpha/beta/stopped before the last one (which rewrites sc) gets here
+  partial_done(block_sum(acc, red), f);
 }
 
 // p = r + beta p
@@ -497,16 +530,21 @@ static int cg_iteration(spmat_s *A, double *x, double *rr_hist, cudaStream_t s) 
     const int32_t *rp = A->rowptr_d.get(), *cl = A->col_d.get();
     const double *vl = A->val_d.get();
     const unsigned g = (unsigned)fused_grid;
+    const double *rr = r;  // p_i = r + beta p_{i-1} formed on the fly (the p update folded in)
     cudaError_t e;
     switch (A->lanes) {
-      case 1: e = launch_pdl(k_cg_spmv_dot<1>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
-      case 2: e = launch_pdl(k_cg_spmv_dot<2>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
-      case 4: e = launch_pdl(k_cg_spmv_dot<4>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
-      case 8: e = launch_pdl(k_cg_spmv_dot<8>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
-      case 16: e = launch_pdl(k_cg_spmv_dot<16>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
-      default: e = launch_pdl(k_cg_spmv_dot<32>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f); break;
+      case 1: e = launch_pdl(k_cg_spmv_dot<1>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f, rr); break;
+      case 2: e = launch_pdl(k_cg_spmv_dot<2>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f, rr); break;
+      case 4: e = launch_pdl(k_cg_spmv_dot<4>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f, rr); break;
+      case 8: e = launch_pdl(k_cg_spmv_dot<8>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f, rr); break;
+      case 16: e = launch_pdl(k_cg_spmv_dot<16>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f, rr); break;
+      default: e = launch_pdl(k_cg_spmv_dot<32>, g, kDotThreads, 0, s, rp, cl, vl, (const double *)p, q, m, f, rr); break;
     }
     SP_CUDA(e);
+    // x, r update with p_i formed and stored here; no separate p update
+    SP_CUDA(launch_pdl(k_cg_update_p, nb, kDotThreads, 0, s, x, r, p, (const double *)q, m,
+                       fin_args(A, OP_CG_BETA, nullptr, rr_hist)));
+    return SPMAT_OK;
   } else {
     SP_TRY(spmat_mult_part(A, p, q, 7, s));                            // q = A p
     SP_CUDA(launch_pdl(aligned16(p, q) ? k_dot_partial<true> : k_dot_partial<false>, pure_dot_blocks(A),
