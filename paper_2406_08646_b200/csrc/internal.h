@@ -404,7 +404,7 @@ struct spmat_s {
   spmat::DevBuf<unsigned long long> d_epoch;  // completed NVLink-halo MatMults (device)
   int64_t ghost_stride = 0;         // lines per epoch buffer of `ghost`
   // CUDA graph of one CG iteration (krylov.cu), keyed by the caller's x / history pointers
-  cudaGraphExec_t cg_exec = nullptr;
+  cudaGraphExec_t cg_exec = nullptr, cg_exec_batch = nullptr;  // one iteration / kCgBatch iterations
   const void *cg_key_x = nullptr, *cg_key_h = nullptr;
   cudaStream_t cg_stream = nullptr;
   cudaEvent_t cg_ev[2] = {nullptr, nullptr};

@@ -559,6 +559,8 @@ static int cg_iteration(spmat_s *A, double *x, double *rr_hist, cudaStream_t s) 
   return SPMAT_OK;
 }
 
+constexpr int kCgBatch = 8;  // CG iterations per graph launch
+
 static bool graph_ok(spmat_s *A) {
   const char *e = getenv("SPMAT_GRAPH");
   if (e && !strcmp(e, "0")) return false;
@@ -567,9 +569,14 @@ static bool graph_ok(spmat_s *A) {
   return A->peer && A->comm->board_ok;  // NCCL stays out of captured graphs
 }
 
-void cg_graph_release(spmat_s *A) {
+static void cg_graph_release_execs(spmat_s *A) {
   if (A->cg_exec) cudaGraphExecDestroy(A->cg_exec);
-  A->cg_exec = nullptr;
+  if (A->cg_exec_batch) cudaGraphExecDestroy(A->cg_exec_batch);
+  A->cg_exec = A->cg_exec_batch = nullptr;
+}
+
+void cg_graph_release(spmat_s *A) {
+  cg_graph_release_execs(A);
   if (A->cg_stream) cudaStreamDestroy(A->cg_stream);
   A->cg_stream = nullptr;
   for (auto &e : A->cg_ev)
@@ -632,22 +639,29 @@ int spmat_cg(spmat_t A, const double *b, double *x, int maxit, double *rr_hist, 
     for (int k = 0; k < maxit; ++k) SP_TRY(cg_iteration(A, x, rr_hist, s));
     return SPMAT_OK;
   }
+  // two graphs: one iteration, and kCgBatch iterations (one graph launch per kCgBatch
+  // iterations: for small systems the per-launch cost of a graph is a large part of an iteration)
   if (!A->cg_exec || A->cg_key_x != x || A->cg_key_h != rr_hist) {
-    if (A->cg_exec) cudaGraphExecDestroy(A->cg_exec);
-    A->cg_exec = nullptr;
-    cudaGraph_t graph;
-    SP_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    int st = cg_iteration(A, x, rr_hist, cs);
-    cudaError_t e = cudaStreamEndCapture(cs, &graph);
-    if (st != SPMAT_OK) return st;
-    if (e != cudaSuccess) return fail(SPMAT_ERR_CUDA, "spmat_cg: graph capture: %s", cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&A->cg_exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (e != cudaSuccess) return fail(SPMAT_ERR_CUDA, "spmat_cg: graph instantiate: %s", cudaGetErrorString(e));
+    cg_graph_release_execs(A);
+    for (int w = 0; w < 2; ++w) {
+      const int iters = w == 0 ? 1 : kCgBatch;
+      cudaGraph_t graph;
+      SP_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      int st = SPMAT_OK;
+      for (int k = 0; k < iters && st == SPMAT_OK; ++k) st = cg_iteration(A, x, rr_hist, cs);
+      cudaError_t e = cudaStreamEndCapture(cs, &graph);
+      if (st != SPMAT_OK) return st;
+      if (e != cudaSuccess) return fail(SPMAT_ERR_CUDA, "spmat_cg: graph capture: %s", cudaGetErrorString(e));
+      e = cudaGraphInstantiate(w == 0 ? &A->cg_exec : &A->cg_exec_batch, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) return fail(SPMAT_ERR_CUDA, "spmat_cg: graph instantiate: %s", cudaGetErrorString(e));
+    }
     A->cg_key_x = x;
     A->cg_key_h = rr_hist;
   }
-  for (int k = 0; k < maxit; ++k) SP_CUDA(cudaGraphLaunch(A->cg_exec, cs));
+  int k = 0;
+  for (; k + kCgBatch <= maxit; k += kCgBatch) SP_CUDA(cudaGraphLaunch(A->cg_exec_batch, cs));
+  for (; k < maxit; ++k) SP_CUDA(cudaGraphLaunch(A->cg_exec, cs));
   SP_CUDA(cudaEventRecord(A->cg_ev[1], cs));
   SP_CUDA(cudaStreamWaitEvent(s, A->cg_ev[1], 0));
   return SPMAT_OK;
