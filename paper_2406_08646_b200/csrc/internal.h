@@ -360,7 +360,9 @@ struct spmat_s {
   bool values_set = false;
   // SpMV schedule
   int kernel_id = 0;
-  int kernel_id_csr = 0;             // the CSR kernel chosen at create (restored by set_block_size(A, 1))
+  int kernel_id_csr = 0;
+  spmat::DevBuf<int32_t> ro_of_row;  // row -> compressed off-diagonal row or -1 (k_spmv_direct_halo)
+  int direct_halo_ok = -1;           // -1 not yet known             // the CSR kernel chosen at create (restored by set_block_size(A, 1))
   int64_t n_rowblocks = 0, max_row_nnz = 0;
   int lanes = 1;                     // lanes per row of the diagonal SpMV (row statistics)
   spmat::DevBuf<int2> rbp;           // n_rowblocks + 1 (first row, first nonzero) pairs
@@ -465,6 +467,8 @@ int spmv_prepare(spmat_s *A, cudaStream_t stream);  // row blocks + kernel choic
 int spmv_diag(spmat_s *A, const double *x, double *y, cudaStream_t stream, bool fuse_put = false,
               bool fuse_tail = false);
 int spmv_offdiag(spmat_s *A, double *y, cudaStream_t stream);
+int spmv_direct_halo(spmat_s *A, const double *x, double *y, cudaStream_t s);  // small matrix, NVLink halo, one launch
+int direct_halo_ok(spmat_s *A);  // its grid fits a cooperative launch
 void cg_graph_release(spmat_s *A);            // drop the captured CG iteration
 int bsr_refresh(spmat_s *A, cudaStream_t s, bool diag = true);  // bval (diag) and ob_val from the CSR values
 int csr_sync(spmat_s *A, cudaStream_t s);  // val_d from bval when set_values wrote bval directly

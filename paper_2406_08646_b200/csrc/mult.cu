@@ -38,6 +38,8 @@ static int mult_impl(spmat_s *A, const double *x, double *y, int part, cudaStrea
     }
   }
   if (multi && A->peer) {  // device-initiated halo over NVLink (halo.cu)
+    if (part == 7 && A->kernel_id == 5 && A->bs == 1 && A->m > 0 && !A->env_no_fuse && direct_halo_ok(A))
+      return spmv_direct_halo(A, x, y, s);  // small matrix: puts, SpMV and off-diagonal add in one launch
     bool fused = false;
     if (part & 2) {
       // the epoch lives on the device (A->d_epoch): kernels read it, the MatMult's last kernel

@@ -113,6 +113,10 @@ __global__ void k_boundary_blocks(const int2 *__restrict__ rb, int64_t nb, const
   }
 }
 
+__global__ void k_scatter_ro(const int32_t *__restrict__ rows_o, int64_t nro, int32_t *__restrict__ ro_of_row) {
+  GRID_STRIDE(q, nro) ro_of_row[rows_o[q]] = (int32_t)q;
+}
+
 // blocks4[c] = (r0, r1, p0, p1) of the row block claimed c-th (order == nullptr: identity)
 __global__ void k_blocks4(const int2 *__restrict__ rb, const int32_t *__restrict__ order, int64_t nb,
                           int4 *__restrict__ out) {
@@ -400,6 +404,75 @@ __global__ void __launch_bounds__(128) k_spmv_direct(const int32_t *__restrict__
   if (valid && lane == 0) y[row] = s;
 }
 
+// Small matrices with the NVLink halo (Kuu-sized systems on several GPUs): ONE cooperative
+// launch per MatMult -- warps of the first CTAs store this rank's boundary x as flagged lines into
+// the neighbours' ghost buffers (halo_put_warp) at kernel start, every row group computes its
+// diagonal sum as in k_spmv_direct, and a row with off-diagonal entries (ro_of_row[r] = q >= 0)
+// adds them from the ghost lines once they carry this epoch: y = S_d + S_o, written once.  The
+// last CTA releases the ghost buffer to the senders and ends the epoch.  Cooperative, because
+// rows spin on data the peers' CTAs store.
+template <int W>
+__global__ void __launch_bounds__(128) k_spmv_direct_halo(
+    const int32_t *__restrict__ rowptr, const int32_t *__restrict__ col, const double *__restrict__ val,
+    const double *__restrict__ x, double *__restrict__ y, int64_t m, const int32_t *__restrict__ ro_of_row,
+    const int32_t *__restrict__ rowptr_o, const int32_t *__restrict__ col_o, const double *__restrict__ val_o,
+    const SpmvHalo halo, const uint4 *ghost, int64_t ghost_stride, const HaloWait *__restrict__ waits, int nwaits,
+    unsigned int *counter) {
+  constexpr int U = 8;
+  const unsigned long long epoch = *halo.epoch_ctr + 1ull;
+  const int warp_g = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (warp_g < halo.put_chunks) halo_put_warp(halo.puts, halo.nputs, warp_g, x, epoch, halo.err);
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / W;
+  const int lane = threadIdx.x & (W - 1);
+  const bool valid = row < m;
+  int a = valid ? __ldg(rowptr + row) : 0, z = valid ? __ldg(rowptr + row + 1) : 0;
+  double s = 0.0;
+  for (int e0 = a + lane; e0 < z; e0 += U * W) {
+    int c[U];
+    double v[U], xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * W;
+      c[u] = e < z ? __ldg(col + e) : 0;
+      v[u] = e < z ? __ldg(val + e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) xv[u] = __ldg(x + c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * W < z) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+  }
+#pragma unroll
+  for (int o = W >> 1; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o, W));
+  // off-diagonal part of the row (ghost lines of this epoch), reduced over the same W lanes
+  const int q = valid ? __ldg(ro_of_row + row) : -1;
+  double so = 0.0;
+  if (q >= 0) {
+    const uint4 *gl = ghost + (int64_t)(epoch & 1) * ghost_stride;
+    const uint32_t flag = ll_flag(epoch);
+    a = __ldg(rowptr_o + q);
+    z = __ldg(rowptr_o + q + 1);
+    for (int e = a + lane; e < z; e += W)
+      so = __dadd_rn(so, __dmul_rn(__ldg(val_o + e), ll_load(gl + __ldg(col_o + e), flag, halo.err)));
+  }
+  const unsigned qmask = __ballot_sync(0xffffffffu, q >= 0);
+  if (qmask) {
+#pragma unroll
+    for (int o = W >> 1; o > 0; o >>= 1) so = __dadd_rn(so, __shfl_down_sync(0xffffffffu, so, o, W));
+  }
+  if (valid && lane == 0) y[row] = q >= 0 ? __dadd_rn(s, so) : s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(counter, 1u) == gridDim.x - 1) {
+      atomicExch(counter, 0u);
+      __threadfence();
+      for (int w = 0; w < nwaits; ++w) st_release_sys(waits[w].peer_done, epoch);
+      *halo.epoch_ctr = epoch;  // this MatMult is done
+    }
+  }
+}
+
 // ------------------------------------------------------------------ alternative: vector
 template <int W>
 __global__ void __launch_bounds__(256) k_spmv_vector(const int32_t *__restrict__ rowptr,
@@ -508,7 +581,8 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   A->kernel_id = KERNEL_TMA;
   // small matrices on one rank (or with the NCCL halo): the direct kernel; the NVLink halo
   // needs the comm warps of the bulk-copy kernel
-  const bool small = 12 * nnz + 20 * m < kSmallBytes && (A->comm->nranks == 1 || (getenv("SPMAT_HALO") && !strcmp(getenv("SPMAT_HALO"), "nccl")));
+  // (several ranks with the NVLink halo: k_spmv_direct_halo, the halo fused into the direct kernel)
+  const bool small = 12 * nnz + 20 * m < kSmallBytes;
   if (small) A->kernel_id = KERNEL_DIRECT;
   const char *env = getenv("SPMAT_SPMV_KERNEL");
   if (env && !strcmp(env, "tma")) A->kernel_id = KERNEL_TMA;
@@ -674,6 +748,72 @@ static cudaError_t launch_direct(spmat_s *A, const double *x, double *y, cudaStr
   const unsigned grid = (unsigned)std::max<int64_t>(1, (threads + 127) / 128);
   return launch_pdl(k_spmv_direct<W>, grid, 128, 0, s, (const int32_t *)A->rowptr_d.get(),
                     (const int32_t *)A->col_d.get(), (const double *)A->val_d.get(), x, y, A->m);
+}
+
+template <int W>
+static int64_t direct_halo_grid(spmat_s *A) {
+  const int64_t threads = std::max<int64_t>(A->m * W, 32LL * A->put_chunks_total);
+  return std::max<int64_t>(1, (threads + 127) / 128);
+}
+
+// 1 if the one-launch small MatMult fits a cooperative launch (every CTA resident)
+template <int W>
+static int direct_halo_fits(spmat_s *A) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmv_direct_halo<W>, 128, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return direct_halo_grid<W>(A) <= (int64_t)per_sm * A->comm->num_sms ? 1 : 0;
+}
+
+int direct_halo_ok(spmat_s *A) {
+  if (A->direct_halo_ok < 0) {
+    switch (A->lanes) {
+      case 1: A->direct_halo_ok = direct_halo_fits<1>(A); break;
+      case 2: A->direct_halo_ok = direct_halo_fits<2>(A); break;
+      case 4: A->direct_halo_ok = direct_halo_fits<4>(A); break;
+      case 8: A->direct_halo_ok = direct_halo_fits<8>(A); break;
+      case 16: A->direct_halo_ok = direct_halo_fits<16>(A); break;
+      default: A->direct_halo_ok = direct_halo_fits<32>(A); break;
+    }
+  }
+  return A->direct_halo_ok;
+}
+
+template <int W>
+static cudaError_t launch_direct_halo(spmat_s *A, const double *x, double *y, cudaStream_t s) {
+  const unsigned grid = (unsigned)direct_halo_grid<W>(A);
+  SpmvHalo h{A->halo_puts.get(), A->n_puts, A->put_chunks_total, A->d_epoch.get(), 1, A->halo_err.get()};
+  return launch_coop(k_spmv_direct_halo<W>, grid, 128, 0, s, (const int32_t *)A->rowptr_d.get(),
+                     (const int32_t *)A->col_d.get(), (const double *)A->val_d.get(), x, y, A->m,
+                     (const int32_t *)A->ro_of_row.get(), (const int32_t *)A->rowptr_o.get(),
+                     (const int32_t *)A->col_o.get(), (const double *)A->val_o.get(), h,
+                     (const uint4 *)A->ghost.get(), A->ghost_stride, (const HaloWait *)A->halo_waits.get(),
+                     A->n_waits, A->halo_counter.get());
+}
+
+// the whole MatMult of a small matrix with the NVLink halo in one launch (k_spmv_direct_halo)
+int spmv_direct_halo(spmat_s *A, const double *x, double *y, cudaStream_t s) {
+  if (!A->ro_of_row.get()) {  // row -> compressed off-diagonal row (or -1), built on first use
+    SP_TRY(A->ro_of_row.alloc(std::max<int64_t>(A->m, 1)));
+    SP_CUDA(cudaMemsetAsync(A->ro_of_row.get(), 0xff, std::max<int64_t>(A->m, 1) * 4, s));
+    if (A->n_ro > 0) {
+      k_scatter_ro<<<nblk(A->n_ro), 256, 0, s>>>(A->rows_o.get(), A->n_ro, A->ro_of_row.get());
+      SP_LAUNCH();
+    }
+  }
+  cudaError_t e;
+  switch (A->lanes) {
+    case 1: e = launch_direct_halo<1>(A, x, y, s); break;
+    case 2: e = launch_direct_halo<2>(A, x, y, s); break;
+    case 4: e = launch_direct_halo<4>(A, x, y, s); break;
+    case 8: e = launch_direct_halo<8>(A, x, y, s); break;
+    case 16: e = launch_direct_halo<16>(A, x, y, s); break;
+    default: e = launch_direct_halo<32>(A, x, y, s); break;
+  }
+  SP_CUDA(e);
+  return SPMAT_OK;
 }
 
 template <int W>

@@ -42,6 +42,7 @@ def test_multirank_offdiag_lanes(ro_w, fuse):
     env = dict(os.environ)
     env["SPMAT_RO_W"] = ro_w
     env["SPMAT_FUSE_TAIL"] = fuse
+    env["SPMAT_SPMV_KERNEL"] = "tma"  # the small cases would take the one-launch direct kernel
     port = 29661 + int(ro_w) + 40 * int(fuse)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(HERE, "mp_gpu_parity.py")]
@@ -79,6 +80,27 @@ def test_multirank_offdiag_3x3(k):
     assert r.returncode == 0
     assert f"MULTIRANK P={P} failures=0" in r.stdout
     assert "PASS full-c5" in r.stdout
+
+
+@pytest.mark.parametrize("split", ["1", "0"])
+def test_multirank_tma_tails(split):
+    """The bulk-copy SpMV with its fused off-diagonal tail on every small case (they default to
+    the one-launch direct kernel): the split tail (sums during the sweep, add pass after; the
+    default for box partitions) forced on, and the boundary-first tail forced on."""
+    P = 2
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    env = dict(os.environ)
+    env["SPMAT_SPMV_KERNEL"] = "tma"
+    env["SPMAT_SPLIT_TAIL"] = split
+    env["MP_CASES"] = "stencil,q1,elasticity,random,box"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr=127.0.0.1", f"--master-port={29731 + int(split)}", os.path.join(HERE, "mp_gpu_parity.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    sys.stdout.write(r.stdout[-6000:])
+    sys.stderr.write(r.stderr[-6000:])
+    assert r.returncode == 0
+    assert f"MULTIRANK P={P} failures=0" in r.stdout
 
 
 def test_multirank_nccl_board():
