@@ -1,5 +1,5 @@
 # Round-2 final evidence on 4 GPUs (run at the tip; results copied into profiles/ by hand)
-D=gpurun_out/r02final; mkdir -p $D
+D=gpurun_out/${R02_OUT:-r02final}; mkdir -p $D
 { echo "tip: $(cat .tip_sha 2>/dev/null)"; date -u; nvidia-smi -L; } > $D/pytest_gpu_4gpu.log
 timeout 2400 python -m pytest tests -m gpu -rA -p no:cacheprovider >> $D/pytest_gpu_4gpu.log 2>&1; echo "pytest rc=$?"; tail -3 $D/pytest_gpu_4gpu.log
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $D/smoke.log 2>&1; tail -1 $D/smoke.log
