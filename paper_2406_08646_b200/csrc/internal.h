@@ -435,7 +435,7 @@ struct spmat_s {
   int bsr_fuse_mode = 2;         // SPMAT_BSR_FUSE: 2 comm warps (default), 1 in-kernel add, 0 standalone kernels
   int64_t ob_nbblocks = 0;       // row blocks with off-diagonal block rows
   spmat::DevBuf<unsigned int> ob_ctr;  // comm-warp tail counters
-  bool env_bsr_fma = false;      // SPMAT_BSR_FMA=1: fused multiply-adds in the block SpMV
+  bool env_bsr_fma = true;       // SPMAT_BSR_FMA=0: separately rounded products in the block SpMV
   spmat::DevBuf<int32_t> ob_rows, ob_rowptr, ob_col;
   spmat::DevBuf<double> ob_val;
   spmat::DevBuf<int2> ob_range;

@@ -55,15 +55,15 @@ def test_multirank_offdiag_lanes(ro_w, fuse):
 
 ENV3 = [{"SPMAT_BSR_FUSE": "1"}, {"SPMAT_BSR_FUSE": "0", "SPMAT_OB_W": "1"},
         {"SPMAT_BSR_FUSE": "0", "SPMAT_OB_W": "8"}, {"SPMAT_BSR_OFFDIAG": "0"}, {"SPMAT_HALO": "nccl"},
-        {"SPMAT_BSR_FMA": "1"}]
+        {"SPMAT_BSR_FMA": "0"}]
 
 
 @pytest.mark.parametrize("k", range(len(ENV3)))
 def test_multirank_offdiag_3x3(k):
     """3x3 off-diagonal blocks: by the block SpMV's comm warps (default), by its consumers
     (SPMAT_BSR_FUSE=1), by the standalone kernel (SPMAT_BSR_FUSE=0) with forced lanes per block
-    row, switched off (CSR off-diagonal kernels), on the NCCL ghost vector, and with the FMA
-    block SpMV -- elasticity cases (real and integer) and full-size C5."""
+    row, switched off (CSR off-diagonal kernels), on the NCCL ghost vector, and with separately
+    rounded products in the block SpMV -- elasticity cases (real and integer) and full-size C5."""
     env = ENV3[k]
     P = 2
     if torch.cuda.device_count() < P:
