@@ -189,6 +189,19 @@ int spmat_mult(spmat_t A, const double *x, double *y, void *stream);
    Collective. */
 int spmat_mult_async(spmat_t A, const double *x, double *y, void *stream);
 
+/* spmat_mult_async for a stream of MatMults on pinned host buffers (a serving loop): the SpMV
+   runs on an internal stream and the caller's `stream` is made to wait for this call's download
+   of y only at the NEXT call on this matrix (any spmat_mult* call) or at spmat_mult_flush -- so
+   call k+1's SpMV also overlaps call k's download.  y of a call is valid once `stream` has
+   completed the work enqueued up to the next call or flush.  Work the caller enqueues on
+   `stream` after the call is ordered after this call's SpMV (set_values may follow safely).
+   Device pointers: as spmat_mult.  Collective. */
+int spmat_mult_pipelined(spmat_t A, const double *x, double *y, void *stream);
+
+/* Make `stream` wait for the download of y left pending by the last spmat_mult_pipelined call
+   (no-op if none).  Enqueue only. */
+int spmat_mult_flush(spmat_t A, void *stream);
+
 /* MatMultTranspose: y = A^T x (collective, enqueue-only).  x: DEVICE array of m_local doubles
    (the row layout), y: DEVICE array of n_local doubles (the column layout).  PETSc's MPIAIJ
    order: lvec = A_o^T x, y = A_d^T x, then the halo star forest reduces lvec into the owners' y

@@ -14,7 +14,8 @@ MatSetValuesCOO / MatMult / PetscSFBcastBegin/End):
     comm_unique_id, comm_create, comm_check, comm_destroy,
     sf_create, sf_bcast_begin, sf_bcast_end, sf_reduce_begin, sf_reduce_end, sf_get_info, sf_export,
     sf_transport, sf_check, sf_destroy,
-    spmat_create_coo, spmat_set_values_coo, spmat_mult, spmat_mult_async, spmat_mult_transpose, spmat_mult_part,
+    spmat_create_coo, spmat_set_values_coo, spmat_mult, spmat_mult_async, spmat_mult_pipelined,
+    spmat_mult_flush, spmat_mult_transpose, spmat_mult_part,
     spmat_get_info, spmat_export, spmat_get_halo_sf, spmat_profile, spmat_profile_read,
     spmat_destroy
 
@@ -56,7 +57,7 @@ ABI_SYMBOLS = (
     "spmat_comm_check", "spmat_comm_destroy", "sf_create", "sf_bcast_begin", "sf_bcast_end",
     "sf_reduce_begin", "sf_reduce_end",
     "sf_get_info", "sf_export", "sf_transport", "sf_check", "sf_destroy", "spmat_create_coo", "spmat_set_values_coo",
-    "spmat_mult", "spmat_mult_async", "spmat_mult_transpose", "spmat_mult_part", "spmat_get_info", "spmat_export", "spmat_get_halo_sf",
+    "spmat_mult", "spmat_mult_async", "spmat_mult_pipelined", "spmat_mult_flush", "spmat_mult_transpose", "spmat_mult_part", "spmat_get_info", "spmat_export", "spmat_get_halo_sf",
     "spmat_profile", "spmat_profile_read", "spmat_check", "spmat_halo_mode", "spmat_trace_read",
     "spmat_vec_dot", "spmat_cg", "spmat_set_block_size",
     "spmat_destroy")
@@ -104,6 +105,8 @@ def load(path: str = LIB_PATH):
         "spmat_set_values_coo": ([p, p, i32, p], i32),
         "spmat_mult": ([p, p, p, p], i32),
         "spmat_mult_async": ([p, p, p, p], i32),
+        "spmat_mult_pipelined": ([p, p, p, p], i32),
+        "spmat_mult_flush": ([p, p], i32),
         "spmat_mult_transpose": ([p, p, p, p], i32),
         "spmat_mult_part": ([p, p, p, i32, p], i32),
         "spmat_get_info": ([p, p], i32),
@@ -248,6 +251,14 @@ def spmat_mult(A_h, x, y, stream=None):
 
 def spmat_mult_async(A_h, x, y, stream=None):
     _check(load().spmat_mult_async(A_h, _ptr(x), _ptr(y), _stream(stream)), "spmat_mult_async")
+
+
+def spmat_mult_pipelined(A_h, x, y, stream=None):
+    _check(load().spmat_mult_pipelined(A_h, _ptr(x), _ptr(y), _stream(stream)), "spmat_mult_pipelined")
+
+
+def spmat_mult_flush(A_h, stream=None):
+    _check(load().spmat_mult_flush(A_h, _stream(stream)), "spmat_mult_flush")
 
 
 def spmat_mult_transpose(A_h, x, y, stream=None):
@@ -420,6 +431,13 @@ class Mat:
     def mult_async(self, x, y, stream=None):
         """spmat_mult_async: enqueue only, also for (pinned) host x / y."""
         spmat_mult_async(self.h, x, y, stream)
+
+    def mult_pipelined(self, x, y, stream=None):
+        """spmat_mult_pipelined: enqueue only; y complete after the next call or flush()."""
+        spmat_mult_pipelined(self.h, x, y, stream)
+
+    def flush(self, stream=None):
+        spmat_mult_flush(self.h, stream)
 
     def mult_transpose(self, x, y, stream=None):
         spmat_mult_transpose(self.h, x, y, stream)

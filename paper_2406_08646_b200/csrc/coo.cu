@@ -1217,6 +1217,7 @@ int spmat_destroy(spmat_t A) {
     for (cudaEvent_t e : A->pipe_ev) cudaEventDestroy(e);
     if (A->pipe_in) cudaStreamDestroy(A->pipe_in);
     if (A->pipe_out) cudaStreamDestroy(A->pipe_out);
+    if (A->pipe_comp) cudaStreamDestroy(A->pipe_comp);
     if (A->pipe_comm) cudaStreamDestroy(A->pipe_comm);
     if (A->ev_send_ready) cudaEventDestroy(A->ev_send_ready);
     if (A->ev_recv_done) cudaEventDestroy(A->ev_recv_done);

@@ -449,6 +449,9 @@ struct spmat_s {
   spmat::DevBuf<int4> pipe_blocks4;        // row-ordered block table (when the claim order differs)
   cudaStream_t pipe_comm = nullptr;        // high-priority stream of the standalone put
   cudaStream_t pipe_in = nullptr, pipe_out = nullptr;
+  cudaStream_t pipe_comp = nullptr;        // SpMV chunks of pipelined calls (spmat_mult_pipelined)
+  bool pipe_pending = false;               // a pipelined call's download not yet waited for by the caller's stream
+  cudaEvent_t pipe_ev_pending = nullptr;
   std::vector<cudaEvent_t> pipe_ev;                        // 2 * chunks + 2
   // CG / dot workspace (krylov.cu), allocated on first use
   spmat::DevBuf<double> cg_r, cg_p, cg_q, cg_partial, cg_scalars, cg_reduced;

@@ -126,15 +126,32 @@ static bool pipeline_ok(spmat_s *A) {
 }
 
 // Calls alternate between two staging slots (x and y copies on the device), so with
-// asynchronous calls (spmat_mult_async) call k+1's upload overlaps call k's download -- PCIe is
-// full duplex.  Slot reuse is ordered by events: the upload into a slot waits for the SpMV
-// that read it two calls ago, the SpMV writing a slot's y for that slot's last download; the
-// put of the next call (several ranks) for this call's epoch end.  The caller's stream waits
-// for this call's last download, so its completion means y is on the host.
-static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStream_t s, bool async) {
+// asynchronous calls call k+1's upload overlaps call k's download -- PCIe is full duplex.  Slot
+// reuse is ordered by events: the upload into a slot waits for the SpMV that read it two calls
+// ago, the SpMV writing a slot's y for that slot's last download; the put of the next call
+// (several ranks) for this call's epoch end.
+//   mode 0 (spmat_mult): the call returns after y is on the host.
+//   mode 1 (spmat_mult_async): enqueue only; the caller's stream waits for this call's
+//     download, so its completion means y is on the host (the next call's SpMV, on that stream,
+//     then also waits for it).
+//   mode 2 (spmat_mult_pipelined): enqueue only; the SpMV runs on an internal stream and the
+//     caller's stream waits for this call's download only at the NEXT call on this matrix (or
+//     spmat_mult_flush) -- so call k+1's SpMV overlaps call k's download too.
+enum { MULT_SYNC = 0, MULT_ASYNC = 1, MULT_PIPELINED = 2 };
+
+// the caller's stream waits for the download a pipelined call left pending
+static int flush_pending(spmat_s *A, cudaStream_t s) {
+  if (A->pipe_pending) {
+    SP_CUDA(cudaStreamWaitEvent(s, A->pipe_ev_pending, 0));
+    A->pipe_pending = false;
+  }
+  return SPMAT_OK;
+}
+
+static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStream_t s, int mode) {
   // asynchronous calls overlap across calls, so few chunks (less per-copy and per-kernel
   // overhead); synchronous calls need the chunks to overlap within the call
-  SP_TRY(spmv_pipe_prepare(A, async ? A->env_pipe_chunks_async : A->env_pipe_chunks));
+  SP_TRY(spmv_pipe_prepare(A, mode != MULT_SYNC ? A->env_pipe_chunks_async : A->env_pipe_chunks));
   const int nc = A->pipe_chunks;
   const bool multi = A->comm->nranks > 1;
   ++A->stat_mults;
@@ -144,11 +161,13 @@ static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStrea
     SP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     SP_CUDA(cudaStreamCreateWithFlags(&A->pipe_in, cudaStreamNonBlocking));
     SP_CUDA(cudaStreamCreateWithFlags(&A->pipe_out, cudaStreamNonBlocking));
+    SP_CUDA(cudaStreamCreateWithFlags(&A->pipe_comp, cudaStreamNonBlocking));
     SP_CUDA(cudaStreamCreateWithPriority(&A->pipe_comm, cudaStreamNonBlocking, hi));
   }
   // [0,nc) x chunk in, [nc,2nc) y chunk done, 2nc start, 2nc+1 end, 2nc+2 puts done,
-  // 2nc+3+slot: slot's x free (its SpMV done), 2nc+5+slot: slot's y downloaded, 2nc+7 epoch end
-  while (A->pipe_ev.size() < (size_t)(2 * nc + 8)) {
+  // 2nc+3+slot: slot's x free (its SpMV done), 2nc+5+slot: slot's y downloaded, 2nc+7 epoch end,
+  // 2nc+8 this call's compute done
+  while (A->pipe_ev.size() < (size_t)(2 * nc + 9)) {
     cudaEvent_t e;
     SP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     A->pipe_ev.push_back(e);
@@ -160,13 +179,21 @@ static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStrea
   double *dx = A->xstage.get() + (size_t)slot * A->n, *dy = A->ystage.get() + (size_t)slot * A->m;
   cudaEvent_t *ev = A->pipe_ev.data();
   cudaEvent_t ev_xfree = ev[2 * nc + 3 + slot], ev_yfree = ev[2 * nc + 5 + slot], ev_epoch = ev[2 * nc + 7];
-  if (!async) {  // earlier work on s (e.g. a device-pointer MatMult using the same buffers)
+  // the compute stream: the caller's, or (pipelined) an internal one that starts after the
+  // caller's work so far -- recorded BEFORE the caller's stream waits for the previous download
+  cudaStream_t cs = s;
+  if (mode == MULT_PIPELINED) {
+    cs = A->pipe_comp;
+    SP_CUDA(cudaEventRecord(ev[2 * nc], s));
+    SP_CUDA(cudaStreamWaitEvent(cs, ev[2 * nc], 0));
+    SP_TRY(flush_pending(A, s));
+  } else if (mode == MULT_SYNC) {  // earlier work on s (e.g. a device-pointer MatMult using the same buffers)
     SP_CUDA(cudaEventRecord(ev[2 * nc], s));
     SP_CUDA(cudaStreamWaitEvent(A->pipe_in, ev[2 * nc], 0));
     SP_CUDA(cudaStreamWaitEvent(A->pipe_out, ev[2 * nc], 0));
   }
   SP_CUDA(cudaStreamWaitEvent(A->pipe_in, ev_xfree, 0));  // the SpMV of two calls ago read this slot
-  SP_CUDA(cudaStreamWaitEvent(s, ev_yfree, 0));           // this slot's y of two calls ago is downloaded
+  SP_CUDA(cudaStreamWaitEvent(cs, ev_yfree, 0));          // this slot's y of two calls ago is downloaded
   std::vector<int> order;
   for (int pass = 0; pass < 2; ++pass)  // chunks the puts read first
     for (int k = 0; k < nc; ++k)
@@ -177,7 +204,7 @@ static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStrea
     SP_CUDA(cudaEventRecord(ev[k], A->pipe_in));
   }
   if (multi) {
-    if (!async) SP_CUDA(cudaStreamWaitEvent(A->pipe_comm, ev[2 * nc], 0));
+    if (mode == MULT_SYNC) SP_CUDA(cudaStreamWaitEvent(A->pipe_comm, ev[2 * nc], 0));
     SP_CUDA(cudaStreamWaitEvent(A->pipe_comm, ev_epoch, 0));  // the previous call's epoch is over
     for (int k = 0; k < nc; ++k)
       if (A->pipe_put_chunk[k]) SP_CUDA(cudaStreamWaitEvent(A->pipe_comm, ev[k], 0));
@@ -188,35 +215,44 @@ static int mult_host_pipelined(spmat_s *A, const double *x, double *y, cudaStrea
   for (int k = 0; k < nc; ++k) {
     for (int j = 0; j < nc; ++j)  // every x chunk holding a column this row chunk reads
       if (A->pipe_row[j] <= A->pipe_xneed[k] && A->pipe_row[j + 1] > A->pipe_xmin[k])
-        SP_CUDA(cudaStreamWaitEvent(s, ev[j], 0));
-    SP_TRY(spmv_diag_chunk(A, dx, dy, k, s));
+        SP_CUDA(cudaStreamWaitEvent(cs, ev[j], 0));
+    SP_TRY(spmv_diag_chunk(A, dx, dy, k, cs));
     if (multi && A->pipe_q[k + 1] > A->pipe_q[k]) {
       // my puts are out before this stream spins on the neighbours' lines: no rank can hold
       // every SM waiting while its own puts are still queued
-      if (!put_waited) SP_CUDA(cudaStreamWaitEvent(s, ev[2 * nc + 2], 0));
+      if (!put_waited) SP_CUDA(cudaStreamWaitEvent(cs, ev[2 * nc + 2], 0));
       put_waited = true;
-      SP_TRY(halo_peer_offdiag_range(A, dy, A->pipe_q[k], A->pipe_q[k + 1], s));
+      SP_TRY(halo_peer_offdiag_range(A, dy, A->pipe_q[k], A->pipe_q[k + 1], cs));
     }
-    SP_CUDA(cudaEventRecord(ev[nc + k], s));
+    SP_CUDA(cudaEventRecord(ev[nc + k], cs));
     SP_CUDA(cudaStreamWaitEvent(A->pipe_out, ev[nc + k], 0));
     const int64_t r0 = A->pipe_row[k], r1 = A->pipe_row[k + 1];
     SP_CUDA(cudaMemcpyAsync(y + r0, dy + r0, (r1 - r0) * 8, cudaMemcpyDeviceToHost, A->pipe_out));
   }
   if (multi) {  // the put read this epoch's number: it must be done before the epoch advances
-    if (!put_waited) SP_CUDA(cudaStreamWaitEvent(s, ev[2 * nc + 2], 0));
-    SP_TRY(halo_peer_epoch_end(A, s));
-    SP_CUDA(cudaEventRecord(ev_epoch, s));
+    if (!put_waited) SP_CUDA(cudaStreamWaitEvent(cs, ev[2 * nc + 2], 0));
+    SP_TRY(halo_peer_epoch_end(A, cs));
+    SP_CUDA(cudaEventRecord(ev_epoch, cs));
   }
-  SP_CUDA(cudaEventRecord(ev_xfree, s));
+  SP_CUDA(cudaEventRecord(ev_xfree, cs));
   SP_CUDA(cudaEventRecord(ev_yfree, A->pipe_out));
+  if (mode == MULT_PIPELINED) {
+    // the caller's later work (e.g. set_values on this matrix) must follow this call's SpMV;
+    // its wait for the download is deferred to the next call / spmat_mult_flush
+    SP_CUDA(cudaEventRecord(ev[2 * nc + 8], cs));
+    SP_CUDA(cudaStreamWaitEvent(s, ev[2 * nc + 8], 0));
+    A->pipe_ev_pending = ev_yfree;
+    A->pipe_pending = true;
+    return SPMAT_OK;
+  }
   SP_CUDA(cudaStreamWaitEvent(s, ev_yfree, 0));
-  if (!async) SP_CUDA(cudaStreamSynchronize(s));
+  if (mode == MULT_SYNC) SP_CUDA(cudaStreamSynchronize(s));
   return SPMAT_OK;
 }
 
 // spmat_mult / spmat_mult_async body: device pointers enqueue only; host pointers are staged
 // (pipelined when large enough), and with async == false the call returns after y is written
-static int mult_entry(spmat_t A, const double *x, double *y, void *stream, bool async, const char *who) {
+static int mult_entry(spmat_t A, const double *x, double *y, void *stream, int mode, const char *who) {
   if (!A) return fail(SPMAT_ERR_ARG, "%s: null matrix", who);
   if ((A->n > 0 && !x) || (A->m > 0 && !y)) return fail(SPMAT_ERR_ARG, "%s: null x or y", who);
   if (x && (const void *)x == (const void *)y) return fail(SPMAT_ERR_ARG, "%s: x and y alias", who);
@@ -226,8 +262,11 @@ static int mult_entry(spmat_t A, const double *x, double *y, void *stream, bool 
   cudaStream_t s = (cudaStream_t)stream;
   const bool hx = A->n > 0 && !is_device_ptr(x);
   const bool hy = A->m > 0 && !is_device_ptr(y);
+  const bool pipe = hx && hy && pipeline_ok(A);
+  if (!(pipe && mode == MULT_PIPELINED)) SP_TRY(flush_pending(A, s));
   if (!hx && !hy) return mult_impl(A, x, y, 7, s);
-  if (hx && hy && pipeline_ok(A)) return mult_host_pipelined(A, x, y, s, async);
+  if (pipe) return mult_host_pipelined(A, x, y, s, mode);
+  const bool async = mode != MULT_SYNC;
   // host buffers: stage through device copies inside the stream order
   const double *dx = x;
   double *dy = y;
@@ -254,12 +293,23 @@ extern "C" {
 
 int spmat_mult(spmat_t A, const double *x, double *y, void *stream) {
   SP_NVTX("spmat_mult");
-  return mult_entry(A, x, y, stream, false, "spmat_mult");
+  return mult_entry(A, x, y, stream, MULT_SYNC, "spmat_mult");
 }
 
 int spmat_mult_async(spmat_t A, const double *x, double *y, void *stream) {
   SP_NVTX("spmat_mult_async");
-  return mult_entry(A, x, y, stream, true, "spmat_mult_async");
+  return mult_entry(A, x, y, stream, MULT_ASYNC, "spmat_mult_async");
+}
+
+int spmat_mult_pipelined(spmat_t A, const double *x, double *y, void *stream) {
+  SP_NVTX("spmat_mult_pipelined");
+  return mult_entry(A, x, y, stream, MULT_PIPELINED, "spmat_mult_pipelined");
+}
+
+int spmat_mult_flush(spmat_t A, void *stream) {
+  if (!A) return fail(SPMAT_ERR_ARG, "spmat_mult_flush: null matrix");
+  DeviceGuard g(A->comm->device);
+  return flush_pending(A, (cudaStream_t)stream);
 }
 
 int spmat_mult_part(spmat_t A, const double *x, double *y, int part, void *stream) {

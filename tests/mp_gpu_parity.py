@@ -365,6 +365,14 @@ def case_host_pipeline(c, kind):
     s.synchronize()
     for k, (yk, w) in enumerate(zip(yhs, want)):
         assert torch.equal(yk, w), f"async host pipeline {kind} rank {r} call {k}"
+    for yk in yhs:  # pipelined calls: downloads waited for at the next call / flush
+        yk.fill_(float("nan"))
+    for xk, yk in zip(xhs, yhs):
+        A.mult_pipelined(xk, yk, s)
+    A.flush(s)
+    s.synchronize()
+    for k, (yk, w) in enumerate(zip(yhs, want)):
+        assert torch.equal(yk, w), f"pipelined host calls {kind} rank {r} call {k}"
     A.check()
     A.close()
 

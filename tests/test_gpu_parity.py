@@ -628,6 +628,22 @@ def test_host_pipeline_matches_device(sp, comm):
     s.synchronize()
     for yk, w in zip(yhs, want):
         assert torch.equal(yk, w)
+    # pipelined calls (download waited for at the next call / flush), then values changed on
+    # the stream right after a call: the SpMV of that call must still see the old values
+    for yk in yhs:
+        yk.fill_(float("nan"))
+    for xk, yk in zip(xhs, yhs):
+        A.mult_pipelined(xk, yk, s)
+    A.flush(s)
+    s.synchronize()
+    for yk, w in zip(yhs, want):
+        assert torch.equal(yk, w)
+    A.mult_pipelined(xhs[0], yhs[0], s)
+    A.set_values(v * 2, stream=s)  # ordered after the pipelined call's SpMV
+    A.mult_pipelined(xhs[1], yhs[1], s)
+    A.flush(s)
+    s.synchronize()
+    assert torch.equal(yhs[0], want[0]) and torch.equal(yhs[1], 2 * want[1])
     A.close()
 
 
