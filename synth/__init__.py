@@ -93,14 +93,18 @@ def offsets_from_sizes(sizes) -> list[int]:
     return out
 
 
+def slab_planes(nz: int, P: int) -> list[int]:
+    """z-planes per rank: nz/P each, the remainder to the low ranks (exact when P divides nz)."""
+    return [nz // P + (1 if r < nz % P else 0) for r in range(P)]
+
+
 def slab_sizes(shape, P: int, dof: int = 1) -> list[int]:
-    """Exact z-slabs: nz/P planes per rank, lexicographic rows."""
-    nz = shape[-1]
-    assert nz % P == 0, "slab partition needs nz divisible by P"
+    """z-slabs: whole planes per rank (nz/P when P divides nz, else the
+    remainder to the low ranks), lexicographic rows."""
     plane = 1
     for s in shape[:-1]:
         plane *= s
-    return [plane * (nz // P) * dof] * P
+    return [plane * k * dof for k in slab_planes(shape[-1], P)]
 
 
 # ----------------------------------------------------------------------------------------
@@ -247,9 +251,10 @@ def q1_slab_elems(n: int, P: int, r: int):
     """Elements generated by rank r under node z-slabs of n/P planes: those whose lowest
     node plane lies in the rank's slab (the top face then belongs to rank r+1, so the
     slab boundary produces off-rank COO rows that exercise the remote path)."""
-    assert n % P == 0
     ne = n - 1
-    z0, z1 = r * (n // P), min((r + 1) * (n // P), ne)
+    planes = slab_planes(n, P)
+    z0 = sum(planes[:r])
+    z1 = min(z0 + planes[r], ne)
     return (z0 * ne * ne, max(z1, z0) * ne * ne)
 
 
@@ -420,7 +425,7 @@ def config_rank_coo(name: str, P: int, r: int, values: str = "int", seed: int = 
     c = CONFIGS[name]
     if c["kind"] == "stencil":
         shape = config_shape(name, P)
-        sizes = slab_sizes(shape, P) if shape[-1] % P == 0 else split_sizes(config_rows(name, P), P)
+        sizes = slab_sizes(shape, P)
         off = offsets_from_sizes(sizes)
         i, j, v = stencil_coo(shape, c["npts"], rows=(off[r], off[r + 1]), values=values,
                               seed=seed, device=device)
@@ -437,8 +442,8 @@ def config_rank_coo(name: str, P: int, r: int, values: str = "int", seed: int = 
         return i, j, v, sizes
     n = c["n"]
     sizes = slab_sizes((n, n, n), P, dof=3)
-    nodes = sizes[0] // 3
-    i, j, v = elasticity_coo(n, nodes=(r * nodes, (r + 1) * nodes), values=values, seed=seed,
+    off = offsets_from_sizes(sizes)
+    i, j, v = elasticity_coo(n, nodes=(off[r] // 3, off[r + 1] // 3), values=values, seed=seed,
                              device=device)
     return i, j, v, sizes
 

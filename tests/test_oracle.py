@@ -328,8 +328,9 @@ def test_partitioned_equivalence(values):
     A1, *_ = build_stencil(shape, 7, P=1, values=values)
     x = synth.x_vector(0, M, values).numpy()
     y1 = A1.mult(x)
-    for P in (2, 4, 8):
+    for P in (2, 3, 4, 5, 8):  # 3 and 5: uneven slabs (remainder planes to the low ranks)
         sizes = synth.slab_sizes(shape, P)
+        assert sum(sizes) == M and all(s % (6 * 5) == 0 for s in sizes)
         AP, *_ = build_stencil(shape, 7, P=P, values=values, sizes=sizes)
         yP = AP.mult(x)
         assert np.array_equal(AP.dense(), A1.dense())  # assembled values: same (src,k) order
