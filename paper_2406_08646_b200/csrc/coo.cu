@@ -289,6 +289,125 @@ __global__ void __launch_bounds__(256) k_numeric_seg(
   }
 }
 
+// Element COO without received contributions (n_mixed == 0): the same canonical sums as
+// k_numeric_seg with the bookkeeping removed -- no local flag, no perm >= ncoo test, one perm
+// base address per nonzero (the kSeg loads use immediate offsets), the slots past the segment
+// hold +0.0 and are added unconditionally (s starts at +0.0 and so is never -0.0: s + (+0.0) == s
+// bit for bit, also for inf and NaN), and kZ nonzeros per thread (z, z+256, ...) for more loads
+// in flight.  Segments longer than kSeg finish in a serial loop, still in canonical order.
+template <int kSeg, int kZ, bool kInsert>
+__global__ void __launch_bounds__(256) k_numeric_seg_lean(
+    const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm, const double *__restrict__ v,
+    int64_t nnz_d, int64_t nnz, double *__restrict__ val_d, double *__restrict__ val_o) {
+  const int64_t zb = (int64_t)blockIdx.x * (256 * kZ) + threadIdx.x;
+  uint32_t t0[kZ], n[kZ];
+#pragma unroll
+  for (int j = 0; j < kZ; ++j) {
+    const int64_t z = zb + 256 * j;
+    t0[j] = 0u;
+    n[j] = 0u;
+    if (z < nnz) {
+      t0[j] = __ldg(jmap + z);
+      n[j] = __ldg(jmap + z + 1) - t0[j];
+    }
+  }
+  double w[kZ][kSeg];
+#pragma unroll
+  for (int j = 0; j < kZ; ++j) {
+    const uint32_t *pp = perm + t0[j];
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) {
+      w[j][k] = 0.0;
+      if ((uint32_t)k < n[j]) w[j][k] = __ldg(v + __ldg(pp + k));
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kZ; ++j) {
+    const int64_t z = zb + 256 * j;
+    if (z >= nnz) continue;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) s = __dadd_rn(s, w[j][k]);
+    for (uint32_t a = t0[j] + kSeg; a < t0[j] + n[j]; ++a) s = __dadd_rn(s, __ldg(v + __ldg(perm + a)));
+    double *dst = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
+    *dst = kInsert ? __dadd_rn(0.0, s) : __dadd_rn(*dst, s);
+  }
+}
+
+template <int S, int T>
+struct PipeCfg {
+  static constexpr int first = S, second = T;
+};
+
+// The same sums, software-pipelined over a grid-stride loop: while the v gathers of nonzero z
+// are in flight, the perm loads of z + stride and the jmap loads of z + 2 stride are too, so
+// each thread keeps three dependent stages of different nonzeros outstanding.
+template <int kSeg, int kTail, bool kInsert, bool kMixed>
+__global__ void __launch_bounds__(256) k_numeric_seg_pipe(
+    const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm, const double *__restrict__ v,
+    uint32_t ncoo, int64_t nnz_d, int64_t nnz, double *__restrict__ val_d, double *__restrict__ val_o) {
+  // perm entries >= ncoo are received contributions (several ranks): such a nonzero is left for
+  // k_numeric_mixed, as in k_numeric_seg
+  const int64_t stride = (int64_t)gridDim.x * 256;
+  int64_t z = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  uint32_t a0 = 0u, n0 = 0u, a1 = 0u, n1 = 0u;
+  if (z < nnz) {
+    a0 = __ldg(jmap + z);
+    n0 = __ldg(jmap + z + 1) - a0;
+  }
+  if (z + stride < nnz) {
+    a1 = __ldg(jmap + z + stride);
+    n1 = __ldg(jmap + z + stride + 1) - a1;
+  }
+  uint32_t q[kSeg];
+#pragma unroll
+  for (int k = 0; k < kSeg; ++k) q[k] = (uint32_t)k < n0 ? __ldg(perm + a0 + k) : 0u;
+  for (; z < nnz; z += stride) {
+    double w[kSeg];
+    bool local = true;
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) {
+      const bool in = (uint32_t)k < n0, mine = !kMixed || q[k] < ncoo;
+      w[k] = 0.0;
+      if (in && mine) w[k] = __ldg(v + q[k]);
+      if (kMixed) local = local && (!in || mine);
+    }
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) q[k] = (uint32_t)k < n1 ? __ldg(perm + a1 + k) : 0u;
+    uint32_t a2 = 0u, n2 = 0u;
+    if (z + 2 * stride < nnz) {
+      a2 = __ldg(jmap + z + 2 * stride);
+      n2 = __ldg(jmap + z + 2 * stride + 1) - a2;
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kSeg; ++k) s = __dadd_rn(s, w[k]);
+    for (uint32_t a = kSeg; a < n0; a += kTail) {  // longer segments: kTail at a time
+      double u[kTail];
+#pragma unroll
+      for (int k = 0; k < kTail; ++k) {
+        u[k] = 0.0;
+        if (a + k < n0) {
+          const uint32_t p = __ldg(perm + a0 + a + k);
+          const bool mine = !kMixed || p < ncoo;
+          if (mine) u[k] = __ldg(v + p);
+          if (kMixed) local = local && mine;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kTail; ++k) s = __dadd_rn(s, u[k]);
+    }
+    if (local) {
+      double *dst = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
+      *dst = kInsert ? __dadd_rn(0.0, s) : __dadd_rn(*dst, s);
+    }
+    a0 = a1;
+    n0 = n1;
+    a1 = a2;
+    n1 = n2;
+  }
+}
+
 // Element COO, warp-cooperative: a warp takes 32 consecutive nonzeros, whose contribution
 // segments are one contiguous range of perm (<= kWSpan entries): the lanes load that range
 // coalesced (8 perm loads, then their 8 v gathers, per lane in flight) into shared memory, then
@@ -1008,7 +1127,14 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
     // varying count (element COO) one nonzero per thread with its segment read kSeg at a time
     const char *nk = getenv("SPMAT_NUMERIC_KERNEL");
     int kind = (double)A->ncontrib > 1.5 * (double)nnz ? 2 : 0;  // 0 ilp, 1 plain, 2 seg
-    if (nk) kind = !strcmp(nk, "plain") ? 1 : (!strcmp(nk, "seg") ? 2 : (!strcmp(nk, "warp") ? 3 : 0));
+    if (nk)
+      kind = !strcmp(nk, "plain") ? 1 : !strcmp(nk, "seg") ? 2 : !strcmp(nk, "warp") ? 3
+           : !strcmp(nk, "lean") ? 4 : !strcmp(nk, "lean2") ? 5 : !strcmp(nk, "lean4") ? 6
+           : !strcmp(nk, "pipe") ? 7 : !strcmp(nk, "pipe4") ? 8 : !strcmp(nk, "pipe2") ? 9
+           : !strcmp(nk, "pipe2s") ? 10 : !strcmp(nk, "pipe1") ? 11 : !strcmp(nk, "pipe3") ? 12 : 0;
+    else if (kind == 2)
+      kind = 9;  // k_numeric_seg_pipe<2, 2>
+    if (kind >= 4 && kind <= 6 && A->n_mixed > 0) kind = 2;  // the lean kernels need all-local contributions
     const int64_t z0 = direct_bsr ? A->nnz_d : 0;  // direct_bsr: off-diagonal nonzeros only
     // one contribution per nonzero (every nonzero has at least one): jmap is the identity
     const bool one = A->ncontrib == nnz && !A->env_numeric_jmap;
@@ -1030,6 +1156,48 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
       } else if (kind == 1) {
         k_numeric_local<<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
                                                   A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
+      } else if (kind >= 7 && z0 == 0) {
+        const bool ins = mode == SPMAT_INSERT;
+        const uint32_t *jm = A->jmap.get(), *pm = A->perm.get();
+        double *vd = A->val_d.get(), *vo = A->val_o.get();
+        // (kSeg, kTail): 7 (8,8)  8 (4,1)  9 (2,2)  10 (2,1)  11 (1,1)  12 (3,1)
+        const bool mixed = A->n_mixed > 0;
+        auto pick = [&](auto tag) -> const void * {
+          constexpr int S = decltype(tag)::first, T = decltype(tag)::second;
+          return mixed ? (ins ? (const void *)k_numeric_seg_pipe<S, T, true, true>
+                              : (const void *)k_numeric_seg_pipe<S, T, false, true>)
+                       : (ins ? (const void *)k_numeric_seg_pipe<S, T, true, false>
+                              : (const void *)k_numeric_seg_pipe<S, T, false, false>);
+        };
+        const void *fn = kind == 7    ? pick(PipeCfg<8, 8>{})
+                         : kind == 8  ? pick(PipeCfg<4, 1>{})
+                         : kind == 9  ? pick(PipeCfg<2, 2>{})
+                         : kind == 10 ? pick(PipeCfg<2, 1>{})
+                         : kind == 11 ? pick(PipeCfg<1, 1>{})
+                                      : pick(PipeCfg<3, 1>{});
+        int per_sm = 0;
+        SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
+        const unsigned g = (unsigned)std::max<int64_t>(
+            1, std::min<int64_t>((nnz + 255) / 256, (int64_t)A->comm->num_sms * std::max(per_sm, 1)));
+        const int64_t nd = A->nnz_d;
+        const uint32_t lim = A->n_mixed > 0 ? (uint32_t)A->ncoo : 0xffffffffu;
+        void *args[] = {(void *)&jm, (void *)&pm, (void *)&v, (void *)&lim, (void *)&nd, (void *)&nnz, (void *)&vd, (void *)&vo};
+        SP_CUDA(cudaLaunchKernel(fn, dim3(g), dim3(256), args, 0, s));
+      } else if (kind >= 4 && z0 == 0) {
+        const bool ins = mode == SPMAT_INSERT;
+        const int kz = kind == 4 ? 1 : 2;
+        const unsigned g = (unsigned)std::max<int64_t>(1, (nnz + 256 * kz - 1) / (256 * kz));
+        const uint32_t *jm = A->jmap.get(), *pm = A->perm.get();
+        double *vd = A->val_d.get(), *vo = A->val_o.get();
+        if (kind == 4)
+          ins ? k_numeric_seg_lean<8, 1, true><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo)
+              : k_numeric_seg_lean<8, 1, false><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo);
+        else if (kind == 5)
+          ins ? k_numeric_seg_lean<8, 2, true><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo)
+              : k_numeric_seg_lean<8, 2, false><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo);
+        else
+          ins ? k_numeric_seg_lean<4, 2, true><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo)
+              : k_numeric_seg_lean<4, 2, false><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo);
       } else if (kind == 2 && z0 == 0) {
         // contributions read 8 at a time (C3, same box: 1.149 ms vs 1.200 ms 4 at a time,
         // 1.206 ms for the plain serial loop)
