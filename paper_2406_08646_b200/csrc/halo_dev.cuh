@@ -343,36 +343,44 @@ static __device__ __noinline__ void split_tail(const SpmvTail tail, unsigned lon
                     tail.obuf);
     }
   }
-  // 2. every row block written (and this warp's sums visible: the fence below orders them
-  //    before the adds of any warp that reads them after the same counter)
+  // 2. every warp's sums out (early: the sums take ~30 us of a ~250 us sweep).  The fence
+  //    orders this warp's sums before the adds of any warp that reads them after the counter.
   __syncwarp();
   if (lane == 0) {
     __threadfence();
     atomicAdd(tail.ctr + 3, 1u);  // comm warps whose sums are out
-    wait_ctr(tail.ctr, (unsigned)(consumer_warps * tail.n_bblocks), err);
     wait_ctr(tail.ctr + 3, gridDim.x, err);
-    if (trc) trc[4] = gtimer();
   }
   __syncwarp();
-  const int64_t per2 = 32 * 8;  // 3. y[rows[q]] += obuf[q], 8 rows per lane in flight
+  // 3. y[rows[q]] += obuf[q] over static chunks of kAddU rows per lane (chunk c = CTA, + grid):
+  //    the first chunk's rows and sums are loaded BEFORE the wait for the sweep, so after it
+  //    only the y loads and stores remain on the critical path
+  constexpr int kAddU = 10;
+  const int64_t per2 = 32 * kAddU;
   const int64_t n2 = (tail.n_ro + per2 - 1) / per2;
-  for (;;) {
-    int64_t c = 0;
-    if (lane == 0) c = atomicAdd(tail.ctr + 4, 1u);
-    c = __shfl_sync(0xffffffffu, c, 0);
-    if (c >= n2) break;
-    int r[8];
-    double o[8], yv[8];
+  int r[kAddU];
+  double o[kAddU], yv[kAddU];
+  auto load_chunk = [&](int64_t c) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < kAddU; ++u) {
       const int64_t q = c * per2 + u * 32 + lane;
       r[u] = q < tail.n_ro ? tail.rows[q] : -1;
       o[u] = q < tail.n_ro ? __ldcg(tail.obuf + q) : 0.0;
     }
+  };
+  int64_t c = blockIdx.x;
+  if (c < n2) load_chunk(c);
+  if (lane == 0) {  // every row block written
+    wait_ctr(tail.ctr, (unsigned)(consumer_warps * tail.n_bblocks), err);
+    if (trc) trc[4] = gtimer();
+  }
+  __syncwarp();
+  for (; c < n2; c += gridDim.x) {
+    if (c != blockIdx.x) load_chunk(c);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) yv[u] = r[u] >= 0 ? __ldcg(y + r[u]) : 0.0;
+    for (int u = 0; u < kAddU; ++u) yv[u] = r[u] >= 0 ? __ldcg(y + r[u]) : 0.0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < kAddU; ++u)
       if (r[u] >= 0) y[r[u]] = __dadd_rn(yv[u], o[u]);
   }
   __syncwarp();

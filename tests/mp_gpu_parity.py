@@ -444,6 +444,56 @@ def case_full_c4(c):
     torch.cuda.empty_cache()
 
 
+def case_full_c4b(c):
+    """C4b at full size (256^3 rows per rank, box decomposition with per-rank renumbering): the
+    split off-diagonal tail, whose sums the consumer warps fold into most boundary rows as they
+    write them (the rest by the add pass after the sweep).  A.1 over EVERY row against the
+    out-of-grid neighbour count (P3, integer values, exact), then real values on sampled rows
+    vs the oracle from the COO definition, over several halo epochs."""
+    P, r = c.P, c.r
+    shape, procs = synth.config_shape("c4b", P), synth.box_procs(P)
+    sizes = synth.box_sizes(shape, procs)
+    off = synth.offsets_from_sizes(sizes)
+    M = off[-1]
+    i, j, vi, _ = synth.config_rank_coo("c4b", P, r, values="int", device="cuda")
+    A = sp.Mat(c.comm, sizes[r], sizes[r], M, M, i, j)
+    A.set_values(vi)
+    del vi
+    y = torch.empty(sizes[r], dtype=torch.float64, device="cuda")
+    ones = torch.ones(sizes[r], dtype=torch.float64, device="cuda")
+    px, py, pz = procs
+    bx, by, bz = r % px, (r // px) % py, r // (px * py)
+    lo = [(b * n) // p for b, n, p in zip((bx, by, bz), shape, procs)]
+    ext = [((b + 1) * n) // p - (b * n) // p for b, n, p in zip((bx, by, bz), shape, procs)]
+    loc = torch.arange(sizes[r], device="cuda")
+    coords = [lo[0] + loc % ext[0], lo[1] + (loc // ext[0]) % ext[1], lo[2] + loc // (ext[0] * ext[1])]
+    want = torch.zeros_like(y)
+    for cc, n in zip(coords, shape):
+        want += (cc == 0).double() + (cc == n - 1).double()
+    for it in range(4):  # several epochs: the fold and the add pass both see every flag parity
+        A.mult(ones, y)
+        assert torch.equal(y, want), f"full-size C4b A.1 rank {r} epoch {it}: {int((y != want).sum())} rows differ"
+    _, _, v, _ = synth.config_rank_coo("c4b", P, r, values="real", device="cuda")
+    A.set_values(v)
+    xg = synth.x_vector(0, M, "real", device="cuda")
+    x = xg[off[r]:off[r + 1]].contiguous()
+    for _ in range(3):
+        A.mult(x, y)
+    A.check()
+    g = torch.Generator().manual_seed(200 + r)
+    rows = torch.unique(torch.cat([torch.randint(off[r], off[r + 1], (600,), generator=g),
+                                   torch.tensor([off[r], off[r + 1] - 1]),
+                                   off[r] + torch.arange(0, sizes[r], ext[0])[:200]]))  # x-face rows
+    sel = torch.isin(i, rows.cuda())
+    ih, jh, vh = i[sel].cpu(), j[sel].cpu(), v[sel].cpu()
+    del i, j, v
+    ys = oracle.sample_rows(ih, jh, vh, rows.numpy(), xg.cpu().numpy())
+    got = y[(rows - off[r]).cuda()].cpu().numpy()
+    assert rel_err(got, ys) <= TOL, f"full-size C4b rank {r}"
+    A.close()
+    torch.cuda.empty_cache()
+
+
 def case_full_c5(c):
     """C5 at full size (24 M rows, 1.92 G nonzeros, z-slabs of 200/P planes) with 3x3 blocks
     (diagonal and off-diagonal) and with CSR: A.1 over EVERY row of every rank against the
@@ -545,7 +595,8 @@ def main():
     cases += [("host-pipeline-slab", lambda: case_host_pipeline(c, "slab")),
               ("host-pipeline-box", lambda: case_host_pipeline(c, "box"))]
     cases += [(f"transpose{s}", (lambda s=s: case_transpose(c, s))) for s in range(6)]
-    cases += [("full-c4", lambda: case_full_c4(c)), ("full-c5", lambda: case_full_c5(c))]
+    cases += [("full-c4", lambda: case_full_c4(c)), ("full-c4b", lambda: case_full_c4b(c)),
+              ("full-c5", lambda: case_full_c5(c))]
     cases += [("errors", lambda: case_errors(c))]
     only = [s for s in os.environ.get("MP_CASES", "").split(",") if s]
     if only:
