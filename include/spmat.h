@@ -209,7 +209,8 @@ int spmat_mult_flush(spmat_t A, void *stream);
    ascending order, then the other ranks' sums are added in ascending rank order -- a fixed,
    rank-count-independent order (real-valued results reproducible bit for bit).  The transposed blocks are built on
    the first call (device radix sort, host-synchronising) and their values re-gathered after
-   every spmat_set_values_coo.  Host x or y: SPMAT_ERR_ARG. */
+   every spmat_set_values_coo; the first call also builds the halo SF's NVLink transport
+   (collective, host-synchronising; see spmat_get_halo_sf).  Host x or y: SPMAT_ERR_ARG. */
 int spmat_mult_transpose(spmat_t A, const double *x, double *y, void *stream);
 
 /* MatSetBlockSize analogue for the SpMV storage (block-CSR on GPU): bs = 3 checks that
@@ -235,7 +236,10 @@ int spmat_mult_part(spmat_t A, const double *x, double *y, int part, void *strea
    too), offdiag_lanes, halo_mode (0 one rank, 1 NCCL, 2 NVLink stores), and cumulative
    counters since create (host-side, counted when work is enqueued): nccl_bytes_sent,
    nccl_bytes_recv (COO value exchange + NCCL-mode halo), nvlink_bytes_put (halo lines stored
-   into peers: 16 B per value), n_mult, n_set_values, then spmv_grid, offdiag_grid, 0...
+   into peers: 16 B per value), n_mult, n_set_values, then spmv_grid, offdiag_grid (the
+   grid with the fused off-diagonal add, incl. CTAs that only run it),
+   halo_sf_transport (the halo SF's own transport: 0 not built yet / one rank, 1 NCCL,
+   2 NVLink), 0...
    The caller provides 32 entries. */
 int spmat_get_info(spmat_t A, int64_t info[32]);
 
@@ -250,7 +254,11 @@ int spmat_get_info(spmat_t A, int64_t info[32]);
    *len = full length; min(cap, len) values are copied. */
 int spmat_export(spmat_t A, int what, void *host_buf, int64_t cap, int64_t *len);
 
-/* The halo SF (leaves = ghost columns in colmap order).  Borrowed: do not destroy. */
+/* The halo SF (leaves = ghost columns in colmap order).  Borrowed: do not destroy.
+   Collective on the first call with several ranks: the SF's NVLink transport (staging lines
+   and peer mappings) is built then, not at create, when the matrix's own MatMult halo has its
+   NVLink path -- only MatMultTranspose and borrowed SFs use it.  The first
+   spmat_mult_transpose builds it the same way. */
 int spmat_get_halo_sf(spmat_t A, sf_t *borrowed);
 
 /* Per-kernel timing with CUDA events recorded on the launching streams.  enable=1 starts

@@ -45,7 +45,7 @@ INFO_KEYS = ("rstart", "rend", "cstart", "cend", "nnz_d", "nnz_o", "n_ghost", "n
              "n_contrib", "n_send", "n_recv", "n_mixed", "spmv_kernel_id", "n_rowblocks",
              "max_row_nnz", "plan_builds", "block_size", "offdiag_3x3", "offdiag_lanes", "halo_mode",
              "nccl_bytes_sent", "nccl_bytes_recv", "nvlink_bytes_put", "n_mult", "n_set_values",
-             "spmv_grid", "offdiag_grid")
+             "spmv_grid", "offdiag_grid", "halo_sf_transport")
 SF_INFO_KEYS = ("nroots", "nleaves", "n_send_nbr", "n_recv_nbr", "n_send", "n_recv", "n_self",
                 "packed")
 SF_EXPORT = dict(recv_ranks=0, recv_counts=1, leaf_idx=2, send_ranks=3, send_counts=4,

@@ -1066,9 +1066,10 @@ static int create_impl(spmat_comm_s *c, int64_t m_local, int64_t n_local, int64_
   }
   return SPMAT_OK;
   }(), who));
-  SP_TRY(sf_build(c, n_local, A->n_ghost, nullptr, own.data(), off.data(), &A->halo));
+  SP_TRY(sf_build(c, n_local, A->n_ghost, nullptr, own.data(), off.data(), &A->halo, true));
   SP_TRY(c->agree(spmv_prepare(A, st), who));
   SP_TRY(halo_peer_setup(A));
+  if (!A->peer) SP_TRY(sf_ensure_peer(A->halo));  // the MatMult halo goes through the SF (A->peer is agreed)
   SP_CUDA(cudaStreamSynchronize(st));
   A->plan_builds = 1;
   *out = guard.release();
@@ -1246,7 +1247,9 @@ int spmat_get_info(spmat_t A, int64_t info[32]) {
                    A->n_rowblocks, A->max_row_nnz, A->plan_builds,
                    A->bs, A->ob_ok ? 1 : 0, A->ob_ok ? A->ob_w : A->ro_w, mode,
                    A->stat_nccl_sent, A->stat_nccl_recv, A->stat_nvlink_put, A->stat_mults,
-                   A->stat_setvals, A->bs == 3 ? A->bsr_grid : A->tma_grid, 0};
+                   A->stat_setvals, A->bs == 3 ? A->bsr_grid : A->tma_grid,
+                   A->bs == 3 ? A->bsr_grid : A->tma_grid_tail,
+                   A->halo ? (A->halo->peer_deferred ? 0 : (A->halo->peer ? 2 : 1)) : 0, 0};
   memcpy(info, v, sizeof v);
   return SPMAT_OK;
 }
@@ -1280,6 +1283,8 @@ int spmat_halo_mode(spmat_t A) {
 
 int spmat_get_halo_sf(spmat_t A, sf_t *borrowed) {
   if (!A || !borrowed) return fail(SPMAT_ERR_ARG, "spmat_get_halo_sf: null argument");
+  DeviceGuard g(A->comm->device);
+  SP_TRY(sf_ensure_peer(A->halo));  // collective on first call
   *borrowed = A->halo;
   return SPMAT_OK;
 }

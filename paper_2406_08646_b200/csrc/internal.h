@@ -256,6 +256,7 @@ struct sf_s {
   bool take_captured = false;            // ev_take was recorded inside a stream capture
   cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;  // profiling (comm stream)
   bool pending = false;
+  bool peer_deferred = false;            // the NVLink transport is set up on first use (sf_ensure_peer)
   const double *p_root = nullptr;
   double *p_leaf = nullptr;
   int p_op = -1;
@@ -288,7 +289,7 @@ struct sf_s {
 namespace spmat {
 // build an SF from host leaf arrays (ilocal may be null); collective
 int sf_build(spmat_comm_s *comm, int64_t nroots, int64_t nleaves, const int64_t *h_ilocal,
-             const int32_t *h_rank, const int64_t *h_offset, sf_s **out);
+             const int32_t *h_rank, const int64_t *h_offset, sf_s **out, bool defer_peer = false);
 int sf_begin(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stream,
              cudaEvent_t *prof /* optional pair recorded on the comm stream */);
 int sf_end(sf_s *sf, const double *root, double *leaf, int op, cudaStream_t stream);
@@ -490,7 +491,8 @@ int peer_put_launch(const HaloPut *puts, int nputs, int chunks, const double *sr
                     const unsigned long long *epoch_ctr, int *err, cudaStream_t s);
 int put_chunks_of(int64_t count);   // put warps (chunks) for `count` values (flagged lines)
 int bulk_chunks_of(int64_t count);  // put warps of a bulk segment (one fence + flag per chunk)
-int sf_peer_setup(sf_s *sf);       // collective; leaves sf->peer false (NCCL) when unavailable
+int sf_peer_setup(sf_s *sf);
+int sf_ensure_peer(sf_s *sf);      // collective; the deferred sf_peer_setup of a matrix halo SF       // collective; leaves sf->peer false (NCCL) when unavailable
 int halo_peer_setup(spmat_s *A);                  // collective; leaves A->peer false on NCCL
 void halo_peer_release(spmat_s *A);
 int halo_peer_put(spmat_s *A, const double *x, cudaStream_t s);  // standalone put kernel

@@ -59,7 +59,7 @@ void sf_free(sf_s *sf) {
 }
 
 int sf_build(spmat_comm_s *comm, int64_t nroots, int64_t nleaves, const int64_t *h_ilocal,
-             const int32_t *h_rank, const int64_t *h_offset, sf_s **out) {
+             const int32_t *h_rank, const int64_t *h_offset, sf_s **out, bool defer_peer) {
   *out = nullptr;
   const int P = comm->nranks, me = comm->rank;
   // ---- local validation, agreed collectively so that no rank is left in a collective
@@ -272,7 +272,11 @@ int sf_build(spmat_comm_s *comm, int64_t nroots, int64_t nleaves, const int64_t 
     sf_free(sf);
     return fail(SPMAT_ERR_CUDA, "sf_create: event creation failed");
   }
-  if ((s = sf_peer_setup(sf)) != SPMAT_OK) {
+  // a matrix's halo SF: its MatMult has its own NVLink buffers (halo.cu), so the SF's transport
+  // is built on first use (MatMultTranspose, a borrowed SF, or the MatMult halo when that has
+  // no NVLink path of its own)
+  sf->peer_deferred = defer_peer && comm->nranks > 1;
+  if (!sf->peer_deferred && (s = sf_peer_setup(sf)) != SPMAT_OK) {
     sf_free(sf);
     return s;
   }
@@ -286,6 +290,12 @@ int sf_build(spmat_comm_s *comm, int64_t nroots, int64_t nleaves, const int64_t 
 // (flagged lines straight into the consumer's buffer over NVLink, after the consumer released
 // that buffer two epochs ago) and a consuming kernel that reads each line once it carries the
 // epoch, applies the op, and releases the buffer.  No NCCL kernel, no host synchronisation.
+int sf_ensure_peer(sf_s *sf) {
+  if (!sf || !sf->peer_deferred) return SPMAT_OK;
+  sf->peer_deferred = false;
+  return sf_peer_setup(sf);
+}
+
 int sf_peer_setup(sf_s *sf) {
   spmat_comm_s *c = sf->comm;
   const int P = c->nranks, me = c->rank;
@@ -773,6 +783,7 @@ int sf_bcast_begin(sf_t sf, const double *rootdata, double *leafdata, int op, vo
   if ((sf->nrecv > 0 || sf->nself > 0) && !leafdata)
     return fail(SPMAT_ERR_ARG, "sf_bcast_begin: null leafdata");
   DeviceGuard g(sf->comm->device);
+  SP_TRY(sf_ensure_peer(sf));
   return sf_begin(sf, rootdata, leafdata, op, (cudaStream_t)stream, nullptr);
 }
 
@@ -790,6 +801,7 @@ int sf_reduce_begin(sf_t sf, const double *leafdata, double *rootdata, int op, v
     return fail(SPMAT_ERR_ARG, "sf_reduce_begin: null leafdata");
   if (sf->n_touched > 0 && !rootdata) return fail(SPMAT_ERR_ARG, "sf_reduce_begin: null rootdata");
   DeviceGuard g(sf->comm->device);
+  SP_TRY(sf_ensure_peer(sf));
   return sf_reduce_begin_impl(sf, leafdata, rootdata, op, (cudaStream_t)stream);
 }
 

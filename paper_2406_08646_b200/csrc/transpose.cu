@@ -172,6 +172,7 @@ int spmat_mult_transpose(spmat_t A, const double *x, double *y, void *stream) {
     return fail(SPMAT_ERR_ARG, "spmat_mult_transpose: x and y must be device arrays");
   DeviceGuard g(A->comm->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (A->comm->nranks > 1) SP_TRY(sf_ensure_peer(A->halo));  // collective on first call
   SP_TRY(transpose_prepare(A, s));
   const bool multi = A->comm->nranks > 1 && A->halo;
   if (multi && A->n_ghost > 0) {  // lvec = A_o^T x, one value per ghost column

@@ -93,8 +93,14 @@ def check_matrix(c, name, M, N, row_sizes, col_sizes, coo, values, x_global, exa
     assert np.array_equal(A.export("cpos"), opos), f"{name}: contribution positions differ"
     for key in ("val_d", "val_o"):
         assert np.array_equal(canon(A.export(key)), canon(O.export(r, key))), f"{name}: {key} differ"
-    # halo SF plan
+    # halo SF plan; its own NVLink transport is built on first use when the MatMult halo has
+    # its own NVLink path (halo_mode 2), right at create otherwise
+    i_pre = A.info()
+    if i_pre["halo_mode"] == 2:
+        assert i_pre["halo_sf_transport"] == 0, f"{name}: halo SF transport built eagerly"
     hs = A.halo_sf()
+    if P > 1:
+        assert A.info()["halo_sf_transport"] in (1, 2), f"{name}: halo SF transport missing"
     lo, lof = O.export(r, "leaf_owner"), O.export(r, "leaf_offset")
     nbrs = [q for q in range(P) if np.any(lo == q)]
     assert list(sp.sf_export(hs, "recv_ranks")) == nbrs
