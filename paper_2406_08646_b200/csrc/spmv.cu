@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 
 #include "halo_dev.cuh"
@@ -67,9 +68,9 @@ static inline unsigned nblk(int64_t n, int t = 256) {
 // ------------------------------------------------------------------ row-block schedule
 // candidate t < n_cost: first row r with rowptr[r] + kAlpha * r >= t * kBudget
 __global__ void k_rb_candidates(const int32_t *__restrict__ rowptr, int64_t m, int64_t n_cost,
-                                int32_t *__restrict__ cand) {
+                                int32_t *__restrict__ cand, int budget) {
   GRID_STRIDE(t, n_cost) {
-    const int64_t target = t * (int64_t)kBudget;
+    const int64_t target = t * (int64_t)budget;
     int64_t lo = 0, hi = m;
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
@@ -621,8 +622,32 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   SP_CUDA(cudaStreamSynchronize(st));
   A->max_row_nnz = h[0];
   const int64_t nlong = h[1];
+  // Row-block budget.  The consumers cover a block's rows with W lanes per row (the largest
+  // power of two with rows * W <= 256); with more than 256 / W rows, or more than 8 entries per
+  // lane, a block costs them two rounds of dependent x gathers.  When kBudget gives two rounds
+  // and a budget sized for ONE (256 / W' rows, W' the smallest power of two with <= 8 entries
+  // per lane, 2 % slack for shorter boundary rows) keeps >= 85 % of kBudget, use it: C3 (27-point,
+  // 70 rows at W = 2 -> ~63 at W = 4): 0.2225 -> 0.2068 ms.  Smaller blocks cost more than the
+  // second round saves (Bump 45-point at 1442: 0.2486 -> 0.2744 ms; Q2 with the slack: +2 %), so
+  // C4, Q2 and Bump keep kBudget.  SPMAT_RB_BUDGET overrides (0: kBudget).
+  A->rb_budget = kBudget;
+  if (m > 0) {
+    const double L = (double)nnz / (double)m;
+    const double rows = std::floor(kBudget / (L + kAlpha));  // rows of a typical block
+    int w0 = 1;
+    while (w0 < 32 && rows * 2 * w0 <= kThreads) w0 *= 2;
+    const bool two_rounds = rows > kThreads / w0 || L > 8.0 * w0;
+    int w1 = 1;
+    while (w1 < 32 && L > 8.0 * w1) w1 *= 2;
+    const double b1 = 0.98 * (kThreads / w1) * (L + kAlpha);
+    if (two_rounds && b1 >= 0.85 * kBudget && b1 < kBudget) A->rb_budget = (int)b1;
+  }
+  if (const char *e = getenv("SPMAT_RB_BUDGET")) {
+    const int b = atoi(e);
+    A->rb_budget = b <= 0 ? kBudget : std::max(64, std::min(kBudget, b));
+  }
   const int64_t total_cost = nnz + kAlpha * m;
-  const int64_t n_cost = (total_cost + kBudget - 1) / kBudget;  // t = 0 .. n_cost-1, plus m
+  const int64_t n_cost = (total_cost + A->rb_budget - 1) / A->rb_budget;  // t = 0 .. n_cost-1, plus m
   const int64_t ncand = n_cost + 1 + 2 * nlong;
   DevBuf<int32_t> cand, sorted, uniq;
   DevBuf<int> dn;
@@ -630,7 +655,7 @@ int spmv_prepare(spmat_s *A, cudaStream_t st) {
   SP_TRY(sorted.alloc(ncand));
   SP_TRY(uniq.alloc(ncand));
   SP_TRY(dn.alloc(1));
-  k_rb_candidates<<<nblk(n_cost), 256, 0, st>>>(A->rowptr_d.get(), m, n_cost, cand.get());
+  k_rb_candidates<<<nblk(n_cost), 256, 0, st>>>(A->rowptr_d.get(), m, n_cost, cand.get(), A->rb_budget);
   SP_LAUNCH();
   if (nlong > 0) {
     k_long_bounds<<<nblk(nlong), 256, 0, st>>>(longrows.get(), nlong, cand.get() + n_cost + 1);
