@@ -1,5 +1,6 @@
 """Multi-rank GPU parity: launches tests/mp_gpu_parity.py with torchrun on P GPUs (NCCL
-bootstrap), once per halo transport (device-initiated NVLink stores, and NCCL send/recv)."""
+bootstrap), once per halo transport (device-initiated NVLink stores, and NCCL send/recv);
+P = 3 exercises uneven z-slabs (the low ranks take the remainder planes)."""
 import os
 import subprocess
 import sys
@@ -13,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 @pytest.mark.parametrize("halo", ["peer", "nccl"])
-@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
 def test_multirank_parity(P, halo):
     if torch.cuda.device_count() < P:
         pytest.skip(f"needs {P} GPUs")
