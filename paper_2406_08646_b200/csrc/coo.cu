@@ -594,6 +594,40 @@ __global__ void __launch_bounds__(256) k_numeric_bsr3_one(
   }
 }
 
+// One contribution per nonzero (jmap[z] == z: stencil and node-block COO), no loop: each thread
+// loads U perm entries (coalesced), then their U v values (nearly coalesced: perm permutes only
+// within a row), then stores val -- s = +0.0 + v, INSERT val = +0.0 + s, ADD val = val + s, the
+// canonical sums of a one-term segment.  kMixed: perm entries >= lim are received
+// contributions (several ranks), left for k_numeric_mixed.
+template <int U, bool kInsert, bool kMixed>
+__global__ void __launch_bounds__(256) k_numeric_one(const uint32_t *__restrict__ perm, const double *__restrict__ v,
+                                                     uint32_t lim, int64_t z0, int64_t nnz_d, int64_t nnz,
+                                                     double *__restrict__ val_d, double *__restrict__ val_o) {
+  const int64_t zb = z0 + (int64_t)blockIdx.x * (256 * U) + threadIdx.x;
+  uint32_t q[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t z = zb + 256 * u;
+    q[u] = z < nnz ? __ldg(perm + z) : 0u;
+  }
+  double w[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t z = zb + 256 * u;
+    w[u] = 0.0;
+    if (z < nnz && (!kMixed || q[u] < lim)) w[u] = __ldg(v + q[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t z = zb + 256 * u;
+    if (z < nnz && (!kMixed || q[u] < lim)) {
+      double *dst = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
+      const double sum = __dadd_rn(0.0, w[u]);
+      *dst = kInsert ? __dadd_rn(0.0, sum) : __dadd_rn(*dst, sum);
+    }
+  }
+}
+
 // Default numeric kernel (ONE: jmap[z] == z, as in k_numeric_bsr3): each thread finishes kNumU nonzeros z = base + u*blockDim + tid
 // (coalesced across the warp), advancing all of them one contribution per round so every
 // level of the jmap -> perm -> v chain has kNumU loads in flight.  Each nonzero is still
@@ -1208,6 +1242,20 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
         else
           k_numeric_seg<4><<<nblk(nnz), 256, 0, s>>>(A->jmap.get(), A->perm.get(), v, (uint64_t)A->ncoo,
                                                      A->nnz_d, nnz, A->val_d.get(), A->val_o.get(), mode);
+      } else if (one && !(nk && !strcmp(nk, "ilp"))) {
+        constexpr int U = 8;
+        const unsigned g = (unsigned)std::max<int64_t>(1, (nnz - z0 + 256 * U - 1) / (256 * U));
+        const bool ins = mode == SPMAT_INSERT, mixed = A->n_mixed > 0;
+        const uint32_t lim = (uint32_t)A->ncoo;
+        const uint32_t *pm = A->perm.get();
+        double *vd = A->val_d.get(), *vo = A->val_o.get();
+        const int64_t nd = A->nnz_d;
+        if (ins)
+          mixed ? k_numeric_one<U, true, true><<<g, 256, 0, s>>>(pm, v, lim, z0, nd, nnz, vd, vo)
+                : k_numeric_one<U, true, false><<<g, 256, 0, s>>>(pm, v, lim, z0, nd, nnz, vd, vo);
+        else
+          mixed ? k_numeric_one<U, false, true><<<g, 256, 0, s>>>(pm, v, lim, z0, nd, nnz, vd, vo)
+                : k_numeric_one<U, false, false><<<g, 256, 0, s>>>(pm, v, lim, z0, nd, nnz, vd, vo);
       } else {
         const int64_t blocks = std::min<int64_t>((nnz - z0 + 256 * kNumU - 1) / (256 * kNumU),
                                                  (int64_t)A->comm->num_sms * 32);
