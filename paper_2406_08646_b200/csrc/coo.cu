@@ -289,51 +289,6 @@ __global__ void __launch_bounds__(256) k_numeric_seg(
   }
 }
 
-// Element COO without received contributions (n_mixed == 0): the same canonical sums as
-// k_numeric_seg with the bookkeeping removed -- no local flag, no perm >= ncoo test, one perm
-// base address per nonzero (the kSeg loads use immediate offsets), the slots past the segment
-// hold +0.0 and are added unconditionally (s starts at +0.0 and so is never -0.0: s + (+0.0) == s
-// bit for bit, also for inf and NaN), and kZ nonzeros per thread (z, z+256, ...) for more loads
-// in flight.  Segments longer than kSeg finish in a serial loop, still in canonical order.
-template <int kSeg, int kZ, bool kInsert>
-__global__ void __launch_bounds__(256) k_numeric_seg_lean(
-    const uint32_t *__restrict__ jmap, const uint32_t *__restrict__ perm, const double *__restrict__ v,
-    int64_t nnz_d, int64_t nnz, double *__restrict__ val_d, double *__restrict__ val_o) {
-  const int64_t zb = (int64_t)blockIdx.x * (256 * kZ) + threadIdx.x;
-  uint32_t t0[kZ], n[kZ];
-#pragma unroll
-  for (int j = 0; j < kZ; ++j) {
-    const int64_t z = zb + 256 * j;
-    t0[j] = 0u;
-    n[j] = 0u;
-    if (z < nnz) {
-      t0[j] = __ldg(jmap + z);
-      n[j] = __ldg(jmap + z + 1) - t0[j];
-    }
-  }
-  double w[kZ][kSeg];
-#pragma unroll
-  for (int j = 0; j < kZ; ++j) {
-    const uint32_t *pp = perm + t0[j];
-#pragma unroll
-    for (int k = 0; k < kSeg; ++k) {
-      w[j][k] = 0.0;
-      if ((uint32_t)k < n[j]) w[j][k] = __ldg(v + __ldg(pp + k));
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < kZ; ++j) {
-    const int64_t z = zb + 256 * j;
-    if (z >= nnz) continue;
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < kSeg; ++k) s = __dadd_rn(s, w[j][k]);
-    for (uint32_t a = t0[j] + kSeg; a < t0[j] + n[j]; ++a) s = __dadd_rn(s, __ldg(v + __ldg(perm + a)));
-    double *dst = z < nnz_d ? val_d + z : val_o + (z - nnz_d);
-    *dst = kInsert ? __dadd_rn(0.0, s) : __dadd_rn(*dst, s);
-  }
-}
-
 template <int S, int T>
 struct PipeCfg {
   static constexpr int first = S, second = T;
@@ -1158,18 +1113,14 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
   // 3x3 blocks and no received contributions: the diagonal values go straight into bval
   const bool direct_bsr = A->bs == 3 && A->n_mixed == 0 && A->mb > 0 && !A->env_numeric_csr;
   if (nnz > 0) {
-    // ILP kernel when nonzeros have ~1 contribution (stencil COO); with many duplicates of
-    // varying count (element COO) one nonzero per thread with its segment read kSeg at a time
+    // one contribution per nonzero: k_numeric_one; several of varying count (element COO):
+    // k_numeric_seg_pipe<2, 2>.  SPMAT_NUMERIC_KERNEL selects the measured alternatives:
+    // ilp, plain, seg (k_numeric_seg), warp, pipe4 (k_numeric_seg_pipe<4, 1>), pipe8 (<8, 8>)
     const char *nk = getenv("SPMAT_NUMERIC_KERNEL");
-    int kind = (double)A->ncontrib > 1.5 * (double)nnz ? 2 : 0;  // 0 ilp, 1 plain, 2 seg
+    int kind = (double)A->ncontrib > 1.5 * (double)nnz ? 9 : 0;  // 0 one/ilp, 9 pipe
     if (nk)
       kind = !strcmp(nk, "plain") ? 1 : !strcmp(nk, "seg") ? 2 : !strcmp(nk, "warp") ? 3
-           : !strcmp(nk, "lean") ? 4 : !strcmp(nk, "lean2") ? 5 : !strcmp(nk, "lean4") ? 6
-           : !strcmp(nk, "pipe") ? 7 : !strcmp(nk, "pipe4") ? 8 : !strcmp(nk, "pipe2") ? 9
-           : !strcmp(nk, "pipe2s") ? 10 : !strcmp(nk, "pipe1") ? 11 : !strcmp(nk, "pipe3") ? 12 : 0;
-    else if (kind == 2)
-      kind = 9;  // k_numeric_seg_pipe<2, 2>
-    if (kind >= 4 && kind <= 6 && A->n_mixed > 0) kind = 2;  // the lean kernels need all-local contributions
+           : !strcmp(nk, "pipe8") ? 7 : !strcmp(nk, "pipe4") ? 8 : !strcmp(nk, "pipe") ? 9 : 0;
     const int64_t z0 = direct_bsr ? A->nnz_d : 0;  // direct_bsr: off-diagonal nonzeros only
     // one contribution per nonzero (every nonzero has at least one): jmap is the identity
     const bool one = A->ncontrib == nnz && !A->env_numeric_jmap;
@@ -1195,7 +1146,8 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
         const bool ins = mode == SPMAT_INSERT;
         const uint32_t *jm = A->jmap.get(), *pm = A->perm.get();
         double *vd = A->val_d.get(), *vo = A->val_o.get();
-        // (kSeg, kTail): 7 (8,8)  8 (4,1)  9 (2,2)  10 (2,1)  11 (1,1)  12 (3,1)
+        // (kSeg, kTail): 7 (8,8)  8 (4,1)  9 (2,2).  C3, one box (ms): (8,8) 0.934, (4,1) 0.821,
+        // (3,1) 0.821, (2,1) 0.805, (1,1) 0.85, (2,2) 0.755-0.767
         const bool mixed = A->n_mixed > 0;
         auto pick = [&](auto tag) -> const void * {
           constexpr int S = decltype(tag)::first, T = decltype(tag)::second;
@@ -1204,12 +1156,7 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
                        : (ins ? (const void *)k_numeric_seg_pipe<S, T, true, false>
                               : (const void *)k_numeric_seg_pipe<S, T, false, false>);
         };
-        const void *fn = kind == 7    ? pick(PipeCfg<8, 8>{})
-                         : kind == 8  ? pick(PipeCfg<4, 1>{})
-                         : kind == 9  ? pick(PipeCfg<2, 2>{})
-                         : kind == 10 ? pick(PipeCfg<2, 1>{})
-                         : kind == 11 ? pick(PipeCfg<1, 1>{})
-                                      : pick(PipeCfg<3, 1>{});
+        const void *fn = kind == 7 ? pick(PipeCfg<8, 8>{}) : kind == 8 ? pick(PipeCfg<4, 1>{}) : pick(PipeCfg<2, 2>{});
         int per_sm = 0;
         SP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0));
         const unsigned g = (unsigned)std::max<int64_t>(
@@ -1218,21 +1165,6 @@ int spmat_set_values_coo(spmat_t A, const double *v, int mode, void *stream) {
         const uint32_t lim = A->n_mixed > 0 ? (uint32_t)A->ncoo : 0xffffffffu;
         void *args[] = {(void *)&jm, (void *)&pm, (void *)&v, (void *)&lim, (void *)&nd, (void *)&nnz, (void *)&vd, (void *)&vo};
         SP_CUDA(cudaLaunchKernel(fn, dim3(g), dim3(256), args, 0, s));
-      } else if (kind >= 4 && z0 == 0) {
-        const bool ins = mode == SPMAT_INSERT;
-        const int kz = kind == 4 ? 1 : 2;
-        const unsigned g = (unsigned)std::max<int64_t>(1, (nnz + 256 * kz - 1) / (256 * kz));
-        const uint32_t *jm = A->jmap.get(), *pm = A->perm.get();
-        double *vd = A->val_d.get(), *vo = A->val_o.get();
-        if (kind == 4)
-          ins ? k_numeric_seg_lean<8, 1, true><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo)
-              : k_numeric_seg_lean<8, 1, false><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo);
-        else if (kind == 5)
-          ins ? k_numeric_seg_lean<8, 2, true><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo)
-              : k_numeric_seg_lean<8, 2, false><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo);
-        else
-          ins ? k_numeric_seg_lean<4, 2, true><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo)
-              : k_numeric_seg_lean<4, 2, false><<<g, 256, 0, s>>>(jm, pm, v, A->nnz_d, nnz, vd, vo);
       } else if (kind == 2 && z0 == 0) {
         // contributions read 8 at a time (C3, same box: 1.149 ms vs 1.200 ms 4 at a time,
         // 1.206 ms for the plain serial loop)

@@ -538,7 +538,7 @@ def test_kernel_variants(sp, comm, kernel, case, monkeypatch):
     A.close()
 
 
-@pytest.mark.parametrize("numeric", ["ilp", "plain", "seg", "seg-4", "warp", "lean", "lean2", "lean4", "pipe", "pipe4", "pipe2", "pipe2s", "pipe1", "pipe3", "one", "ilp-jmap"])
+@pytest.mark.parametrize("numeric", ["ilp", "plain", "seg", "seg-4", "warp", "pipe", "pipe4", "pipe8", "one", "ilp-jmap"])
 def test_numeric_kernels(sp, comm, numeric, monkeypatch):
     """Every COO numeric kernel gives the oracle's values bit for bit (Z1 order), also with
     ~20 contributions per nonzero, and with one contribution per nonzero (stencil COO: jmap is
