@@ -22,9 +22,10 @@ for f in ("bench_default", "bench_reference", "bench_reference_p4"):
     open(f"{P_}/r02_{f}.json", "w").write(last(f"{D}/{f}.json") + "\n")
 for c in ("c1", "c2", "c3", "q2", "bump", "c4b", "c5"):
     open(f"{P_}/r02_bench_{c}_p1.json", "w").write(last(f"{D}/{c}_p1.json") + "\n")
-for P in (2, 4):
+for P in (2, 3, 4):
     for c in ("c4", "c4b", "c5"):
-        open(f"{P_}/r02_bench_{c}_p{P}.json", "w").write(last(f"{D}/{c}_p{P}.json") + "\n")
+        if os.path.exists(f"{D}/{c}_p{P}.json"):
+            open(f"{P_}/r02_bench_{c}_p{P}.json", "w").write(last(f"{D}/{c}_p{P}.json") + "\n")
 open(f"{P_}/r02_bench_c4_p2_nccl.json", "w").write(last(f"{D}/c4_p2_nccl.json") + "\n")
 for P in (1, 2, 4):
     shutil.copy(f"{D}/cg_p{P}.log", f"{P_}/r02_cg_p{P}.log")
@@ -35,11 +36,12 @@ tip = open(f"{D}/pytest_gpu_4gpu.log").readline().split()[-1][:7]
 out = open(f"{P_}/r02_scaling.md", "w")
 out.write(f"# Round-2 bench lines on one 4-GPU box at commit {tip} (tools/r02_final4.sh, `--steps 20 --warmup 5`)\n\n")
 out.write("Median of 5 trials of 20 MatMults (CUDA-graph replay), max over ranks; clocks sampled during the trials.\n")
-out.write("`frac` = the dominant kernel's algorithmic bytes per launch / its in-library CUDA-event duration / 6542.7 GB/s.\n\n")
+out.write("`frac` = the dominant kernel's algorithmic bytes per launch / its launch duration (`duration_source`: the timed "
+          "region / K when a step is one graph-replayed launch, else in-library CUDA events) / 6542.7 GB/s.\n\n")
 out.write("| config | P | ms/step | GFLOP/s | frac | e2e GFLOP/s (pinned host x/y) | SM MHz, reasons | efficiency |\n|---|---|---|---|---|---|---|---|\n")
 base = {}
 for cfg in ("c1", "c2", "c3", "q2", "bump", "c4", "c4b", "c5"):
-    for P in (1, 2, 4):
+    for P in (1, 2, 3, 4):
         f = f"{P_}/r02_bench_{cfg}_p{P}.json" if not (cfg == "c4" and P == 1) else f"{P_}/r02_bench_default.json"
         if not os.path.exists(f):
             continue

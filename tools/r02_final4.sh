@@ -6,7 +6,7 @@ python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $D/smoke.log 2>&
 python bench.py --steps 20 --warmup 5 > $D/bench_default.json 2> $D/bench_default.err; echo "bench rc=$?"
 python bench.py --impl reference --steps 20 --warmup 5 > $D/bench_reference.json 2> $D/bench_reference.err; echo "ref rc=$?"
 for cfg in c1 c2 c3 q2 bump c4b c5; do python bench.py --config $cfg --steps 20 --warmup 5 --no-cpu > $D/${cfg}_p1.json 2> $D/${cfg}_p1.err; done
-for P in 2 4; do for cfg in c4 c4b c5; do
+for P in 2 3 4; do for cfg in c4 c4b c5; do
   python -m torch.distributed.run --nnodes=1 --nproc-per-node $P --master-addr 127.0.0.1 --master-port 2969$P bench.py --gpus $P --config $cfg --steps 20 --warmup 5 --no-cpu > $D/${cfg}_p$P.json 2> $D/${cfg}_p$P.err
 done; done
 SPMAT_HALO=nccl python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29681 bench.py --gpus 2 --steps 20 --warmup 5 --no-cpu --no-e2e > $D/c4_p2_nccl.json 2> $D/c4_p2_nccl.err
