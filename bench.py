@@ -493,28 +493,55 @@ def main():
     t_halo = prof_ms[2] / max(prof_n[2], 1) / 1e3 if prof_n[2] else 0.0
 
     # ---- isolated phases (diag only / halo only / offdiag only, the halo then both SpMVs with
-    # no overlap, and the whole MatMult), eager launches, 3 interleaved rounds, median per phase:
-    # power and clock drift over the run hits every phase alike
+    # no overlap, and the whole MatMult), launched like the headline trials (K calls captured
+    # as one CUDA graph when those were), 3 interleaved rounds, median per phase: power and
+    # clock drift over the run hits every phase alike
     phases = [("all", 7), ("diag", sp.PART_DIAG)]
     if P > 1:
         phases += [("halo", sp.PART_HALO), ("offdiag", sp.PART_OFFDIAG), ("sequential", None)]
     samples = {name: [] for name, _ in phases}
     kk = max(10, min(a.steps, 100))
+
+    def phase_calls(part, st):
+        for _ in range(kk):
+            if part is None:
+                A.mult_part(x, y, sp.PART_HALO, st)
+                A.mult_part(x, y, sp.PART_DIAG | sp.PART_OFFDIAG, st)
+            else:
+                A.mult_part(x, y, part, st)
+
+    phase_graphs = {}
+    if graph is not None:
+        try:
+            for name, part in phases:
+                gs = torch.cuda.Stream()
+                gs.wait_stream(stream)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=gs):
+                    phase_calls(part, gs)
+                stream.wait_stream(gs)
+                g.replay()
+                phase_graphs[name] = g
+            torch.cuda.synchronize()
+        except Exception:
+            phase_graphs = {}
+            torch.cuda.synchronize()
+    iso_launch = "cuda_graph" if len(phase_graphs) == len(phases) else "eager"
+    iso_launch = sdist_agree_launch(iso_launch, max_over_ranks)
     for _round in range(3):
         for name, part in phases:
             barrier()
             torch.cuda.synchronize()
             ev0.record(stream)
-            for _ in range(kk):
-                if part is None:
-                    A.mult_part(x, y, sp.PART_HALO, stream)
-                    A.mult_part(x, y, sp.PART_DIAG | sp.PART_OFFDIAG, stream)
-                else:
-                    A.mult_part(x, y, part, stream)
+            if iso_launch == "cuda_graph":
+                phase_graphs[name].replay()
+            else:
+                phase_calls(part, stream)
             ev1.record(stream)
             torch.cuda.synchronize()
             barrier()
             samples[name].append(max_over_ranks(ev0.elapsed_time(ev1) / kk))
+    del phase_graphs
     iso = {name: statistics.median(v) for name, v in samples.items()}
     A.mult(x, y, stream)  # restore y = A x after the partial products
     torch.cuda.synchronize()
@@ -693,7 +720,7 @@ def main():
                      "inputs_exceed_l2": diag_bytes + off_bytes > l2_bytes},
         "phases_ms": {"diag_spmv": t_diag * 1e3, "offdiag_spmv": t_off * 1e3,
                       "halo_comm_stream": t_halo * 1e3, "halo_bytes": halo_bytes,
-                      "isolated": iso, "overlap_efficiency": overlap},
+                      "isolated": iso, "isolated_launch": iso_launch, "overlap_efficiency": overlap},
         "halo": halo,
         "assembly": {"create_coo_s": t_create, "set_values_coo_ms": t_setvals * 1e3,
                      "coo_entries_per_rank": ncoo,
