@@ -220,6 +220,7 @@ struct BsrOff {
   int n_bblocks;                        // row blocks with off-diagonal block rows (claimed first)
   int64_t nobr;
   unsigned int *ctr;                    // [0] boundary-block warps done, [1] chunk claims, [2] comm warps done
+  int wmax;                             // cap on the lanes per block row of the diagonal product
 };
 
 // W = 4 lanes per off-diagonal block row, every consumer thread of the CTA takes part
@@ -463,12 +464,12 @@ __global__ void __launch_bounds__(kCtaT, 3)
     const double *sv = st[s].val + ((9 * (int64_t)bp0) & 1);
     const int *sc = st[s].col + (bp0 & 3);
     const int *rp = st[s].rp - (br0 & ~3);
-    const int nbr = br1 - br0;
-    if (nbr * 2 > NT) brows_w<1, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 4 > NT) brows_w<2, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 8 > NT) brows_w<4, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 16 > NT) brows_w<8, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
-    else if (nbr * 32 > NT) brows_w<16, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    const int nbr = br1 - br0, wm = off.wmax;
+    if (nbr * 2 > NT || wm <= 1) brows_w<1, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 4 > NT || wm <= 2) brows_w<2, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 8 > NT || wm <= 4) brows_w<4, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 16 > NT || wm <= 8) brows_w<8, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
+    else if (nbr * 32 > NT || wm <= 16) brows_w<16, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
     else brows_w<32, FMA, NT>(br0, br1, bp0, rp, sc, sv, x, y, tid);
     __syncwarp();
     if (lane32 == 0) mbar_arrive(&empty[s]);
@@ -714,6 +715,7 @@ int csr_sync(spmat_s *A, cudaStream_t s) {
 
 int bsr_spmv(spmat_s *A, const double *x, double *y, cudaStream_t s, int mode) {
   BsrOff off{};
+  off.wmax = A->env_bsr_wmax;
   if (mode) {  // NVLink halo: off-diagonal blocks inside the kernel, which ends the epoch
     off.range = A->ob_range.get();
     off.rows = A->ob_rows.get();
@@ -822,6 +824,12 @@ static int bsr_o_env(spmat_s *A) {
   // the 1 kW power cap -- measured 0.8-1.4 % faster on one box (2.760 / 2.752 vs 2.782 / 2.791 ms)
   e = getenv("SPMAT_BSR_FMA");
   A->env_bsr_fma = !(e && atoi(e) == 0);
+  // lanes per block row of the diagonal product: at most 8 (C5: ~11 block rows of 27 blocks
+  // per row block; 16 lanes fill more threads but spend ~40 % of the instructions on the
+  // shuffle reductions -- 8 lanes: 1.086 G -> 0.770 G instructions, 2.79 -> 2.62 ms at P=1 under
+  // the power cap, 0.641 -> 0.629 ms at P=4; 4 lanes: 2.92 ms).  SPMAT_BSR_WMAX overrides.
+  e = getenv("SPMAT_BSR_WMAX");
+  A->env_bsr_wmax = e ? std::max(1, atoi(e)) : 8;
   // off-diagonal blocks with the NVLink halo: 2 = comm warps of the block SpMV (puts + tail,
   // default), 1 = added by the consumers themselves (measured slower: each boundary row block
   // stalls its CTA's stage ring for a ghost-read latency chain, 0.859 vs 0.836 ms at P=4),

@@ -369,6 +369,7 @@ struct spmat_s {
   spmat::DevBuf<int2> rbp;           // n_rowblocks + 1 (first row, first nonzero) pairs
   spmat::DevBuf<int32_t> longrows;   // rows with more than kLong nonzeros
   int64_t n_long = 0;
+  int env_bsr_wmax = 8;              // SPMAT_BSR_WMAX: cap on the lanes per block row (k_spmv_bsr3)
   int rb_budget = 0;                 // row-block cost budget (spmv_prepare; <= kBudget)
   int tma_grid = 0;                  // persistent grid of the bulk-copy SpMV
   int tma_grid_tail = 0;             // its grid with the fused off-diagonal add (>= tma_grid)
