@@ -457,7 +457,7 @@ struct spmat_s {
   cudaEvent_t pipe_ev_pending = nullptr;
   std::vector<cudaEvent_t> pipe_ev;                        // 2 * chunks + 2
   // CG / dot workspace (krylov.cu), allocated on first use
-  spmat::DevBuf<double> cg_r, cg_p, cg_q, cg_partial, cg_scalars, cg_reduced;
+  spmat::DevBuf<double> cg_r, cg_p, cg_q, cg_partial, cg_partial2, cg_scalars, cg_reduced;
   // MatMultTranspose (transpose.cu): transposed diagonal / off-diagonal blocks, built lazily
   bool t_built = false;
   int64_t val_version = 0, t_val_version = -1;  // set_values count / values gathered for

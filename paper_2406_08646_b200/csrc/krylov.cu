@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "halo_dev.cuh"
 #include "internal.h"
 #include "ptx.cuh"
@@ -127,12 +129,17 @@ struct FinArgs {
 // One CTA: local sum of the np partials (fixed order), the cross-rank sum through the scalar
 // board (or the NCCL-reduced value), then the scalar step of CG.  The board epoch is read from
 // and written back to device memory.
+// the fixed-order local sum of np partials (valid in thread 0)
+__device__ __forceinline__ double fold_partials(const double *partial, int np, double *red) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += kDotThreads) s = __dadd_rn(s, __ldcg(partial + i));
+  return block_sum(s, red);
+}
+
 __device__ void finalize_cta(const FinArgs &f, int np) {
   __shared__ double red[kDotThreads / 32];
   __shared__ double total;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < np; i += kDotThreads) s = __dadd_rn(s, __ldcg(f.partial + i));
-  s = block_sum(s, red);
+  double s = fold_partials(f.partial, np, red);
   if (threadIdx.x == 0) total = s;
   __syncthreads();
   if (f.preduced) {  // NCCL already summed the local values over ranks
@@ -444,6 +451,116 @@ __global__ void k_cg_pupdate(double *__restrict__ p, const double *__restrict__ 
   for (; i < n; i += stride) p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
 }
 
+// Small matrices on one rank: ALL maxit iterations in one cooperative launch.  Each iteration
+// is the small path's two kernels (k_cg_spmv_dot's q = A p_i with p_i = r + beta p_{i-1} on the
+// fly and its p.q partials over the same ga CTAs; k_cg_update_p's p/x/r update and r.r partials
+// over the same nb chunks) separated by grid barriers, and instead of a last CTA finalizing each
+// dot, EVERY CTA folds the partials itself (fold_partials: the same order, so the same alpha
+// and beta in every CTA and the same bits as the two-kernel path); CTA 0 records the residual
+// history and leaves the scalars in sc.  Two grid barriers per iteration instead of two kernel
+// launches; partials of the two dots go to separate arrays, so a CTA still folding one dot
+// never races a CTA already writing the next.
+template <int W>
+__global__ void __launch_bounds__(kDotThreads) k_cg_persist(const int32_t *__restrict__ rowptr,
+                                                            const int32_t *__restrict__ col,
+                                                            const double *__restrict__ val, double *x,
+                                                            double *r, double *p, double *q, int64_t m, int ga,
+                                                            int nb, int maxit, double *partA, double *partB,
+                                                            CgScalars *sc, double *hist) {
+  __shared__ double red[kDotThreads / 32];
+  __shared__ double total;
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  double rr = sc->rr, alpha = sc->alpha, beta = sc->beta;
+  int stopped = sc->stopped, iter = sc->iter;
+  const int b = blockIdx.x;
+  constexpr int U = 8;
+  for (int it = 0; it < maxit; ++it) {
+    // ---- q = A p_i, partials of p_i . q (k_cg_spmv_dot)
+    if (b < ga) {
+      auto pv = [&](int64_t c) { return __dadd_rn(r[c], __dmul_rn(beta, p[c])); };
+      const int64_t row = (b * (int64_t)kDotThreads + threadIdx.x) / W;
+      const int lane = threadIdx.x & (W - 1);
+      const bool valid = row < m;
+      const int a = valid ? __ldg(rowptr + row) : 0, z = valid ? __ldg(rowptr + row + 1) : 0;
+      double s = 0.0;
+      for (int e0 = a + lane; e0 < z; e0 += U * W) {
+        int c[U];
+        double v[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * W;
+          c[u] = e < z ? __ldg(col + e) : 0;
+          v[u] = e < z ? __ldg(val + e) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) xv[u] = pv(c[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (e0 + u * W < z) s = __dadd_rn(s, __dmul_rn(v[u], xv[u]));
+      }
+#pragma unroll
+      for (int o = W >> 1; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(0xffffffffu, s, o, W));
+      double pq = 0.0;
+      if (valid && lane == 0) {
+        q[row] = s;
+        pq = __dmul_rn(pv(row), s);
+      }
+      pq = block_sum(pq, red);
+      if (threadIdx.x == 0) partA[b] = pq;
+    }
+    grid.sync();
+    {  // alpha (the OP_CG_ALPHA step of finalize_cta)
+      const double g = fold_partials(partA, ga, red);
+      if (threadIdx.x == 0) total = g;
+      __syncthreads();
+      const double gg = total;
+      if (gg == 0.0 || rr == 0.0) stopped = 1;
+      alpha = stopped ? 0.0 : rr / gg;
+      if (b == 0 && threadIdx.x == 0) sc->pq = gg;
+    }
+    // ---- p_i stored, x += alpha p_i, r -= alpha q, partials of r.r (k_cg_update_p)
+    if (b < nb) {
+      const int64_t chunk = (m + nb - 1) / nb;
+      const int64_t lo = b * chunk, hi = min(m, lo + chunk);
+      double acc = 0.0;
+      for (int64_t i = lo + threadIdx.x; i < hi; i += kDotThreads) {
+        double ri = r[i];
+        if (!stopped) {
+          const double pi = __dadd_rn(ri, __dmul_rn(beta, p[i]));
+          p[i] = pi;
+          x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pi));
+          ri = __dsub_rn(ri, __dmul_rn(alpha, q[i]));
+          r[i] = ri;
+        }
+        acc = __dadd_rn(acc, __dmul_rn(ri, ri));
+      }
+      acc = block_sum(acc, red);
+      if (threadIdx.x == 0) partB[b] = acc;
+    }
+    grid.sync();
+    {  // beta, rr (the OP_CG_BETA step)
+      const double g = fold_partials(partB, nb, red);
+      if (threadIdx.x == 0) total = g;
+      __syncthreads();
+      const double gg = total;
+      if (!stopped) {
+        beta = gg / rr;
+        rr = gg;
+      }
+      iter += 1;
+      if (b == 0 && threadIdx.x == 0 && hist) hist[iter] = rr;
+      __syncthreads();  // total is rewritten by the next fold
+    }
+  }
+  if (b == 0 && threadIdx.x == 0) {
+    sc->rr = rr;
+    sc->alpha = alpha;
+    sc->beta = beta;
+    sc->stopped = stopped;
+    sc->iter = iter;
+  }
+}
+
 // ------------------------------------------------------------------ host side
 static int max_dot_blocks(spmat_s *A) { return A->comm->num_sms * 4; }
 
@@ -559,6 +676,55 @@ static int cg_iteration(spmat_s *A, double *x, double *rr_hist, cudaStream_t s) 
   return SPMAT_OK;
 }
 
+// the persistent small-matrix CG: one rank, the direct SpMV regime, every CTA resident
+static int64_t fused_grid_of(spmat_s *A) { return (A->m * A->lanes + kDotThreads - 1) / kDotThreads; }
+
+static bool persist_ok(spmat_s *A) {
+  const char *e = getenv("SPMAT_CG_PERSIST");
+  if (e && !strcmp(e, "0")) return false;
+  return A->comm->nranks == 1 && A->kernel_id == 5 && A->bs == 1 && A->m > 0 &&
+         fused_grid_of(A) <= max_dot_blocks(A) && !A->profile;
+}
+
+template <int W>
+static cudaError_t launch_persist(spmat_s *A, double *x, double *hist, int maxit, int ga, int nb, int grid,
+                                  cudaStream_t s) {
+  auto kern = k_cg_persist<W>;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDotThreads, 0);
+  if (e != cudaSuccess) return e;
+  if ((int64_t)per_sm * A->comm->num_sms < grid) return cudaErrorCooperativeLaunchTooLarge;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kDotThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  double *partA = A->cg_partial.get(), *partB = A->cg_partial2.get();
+  return cudaLaunchKernelEx(&cfg, kern, (const int32_t *)A->rowptr_d.get(), (const int32_t *)A->col_d.get(),
+                            (const double *)A->val_d.get(), x, A->cg_r.get(), A->cg_p.get(), A->cg_q.get(), A->m,
+                            ga, nb, maxit, partA, partB, (CgScalars *)A->cg_scalars.get(), hist);
+}
+
+static int cg_persist(spmat_s *A, double *x, double *hist, int maxit, cudaStream_t s) {
+  if (A->cg_partial2.n == 0) SP_TRY(A->cg_partial2.alloc(max_dot_blocks(A)));
+  const int ga = (int)fused_grid_of(A), nb = dot_blocks(A), grid = std::max(ga, nb);
+  cudaError_t e;
+  switch (A->lanes) {
+    case 1: e = launch_persist<1>(A, x, hist, maxit, ga, nb, grid, s); break;
+    case 2: e = launch_persist<2>(A, x, hist, maxit, ga, nb, grid, s); break;
+    case 4: e = launch_persist<4>(A, x, hist, maxit, ga, nb, grid, s); break;
+    case 8: e = launch_persist<8>(A, x, hist, maxit, ga, nb, grid, s); break;
+    case 16: e = launch_persist<16>(A, x, hist, maxit, ga, nb, grid, s); break;
+    default: e = launch_persist<32>(A, x, hist, maxit, ga, nb, grid, s); break;
+  }
+  SP_CUDA(e);
+  return SPMAT_OK;
+}
+
 constexpr int kCgBatch = 8;  // CG iterations per graph launch
 
 static bool graph_ok(spmat_s *A) {
@@ -635,6 +801,14 @@ int spmat_cg(spmat_t A, const double *b, double *x, int maxit, double *rr_hist, 
   SP_CUDA(launch_pdl(k_cg_init, nb, kDotThreads, 0, cs, b, (const double *)q, r, p, m,
                      fin_args(A, OP_CG_INIT, nullptr, rr_hist)));
   SP_TRY(finish_nccl(A, OP_CG_INIT, nullptr, rr_hist, nb, cs));
+  if (maxit > 0 && persist_ok(A)) {  // every iteration in one cooperative launch
+    SP_TRY(cg_persist(A, x, rr_hist, maxit, cs));
+    if (use_graph) {
+      SP_CUDA(cudaEventRecord(A->cg_ev[1], cs));
+      SP_CUDA(cudaStreamWaitEvent(s, A->cg_ev[1], 0));
+    }
+    return SPMAT_OK;
+  }
   if (!use_graph) {
     for (int k = 0; k < maxit; ++k) SP_TRY(cg_iteration(A, x, rr_hist, s));
     return SPMAT_OK;

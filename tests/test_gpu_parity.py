@@ -599,6 +599,48 @@ def test_vec_dot_and_cg_single_rank(sp, comm):
     A.close()
 
 
+@pytest.mark.parametrize("shape,npts", [((24, 24), 5), ((13, 13, 13), 27), ((40, 40, 8), 7)])
+def test_cg_persistent_matches_graph_path(sp, comm, shape, npts, monkeypatch):
+    """The one-launch CG of small single-rank matrices (every iteration in a cooperative kernel
+    with grid barriers) gives the two-kernel graph path's iterates and residual history bit for
+    bit, also when iterations stop early (zero residual), and both agree with the oracle."""
+    M = int(np.prod(shape))
+    i, j, v = synth.stencil_coo(shape, npts, values="real")
+    # symmetric positive definite: A + A^T + 2*npts*I built through ADD of the transposed COO
+    ii = torch.cat([i, j, torch.arange(M)])
+    jj = torch.cat([j, i, torch.arange(M)])
+    vv = torch.cat([v, v, torch.full((M,), 2.0 * npts, dtype=torch.float64)])
+    keep = (ii >= 0) & (jj >= 0)
+    ii, jj, vv = ii[keep], jj[keep], vv[keep]
+    O = oracle.OracleMat(M, M, [M], [M], [ii], [jj])
+    O.set_values([vv])
+    rhs = synth.x_vector(0, M, "real", seed=5)
+    out = {}
+    for persist in ("1", "0"):
+        monkeypatch.setenv("SPMAT_CG_PERSIST", persist)
+        A = sp.Mat(comm, M, M, M, M, dev(ii), dev(jj))
+        A.set_values(dev(vv))
+        res = []
+        for iters in (1, 7, 60):
+            x = torch.zeros(M, dtype=torch.float64, device="cuda")
+            hist = torch.zeros(iters + 1, dtype=torch.float64, device="cuda")
+            A.cg(dev(rhs), x, iters, hist)
+            res.append((x.cpu(), hist.cpu()))
+        # zero right-hand side: stopped from the start, x stays 0
+        x0 = torch.zeros(M, dtype=torch.float64, device="cuda")
+        h0 = torch.ones(4, dtype=torch.float64, device="cuda")
+        A.cg(torch.zeros(M, dtype=torch.float64, device="cuda"), x0, 3, h0)
+        res.append((x0.cpu(), h0.cpu()))
+        out[persist] = res
+        A.close()
+    for (xa, ha), (xb, hb) in zip(out["1"], out["0"]):
+        assert torch.equal(xa, xb) and torch.equal(ha, hb)
+    xo, ho = O.cg(rhs.numpy(), np.zeros(M), 60)
+    assert rel_err(out["1"][2][0].numpy(), xo) <= 1e-10
+    assert np.max(np.abs(out["1"][2][1].numpy() - ho) / ho[0]) <= 1e-10
+    assert not out["1"][3][0].any() and torch.equal(out["1"][3][1], torch.zeros(4, dtype=torch.float64))
+
+
 def test_host_pipeline_matches_device(sp, comm):
     """Host x/y take the chunked upload/compute/download pipeline for large matrices; the
     result equals the device-pointer MatMult bit for bit."""
