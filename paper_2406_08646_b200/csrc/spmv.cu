@@ -15,8 +15,10 @@
 // right from +0.0 with separately rounded products -- bit-identical to a serial CSR loop.
 //
 // Row blocks: boundaries where the running cost rowptr[r] + kAlpha * r crosses a multiple of
-// kBudget, plus a block of its own for every row longer than kLong; so a block has at most
-// kBudget / kAlpha rows and at most kBudget + kLong nonzeros (fits one stage).
+// the budget (kBudget, or less when a smaller budget lets the consumers finish every block in
+// one round of x gathers -- spmv_prepare), plus a block of its own for every row longer than
+// kLong; so a block has at most kBudget / kAlpha rows and at most kBudget + kLong nonzeros
+// (fits one stage).
 //
 // Alternatives kept for A/B measurement (SPMAT_SPMV_KERNEL=stream|vector): a non-persistent
 // CTA-per-row-block kernel that stages products in shared memory, and a plain sub-warp
