@@ -403,8 +403,48 @@ __global__ void __launch_bounds__(kDotThreads) k_cg_update(double *__restrict__ 
   partial_done(block_sum(combine(acc), red), f);
 }
 
-// The small path's update: p_i = r + beta p_{i-1} formed and stored here (the p update folded
-// in, one kernel fewer per iteration), then x += alpha p_i, r -= alpha q, r.r partials.
+// The small path's update of one chunk [lo, hi): p_i = r + beta p_{i-1} formed and stored
+// (the p update folded in), x += alpha p_i, r -= alpha q; returns this thread's r.r partial.
+// kU elements per thread in flight (kU accumulators, combined in a fixed tree), so a short
+// chunk costs ~2 rounds of loads instead of one per element.  Shared by k_cg_update_p and
+// k_cg_persist, so both give the same bits.
+__device__ __forceinline__ double update_p_chunk(double *__restrict__ x, double *__restrict__ r,
+                                                 double *__restrict__ p, const double *__restrict__ q,
+                                                 int64_t lo, int64_t hi, double alpha, double beta, bool go) {
+  double acc[kU];
+#pragma unroll
+  for (int u = 0; u < kU; ++u) acc[u] = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += kU * kDotThreads) {
+    double rv[kU], pv[kU], xv[kU], qv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t k = i + u * kDotThreads;
+      const bool in = k < hi;
+      rv[u] = in ? r[k] : 0.0;
+      if (go && in) {
+        pv[u] = p[k];
+        xv[u] = x[k];
+        qv[u] = q[k];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t k = i + u * kDotThreads;
+      if (k >= hi) continue;
+      if (go) {
+        const double pi = __dadd_rn(rv[u], __dmul_rn(beta, pv[u]));
+        p[k] = pi;
+        x[k] = __dadd_rn(xv[u], __dmul_rn(alpha, pi));
+        rv[u] = __dsub_rn(rv[u], __dmul_rn(alpha, qv[u]));
+        r[k] = rv[u];
+      }
+      acc[u] = __dadd_rn(acc[u], __dmul_rn(rv[u], rv[u]));
+    }
+  }
+  return combine(acc);
+}
+
+// The small path's update kernel (one chunk per CTA)
 __global__ void __launch_bounds__(kDotThreads) k_cg_update_p(double *__restrict__ x, double *__restrict__ r,
                                                              double *__restrict__ p, const double *__restrict__ q,
                                                              int64_t n, FinArgs f) {
@@ -414,18 +454,7 @@ __global__ void __launch_bounds__(kDotThreads) k_cg_update_p(double *__restrict_
   const bool go = !f.sc->stopped;
   const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
-  double acc = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += kDotThreads) {
-    double ri = r[i];
-    if (go) {
-      const double pi = __dadd_rn(ri, __dmul_rn(beta, p[i]));
-      p[i] = pi;
-      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pi));
-      ri = __dsub_rn(ri, __dmul_rn(alpha, q[i]));
-      r[i] = ri;
-    }
-    acc = __dadd_rn(acc, __dmul_rn(ri, ri));
-  }
+  const double acc = update_p_chunk(x, r, p, q, lo, hi, alpha, beta, go);
   // every CTA has read sc->alpha/beta/stopped before the last one (which rewrites sc) gets here
   partial_done(block_sum(acc, red), f);
 }
@@ -522,19 +551,7 @@ __global__ void __launch_bounds__(kDotThreads) k_cg_persist(const int32_t *__res
     if (b < nb) {
       const int64_t chunk = (m + nb - 1) / nb;
       const int64_t lo = b * chunk, hi = min(m, lo + chunk);
-      double acc = 0.0;
-      for (int64_t i = lo + threadIdx.x; i < hi; i += kDotThreads) {
-        double ri = r[i];
-        if (!stopped) {
-          const double pi = __dadd_rn(ri, __dmul_rn(beta, p[i]));
-          p[i] = pi;
-          x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pi));
-          ri = __dsub_rn(ri, __dmul_rn(alpha, q[i]));
-          r[i] = ri;
-        }
-        acc = __dadd_rn(acc, __dmul_rn(ri, ri));
-      }
-      acc = block_sum(acc, red);
+      const double acc = block_sum(update_p_chunk(x, r, p, q, lo, hi, alpha, beta, !stopped), red);
       if (threadIdx.x == 0) partB[b] = acc;
     }
     grid.sync();
@@ -564,12 +581,14 @@ __global__ void __launch_bounds__(kDotThreads) k_cg_persist(const int32_t *__res
 // ------------------------------------------------------------------ host side
 static int max_dot_blocks(spmat_s *A) { return A->comm->num_sms * 4; }
 
-// CTAs of the update kernels (x/r update + r.r, CG init): ~8 elements per thread, at most 4
-// CTAs per SM; of a pure dot (p.q, spmat_vec_dot): one CTA up to 64 elements per thread (the
-// cross-CTA handshake costs more than the loop), else the same.  Functions of m only, so every
-// dot of a matrix reduces in the same fixed order.
+// CTAs of the update kernels (x/r update + r.r, CG init): ~2 elements per thread (the update
+// keeps kU = 4 in flight, so a chunk is one round of loads; Kuu-sized one-launch CG: 9.0 µs per
+// iteration vs 9.0 µs at ~8 per thread), at most 4 CTAs per SM; of a pure dot (p.q,
+// spmat_vec_dot): one CTA up to 64 elements per thread (the cross-CTA handshake costs more than
+// the loop), else the same.  Functions of m only, so every dot of a matrix reduces in the same
+// fixed order.
 static int dot_blocks(spmat_s *A) {
-  const int64_t want = (A->m + 8 * kDotThreads - 1) / (8 * kDotThreads);
+  const int64_t want = (A->m + 2 * kDotThreads - 1) / (2 * kDotThreads);
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, max_dot_blocks(A)));
 }
 static int pure_dot_blocks(spmat_s *A) { return A->m <= 64 * kDotThreads ? 1 : dot_blocks(A); }
