@@ -417,6 +417,8 @@ def main():
     torch.cuda.empty_cache()
     info = A.info()
     nnz_local = info["nnz_d"] + info["nnz_o"]
+    n_contrib = info["n_contrib"]
+    setv_bytes = 12 * n_contrib + (0 if n_contrib == nnz_local else 4 * (nnz_local + 1)) + 8 * nnz_local
     nnz_global = sdist.sum_over_ranks(nnz_local)
 
     x = synth.x_vector(off[rank], off[rank + 1], a.values, device="cuda")
@@ -724,7 +726,11 @@ def main():
         "halo": halo,
         "assembly": {"create_coo_s": t_create, "set_values_coo_ms": t_setvals * 1e3,
                      "coo_entries_per_rank": ncoo,
-                     "set_values_GBps": (12 * ncoo + 12 * nnz_local) / t_setvals / 1e9},
+                     # compulsory bytes: v (8) and perm (4) per contribution, jmap (4 per nonzero;
+                     # not read with one contribution per nonzero), the values written (8 per nonzero)
+                     "set_values_bytes": setv_bytes,
+                     "set_values_GBps": setv_bytes / t_setvals / 1e9,
+                     "set_values_GBps_model_12_12": (12 * ncoo + 12 * nnz_local) / t_setvals / 1e9},
         "e2e": e2e,
         "gpu_launches": per_step_kernels * a.steps * TRIALS,
         "clocks": clk.summary(),
